@@ -1,0 +1,259 @@
+/*
+ * hetpar_b200.h -- C ABI of the B200-native data-parallel training step.
+ *
+ * Drop-in boundary for the reference's per-rank DP step (arxiv/paper_2009_14783,
+ * "hetpar"): the C++ wrapper include/hetpar_b200/step_engine.hpp and the Python
+ * binding paper_2009_14783_b200/_lib.py sit on top of exactly these entry points.
+ * Every reference interface an entry point replaces is cited beside it
+ * (paths relative to the reference's proj/ directory).
+ *
+ * Conventions: plain pointers and sizes, no torch types; every call returns an
+ * hp_status; on failure hp_last_error() (thread-local) holds the message.  The
+ * status codes map 1:1 onto the reference's error taxonomy
+ * (include/hetpar/common.hpp:14-34) so a C++ caller can re-throw the matching
+ * hetpar::*_error.
+ */
+#ifndef HETPAR_B200_H
+#define HETPAR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HP_OK = 0,
+  HP_ESHAPE = 1,   /* shape_error   common.hpp:17 */
+  HP_ECONFIG = 2,  /* config_error  common.hpp:20 */
+  HP_EINDEX = 3,   /* index_error   common.hpp:23 */
+  HP_EIO = 4,      /* io_error      common.hpp:26 */
+  HP_ECOMM = 5,    /* comm_error    common.hpp:29 */
+  HP_ENUMERIC = 6, /* numeric_error common.hpp:32 */
+  HP_ECUDA = 7     /* device failure (no reference counterpart) */
+} hp_status;
+
+const char* hp_last_error(void);
+const char* hp_version(void);
+
+/* ------------------------------------------------------------------------
+ * Host data path (bit-exact with the reference).
+ * ---------------------------------------------------------------------- */
+
+/* SeededRng::next_u64 stream (include/hetpar/rng.hpp:15-22). */
+hp_status hp_splitmix64(uint64_t seed, uint64_t n, uint64_t* out);
+/* shuffle(iota(n), SeededRng(seed)) (rng.hpp:74-82). */
+hp_status hp_shuffle_iota(uint64_t seed, uint64_t n, uint64_t* out);
+
+/* build_epoch_batches (src/dataset.cpp:52-88). order[n] receives the shuffled
+ * global ids, sizes[*nbatches] the batch lengths (batch b is the next
+ * sizes[b] ids of order). HP_ECONFIG when an instance exceeds max_tokens. */
+hp_status hp_build_epoch_batches(const uint32_t* token_lengths, uint64_t n,
+                                 uint64_t max_sentences, uint64_t max_tokens,
+                                 uint64_t base_seed, uint64_t epoch,
+                                 uint64_t* order, uint64_t* sizes,
+                                 uint64_t* nbatches);
+
+/* partition_for_rank (src/dataset.cpp:90-117): rounds = ceil(nbatches/world)
+ * entries; batch_index/dummy have capacity for them. */
+hp_status hp_partition_for_rank(uint64_t nbatches, uint64_t world,
+                                uint64_t rank, uint64_t* batch_index,
+                                uint8_t* dummy, uint64_t* rounds);
+
+/* Synthetic MLM record stream: generate_mlm_shards' record sequence
+ * (src/datagen.cpp:71-127; make_nsp_pair / assemble_pair / mask_tokens,
+ * src/textgen.cpp:24-95), in memory instead of HSD1 shards.  max_seq_tokens>0
+ * is a repo extension: BERT-style truncation of the pair (no extra draws). */
+typedef struct {
+  uint64_t n;
+  int64_t vocab;
+  uint64_t docs;
+  uint64_t sentences_per_doc;
+  uint64_t min_words;
+  uint64_t max_words;
+  double p_select;
+  double p_mask;
+  double p_random;
+  uint64_t seed;
+  uint64_t max_seq_tokens;
+} hp_mlm_gen_desc;
+
+hp_status hp_mlm_generate_size(const hp_mlm_gen_desc* d, uint64_t* tokens_total,
+                               uint64_t* masks_total);
+/* CSR output: tok_off[n+1], tokens/segments[tokens_total];
+ * mask_off[n+1], mask_pos/mask_orig[masks_total]; label[n]. */
+hp_status hp_mlm_generate(const hp_mlm_gen_desc* d, uint64_t* tok_off,
+                          int64_t* tokens, int64_t* segments,
+                          uint64_t* mask_off, int64_t* mask_pos,
+                          int64_t* mask_orig, int64_t* label);
+
+/* ------------------------------------------------------------------------
+ * Model description and canonical parameter table.
+ * ---------------------------------------------------------------------- */
+enum {
+  HP_ARCH_MASKED_TOKEN_MODEL = 3, /* Arch::masked_token_model, model.hpp:16 */
+  HP_ARCH_BERT_ENCODER = 16       /* repo extension: L post-LN BERT blocks   */
+};
+
+/* ModelSpec (include/hetpar/model.hpp:28-67) + the extension's fields. */
+typedef struct {
+  int arch;
+  uint64_t d_model;
+  uint64_t heads;
+  uint64_t vocab;
+  uint64_t max_seq;
+  uint64_t layers; /* bert_encoder only */
+  uint64_t d_ff;   /* bert_encoder only */
+  int with_nsp;
+  double label_smooth_eps;
+} hp_model_desc;
+
+enum { HP_PARAM_WEIGHT = 0, HP_PARAM_TABLE = 1, HP_PARAM_BIAS = 2, HP_PARAM_GAIN = 3 };
+
+/* param_shapes (model.hpp:91-142): count and flat element total. */
+hp_status hp_param_count(const hp_model_desc* m, uint64_t* nparams,
+                         uint64_t* nelems);
+hp_status hp_param_info(const hp_model_desc* m, uint64_t i, char* name,
+                        uint64_t name_cap, uint64_t* rows, uint64_t* cols,
+                        uint64_t* offset, int* kind);
+/* init_parameters<double> with derived_rng(seed, 0) (model.hpp:171-184). */
+hp_status hp_init_parameters(const hp_model_desc* m, uint64_t seed, double* out);
+
+/* Gradient buckets: whole parameters walked in reverse canonical
+ * order, closed when the next would exceed bucket_bytes (fp32). bucket i is
+ * the flat range [lo[i], hi[i]).  Capacity nparams. */
+hp_status hp_bucket_plan(const hp_model_desc* m, double bucket_mb,
+                         uint64_t* lo, uint64_t* hi, uint64_t* nbuckets);
+
+/* ------------------------------------------------------------------------
+ * Communicator: one process per GPU, NCCL over NVLink/NVSwitch.  The 128-byte
+ * id is created on rank 0 and shipped with ProcessGroup::broadcast
+ * (comm.hpp:25-27) or torch.distributed.
+ * ---------------------------------------------------------------------- */
+typedef struct hp_comm hp_comm;
+hp_status hp_comm_unique_id(uint8_t id[128]);
+hp_status hp_comm_create(int world, int rank, int device, const uint8_t id[128],
+                         hp_comm** out);
+hp_status hp_comm_destroy(hp_comm* c);
+
+/* ------------------------------------------------------------------------
+ * Step engine: StepEngine<T>::round (include/hetpar/engine.hpp:125-165).
+ * ---------------------------------------------------------------------- */
+typedef struct hp_engine hp_engine;
+
+enum { HP_OPT_SGD = 0, HP_OPT_ADAM = 1 };           /* OptKind, optim.hpp:77 */
+enum { HP_POLICY_SENTENCES = 1, HP_POLICY_TOKENS = 2 }; /* WeightPolicy */
+enum { HP_COMPUTE_F32 = 0, HP_COMPUTE_BF16 = 1 };
+
+typedef struct {
+  int kind;
+  double beta1, beta2, eps;
+} hp_optim_desc;
+
+typedef struct {
+  int compute;          /* HP_COMPUTE_F32: fp32 parity path; BF16: tcgen05 */
+  int policy;           /* weight policy */
+  int device;           /* CUDA ordinal */
+  double bucket_mb;     /* gradient bucket cap */
+  uint64_t max_tokens;  /* capacity: tokens per rank batch */
+  uint64_t max_batch;   /* capacity: instances per rank batch */
+  uint64_t max_masks;   /* capacity: masked positions per rank batch */
+  uint64_t update_freq; /* K micro rounds per update (Accumulator) */
+} hp_exec_desc;
+
+/* Batch = vector<Instance> (model.hpp:72-83), flattened to CSR. */
+typedef struct {
+  uint64_t n_inst;
+  const uint64_t* tok_off;   /* [n_inst+1] */
+  const int64_t* tokens;     /* [tok_off[n]] */
+  const int64_t* segments;   /* [tok_off[n]] */
+  const uint64_t* mask_off;  /* [n_inst+1] */
+  const int64_t* mask_pos;   /* within-instance positions */
+  const int64_t* mask_orig;
+  const int64_t* label;      /* [n_inst] NSP label */
+} hp_batch;
+
+/* StepReport (engine.hpp:26-32) minus the host timing fields. */
+typedef struct {
+  int updated;       /* 1 when this round completed an update (K-th round) */
+  uint64_t step;     /* P after this update */
+  double loss;       /* global loss_sum / weight of the update */
+  double weight;     /* global weight of the update */
+  double local_loss_sum;
+  double local_weight;
+} hp_round_out;
+
+hp_status hp_engine_create(const hp_model_desc* m, const hp_optim_desc* o,
+                           const hp_exec_desc* x, hp_comm* comm /* NULL: world 1 */,
+                           hp_engine** out);
+hp_status hp_engine_destroy(hp_engine* e);
+/* canonical flat parameters (params_to_bytes order, model.hpp:190-195);
+ * dtype 0 = f32, 1 = f64. */
+hp_status hp_engine_set_params(hp_engine* e, const void* flat, uint64_t n, int dtype);
+hp_status hp_engine_get_params(hp_engine* e, void* flat, uint64_t n, int dtype);
+/* rank root's parameters win (engine.hpp:263-264). */
+hp_status hp_engine_broadcast_params(hp_engine* e, int root);
+/* Adam state (for HCK1): m, v in canonical order, t. */
+hp_status hp_engine_get_adam(hp_engine* e, float* m, float* v, uint64_t* t);
+hp_status hp_engine_set_adam(hp_engine* e, const float* m, const float* v, uint64_t t);
+/* local (pre-reduce) gradient of the last round, canonical order; valid after
+ * hp_engine_round_sync when debug capture is on. */
+hp_status hp_engine_set_capture(hp_engine* e, int on);
+hp_status hp_engine_get_local_grads(hp_engine* e, float* flat, uint64_t n);
+
+/* Stage a rank batch: host CSR -> pinned -> one H2D copy on the engine's
+ * stream.  Returns as soon as the copy is enqueued. */
+hp_status hp_engine_stage_batch(hp_engine* e, const hp_batch* b);
+/* One lockstep round on the staged batch: forward -> [loss, weight] allreduce
+ * -> backward with bucketed gradient allreduce on a side stream -> (K-th round)
+ * /sum(weight) and the optimizer update.  lr = scheduled_lr(P+1).  _async
+ * enqueues only; _sync waits and fills out (and raises numeric errors the way
+ * engine.hpp:134-138 does). hp_engine_round = async + sync. */
+hp_status hp_engine_round_async(hp_engine* e, int dummy, double lr);
+hp_status hp_engine_round_sync(hp_engine* e, hp_round_out* out);
+hp_status hp_engine_round(hp_engine* e, int dummy, double lr, hp_round_out* out);
+/* params_digest (model.hpp:211-217): FNV-1a over the f32 parameter bytes. */
+hp_status hp_engine_params_digest(hp_engine* e, uint64_t* digest);
+/* Number of this library's kernels launched since creation (for bench). */
+hp_status hp_engine_kernel_launches(hp_engine* e, uint64_t* n);
+/* CUDA-event time (ms) of the dominant kernel class over the last sync
+ * window; name receives its label. */
+hp_status hp_engine_timers(hp_engine* e, int enable);
+hp_status hp_engine_timer_read(hp_engine* e, int which, char* name, uint64_t cap,
+                               double* ms, uint64_t* launches, double* bytes,
+                               double* flops);
+hp_status hp_engine_step_count(hp_engine* e, uint64_t* step);
+/* CUDA events on the engine's compute stream (the stream every kernel of the
+ * step is launched on): mark(slot) records, elapsed(a, b) waits for b and
+ * returns milliseconds between the two marks. slots 0..7. */
+hp_status hp_engine_mark(hp_engine* e, int slot);
+hp_status hp_engine_elapsed(hp_engine* e, int a, int b, double* ms);
+hp_status hp_engine_synchronize(hp_engine* e);
+/* bytes one hp_engine_stage_batch copies host->device, and one round copies
+ * device->host (the [loss, weight] readback + status flags). */
+hp_status hp_engine_io_bytes(hp_engine* e, uint64_t* h2d, uint64_t* d2h);
+
+/* ------------------------------------------------------------------------
+ * Test hooks (used by tests/ only): run one GEMM of the engine's dispatch on
+ * caller-owned device buffers.  path: 0 auto, 1 SIMT fp32, 2 tcgen05.
+ * act: 0 none, 1 GELU (pre-activation to aux), 2 dGELU (multiply by
+ * GELU'(aux)).  bn: tcgen05 tile width (0 = heuristic, 128 or 256).
+ * ---------------------------------------------------------------------- */
+hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t lda,
+                        int a_trans, const void* B, int64_t ldb, int b_trans,
+                        int64_t b_group, int64_t b_gstride, void* C, int64_t ldc,
+                        int c_bf16, int64_t c_group, int64_t c_gstride,
+                        const float* bias, int act, void* aux, const void* resid,
+                        int64_t ld_resid, int accumulate, int path, int bn);
+hp_status hp_debug_sync(void);
+/* One Adam (sgd=0) or SGD (sgd=1) update of the device kernel on caller-owned
+ * device fp32 buffers, no scaling: compare with kern::adam_update<float>. */
+hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n,
+                        float lr, float b1, float b2, float eps, float c1, float c2,
+                        int sgd);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETPAR_B200_H */

@@ -1,0 +1,10 @@
+"""hetpar-b200: B200-native data-parallel training step of arXiv 2009.14783.
+
+The product path is the native library libhetpar_b200.so (sm_100a kernels +
+NCCL) behind the C ABI in include/hetpar_b200.h; this package is its Python
+binding and the host-side mirror of the reference API.
+"""
+from .api import *  # noqa: F401,F403
+from .api import __all__ as _api_all
+
+__all__ = list(_api_all)

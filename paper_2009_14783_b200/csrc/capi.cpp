@@ -1,0 +1,419 @@
+// extern "C" boundary (include/hetpar_b200.h).  Every entry point converts
+// exceptions into hp_status + a thread-local message.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "engine.h"
+#include "hetpar_b200.h"
+#include "hostdata.h"
+#include "hp_common.h"
+
+namespace hp {
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace hp
+
+using hp::fail;
+
+struct hp_engine {
+  hp::Engine* e = nullptr;
+};
+
+static void need(const void* p, const char* what) {
+  if (!p) fail(HP_ECONFIG, std::string("null pointer: ") + what);
+}
+
+extern "C" {
+
+const char* hp_last_error(void) { return hp::g_last_error.c_str(); }
+const char* hp_version(void) { return "hetpar_b200 0.1 (sm_100a)"; }
+
+hp_status hp_splitmix64(uint64_t seed, uint64_t n, uint64_t* out) {
+  HP_API_BEGIN
+  need(out, "out");
+  hp::SplitMix r(seed);
+  for (uint64_t i = 0; i < n; ++i) out[i] = r.next();
+  HP_API_END
+}
+
+hp_status hp_shuffle_iota(uint64_t seed, uint64_t n, uint64_t* out) {
+  HP_API_BEGIN
+  need(out, "out");
+  std::vector<uint64_t> a(n);
+  for (uint64_t i = 0; i < n; ++i) a[i] = i;
+  hp::SplitMix r(seed);
+  hp::shuffle_u64(a, r);
+  std::memcpy(out, a.data(), n * 8);
+  HP_API_END
+}
+
+hp_status hp_build_epoch_batches(const uint32_t* lens, uint64_t n, uint64_t max_sentences,
+                                 uint64_t max_tokens, uint64_t base_seed, uint64_t epoch,
+                                 uint64_t* order, uint64_t* sizes, uint64_t* nbatches) {
+  HP_API_BEGIN
+  need(nbatches, "nbatches");
+  if (n) {
+    need(lens, "token_lengths");
+    need(order, "order");
+    need(sizes, "sizes");
+  }
+  auto p = hp::build_epoch_batches(lens, n, max_sentences, max_tokens, base_seed, epoch);
+  if (n) std::memcpy(order, p.order.data(), n * 8);
+  if (!p.sizes.empty()) std::memcpy(sizes, p.sizes.data(), p.sizes.size() * 8);
+  *nbatches = p.sizes.size();
+  HP_API_END
+}
+
+hp_status hp_partition_for_rank(uint64_t nbatches, uint64_t world, uint64_t rank,
+                                uint64_t* batch_index, uint8_t* dummy, uint64_t* rounds) {
+  HP_API_BEGIN
+  need(rounds, "rounds");
+  auto s = hp::partition_for_rank(nbatches, world, rank);
+  need(batch_index, "batch_index");
+  need(dummy, "dummy");
+  for (size_t t = 0; t < s.size(); ++t) {
+    batch_index[t] = s[t].batch_index;
+    dummy[t] = s[t].dummy ? 1 : 0;
+  }
+  *rounds = s.size();
+  HP_API_END
+}
+
+hp_status hp_mlm_generate_size(const hp_mlm_gen_desc* d, uint64_t* tokens_total,
+                               uint64_t* masks_total) {
+  HP_API_BEGIN
+  need(d, "desc");
+  auto r = hp::mlm_generate(*d);
+  *tokens_total = r.tokens.size();
+  *masks_total = r.mask_pos.size();
+  HP_API_END
+}
+
+hp_status hp_mlm_generate(const hp_mlm_gen_desc* d, uint64_t* tok_off, int64_t* tokens,
+                          int64_t* segments, uint64_t* mask_off, int64_t* mask_pos,
+                          int64_t* mask_orig, int64_t* label) {
+  HP_API_BEGIN
+  need(d, "desc");
+  auto r = hp::mlm_generate(*d);
+  std::memcpy(tok_off, r.tok_off.data(), r.tok_off.size() * 8);
+  std::memcpy(tokens, r.tokens.data(), r.tokens.size() * 8);
+  std::memcpy(segments, r.segments.data(), r.segments.size() * 8);
+  std::memcpy(mask_off, r.mask_off.data(), r.mask_off.size() * 8);
+  if (!r.mask_pos.empty()) {
+    std::memcpy(mask_pos, r.mask_pos.data(), r.mask_pos.size() * 8);
+    std::memcpy(mask_orig, r.mask_orig.data(), r.mask_orig.size() * 8);
+  }
+  std::memcpy(label, r.label.data(), r.label.size() * 8);
+  HP_API_END
+}
+
+hp_status hp_param_count(const hp_model_desc* m, uint64_t* nparams, uint64_t* nelems) {
+  HP_API_BEGIN
+  need(m, "model");
+  auto t = hp::param_table(*m);
+  *nparams = t.size();
+  *nelems = t.back().offset + t.back().size();
+  HP_API_END
+}
+
+hp_status hp_param_info(const hp_model_desc* m, uint64_t i, char* name, uint64_t name_cap,
+                        uint64_t* rows, uint64_t* cols, uint64_t* offset, int* kind) {
+  HP_API_BEGIN
+  need(m, "model");
+  auto t = hp::param_table(*m);
+  if (i >= t.size()) fail(HP_EINDEX, "parameter index out of range");
+  const auto& e = t[i];
+  if (name && name_cap) {
+    std::strncpy(name, e.name.c_str(), name_cap - 1);
+    name[name_cap - 1] = 0;
+  }
+  if (rows) *rows = e.rows;
+  if (cols) *cols = e.cols;
+  if (offset) *offset = e.offset;
+  if (kind) *kind = e.kind;
+  HP_API_END
+}
+
+hp_status hp_init_parameters(const hp_model_desc* m, uint64_t seed, double* out) {
+  HP_API_BEGIN
+  need(m, "model");
+  need(out, "out");
+  auto v = hp::init_parameters(*m, seed);
+  std::memcpy(out, v.data(), v.size() * 8);
+  HP_API_END
+}
+
+hp_status hp_bucket_plan(const hp_model_desc* m, double bucket_mb, uint64_t* lo, uint64_t* hi,
+                         uint64_t* nbuckets) {
+  HP_API_BEGIN
+  need(m, "model");
+  auto b = hp::bucket_plan(hp::param_table(*m), bucket_mb);
+  for (size_t i = 0; i < b.size(); ++i) {
+    lo[i] = b[i].lo;
+    hi[i] = b[i].hi;
+  }
+  *nbuckets = b.size();
+  HP_API_END
+}
+
+hp_status hp_comm_unique_id(uint8_t id[128]) {
+  HP_API_BEGIN
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId u;
+  HP_NCCL(ncclGetUniqueId(&u));
+  std::memcpy(id, &u, 128);
+  HP_API_END
+}
+
+hp_status hp_comm_create(int world, int rank, int device, const uint8_t id[128], hp_comm** out) {
+  HP_API_BEGIN
+  need(out, "out");
+  if (world < 1 || rank < 0 || rank >= world)
+    fail(HP_ECOMM, "rank " + std::to_string(rank) + " out of range for world_size " +
+                       std::to_string(world));
+  HP_CUDA(cudaSetDevice(device));
+  auto* c = new hp_comm;
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclResult_t r = ncclCommInitRank(&c->nccl, world, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    fail(HP_ECOMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  *out = c;
+  HP_API_END
+}
+
+hp_status hp_comm_destroy(hp_comm* c) {
+  HP_API_BEGIN
+  if (c) {
+    if (c->nccl) ncclCommDestroy(c->nccl);
+    delete c;
+  }
+  HP_API_END
+}
+
+hp_status hp_engine_create(const hp_model_desc* m, const hp_optim_desc* o, const hp_exec_desc* x,
+                           hp_comm* comm, hp_engine** out) {
+  HP_API_BEGIN
+  need(m, "model");
+  need(o, "optim");
+  need(x, "exec");
+  need(out, "out");
+  auto* h = new hp_engine;
+  try {
+    h->e = new hp::Engine(*m, *o, *x, comm);
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  *out = h;
+  HP_API_END
+}
+
+hp_status hp_engine_destroy(hp_engine* e) {
+  HP_API_BEGIN
+  if (e) {
+    delete e->e;
+    delete e;
+  }
+  HP_API_END
+}
+
+#define ENG(e)           \
+  need(e, "engine");     \
+  hp::Engine& E = *(e)->e
+
+hp_status hp_engine_set_params(hp_engine* e, const void* flat, uint64_t n, int dtype) {
+  HP_API_BEGIN
+  ENG(e);
+  need(flat, "flat");
+  E.set_params(flat, n, dtype);
+  HP_API_END
+}
+hp_status hp_engine_get_params(hp_engine* e, void* flat, uint64_t n, int dtype) {
+  HP_API_BEGIN
+  ENG(e);
+  need(flat, "flat");
+  E.get_params(flat, n, dtype);
+  HP_API_END
+}
+hp_status hp_engine_broadcast_params(hp_engine* e, int root) {
+  HP_API_BEGIN
+  ENG(e);
+  E.broadcast_params(root);
+  HP_API_END
+}
+hp_status hp_engine_get_adam(hp_engine* e, float* m, float* v, uint64_t* t) {
+  HP_API_BEGIN
+  ENG(e);
+  E.get_adam(m, v, t);
+  HP_API_END
+}
+hp_status hp_engine_set_adam(hp_engine* e, const float* m, const float* v, uint64_t t) {
+  HP_API_BEGIN
+  ENG(e);
+  E.set_adam(m, v, t);
+  HP_API_END
+}
+hp_status hp_engine_set_capture(hp_engine* e, int on) {
+  HP_API_BEGIN
+  ENG(e);
+  E.set_capture(on != 0);
+  HP_API_END
+}
+hp_status hp_engine_get_local_grads(hp_engine* e, float* flat, uint64_t n) {
+  HP_API_BEGIN
+  ENG(e);
+  E.get_local_grads(flat, n);
+  HP_API_END
+}
+hp_status hp_engine_stage_batch(hp_engine* e, const hp_batch* b) {
+  HP_API_BEGIN
+  ENG(e);
+  need(b, "batch");
+  E.stage_batch(*b);
+  HP_API_END
+}
+hp_status hp_engine_round_async(hp_engine* e, int dummy, double lr) {
+  HP_API_BEGIN
+  ENG(e);
+  E.round_async(dummy, lr);
+  HP_API_END
+}
+hp_status hp_engine_round_sync(hp_engine* e, hp_round_out* out) {
+  HP_API_BEGIN
+  ENG(e);
+  E.round_sync(out);
+  HP_API_END
+}
+hp_status hp_engine_round(hp_engine* e, int dummy, double lr, hp_round_out* out) {
+  HP_API_BEGIN
+  ENG(e);
+  E.round_async(dummy, lr);
+  E.round_sync(out);
+  HP_API_END
+}
+hp_status hp_engine_params_digest(hp_engine* e, uint64_t* digest) {
+  HP_API_BEGIN
+  ENG(e);
+  *digest = E.digest();
+  HP_API_END
+}
+hp_status hp_engine_kernel_launches(hp_engine* e, uint64_t* n) {
+  HP_API_BEGIN
+  (void)e;
+  *n = hp::kernel_launch_count();
+  HP_API_END
+}
+hp_status hp_engine_timers(hp_engine* e, int enable) {
+  HP_API_BEGIN
+  ENG(e);
+  E.timers(enable != 0);
+  HP_API_END
+}
+hp_status hp_engine_timer_read(hp_engine* e, int which, char* name, uint64_t cap, double* ms,
+                               uint64_t* launches, double* bytes, double* flops) {
+  HP_API_BEGIN
+  ENG(e);
+  std::string nm;
+  E.timer_read(which, &nm, ms, launches, bytes, flops);
+  if (name && cap) {
+    std::strncpy(name, nm.c_str(), cap - 1);
+    name[cap - 1] = 0;
+  }
+  HP_API_END
+}
+hp_status hp_engine_step_count(hp_engine* e, uint64_t* step) {
+  HP_API_BEGIN
+  ENG(e);
+  *step = E.step();
+  HP_API_END
+}
+
+hp_status hp_engine_mark(hp_engine* e, int slot) {
+  HP_API_BEGIN
+  ENG(e);
+  E.mark(slot);
+  HP_API_END
+}
+hp_status hp_engine_elapsed(hp_engine* e, int a, int b, double* ms) {
+  HP_API_BEGIN
+  ENG(e);
+  need(ms, "ms");
+  *ms = E.elapsed(a, b);
+  HP_API_END
+}
+hp_status hp_engine_synchronize(hp_engine* e) {
+  HP_API_BEGIN
+  ENG(e);
+  E.synchronize();
+  HP_API_END
+}
+
+hp_status hp_engine_io_bytes(hp_engine* e, uint64_t* h2d, uint64_t* d2h) {
+  HP_API_BEGIN
+  ENG(e);
+  if (h2d) *h2d = E.stage_bytes();
+  if (d2h) *d2h = E.readback_bytes();
+  HP_API_END
+}
+
+hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t lda, int a_trans,
+                        const void* B, int64_t ldb, int b_trans, int64_t b_group, int64_t b_gstride,
+                        void* C, int64_t ldc, int c_bf16, int64_t c_group, int64_t c_gstride,
+                        const float* bias, int act, void* aux, const void* resid, int64_t ld_resid,
+                        int accumulate, int path, int bn) {
+  HP_API_BEGIN
+  hp::GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.ab = ab_bf16 ? hp::DType::bf16 : hp::DType::f32;
+  g.a = hp::Operand{A, lda, a_trans, 0, 0};
+  g.b = hp::Operand{B, ldb, b_trans, b_group, b_gstride};
+  g.c = C; g.ldc = ldc; g.c_group = c_group; g.c_gstride = c_gstride;
+  g.ct = c_bf16 ? hp::DType::bf16 : hp::DType::f32;
+  g.bias = bias; g.act = act; g.aux = aux; g.resid = resid; g.ld_resid = ld_resid;
+  g.accumulate = accumulate;
+  if (path == 1) {
+    hp::gemm_simt(g, 0);
+  } else if (path == 2) {
+    hp::gemm_tc_set_bn(bn);
+    hp::gemm_tc(g, 0);
+    hp::gemm_tc_set_bn(0);
+  } else {
+    hp::gemm(g, 0);
+  }
+  HP_API_END
+}
+
+hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n, float lr,
+                        float b1, float b2, float eps, float c1, float c2, int sgd) {
+  HP_API_BEGIN
+  int* bad = nullptr;
+  HP_CUDA(cudaMalloc(&bad, 4));
+  HP_CUDA(cudaMemset(bad, 0, 4));
+  hp::AdamArgs a{};
+  a.p = p; a.m = m; a.v = v; a.g = g; a.n = n;
+  a.lr = lr; a.b1 = b1; a.b2 = b2; a.eps = eps; a.c1 = c1; a.c2 = c2;
+  a.bad = bad; a.sgd = sgd;
+  hp::adam_update(a, 0);
+  HP_CUDA(cudaDeviceSynchronize());
+  HP_CUDA(cudaFree(bad));
+  HP_API_END
+}
+
+hp_status hp_debug_sync(void) {
+  HP_API_BEGIN
+  HP_CUDA(cudaDeviceSynchronize());
+  HP_API_END
+}
+
+}  // extern "C"

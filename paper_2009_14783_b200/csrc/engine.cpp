@@ -1,0 +1,820 @@
+// DeviceStepEngine: one rank's share of the data-parallel step on a B200.
+//
+// Reference protocol (include/hetpar/engine.hpp:125-165), per round:
+//   forward -> allreduce [loss_sum, weight] BEFORE backward (engine.hpp:133)
+//   -> backward -> allreduce of the flat gradient (engine.hpp:145)
+//   -> divide by the total weight (engine.hpp:151) -> identical update.
+// B200 mapping:
+//   * forward/backward are sm_100a kernels on the main stream; activations and
+//     the canonical flat parameter / gradient buffers live in HBM;
+//   * the 16-byte [loss, weight] allreduce runs on the comm stream as soon as
+//     the loss kernel retires -- it does not block backward (gradients are
+//     unnormalized sums);
+//   * gradient buckets (contiguous ranges of the canonical flat order, walked
+//     from the end) are allreduced on the comm stream as soon as
+//     backward finishes their parameters, with 1/sum(weight) folded into the
+//     NCCL reduction (ncclRedOpCreatePreMulSum with a device scalar);
+//   * Adam (bit-exact f32 kern::adam_update) updates the fp32 master copy and
+//     refreshes the bf16 working copy the tcgen05 GEMMs read.
+#include "engine.h"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "hp_common.h"
+
+namespace hp {
+
+namespace {
+uint64_t pad8(uint64_t v) { return (v + 7) & ~uint64_t(7); }
+constexpr int kAttnMaxSeq = 128;
+}  // namespace
+
+void* Engine::dalloc(size_t bytes) {
+  void* p = nullptr;
+  HP_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+  allocs_.push_back(p);
+  return p;
+}
+
+int Engine::pidx(const std::string& name) const {
+  for (size_t i = 0; i < table_.size(); ++i)
+    if (table_[i].name == name) return static_cast<int>(i);
+  fail(HP_EINDEX, "no parameter named " + name);
+}
+
+const void* Engine::w(int idx) const {
+  if (bf16_) return static_cast<const __nv_bfloat16*>(shadow_) + shadow_off_[idx];
+  return params_ + table_[idx].offset;
+}
+int64_t Engine::wld(int idx) const {
+  return bf16_ ? static_cast<int64_t>(shadow_ld_[idx]) : static_cast<int64_t>(table_[idx].cols);
+}
+
+Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_desc& x,
+               hp_comm* comm)
+    : m_(m), o_(o), x_(x), comm_(comm) {
+  table_ = param_table(m_);
+  if (x_.update_freq != 1)
+    fail(HP_ECONFIG, "update_freq > 1 is not implemented on the device engine yet");
+  if (x_.max_tokens == 0 || x_.max_batch == 0)
+    fail(HP_ECONFIG, "exec capacities max_tokens/max_batch must be > 0");
+  if (m_.max_seq > static_cast<uint64_t>(kAttnMaxSeq))
+    fail(HP_ECONFIG, "max_seq > 128 is not supported by the attention kernel yet");
+  if (o_.kind != HP_OPT_ADAM && o_.kind != HP_OPT_SGD) fail(HP_ECONFIG, "unknown optimizer kind");
+  if (x_.policy != HP_POLICY_SENTENCES && x_.policy != HP_POLICY_TOKENS)
+    fail(HP_ECONFIG, "unknown weight policy");
+  if (comm_ && comm_->device != x_.device)
+    fail(HP_ECONFIG, "communicator device differs from the engine device");
+  HP_CUDA(cudaSetDevice(x_.device));
+
+  bf16_ = x_.compute == HP_COMPUTE_BF16;
+  at_ = bf16_ ? DType::bf16 : DType::f32;
+  asz_ = bf16_ ? 2 : 4;
+  bert_ = m_.arch == HP_ARCH_BERT_ENCODER;
+  d_ = static_cast<int>(m_.d_model);
+  H_ = static_cast<int>(m_.heads);
+  dk_ = d_ / H_;
+  V_ = static_cast<int>(m_.vocab);
+  Vp_ = static_cast<int>(pad8(m_.vocab));
+  L_ = bert_ ? static_cast<int>(m_.layers) : 1;
+  F_ = bert_ ? static_cast<int>(m_.d_ff) : 0;
+  n_ = table_.back().offset + table_.back().size();
+  buckets_ = bucket_plan(table_, x_.bucket_mb > 0 ? x_.bucket_mb : 25.0);
+
+  // bf16 working-copy layout: every parameter 16-byte aligned, rows padded to
+  // a multiple of 8 elements (TMA strides must be 16-byte multiples).
+  shadow_off_.resize(table_.size());
+  shadow_ld_.resize(table_.size());
+  std::vector<uint64_t> seg;
+  for (size_t i = 0; i < table_.size(); ++i) {
+    shadow_off_[i] = pad8(n_shadow_);
+    shadow_ld_[i] = pad8(table_[i].cols);
+    n_shadow_ = shadow_off_[i] + table_[i].rows * shadow_ld_[i];
+    seg.insert(seg.end(), {table_[i].offset, table_[i].cols, shadow_off_[i], shadow_ld_[i]});
+  }
+  nseg_ = static_cast<int>(table_.size());
+
+  HP_CUDA(cudaStreamCreateWithFlags(&s_main_, cudaStreamNonBlocking));
+  HP_CUDA(cudaStreamCreateWithFlags(&s_comm_, cudaStreamNonBlocking));
+  HP_CUDA(cudaEventCreateWithFlags(&ev_fwd_, cudaEventDisableTiming));
+  HP_CUDA(cudaEventCreateWithFlags(&ev_comm_done_, cudaEventDisableTiming));
+  HP_CUDA(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming));
+  ev_bucket_.resize(buckets_.size());
+  for (auto& e : ev_bucket_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+  params_ = static_cast<float*>(dalloc(n_ * 4));
+  grads_ = static_cast<float*>(dalloc(n_ * 4));
+  adam_m_ = static_cast<float*>(dalloc(n_ * 4));
+  adam_v_ = static_cast<float*>(dalloc(n_ * 4));
+  HP_CUDA(cudaMemset(params_, 0, n_ * 4));
+  HP_CUDA(cudaMemset(grads_, 0, n_ * 4));
+  HP_CUDA(cudaMemset(adam_m_, 0, n_ * 4));
+  HP_CUDA(cudaMemset(adam_v_, 0, n_ * 4));
+  if (bf16_) {
+    shadow_ = dalloc(n_shadow_ * 2);
+    HP_CUDA(cudaMemset(shadow_, 0, n_shadow_ * 2));
+  }
+  seg_table_ = static_cast<uint64_t*>(dalloc(seg.size() * 8));
+  HP_CUDA(cudaMemcpy(seg_table_, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice));
+
+  // sinusoidal positions computed in double then cast (attention.hpp:53-67)
+  {
+    std::vector<float> pe(m_.max_seq * d_);
+    for (uint64_t p = 0; p < m_.max_seq; ++p)
+      for (int i = 0; 2 * i < d_; ++i) {
+        const double ang = static_cast<double>(p) /
+                           std::pow(10000.0, (2.0 * i) / static_cast<double>(d_));
+        pe[p * d_ + 2 * i] = static_cast<float>(std::sin(ang));
+        pe[p * d_ + 2 * i + 1] = static_cast<float>(std::cos(ang));
+      }
+    pe_ = static_cast<float*>(dalloc(pe.size() * 4));
+    HP_CUDA(cudaMemcpy(pe_, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice));
+  }
+
+  // staged batch block (fixed layout at capacity)
+  const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch, Mm = std::max<uint64_t>(x_.max_masks, 1);
+  const size_t ints = 3 * Tm + (Bm + 1) + 2 * Mm + Bm;
+  stage_bytes_ = ((ints * 4 + 7) & ~size_t(7)) + 8;
+  for (int i = 0; i < kStageBufs; ++i) {
+    HP_CUDA(cudaMallocHost(&h_stage_[i], stage_bytes_));
+    std::memset(h_stage_[i], 0, stage_bytes_);
+    HP_CUDA(cudaEventCreateWithFlags(&ev_stage_[i], cudaEventDisableTiming));
+  }
+  d_stage_ = dalloc(stage_bytes_);
+  {
+    int* base = static_cast<int*>(d_stage_);
+    batch_.tok = base;
+    batch_.seg = base + Tm;
+    batch_.pos = base + 2 * Tm;
+    batch_.cu = base + 3 * Tm;
+    batch_.mrow = base + 3 * Tm + Bm + 1;
+    batch_.morig = batch_.mrow + Mm;
+    batch_.label = batch_.morig + Mm;
+    d_weight_ = reinterpret_cast<double*>(static_cast<char*>(d_stage_) + stage_bytes_ - 8);
+  }
+
+  // activations
+  const size_t T = Tm;
+  layers_.resize(L_);
+  for (int l = 0; l < L_; ++l) {
+    Layer& y = layers_[l];
+    y.x = dalloc(T * d_ * asz_);
+    y.qkv = dalloc(T * 3 * d_ * asz_);
+    y.o = dalloc(T * d_ * asz_);
+    y.lse = static_cast<float*>(dalloc(T * H_ * 4));
+    if (bert_) {
+      y.p1 = dalloc(T * d_ * asz_);
+      y.x1 = dalloc(T * d_ * asz_);
+      y.u = dalloc(T * F_ * asz_);
+      y.g = dalloc(T * F_ * asz_);
+      y.p2 = dalloc(T * d_ * asz_);
+      y.mean1 = static_cast<float*>(dalloc(T * 4));
+      y.rstd1 = static_cast<float*>(dalloc(T * 4));
+      y.mean2 = static_cast<float*>(dalloc(T * 4));
+      y.rstd2 = static_cast<float*>(dalloc(T * 4));
+    }
+  }
+  x_final_ = dalloc(T * d_ * asz_);
+  if (bert_) {
+    p0_ = dalloc(T * d_ * asz_);
+    mean0_ = static_cast<float*>(dalloc(T * 4));
+    rstd0_ = static_cast<float*>(dalloc(T * 4));
+  }
+  hm_ = dalloc(Mm * d_ * asz_);
+  dhm_ = dalloc(Mm * d_ * asz_);
+  z_ = static_cast<float*>(dalloc(Mm * Vp_ * 4));
+  dz_ = dalloc(Mm * Vp_ * asz_);
+  HP_CUDA(cudaMemset(dz_, 0, Mm * Vp_ * asz_));
+  row_loss_ = static_cast<float*>(dalloc((Mm + Bm) * 4));
+  const size_t wmax = std::max<size_t>(d_, F_);
+  dA_ = dalloc(T * d_ * asz_);
+  dB_ = dalloc(T * d_ * asz_);
+  dC_ = dalloc(T * wmax * asz_);
+  dU_ = bert_ ? dalloc(T * F_ * asz_) : nullptr;
+  dqkv_ = dalloc(T * 3 * d_ * asz_);
+  const size_t chunksT = (T + 63) / 64, chunksM = (Mm + 63) / 64;
+  const size_t scratch = std::max({chunksT * 2 * wmax + 2 * wmax, chunksM * (size_t)Vp_ + Vp_,
+                                   chunksT * 4 * (size_t)d_ + 4 * (size_t)d_});
+  scratch_ = static_cast<float*>(dalloc(scratch * 4));
+  d_lw_ = static_cast<double*>(dalloc(4 * 8));
+  inv_w_ = static_cast<float*>(dalloc(4));
+  inv_w64_ = static_cast<double*>(dalloc(8));
+  flags_ = static_cast<int*>(dalloc(2 * 4));
+  HP_CUDA(cudaMallocHost(&h_lw_, 4 * 8));
+  HP_CUDA(cudaMallocHost(&h_flags_, 2 * 4));
+  HP_CUDA(cudaMemset(flags_, 0, 8));
+
+  if (comm_) {
+    HP_NCCL(ncclRedOpCreatePreMulSum(&premul_, inv_w_, ncclFloat, ncclScalarDevice, comm_->nccl));
+    have_premul_ = true;
+  }
+  HP_CUDA(cudaDeviceSynchronize());
+}
+
+Engine::~Engine() {
+  if (s_main_) cudaStreamSynchronize(s_main_);
+  if (s_comm_) cudaStreamSynchronize(s_comm_);
+  if (have_premul_ && comm_) ncclRedOpDestroy(premul_, comm_->nccl);
+  for (auto& t : tm_)
+    for (auto& pr : t.ev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  for (void* p : allocs_) cudaFree(p);
+  for (int i = 0; i < kStageBufs; ++i) {
+    if (h_stage_[i]) cudaFreeHost(h_stage_[i]);
+    if (ev_stage_[i]) cudaEventDestroy(ev_stage_[i]);
+  }
+  if (h_lw_) cudaFreeHost(h_lw_);
+  if (h_flags_) cudaFreeHost(h_flags_);
+  if (h_params_) cudaFreeHost(h_params_);
+  for (auto& e : ev_bucket_) cudaEventDestroy(e);
+  for (auto& e : marks_)
+    if (e) cudaEventDestroy(e);
+  if (ev_fwd_) cudaEventDestroy(ev_fwd_);
+  if (ev_comm_done_) cudaEventDestroy(ev_comm_done_);
+  if (ev_done_) cudaEventDestroy(ev_done_);
+  if (s_main_) cudaStreamDestroy(s_main_);
+  if (s_comm_) cudaStreamDestroy(s_comm_);
+}
+
+// ------------------------------------------------------------------ state I/O
+void Engine::set_params(const void* flat, uint64_t n, int dtype) {
+  if (n != n_)
+    fail(HP_EIO, "state dict payload has " + std::to_string(n) + " values, expected " +
+                     std::to_string(n_));
+  std::vector<float> tmp(n_);
+  if (dtype == 1) {
+    const double* s = static_cast<const double*>(flat);
+    for (uint64_t i = 0; i < n_; ++i) tmp[i] = static_cast<float>(s[i]);
+  } else {
+    std::memcpy(tmp.data(), flat, n_ * 4);
+  }
+  HP_CUDA(cudaMemcpyAsync(params_, tmp.data(), n_ * 4, cudaMemcpyHostToDevice, s_main_));
+  if (bf16_) refresh_shadow(params_, shadow_, seg_table_, nseg_, n_, s_main_);
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+}
+
+void Engine::get_params(void* flat, uint64_t n, int dtype) {
+  if (n != n_) fail(HP_ESHAPE, "get_params: wrong element count");
+  std::vector<float> tmp(n_);
+  HP_CUDA(cudaMemcpyAsync(tmp.data(), params_, n_ * 4, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  if (dtype == 1) {
+    double* d = static_cast<double*>(flat);
+    for (uint64_t i = 0; i < n_; ++i) d[i] = tmp[i];
+  } else {
+    std::memcpy(flat, tmp.data(), n_ * 4);
+  }
+}
+
+void Engine::broadcast_params(int root) {
+  if (comm_) {
+    HP_NCCL(ncclBroadcast(params_, params_, n_, ncclFloat, root, comm_->nccl, s_main_));
+    if (bf16_) refresh_shadow(params_, shadow_, seg_table_, nseg_, n_, s_main_);
+  }
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+}
+
+void Engine::get_adam(float* m, float* v, uint64_t* t) {
+  HP_CUDA(cudaMemcpyAsync(m, adam_m_, n_ * 4, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaMemcpyAsync(v, adam_v_, n_ * 4, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  *t = adam_t_;
+}
+
+void Engine::set_adam(const float* m, const float* v, uint64_t t) {
+  HP_CUDA(cudaMemcpyAsync(adam_m_, m, n_ * 4, cudaMemcpyHostToDevice, s_main_));
+  HP_CUDA(cudaMemcpyAsync(adam_v_, v, n_ * 4, cudaMemcpyHostToDevice, s_main_));
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  adam_t_ = t;
+}
+
+void Engine::get_local_grads(float* flat, uint64_t n) {
+  if (!local_grads_) fail(HP_ECONFIG, "gradient capture was not enabled");
+  if (n != n_) fail(HP_ESHAPE, "get_local_grads: wrong element count");
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  HP_CUDA(cudaMemcpy(flat, local_grads_, n_ * 4, cudaMemcpyDeviceToHost));
+}
+
+uint64_t Engine::digest() {
+  // params_digest (model.hpp:211-217): FNV-1a over the parameter bytes in
+  // canonical order.  Host-side: it is byte-serial and runs at cadence only.
+  if (!h_params_) HP_CUDA(cudaMallocHost(&h_params_, n_ * 4));
+  HP_CUDA(cudaMemcpyAsync(h_params_, params_, n_ * 4, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(h_params_);
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (uint64_t i = 0; i < n_ * 4; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+// ------------------------------------------------------------------ staging
+void Engine::stage_batch(const hp_batch& b) {
+  if (b.n_inst == 0)
+    fail(HP_ECONFIG, "model_forward: empty batch (only the dummy path may skip data)");
+  const uint64_t B = b.n_inst;
+  const uint64_t T = b.tok_off[B];
+  const uint64_t M = b.mask_off[B];
+  if (B > x_.max_batch || T > x_.max_tokens || M > std::max<uint64_t>(x_.max_masks, 1))
+    fail(HP_ECONFIG, "batch exceeds the engine capacity (tokens " + std::to_string(T) +
+                         ", instances " + std::to_string(B) + ", masks " + std::to_string(M) + ")");
+  const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch, Mm = std::max<uint64_t>(x_.max_masks, 1);
+  // wait until the previous copy out of this pinned buffer finished
+  HP_CUDA(cudaEventSynchronize(ev_stage_[stage_idx_]));
+  int* h = static_cast<int*>(h_stage_[stage_idx_]);
+  int *tok = h, *seg = h + Tm, *pos = h + 2 * Tm, *cu = h + 3 * Tm, *mrow = cu + Bm + 1,
+      *morig = mrow + Mm, *label = morig + Mm;
+  double weight = 0.0;
+  for (uint64_t i = 0; i < B; ++i) {
+    const uint64_t t0 = b.tok_off[i], t1 = b.tok_off[i + 1];
+    const uint64_t n = t1 - t0;
+    // validation in model_forward order (model.hpp:347-390)
+    if (n == 0) fail(HP_ESHAPE, "masked model: empty token sequence");
+    if (n > m_.max_seq) fail(HP_ESHAPE, "masked model: sequence length exceeds max_seq");
+    cu[i] = static_cast<int>(t0);
+    for (uint64_t t = t0; t < t1; ++t) {
+      const int64_t s = b.segments[t];
+      if (s != 0 && s != 1) fail(HP_EINDEX, "segment id must be 0 or 1");
+      const int64_t id = b.tokens[t];
+      if (id < 0 || static_cast<uint64_t>(id) >= m_.vocab)
+        fail(HP_EINDEX, "gather_rows: row " + std::to_string(id) + " outside [0," +
+                            std::to_string(m_.vocab) + ")");
+      tok[t] = static_cast<int>(id);
+      seg[t] = static_cast<int>(s);
+      pos[t] = static_cast<int>(t - t0);
+    }
+    double inst_w = 0.0;
+    for (uint64_t k = b.mask_off[i]; k < b.mask_off[i + 1]; ++k) {
+      const int64_t p = b.mask_pos[k];
+      if (p < 0 || static_cast<uint64_t>(p) >= n) fail(HP_EINDEX, "mask position outside sequence");
+      const int64_t o = b.mask_orig[k];
+      if (o < 0 || static_cast<uint64_t>(o) >= m_.vocab)
+        fail(HP_EINDEX, "ls_ce: target " + std::to_string(o) + " outside [0," +
+                            std::to_string(m_.vocab) + ")");
+      mrow[k] = static_cast<int>(t0 + p);
+      morig[k] = static_cast<int>(o);
+      inst_w += 1.0;
+    }
+    if (m_.with_nsp) {
+      if (b.label[i] < 0 || b.label[i] > 1)
+        fail(HP_EINDEX, "ls_ce: target " + std::to_string(b.label[i]) + " outside [0,2)");
+      label[i] = static_cast<int>(b.label[i]);
+      inst_w += 1.0;
+    } else {
+      label[i] = 0;
+    }
+    weight += x_.policy == HP_POLICY_SENTENCES ? 1.0 : inst_w;
+  }
+  cu[B] = static_cast<int>(T);
+  *reinterpret_cast<double*>(static_cast<char*>(h_stage_[stage_idx_]) + stage_bytes_ - 8) = weight;
+  HP_CUDA(cudaMemcpyAsync(d_stage_, h_stage_[stage_idx_], stage_bytes_, cudaMemcpyHostToDevice,
+                          s_main_));
+  HP_CUDA(cudaEventRecord(ev_stage_[stage_idx_], s_main_));
+  stage_idx_ = (stage_idx_ + 1) % kStageBufs;
+  batch_.T = static_cast<int>(T);
+  batch_.B = static_cast<int>(B);
+  batch_.M = static_cast<int>(M);
+  local_weight_ = weight;
+  staged_ = true;
+}
+
+// ------------------------------------------------------------------ timers
+void Engine::timers(bool on) {
+  timers_on_ = on;
+  for (auto& t : tm_) {
+    t.used = 0;
+    t.ms = 0;
+    t.flops = t.bytes = 0;
+    t.launches = 0;
+  }
+}
+void Engine::mark(int slot) {
+  if (slot < 0 || slot >= 8) fail(HP_EINDEX, "mark slot out of range");
+  if (!marks_[slot]) HP_CUDA(cudaEventCreate(&marks_[slot]));
+  HP_CUDA(cudaEventRecord(marks_[slot], s_main_));
+}
+double Engine::elapsed(int a, int b) {
+  if (a < 0 || a >= 8 || b < 0 || b >= 8 || !marks_[a] || !marks_[b])
+    fail(HP_EINDEX, "elapsed: unrecorded mark");
+  HP_CUDA(cudaEventSynchronize(marks_[b]));
+  float ms = 0;
+  HP_CUDA(cudaEventElapsedTime(&ms, marks_[a], marks_[b]));
+  return ms;
+}
+void Engine::synchronize() {
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  HP_CUDA(cudaStreamSynchronize(s_comm_));
+}
+
+void Engine::tstart(int cls) {
+  if (!timers_on_) return;
+  TimerAcc& t = tm_[cls];
+  if (t.used == t.ev.size()) {
+    cudaEvent_t a, b;
+    HP_CUDA(cudaEventCreate(&a));
+    HP_CUDA(cudaEventCreate(&b));
+    t.ev.emplace_back(a, b);
+  }
+  HP_CUDA(cudaEventRecord(t.ev[t.used].first, s_main_));
+}
+void Engine::tstop(int cls, double flops, double bytes) {
+  if (!timers_on_) return;
+  TimerAcc& t = tm_[cls];
+  HP_CUDA(cudaEventRecord(t.ev[t.used].second, s_main_));
+  ++t.used;
+  t.flops += flops;
+  t.bytes += bytes;
+  ++t.launches;
+}
+void Engine::timer_read(int which, std::string* name, double* ms, uint64_t* launches,
+                        double* bytes, double* flops) {
+  static const char* names[TM_COUNT] = {"gemm", "attention", "layernorm", "heads", "adam", "embedding"};
+  if (which < 0 || which >= TM_COUNT) fail(HP_EINDEX, "timer index out of range");
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  TimerAcc& t = tm_[which];
+  for (size_t i = 0; i < t.used; ++i) {
+    float e = 0;
+    HP_CUDA(cudaEventElapsedTime(&e, t.ev[i].first, t.ev[i].second));
+    t.ms += e;
+  }
+  t.used = 0;
+  *name = names[which];
+  *ms = t.ms;
+  *launches = t.launches;
+  *bytes = t.bytes;
+  *flops = t.flops;
+}
+
+void Engine::gemm_t(const GemmArgs& g) {
+  tstart(TM_GEMM);
+  gemm(g, s_main_);
+  tstop(TM_GEMM, 2.0 * g.M * g.N * g.K,
+        (double)asz_ * ((double)g.M * g.K + (double)g.K * g.N) +
+            (g.ct == DType::f32 ? 4.0 : 2.0) * g.M * g.N);
+}
+
+// ------------------------------------------------------------------ forward
+void Engine::forward(bool need_grad) {
+  const DevBatch& b = batch_;
+  const int T = b.T;
+  const DType wt = bf16_ ? DType::bf16 : DType::f32;
+  const int iE = 0, iS0 = 1, iS1 = 2;
+  // embedding (model.hpp:354-365)
+  tstart(TM_EMBED);
+  embed_fwd(b, d_, w(iE), w(iS0), w(iS1), wt, pe_, bert_ ? p0_ : layers_[0].x, at_, s_main_);
+  if (bert_) {
+    const int g = pidx("emb_ln.g");
+    layernorm_fwd(T, d_, p0_, at_, pp(g), pp(g + 1), layers_[0].x, at_, mean0_, rstd0_, s_main_);
+  }
+  tstop(TM_EMBED, 0, (double)T * d_ * asz_ * (bert_ ? 4 : 2));
+
+  int cursor = bert_ ? 5 : 3;  // index of the first wq of layer 0
+  for (int l = 0; l < L_; ++l) {
+    Layer& y = layers_[l];
+    const int iq = cursor;
+    const int iwo = iq + 3 * H_;
+    // QKV projections for every head in one GEMM: B is the 3h grouped
+    // [d x dk] blocks of the canonical layout (attention.hpp:44-46)
+    GemmArgs q;
+    q.M = T; q.N = 3 * d_; q.K = d_; q.ab = at_;
+    q.a = Operand{y.x, d_, 0, 0, 0};
+    q.b = Operand{w(iq), wld(iq), 0, dk_, (int64_t)(bf16_ ? shadow_off_[iq + 1] - shadow_off_[iq]
+                                                           : table_[iq + 1].offset - table_[iq].offset)};
+    q.c = y.qkv; q.ldc = 3 * d_; q.ct = at_;
+    gemm_t(q);
+    tstart(TM_ATTN);
+    attention_fwd(b, H_, dk_, y.qkv, y.o, y.lse, at_, s_main_);
+    tstop(TM_ATTN, 4.0 * H_ * dk_ * (double)T * (double)m_.max_seq, 0);
+    void* out = (l + 1 < L_) ? layers_[l + 1].x : x_final_;
+    if (!bert_) {
+      GemmArgs o;
+      o.M = T; o.N = d_; o.K = d_; o.ab = at_;
+      o.a = Operand{y.o, d_, 0, 0, 0};
+      o.b = Operand{w(iwo), wld(iwo), 0, 0, 0};
+      o.c = out; o.ldc = d_; o.ct = at_;
+      gemm_t(o);
+      cursor = iwo + 1;
+    } else {
+      const int ibo = iwo + 1, ig1 = iwo + 2, iw1 = iwo + 4, ib1 = iwo + 5, iw2 = iwo + 6,
+                ib2 = iwo + 7, ig2 = iwo + 8;
+      GemmArgs o;  // P1 = O Wo + bo + X
+      o.M = T; o.N = d_; o.K = d_; o.ab = at_;
+      o.a = Operand{y.o, d_, 0, 0, 0};
+      o.b = Operand{w(iwo), wld(iwo), 0, 0, 0};
+      o.c = y.p1; o.ldc = d_; o.ct = at_;
+      o.bias = pp(ibo); o.resid = y.x; o.ld_resid = d_;
+      gemm_t(o);
+      tstart(TM_NORM);
+      layernorm_fwd(T, d_, y.p1, at_, pp(ig1), pp(ig1 + 1), y.x1, at_, y.mean1, y.rstd1, s_main_);
+      tstop(TM_NORM, 0, (double)T * d_ * asz_ * 2);
+      GemmArgs f1;  // G = gelu(X1 W1 + b1), U saved
+      f1.M = T; f1.N = F_; f1.K = d_; f1.ab = at_;
+      f1.a = Operand{y.x1, d_, 0, 0, 0};
+      f1.b = Operand{w(iw1), wld(iw1), 0, 0, 0};
+      f1.c = y.g; f1.ldc = F_; f1.ct = at_;
+      f1.bias = pp(ib1); f1.act = ACT_GELU; f1.aux = y.u;
+      gemm_t(f1);
+      GemmArgs f2;  // P2 = G W2 + b2 + X1
+      f2.M = T; f2.N = d_; f2.K = F_; f2.ab = at_;
+      f2.a = Operand{y.g, F_, 0, 0, 0};
+      f2.b = Operand{w(iw2), wld(iw2), 0, 0, 0};
+      f2.c = y.p2; f2.ldc = d_; f2.ct = at_;
+      f2.bias = pp(ib2); f2.resid = y.x1; f2.ld_resid = d_;
+      gemm_t(f2);
+      tstart(TM_NORM);
+      layernorm_fwd(T, d_, y.p2, at_, pp(ig2), pp(ig2 + 1), out, at_, y.mean2, y.rstd2, s_main_);
+      tstop(TM_NORM, 0, (double)T * d_ * asz_ * 2);
+      cursor = ig2 + 2;
+    }
+  }
+
+  // heads (model.hpp:367-391)
+  const int iw = pidx("mlm.w"), ib = iw + 1;
+  tstart(TM_HEAD);
+  gather_rows(b.M, d_, b.mrow, x_final_, hm_, at_, s_main_);
+  tstop(TM_HEAD, 0, 0);
+  GemmArgs z;
+  z.M = b.M; z.N = V_; z.K = d_; z.ab = at_;
+  z.a = Operand{hm_, d_, 0, 0, 0};
+  z.b = Operand{w(iw), wld(iw), 0, 0, 0};
+  z.c = z_; z.ldc = Vp_; z.ct = DType::f32; z.bias = pp(ib);
+  if (b.M > 0) gemm_t(z);
+  tstart(TM_HEAD);
+  ls_ce(b.M, V_, z_, Vp_, b.morig, static_cast<float>(m_.label_smooth_eps), row_loss_, dz_, at_,
+        Vp_, s_main_);
+  if (need_grad) HP_CUDA(cudaMemsetAsync(dA_, 0, (size_t)T * d_ * asz_, s_main_));
+  if (m_.with_nsp) {
+    const int in = iw + 2;
+    nsp_head(b, d_, x_final_, at_, pp(in), pp(in + 1), row_loss_ + b.M, gp(in), gp(in + 1), dA_,
+             need_grad ? 1 : 0, s_main_);
+  }
+  tstop(TM_HEAD, 0, (double)b.M * V_ * 8);
+}
+
+// ------------------------------------------------------------------ backward
+void Engine::grads_ready(int first_done) {
+  if (capture_) return;  // deferred: the pre-reduce gradients are copied first
+  while (next_bucket_ < buckets_.size() &&
+         static_cast<int>(buckets_[next_bucket_].first_param) >= first_done)
+    issue_bucket(next_bucket_++);
+}
+
+void Engine::issue_bucket(size_t k) {
+  if (!comm_) return;
+  const Bucket& bk = buckets_[k];
+  HP_CUDA(cudaEventRecord(ev_bucket_[k], s_main_));
+  HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_bucket_[k], 0));
+  HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, premul_,
+                        comm_->nccl, s_comm_));
+}
+
+void Engine::backward() {
+  const DevBatch& b = batch_;
+  const int T = b.T;
+  const int iw = pidx("mlm.w");
+  // MLM head: d(mlm.w) = Hm^T dZ, d(mlm.b) = colsum dZ, dHm = dZ W^T
+  if (b.M > 0) {
+    GemmArgs gw;
+    gw.M = d_; gw.N = V_; gw.K = b.M; gw.ab = at_;
+    gw.a = Operand{hm_, d_, 1, 0, 0};
+    gw.b = Operand{dz_, Vp_, 0, 0, 0};
+    gw.c = gp(iw); gw.ldc = V_; gw.ct = DType::f32;
+    gemm_t(gw);
+    tstart(TM_HEAD);
+    col_sum(b.M, V_, dz_, Vp_, at_, gp(iw + 1), scratch_, s_main_);
+    tstop(TM_HEAD, 0, 0);
+    GemmArgs gd;
+    gd.M = b.M; gd.N = d_; gd.K = V_; gd.ab = at_;
+    gd.a = Operand{dz_, Vp_, 0, 0, 0};
+    gd.b = Operand{w(iw), wld(iw), 1, 0, 0};
+    gd.c = dhm_; gd.ldc = d_; gd.ct = at_;
+    gemm_t(gd);
+    scatter_rows(b.M, d_, b.mrow, dhm_, dA_, at_, s_main_);
+  } else {
+    HP_CUDA(cudaMemsetAsync(gp(iw), 0, sizeof(float) * (size_t)(d_ + 1) * V_, s_main_));
+  }
+  grads_ready(iw);
+
+  // dA_ holds d(final hidden)
+  int first_wq = bert_ ? 5 : 3;
+  const int per_layer = bert_ ? 3 * H_ + 10 : 0;
+  for (int l = L_ - 1; l >= 0; --l) {
+    Layer& y = layers_[l];
+    const int iq = first_wq + l * per_layer;
+    const int iwo = iq + 3 * H_;
+    void* dP1 = nullptr;  // gradient reaching the attention output projection
+    if (bert_) {
+      const int ibo = iwo + 1, ig1 = iwo + 2, iw1 = iwo + 4, ib1 = iwo + 5, iw2 = iwo + 6,
+                ib2 = iwo + 7, ig2 = iwo + 8;
+      tstart(TM_NORM);
+      layernorm_bwd(T, d_, dA_, at_, y.p2, at_, y.mean2, y.rstd2, pp(ig2), dB_, at_, gp(ig2),
+                    gp(ig2 + 1), scratch_, s_main_);
+      tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
+      GemmArgs w2;  // d(ffn.w2) = G^T dP2
+      w2.M = F_; w2.N = d_; w2.K = T; w2.ab = at_;
+      w2.a = Operand{y.g, F_, 1, 0, 0};
+      w2.b = Operand{dB_, d_, 0, 0, 0};
+      w2.c = gp(iw2); w2.ldc = d_; w2.ct = DType::f32;
+      gemm_t(w2);
+      tstart(TM_NORM);
+      col_sum(T, d_, dB_, d_, at_, gp(ib2), scratch_, s_main_);
+      tstop(TM_NORM, 0, 0);
+      GemmArgs du;  // dU = (dP2 W2^T) * gelu'(U)
+      du.M = T; du.N = F_; du.K = d_; du.ab = at_;
+      du.a = Operand{dB_, d_, 0, 0, 0};
+      du.b = Operand{w(iw2), wld(iw2), 1, 0, 0};
+      du.c = dU_; du.ldc = F_; du.ct = at_;
+      du.act = ACT_DGELU; du.aux = y.u;
+      gemm_t(du);
+      GemmArgs w1;  // d(ffn.w1) = X1^T dU
+      w1.M = d_; w1.N = F_; w1.K = T; w1.ab = at_;
+      w1.a = Operand{y.x1, d_, 1, 0, 0};
+      w1.b = Operand{dU_, F_, 0, 0, 0};
+      w1.c = gp(iw1); w1.ldc = F_; w1.ct = DType::f32;
+      gemm_t(w1);
+      tstart(TM_NORM);
+      col_sum(T, F_, dU_, F_, at_, gp(ib1), scratch_, s_main_);
+      tstop(TM_NORM, 0, 0);
+      GemmArgs dx1;  // dX1 = dU W1^T + dP2
+      dx1.M = T; dx1.N = d_; dx1.K = F_; dx1.ab = at_;
+      dx1.a = Operand{dU_, F_, 0, 0, 0};
+      dx1.b = Operand{w(iw1), wld(iw1), 1, 0, 0};
+      dx1.c = dC_; dx1.ldc = d_; dx1.ct = at_;
+      dx1.resid = dB_; dx1.ld_resid = d_;
+      gemm_t(dx1);
+      tstart(TM_NORM);
+      layernorm_bwd(T, d_, dC_, at_, y.p1, at_, y.mean1, y.rstd1, pp(ig1), dB_, at_, gp(ig1),
+                    gp(ig1 + 1), scratch_, s_main_);
+      col_sum(T, d_, dB_, d_, at_, gp(ibo), scratch_, s_main_);
+      tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
+      dP1 = dB_;
+    } else {
+      dP1 = dA_;
+    }
+    GemmArgs wo;  // d(wo) = O^T dP1
+    wo.M = d_; wo.N = d_; wo.K = T; wo.ab = at_;
+    wo.a = Operand{y.o, d_, 1, 0, 0};
+    wo.b = Operand{dP1, d_, 0, 0, 0};
+    wo.c = gp(iwo); wo.ldc = d_; wo.ct = DType::f32;
+    gemm_t(wo);
+    GemmArgs dO;  // dO = dP1 Wo^T
+    dO.M = T; dO.N = d_; dO.K = d_; dO.ab = at_;
+    dO.a = Operand{dP1, d_, 0, 0, 0};
+    dO.b = Operand{w(iwo), wld(iwo), 1, 0, 0};
+    dO.c = dC_; dO.ldc = d_; dO.ct = at_;
+    gemm_t(dO);
+    tstart(TM_ATTN);
+    attention_bwd(b, H_, dk_, y.qkv, y.o, dC_, y.lse, dqkv_, at_, s_main_);
+    tstop(TM_ATTN, 8.0 * H_ * dk_ * (double)T * (double)m_.max_seq, 0);
+    const int64_t gstride_w = bf16_ ? (int64_t)(shadow_off_[iq + 1] - shadow_off_[iq])
+                                    : (int64_t)(table_[iq + 1].offset - table_[iq].offset);
+    GemmArgs wq;  // d(wq.*, wk.*, wv.*) = X^T dQKV, scattered into the 3h blocks
+    wq.M = d_; wq.N = 3 * d_; wq.K = T; wq.ab = at_;
+    wq.a = Operand{y.x, d_, 1, 0, 0};
+    wq.b = Operand{dqkv_, 3 * d_, 0, 0, 0};
+    wq.c = gp(iq); wq.ldc = dk_; wq.c_group = dk_;
+    wq.c_gstride = (int64_t)(table_[iq + 1].offset - table_[iq].offset);
+    wq.ct = DType::f32;
+    gemm_t(wq);
+    GemmArgs dx;  // dX = dQKV Wqkv^T (+ dP1 through the residual)
+    dx.M = T; dx.N = d_; dx.K = 3 * d_; dx.ab = at_;
+    dx.a = Operand{dqkv_, 3 * d_, 0, 0, 0};
+    dx.b = Operand{w(iq), wld(iq), 1, dk_, gstride_w};
+    dx.c = bert_ ? dA_ : dB_; dx.ldc = d_; dx.ct = at_;
+    if (bert_) {
+      dx.resid = dP1;
+      dx.ld_resid = d_;
+    }
+    gemm_t(dx);
+    grads_ready(iq);
+  }
+
+  // embedding (+ its LayerNorm for the extension)
+  const void* dx0 = dB_;
+  if (bert_) {
+    const int g = pidx("emb_ln.g");
+    tstart(TM_NORM);
+    layernorm_bwd(T, d_, dA_, at_, p0_, at_, mean0_, rstd0_, pp(g), dB_, at_, gp(g), gp(g + 1),
+                  scratch_, s_main_);
+    tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
+    dx0 = dB_;
+  }
+  tstart(TM_EMBED);
+  HP_CUDA(cudaMemsetAsync(gp(0), 0, sizeof(float) * table_[0].size(), s_main_));
+  embed_bwd(b, d_, dx0, at_, gp(0), gp(1), gp(2), scratch_, s_main_);
+  tstop(TM_EMBED, 0, (double)T * d_ * (asz_ + 8));
+  grads_ready(0);
+}
+
+// ------------------------------------------------------------------ round
+void Engine::round_async(int dummy, double lr) {
+  if (!staged_) fail(HP_ECONFIG, "round: no batch staged");
+  HP_CUDA(cudaSetDevice(x_.device));
+  HP_CUDA(cudaMemsetAsync(flags_, 0, 8, s_main_));
+  // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
+  forward(!dummy);
+  loss_reduce(row_loss_, batch_.M, row_loss_ + batch_.M, m_.with_nsp ? batch_.B : 0, d_lw_,
+              s_main_);
+  // d_lw_ = [loss, weight, local loss, local weight]
+  if (dummy) {
+    HP_CUDA(cudaMemsetAsync(d_lw_, 0, 4 * 8, s_main_));
+  } else {
+    HP_CUDA(cudaMemcpyAsync(d_lw_ + 2, d_lw_, 8, cudaMemcpyDeviceToDevice, s_main_));
+    HP_CUDA(cudaMemcpyAsync(d_lw_ + 1, d_weight_, 8, cudaMemcpyDeviceToDevice, s_main_));
+    HP_CUDA(cudaMemcpyAsync(d_lw_ + 3, d_weight_, 8, cudaMemcpyDeviceToDevice, s_main_));
+  }
+  HP_CUDA(cudaEventRecord(ev_fwd_, s_main_));
+  cudaStream_t sw = s_main_;
+  if (comm_) {
+    // [loss_sum, weight] allreduce BEFORE backward (engine.hpp:133), on the
+    // comm stream so backward proceeds concurrently.
+    HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_fwd_, 0));
+    HP_NCCL(ncclAllReduce(d_lw_, d_lw_, 2, ncclDouble, ncclSum, comm_->nccl, s_comm_));
+    sw = s_comm_;
+  }
+  finalize_weight(d_lw_, inv_w_, inv_w64_, flags_, sw);
+
+  next_bucket_ = 0;
+  if (dummy) {
+    // zero loss, weight and gradient (engine.hpp:141-142)
+    HP_CUDA(cudaMemsetAsync(grads_, 0, n_ * 4, s_main_));
+    grads_ready(0);
+  } else {
+    backward();
+  }
+  if (capture_) {
+    if (!local_grads_) local_grads_ = static_cast<float*>(dalloc(n_ * 4));
+    HP_CUDA(cudaMemcpyAsync(local_grads_, grads_, n_ * 4, cudaMemcpyDeviceToDevice, s_main_));
+    capture_ = false;
+    grads_ready(0);
+    capture_ = true;
+  }
+  if (comm_) {
+    HP_CUDA(cudaEventRecord(ev_comm_done_, s_comm_));
+    HP_CUDA(cudaStreamWaitEvent(s_main_, ev_comm_done_, 0));
+  }
+  // one identical update on every rank (engine.hpp:147-153, optim.hpp:107-146)
+  ++adam_t_;
+  const double c1 = 1.0 / (1.0 - std::pow(o_.beta1, static_cast<double>(adam_t_)));
+  const double c2 = 1.0 / (1.0 - std::pow(o_.beta2, static_cast<double>(adam_t_)));
+  AdamArgs a{};
+  a.p = params_; a.m = adam_m_; a.v = adam_v_; a.g = grads_; a.n = n_;
+  a.lr = static_cast<float>(lr);
+  a.b1 = static_cast<float>(o_.beta1);
+  a.b2 = static_cast<float>(o_.beta2);
+  a.eps = static_cast<float>(o_.eps);
+  a.c1 = static_cast<float>(c1);
+  a.c2 = static_cast<float>(c2);
+  a.inv_w64 = comm_ ? nullptr : inv_w64_;  // with NCCL the scale rode PreMulSum
+  a.flags = flags_;
+  a.bad = flags_ + 1;
+  a.sgd = o_.kind == HP_OPT_SGD;
+  a.shadow = shadow_;
+  a.seg_table = seg_table_;
+  a.nseg = nseg_;
+  tstart(TM_ADAM);
+  adam_update(a, s_main_);
+  tstop(TM_ADAM, 0, 28.0 * (double)n_ + (bf16_ ? 2.0 * (double)n_ : 0.0));
+  ++step_;
+  HP_CUDA(cudaMemcpyAsync(h_lw_, d_lw_, 4 * 8, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaMemcpyAsync(h_flags_, flags_, 2 * 4, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaEventRecord(ev_done_, s_main_));
+  in_flight_ = true;
+  last_dummy_ = dummy != 0;
+}
+
+void Engine::round_sync(hp_round_out* out) {
+  if (!in_flight_) fail(HP_ECONFIG, "round_sync without a round in flight");
+  HP_CUDA(cudaEventSynchronize(ev_done_));
+  in_flight_ = false;
+  const double loss = h_lw_[0], weight = h_lw_[1];
+  if (h_flags_[0] & 1) {
+    --step_;
+    --adam_t_;
+    fail(HP_ENUMERIC, "non-finite aggregated loss after step " + std::to_string(step_));
+  }
+  if (h_flags_[0] & 2) {
+    --step_;
+    --adam_t_;
+    fail(HP_ENUMERIC, "total batch weight is zero: every rank was dummy");
+  }
+  if (h_flags_[1]) fail(HP_ENUMERIC, "non-finite gradient at step " + std::to_string(step_));
+  if (out) {
+    out->updated = 1;
+    out->step = step_;
+    out->loss = loss / weight;
+    out->weight = weight;
+    out->local_loss_sum = h_lw_[2];
+    out->local_weight = h_lw_[3];
+  }
+}
+
+}  // namespace hp

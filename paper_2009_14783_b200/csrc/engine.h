@@ -1,0 +1,153 @@
+// DeviceStepEngine: the B200 implementation of StepEngine<T>::round
+// (include/hetpar/engine.hpp:125-165) for one rank (one process per GPU).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <string>
+#include <vector>
+
+#include "hetpar_b200.h"
+#include "hostdata.h"
+#include "kernels.h"
+
+struct hp_comm {
+  ncclComm_t nccl = nullptr;
+  int world = 1, rank = 0, device = 0;
+};
+
+namespace hp {
+
+// Timer classes for the roofline accounting (CUDA events on the launching
+// stream around every launch of the class).
+enum TimerClass { TM_GEMM = 0, TM_ATTN, TM_NORM, TM_HEAD, TM_ADAM, TM_EMBED, TM_COUNT };
+
+class Engine {
+ public:
+  Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_desc& x, hp_comm* comm);
+  ~Engine();
+
+  uint64_t nparams() const { return n_; }
+  void set_params(const void* flat, uint64_t n, int dtype);
+  void get_params(void* flat, uint64_t n, int dtype);
+  void broadcast_params(int root);
+  void get_adam(float* m, float* v, uint64_t* t);
+  void set_adam(const float* m, const float* v, uint64_t t);
+  void set_capture(bool on) { capture_ = on; }
+  void get_local_grads(float* flat, uint64_t n);
+  void stage_batch(const hp_batch& b);
+  void round_async(int dummy, double lr);
+  void round_sync(hp_round_out* out);
+  uint64_t digest();
+  uint64_t step() const { return step_; }
+  void timers(bool on);
+  void mark(int slot);
+  double elapsed(int a, int b);
+  void synchronize();
+  uint64_t stage_bytes() const { return stage_bytes_; }
+  uint64_t readback_bytes() const { return 4 * 8 + 2 * 4; }
+  void timer_read(int which, std::string* name, double* ms, uint64_t* launches, double* bytes,
+                  double* flops);
+
+ private:
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  void* dalloc(size_t bytes);
+  const void* w(int idx) const;   // GEMM view of a weight (shadow or fp32)
+  int64_t wld(int idx) const;     // its row stride
+  float* gp(int idx) const { return grads_ + table_[idx].offset; }
+  float* pp(int idx) const { return params_ + table_[idx].offset; }
+  int pidx(const std::string& name) const;
+  void gemm_t(const GemmArgs& g);
+  void tstart(int cls);
+  void tstop(int cls, double flops, double bytes);
+  void forward(bool need_grad_state);
+  void backward();
+  void grads_ready(int first_done_param);
+  void issue_bucket(size_t b);
+
+  hp_model_desc m_;
+  hp_optim_desc o_;
+  hp_exec_desc x_;
+  hp_comm* comm_;
+  bool bf16_;
+  DType at_;
+  size_t asz_;
+  int d_, H_, dk_, V_, Vp_, L_, F_;
+  bool bert_;
+  std::vector<ParamEntry> table_;
+  std::vector<Bucket> buckets_;
+  std::vector<uint64_t> shadow_off_, shadow_ld_;
+  uint64_t n_ = 0, n_shadow_ = 0;
+
+  std::vector<void*> allocs_;
+  float *params_ = nullptr, *grads_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
+  void* shadow_ = nullptr;
+  uint64_t* seg_table_ = nullptr;
+  int nseg_ = 0;
+  float* pe_ = nullptr;
+
+  // staged batch
+  static constexpr int kStageBufs = 2;
+  void* h_stage_[kStageBufs] = {nullptr, nullptr};
+  cudaEvent_t ev_stage_[kStageBufs] = {};
+  int stage_idx_ = 0;
+  size_t stage_bytes_ = 0;
+  void* d_stage_ = nullptr;
+  DevBatch batch_;
+  double* d_weight_ = nullptr;  // inside the staged block
+  double local_weight_ = 0;
+  bool staged_ = false;
+
+  // activations
+  struct Layer {
+    void *x = nullptr, *qkv = nullptr, *o = nullptr, *p1 = nullptr, *x1 = nullptr, *u = nullptr,
+         *g = nullptr, *p2 = nullptr;
+    float *lse = nullptr, *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr;
+  };
+  std::vector<Layer> layers_;
+  void *x_final_ = nullptr, *p0_ = nullptr;
+  float *mean0_ = nullptr, *rstd0_ = nullptr;
+  void *hm_ = nullptr, *dz_ = nullptr, *dhm_ = nullptr;
+  float *z_ = nullptr, *row_loss_ = nullptr;
+  void *dA_ = nullptr, *dB_ = nullptr, *dC_ = nullptr, *dqkv_ = nullptr, *dU_ = nullptr;
+  float* scratch_ = nullptr;
+  double* d_lw_ = nullptr;  // [loss, weight] (global after the allreduce)
+  float* inv_w_ = nullptr;
+  double* inv_w64_ = nullptr;
+  int* flags_ = nullptr;  // [0] loss/weight flags, [1] bad grad
+  double* h_lw_ = nullptr;
+  int* h_flags_ = nullptr;
+  float* h_params_ = nullptr;
+
+  cudaStream_t s_main_ = nullptr, s_comm_ = nullptr;
+  cudaEvent_t ev_fwd_ = nullptr, ev_comm_done_ = nullptr, ev_done_ = nullptr;
+  std::vector<cudaEvent_t> ev_bucket_;
+  size_t next_bucket_ = 0;
+  ncclRedOp_t premul_ = ncclSum;
+  bool have_premul_ = false;
+
+  bool capture_ = false;
+  float* local_grads_ = nullptr;
+  uint64_t step_ = 0, adam_t_ = 0;
+  bool in_flight_ = false;
+  bool last_dummy_ = false;
+
+  bool timers_on_ = false;
+  struct TimerAcc {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t used = 0;
+    double flops = 0, bytes = 0;
+    double ms = 0;
+    uint64_t launches = 0;
+    cudaEvent_t cur = nullptr;
+  };
+  std::array<TimerAcc, TM_COUNT> tm_;
+  std::array<cudaEvent_t, 8> marks_{};
+};
+
+}  // namespace hp

@@ -1,0 +1,545 @@
+// tcgen05 + TMA + TMEM bf16 GEMM for sm_100a (fp32 accumulation in TMEM).
+//
+// One CTA computes a 128 x BN output tile.  Warp roles:
+//   warp 0      TMA producer: STAGES-deep ring of (A 128x64, B BNx64) tiles,
+//               128B-swizzled, signalled through full/empty mbarriers
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (UMMA_K=16),
+//               tcgen05.commit frees each smem stage and finally signals the
+//               epilogue
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> bias / GELU /
+//               residual -> vectorized global stores (row r of the tile is TMEM
+//               lane r; warp w may only touch lanes 32*(w%4)..+31)
+//
+// Operands may be K-major or MN-major (the three GEMMs of a linear layer's
+// training step: fwd X.W, dgrad dY.W^T, wgrad X^T.dY all read the canonical
+// row-major weight and token-major activations without transposes), and B may
+// be "grouped" (the per-head [d x dk] projection blocks wq.0..wv.{h-1} of the
+// canonical layout, model.hpp:103-112) through a 3-D tensor map.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <array>
+#include <map>
+#include <mutex>
+
+#include "hp_common.h"
+#include "kernels.h"
+
+namespace hp {
+
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+constexpr int STAGES = 4;
+constexpr int kThreads = 192;
+constexpr uint32_t kATileBytes = BM * BK * 2;  // 16 KB
+
+struct Params {
+  int M, N, K;
+  int a_mn;           // A stored MN-major (A^T row-major)
+  int b_mn;           // B stored MN-major (row-major K x N)
+  int b_grouped;      // B uses the 3-D grouped map (group = 64)
+  void* c;
+  int64_t ldc;
+  int64_t c_group, c_gstride;
+  int c_f32;
+  float alpha;
+  int accumulate;
+  const float* bias;
+  int act;
+  void* aux;
+  const void* resid;
+  int64_t ld_resid;
+  int vec;  // C / aux / resid rows are 16-byte aligned
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
+                                       int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
+                                       int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bit.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                      \
+  asm volatile(                                                                                  \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"             \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),      \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),  \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),            \
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),            \
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
+      : "r"(taddr))
+
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float dgelu_f(float x) {
+  return 0.5f * (1.f + erff(x * 0.70710678118654752f)) +
+         x * 0.39894228040143268f * expf(-0.5f * x * x);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Epilogue for 32 consecutive columns [n, n+32) of row m.
+__device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float* v) {
+  if (m >= p.M) return;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+  const bool full = n + 32 <= p.N && p.vec;
+  const bool inb = n + 32 <= p.N;
+  if (p.bias) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += (inb || n + i < p.N) ? p.bias[n + i] : 0.f;
+  }
+  const int64_t co = p.c_group ? (n / p.c_group) * p.c_gstride + (int64_t)m * p.ldc + n % p.c_group
+                               : (int64_t)m * p.ldc + n;
+  if (p.act == ACT_GELU) {
+    // pre-activation kept for the backward pass (same type as C)
+    if (p.c_f32) {
+      float* a = static_cast<float*>(p.aux) + co;
+      for (int i = 0; i < 32; ++i)
+        if (full || n + i < p.N) a[i] = v[i];
+    } else {
+      __nv_bfloat16* a = static_cast<__nv_bfloat16*>(p.aux) + co;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<uint4*>(a)[q] =
+              make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                         pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (n + i < p.N) a[i] = __float2bfloat16_rn(v[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+  } else if (p.act == ACT_DGELU) {
+    if (p.c_f32) {
+      const float* a = static_cast<const float*>(p.aux) + co;
+      for (int i = 0; i < 32; ++i)
+        if (inb || n + i < p.N) v[i] *= dgelu_f(a[i]);
+    } else {
+      const __nv_bfloat16* a = static_cast<const __nv_bfloat16*>(p.aux) + co;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u = reinterpret_cast<const uint4*>(a)[q];
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 f = __bfloat1622float2(h[e]);
+            v[8 * q + 2 * e] *= dgelu_f(f.x);
+            v[8 * q + 2 * e + 1] *= dgelu_f(f.y);
+          }
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (n + i < p.N) v[i] *= dgelu_f(__bfloat162float(a[i]));
+      }
+    }
+  }
+  if (p.resid) {
+    if (p.c_f32) {
+      const float* r = static_cast<const float*>(p.resid) + (int64_t)m * p.ld_resid + n;
+      for (int i = 0; i < 32; ++i)
+        if (full || n + i < p.N) v[i] += r[i];
+    } else {
+      const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.resid) + (int64_t)m * p.ld_resid + n;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u = reinterpret_cast<const uint4*>(r)[q];
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 f = __bfloat1622float2(h[e]);
+            v[8 * q + 2 * e] += f.x;
+            v[8 * q + 2 * e + 1] += f.y;
+          }
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (n + i < p.N) v[i] += __bfloat162float(r[i]);
+      }
+    }
+  }
+  if (p.c_f32) {
+    float* c = static_cast<float*>(p.c) + co;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if (p.accumulate) {
+          float4 old = reinterpret_cast<const float4*>(c)[q];
+          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+        }
+        reinterpret_cast<float4*>(c)[q] = o;
+      }
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (n + i < p.N) c[i] = p.accumulate ? c[i] + v[i] : v[i];
+    }
+  } else {
+    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.c) + co;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(c)[q] =
+            make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (n + i < p.N) c[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, const Params p) {
+  constexpr uint32_t kBTileBytes = BN * BK * 2;
+  constexpr uint32_t kStageBytes = kATileBytes + kBTileBytes;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], kStageBytes);
+        uint8_t* sa = smem + s * kStageBytes;
+        uint8_t* sb = sa + kATileBytes;
+        const int k0 = kb * BK;
+        if (p.a_mn) {
+          tma_2d(&map_a, &full[s], sa, m0, k0);
+          tma_2d(&map_a, &full[s], sa + 8192, m0 + 64, k0);
+        } else {
+          tma_2d(&map_a, &full[s], sa, k0, m0);
+        }
+        if (p.b_mn) {
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) {
+            if (p.b_grouped)
+              tma_3d(&map_b, &full[s], sb + j * 8192, 0, k0, n0 / 64 + j);
+            else
+              tma_2d(&map_b, &full[s], sb + j * 8192, n0 + 64 * j, k0);
+          }
+        } else {
+          if (p.b_grouped)
+            tma_3d(&map_b, &full[s], sb, 0, n0, kb);
+          else
+            tma_2d(&map_b, &full[s], sb, k0, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // kind::f16 instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                             (static_cast<uint32_t>(p.a_mn) << 15) |
+                             (static_cast<uint32_t>(p.b_mn) << 16) |
+                             (static_cast<uint32_t>(BN >> 3) << 17) |
+                             (static_cast<uint32_t>(BM >> 4) << 24);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = smem_u32(smem + s * kStageBytes);
+        const uint32_t sb = sa + kATileBytes;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          // K-major: 128B rows, 8-row groups 1024B apart, +32B per UMMA_K.
+          // MN-major: 64-wide MN atoms 8KB apart (LBO), 8-row K groups 1024B
+          // apart (SBO), +16 rows (2048B) per UMMA_K.
+          const uint64_t ad = p.a_mn ? umma_desc(sa + k * 2048, 8192, 1024)
+                                     : umma_desc(sa + k * 32, 16, 1024);
+          const uint64_t bd = p.b_mn ? umma_desc(sb + k * 2048, 8192, 1024)
+                                     : umma_desc(sb + k * 32, 16, 1024);
+          umma_bf16(tmem_base, ad, bd, idesc, (kb | k) != 0);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // epilogue warps 2..5
+    const int quarter = warp & 3;
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int m = m0 + quarter * 32 + lane;
+    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      TMEM_LD32(lane_addr + c0, r);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (n0 + c0 < p.N) {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        epilogue32(p, m, n0 + c0, v);
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(BN));
+  }
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------- host side
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    HP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) fail(HP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+using MapKey = std::array<uint64_t, 11>;
+std::mutex g_map_mu;
+std::map<MapKey, CUtensorMap> g_maps;
+
+// rank 2 or 3, dims/strides in elements (bf16), box in elements.
+CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                     const uint32_t* box) {
+  MapKey key{reinterpret_cast<uint64_t>(base), (uint64_t)rank, dims[0], dims[1],
+             rank > 2 ? dims[2] : 0, strides[0], rank > 2 ? strides[1] : 0, box[0], box[1],
+             rank > 2 ? box[2] : 0, 0};
+  std::lock_guard<std::mutex> g(g_map_mu);
+  auto it = g_maps.find(key);
+  if (it != g_maps.end()) return it->second;
+  CUtensorMap m;
+  cuuint64_t gd[3] = {dims[0], dims[1], rank > 2 ? dims[2] : 1};
+  cuuint64_t gs[2] = {strides[0] * 2, rank > 2 ? strides[1] * 2 : 0};
+  cuuint32_t bx[3] = {box[0], box[1], rank > 2 ? box[2] : 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs,
+                           bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(HP_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps[key] = m;
+  return m;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmArgs& g) {
+  if (g.ab != DType::bf16) return false;
+  if (g.M < 1 || g.N < 1 || g.K < 16) return false;
+  if (!aligned16(g.a.p) || !aligned16(g.b.p)) return false;
+  if (g.a.group) return false;
+  // TMA: non-innermost strides multiple of 16 bytes
+  if ((g.a.ld * 2) % 16) return false;
+  if ((g.b.ld * 2) % 16) return false;
+  if (g.b.group && (g.b.group != 64 || (g.b.gstride * 2) % 16)) return false;
+  if (g.b.group && g.b.trans && g.K % 64) return false;
+  if (g.b.group && !g.b.trans && g.N % 64) return false;
+  if (g.c_group && g.c_group % 32) return false;
+  if (g.accumulate && g.ct != DType::f32) return false;
+  return true;
+}
+
+static bool epilogue_vec_ok(const GemmArgs& g) {
+  const int64_t elem = g.ct == DType::f32 ? 4 : 2;
+  if (!aligned16(g.c) || (g.ldc * elem) % 16) return false;
+  if (g.c_group && (g.c_gstride * elem) % 16) return false;
+  if (g.resid && ((g.ld_resid * elem) % 16 || !aligned16(g.resid))) return false;
+  if (g.aux && !aligned16(g.aux)) return false;
+  return true;
+}
+
+template <int BN>
+static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Params& p,
+                      cudaStream_t s) {
+  constexpr size_t smem = tc::STAGES * (tc::kATileBytes + BN * tc::BK * 2) + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = true;
+  }
+  dim3 grid((p.N + BN - 1) / BN, (p.M + tc::BM - 1) / tc::BM);
+  tc::gemm_tc_kernel<BN><<<grid, tc::kThreads, smem, s>>>(ma, mb, p);
+  HP_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+namespace {
+int g_force_bn = 0;
+}
+void gemm_tc_set_bn(int bn) { g_force_bn = bn; }
+
+void gemm_tc(const GemmArgs& g, cudaStream_t s) {
+  if (!gemm_tc_supported(g)) fail(HP_ECONFIG, "gemm_tc: unsupported operand layout");
+  int bn = g_force_bn ? g_force_bn : (g.N >= 2048 ? 256 : 128);
+  CUtensorMap ma, mb;
+  {
+    uint64_t dims[2], str[1];
+    uint32_t box[2];
+    if (g.a.trans) {  // memory [K rows][M cols]
+      dims[0] = g.M; dims[1] = g.K; str[0] = g.a.ld; box[0] = 64; box[1] = 64;
+    } else {          // memory [M rows][K cols]
+      dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = tc::BM;
+    }
+    ma = make_map(g.a.p, 2, dims, str, box);
+  }
+  {
+    uint64_t dims[3], str[2];
+    uint32_t box[3];
+    int rank = 2;
+    if (!g.b.trans) {  // MN-major: memory [K rows][N cols] (or grouped blocks)
+      if (g.b.group) {
+        rank = 3;
+        dims[0] = 64; dims[1] = g.K; dims[2] = g.N / 64;
+        str[0] = g.b.ld; str[1] = g.b.gstride;
+        box[0] = 64; box[1] = 64; box[2] = 1;
+      } else {
+        dims[0] = g.N; dims[1] = g.K; str[0] = g.b.ld; box[0] = 64; box[1] = 64;
+      }
+    } else {           // K-major: memory [N rows][K cols] (or grouped along K)
+      if (g.b.group) {
+        rank = 3;
+        dims[0] = 64; dims[1] = g.N; dims[2] = g.K / 64;
+        str[0] = g.b.ld; str[1] = g.b.gstride;
+        box[0] = 64; box[1] = (uint32_t)bn; box[2] = 1;
+      } else {
+        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64; box[1] = (uint32_t)bn;
+      }
+    }
+    mb = make_map(g.b.p, rank, dims, str, box);
+  }
+  tc::Params p;
+  p.M = g.M; p.N = g.N; p.K = g.K;
+  p.a_mn = g.a.trans ? 1 : 0;
+  p.b_mn = g.b.trans ? 0 : 1;
+  p.b_grouped = g.b.group ? 1 : 0;
+  p.c = g.c; p.ldc = g.ldc; p.c_group = g.c_group; p.c_gstride = g.c_gstride;
+  p.c_f32 = g.ct == DType::f32;
+  p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias; p.act = g.act;
+  p.aux = g.aux; p.resid = g.resid; p.ld_resid = g.ld_resid;
+  p.vec = epilogue_vec_ok(g) ? 1 : 0;
+  if (bn == 256)
+    launch_tc<256>(ma, mb, p, s);
+  else
+    launch_tc<128>(ma, mb, p, s);
+}
+
+}  // namespace hp

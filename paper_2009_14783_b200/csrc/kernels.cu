@@ -1,0 +1,854 @@
+// sm_100a kernels of the DP step that are not tcgen05 GEMMs: embedding,
+// LayerNorm, varlen attention, label-smoothed CE, NSP head, column sums,
+// Adam, and the fp32 SIMT GEMM used by the fp32 parity path.
+//
+// Reference semantics (file:line into the reference's proj/):
+//   embedding       model.hpp:354-365, attention.hpp:53-67
+//   attention       attention.hpp:15-50, tape.hpp:123-140 / 274-286
+//   ls_ce           tape.hpp:180-209 / 302-321
+//   gather/scatter  tape.hpp:144-159 / 287-292
+//   adam / sgd      kernels_scalar.cpp:71-83, optim.hpp:107-146
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cfloat>
+#include <cmath>
+
+#include "hp_common.h"
+#include "kernels.h"
+
+namespace hp {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+uint64_t kernel_launch_count() { return g_launches.load(); }
+void count_launch(int n) { g_launches += n; }
+
+#define LAUNCH_CHECK() HP_CUDA(cudaGetLastError())
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ float tof(float x) { return x; }
+__device__ __forceinline__ float tof(bf16 x) { return __bfloat162float(x); }
+template <class T> __device__ __forceinline__ T fromf(float x);
+template <> __device__ __forceinline__ float fromf<float>(float x) { return x; }
+template <> __device__ __forceinline__ bf16 fromf<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int NT>
+__device__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float r = (threadIdx.x < NT / 32) ? red[threadIdx.x] : 0.f;
+  if (w == 0) r = warp_sum(r);
+  if (threadIdx.x == 0) red[0] = r;
+  __syncthreads();
+  return red[0];
+}
+template <int NT>
+__device__ float block_max(float v, float* red) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float r = (threadIdx.x < NT / 32) ? red[threadIdx.x] : -FLT_MAX;
+  if (w == 0) r = warp_max(r);
+  if (threadIdx.x == 0) red[0] = r;
+  __syncthreads();
+  return red[0];
+}
+
+#define DISPATCH1(dt, T, ...)              \
+  if ((dt) == DType::f32) {                \
+    using T = float;                       \
+    __VA_ARGS__;                           \
+  } else {                                 \
+    using T = bf16;                        \
+    __VA_ARGS__;                           \
+  }
+
+// ------------------------------------------------------------------ embedding
+template <class WT, class XT>
+__global__ void embed_fwd_kernel(int T, int d, const int* __restrict__ tok,
+                                 const int* __restrict__ seg, const int* __restrict__ pos,
+                                 const WT* __restrict__ E, const WT* __restrict__ s0,
+                                 const WT* __restrict__ s1, const float* __restrict__ pe,
+                                 XT* __restrict__ x) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const WT* e = E + (int64_t)tok[t] * d;
+  const WT* sg = seg[t] == 0 ? s0 : s1;
+  const float* p = pe + (int64_t)pos[t] * d;
+  // tape order: (E[tok] + (on0 s0 + on1 s1)) + PE  (model.hpp:361-365)
+  for (int c = lane; c < d; c += 32)
+    x[(int64_t)t * d + c] = fromf<XT>((tof(e[c]) + tof(sg[c])) + p[c]);
+}
+
+void embed_fwd(const DevBatch& b, int d, const void* E, const void* seg0,
+               const void* seg1, DType wt, const float* pe, void* x, DType xt,
+               cudaStream_t s) {
+  if (b.T == 0) return;
+  const int wpb = 8;
+  dim3 grid((b.T + wpb - 1) / wpb);
+  DISPATCH1(wt, W, DISPATCH1(xt, X,
+      embed_fwd_kernel<W, X><<<grid, 256, 0, s>>>(b.T, d, b.tok, b.seg, b.pos,
+          (const W*)E, (const W*)seg0, (const W*)seg1, pe, (X*)x)));
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+template <class XT>
+__global__ void embed_scatter_kernel(int T, int d, const int* __restrict__ tok,
+                                     const XT* __restrict__ dx, float* __restrict__ dE) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  float* row = dE + (int64_t)tok[t] * d;
+  for (int c = lane; c < d; c += 32) atomicAdd(row + c, tof(dx[(int64_t)t * d + c]));
+}
+
+// column sums over row chunks; sel (optional) keeps rows with sel[r] == want
+template <class XT>
+__global__ void colsum_partial_kernel(int R, int N, const XT* __restrict__ x, int64_t ld,
+                                      const int* __restrict__ sel, int want, int rows_per,
+                                      float* __restrict__ part) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  const int r0 = blockIdx.y * rows_per;
+  const int r1 = min(R, r0 + rows_per);
+  float acc = 0.f;
+  for (int r = r0; r < r1; ++r)
+    if (!sel || sel[r] == want) acc += tof(x[(int64_t)r * ld + c]);
+  part[(int64_t)blockIdx.y * N + c] = acc;
+}
+__global__ void colsum_final_kernel(int chunks, int N, const float* __restrict__ part,
+                                    float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  float acc = 0.f;
+  for (int k = 0; k < chunks; ++k) acc += part[(int64_t)k * N + c];
+  out[c] = acc;
+}
+
+static constexpr int kColRows = 64;
+
+template <class XT>
+static void colsum_launch(int R, int N, const XT* x, int64_t ld, const int* sel,
+                          int want, float* out, float* scratch, cudaStream_t s) {
+  const int chunks = (R + kColRows - 1) / kColRows;
+  if (chunks == 0) {
+    HP_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * N, s));
+    return;
+  }
+  dim3 g1((N + 127) / 128, chunks);
+  colsum_partial_kernel<XT><<<g1, 128, 0, s>>>(R, N, x, ld, sel, want, kColRows, scratch);
+  LAUNCH_CHECK();
+  colsum_final_kernel<<<(N + 127) / 128, 128, 0, s>>>(chunks, N, scratch, out);
+  LAUNCH_CHECK();
+  count_launch(2);
+}
+
+void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
+               float* dseg0, float* dseg1, float* scratch, cudaStream_t s) {
+  if (b.T == 0) return;
+  DISPATCH1(xt, X, {
+    embed_scatter_kernel<X><<<(b.T + 7) / 8, 256, 0, s>>>(b.T, d, b.tok, (const X*)dx, dE);
+    LAUNCH_CHECK();
+    count_launch();
+    colsum_launch<X>(b.T, d, (const X*)dx, d, b.seg, 0, dseg0, scratch, s);
+    colsum_launch<X>(b.T, d, (const X*)dx, d, b.seg, 1, dseg1, scratch, s);
+  });
+}
+
+void col_sum(int R, int N, const void* x, int64_t ld, DType t, float* out,
+             float* scratch, cudaStream_t s) {
+  DISPATCH1(t, X, colsum_launch<X>(R, N, (const X*)x, ld, nullptr, 0, out, scratch, s));
+}
+
+// ------------------------------------------------------------------ LayerNorm
+static constexpr float kLnEps = 1e-12f;
+
+template <class XT, class YT>
+__global__ void ln_fwd_kernel(int T, int d, const XT* __restrict__ x, const float* __restrict__ g,
+                              const float* __restrict__ bta, YT* __restrict__ y,
+                              float* __restrict__ mean, float* __restrict__ rstd) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const XT* xr = x + (int64_t)t * d;
+  float s = 0.f;
+  for (int c = lane; c < d; c += 32) s += tof(xr[c]);
+  const float mu = warp_sum(s) / d;
+  float v = 0.f;
+  for (int c = lane; c < d; c += 32) {
+    const float q = tof(xr[c]) - mu;
+    v += q * q;
+  }
+  const float rs = rsqrtf(warp_sum(v) / d + kLnEps);
+  for (int c = lane; c < d; c += 32)
+    y[(int64_t)t * d + c] = fromf<YT>((tof(xr[c]) - mu) * rs * g[c] + bta[c]);
+  if (lane == 0) {
+    mean[t] = mu;
+    rstd[t] = rs;
+  }
+}
+
+template <class DYT, class XT, class DXT>
+__global__ void ln_bwd_kernel(int T, int d, const DYT* __restrict__ dy, const XT* __restrict__ x,
+                              const float* __restrict__ mean, const float* __restrict__ rstd,
+                              const float* __restrict__ g, DXT* __restrict__ dx) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const float mu = mean[t], rs = rstd[t];
+  const DYT* dyr = dy + (int64_t)t * d;
+  const XT* xr = x + (int64_t)t * d;
+  float s1 = 0.f, s2 = 0.f;
+  for (int c = lane; c < d; c += 32) {
+    const float xh = (tof(xr[c]) - mu) * rs;
+    const float dxh = tof(dyr[c]) * g[c];
+    s1 += dxh;
+    s2 += dxh * xh;
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  const float inv_d = 1.f / d;
+  for (int c = lane; c < d; c += 32) {
+    const float xh = (tof(xr[c]) - mu) * rs;
+    const float dxh = tof(dyr[c]) * g[c];
+    dx[(int64_t)t * d + c] = fromf<DXT>(rs * (dxh - (s1 + xh * s2) * inv_d));
+  }
+}
+
+template <class DYT, class XT>
+__global__ void ln_pgrad_partial(int T, int d, const DYT* __restrict__ dy, const XT* __restrict__ x,
+                                 const float* __restrict__ mean, const float* __restrict__ rstd,
+                                 int rows_per, float* __restrict__ part) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(T, r0 + rows_per);
+  float ag = 0.f, ab = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const float g = tof(dy[(int64_t)r * d + c]);
+    ag += g * (tof(x[(int64_t)r * d + c]) - mean[r]) * rstd[r];
+    ab += g;
+  }
+  part[(int64_t)blockIdx.y * 2 * d + c] = ag;
+  part[(int64_t)blockIdx.y * 2 * d + d + c] = ab;
+}
+
+void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
+                   const float* bta, void* y, DType yt, float* mean, float* rstd,
+                   cudaStream_t s) {
+  if (T == 0) return;
+  DISPATCH1(xt, X, DISPATCH1(yt, Y,
+      ln_fwd_kernel<X, Y><<<(T + 7) / 8, 256, 0, s>>>(T, d, (const X*)x, g, bta, (Y*)y, mean, rstd)));
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
+                   DType xt, const float* mean, const float* rstd, const float* g,
+                   void* dx, DType dxt, float* dg, float* db, float* scratch,
+                   cudaStream_t s) {
+  if (T == 0) return;
+  DISPATCH1(dyt, DY, DISPATCH1(xt, X, {
+    DISPATCH1(dxt, DX, ln_bwd_kernel<DY, X, DX><<<(T + 7) / 8, 256, 0, s>>>(
+        T, d, (const DY*)dy, (const X*)x, mean, rstd, g, (DX*)dx));
+    LAUNCH_CHECK();
+    const int chunks = (T + kColRows - 1) / kColRows;
+    ln_pgrad_partial<DY, X><<<dim3((d + 127) / 128, chunks), 128, 0, s>>>(
+        T, d, (const DY*)dy, (const X*)x, mean, rstd, kColRows, scratch);
+    LAUNCH_CHECK();
+    // final: rows of 2d partials -> dg | db
+    colsum_final_kernel<<<(2 * d + 127) / 128, 128, 0, s>>>(chunks, 2 * d, scratch, scratch + (int64_t)chunks * 2 * d);
+    LAUNCH_CHECK();
+    HP_CUDA(cudaMemcpyAsync(dg, scratch + (int64_t)chunks * 2 * d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    HP_CUDA(cudaMemcpyAsync(db, scratch + (int64_t)chunks * 2 * d + d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    count_launch(3);
+  }));
+}
+
+// ------------------------------------------------------------------ attention
+// One CTA per (instance, head); the whole (<=128 token) sequence lives in
+// shared memory in fp32.  smem_mm is a register-blocked (4x4) product
+// C(i,j) = sum_k A(i,k) B(k,j) over strided smem operands.
+struct SMat {
+  const float* p;
+  int si, sk;  // A: (i,k) ; B: (k,j) strides
+};
+
+template <class Store>
+__device__ void smem_mm(int n1, int n2, int kd, SMat A, SMat B, Store store) {
+  const int ti_n = (n1 + 3) >> 2, tj_n = (n2 + 3) >> 2;
+  for (int t = threadIdx.x; t < ti_n * tj_n; t += blockDim.x) {
+    const int i0 = (t / tj_n) * 4, j0 = (t % tj_n) * 4;
+    float acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
+    for (int k = 0; k < kd; ++k) {
+      float a[4], bb[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = A.p[(i0 + r) * A.si + k * A.sk];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) bb[c] = B.p[k * B.si + (j0 + c) * B.sk];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] += a[r] * bb[c];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (i0 + r < n1 && j0 + c < n2) store(i0 + r, j0 + c, acc[r][c]);
+  }
+}
+
+template <class T>
+__device__ void load_head(float* dst, int ld_dst, int n, int n4, int dk, const T* src,
+                          int64_t row0, int64_t ld_src, int col0) {
+  for (int e = threadIdx.x; e < n4 * dk; e += blockDim.x) {
+    const int i = e / dk, c = e % dk;
+    dst[i * ld_dst + c] = i < n ? tof(src[(row0 + i) * ld_src + col0 + c]) : 0.f;
+  }
+}
+
+template <class T>
+__global__ void attn_fwd_kernel(const int* __restrict__ cu, int H, int dk,
+                                const T* __restrict__ qkv, T* __restrict__ o,
+                                float* __restrict__ lse, int T_total) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int row0 = cu[b], n = cu[b + 1] - row0;
+  if (n <= 0) return;
+  const int n4 = (n + 3) & ~3, ldh = dk + 1, lds = n4 + 1;
+  const int d = H * dk;
+  const int64_t ldq = 3 * (int64_t)d;
+  float* Q = sm;
+  float* K = Q + n4 * ldh;
+  float* V = K + n4 * ldh;
+  float* S = V + n4 * ldh;
+  load_head(Q, ldh, n, n4, dk, qkv, row0, ldq, h * dk);
+  load_head(K, ldh, n, n4, dk, qkv, row0, ldq, d + h * dk);
+  load_head(V, ldh, n, n4, dk, qkv, row0, ldq, 2 * d + h * dk);
+  __syncthreads();
+  // scores = (Q K^T) * (1/sqrt(dk))   attention.hpp:21-23
+  const float scale = 1.f / sqrtf((float)dk);
+  smem_mm(n, n, dk, SMat{Q, ldh, 1}, SMat{K, 1, ldh},
+          [&](int i, int j, float v) { S[i * lds + j] = v * scale; });
+  __syncthreads();
+  // row softmax with max shift (tape.hpp:129-137)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = w; i < n; i += nw) {
+    float* r = S + i * lds;
+    float mx = -FLT_MAX;
+    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, r[j]);
+    mx = warp_max(mx);
+    float se = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float e = expf(r[j] - mx);
+      r[j] = e;
+      se += e;
+    }
+    se = warp_sum(se);
+    const float inv = 1.f / se;
+    for (int j = lane; j < n; j += 32) r[j] = r[j] * inv;
+    if (lane == 0) lse[(int64_t)h * T_total + row0 + i] = mx + logf(se);
+  }
+  __syncthreads();
+  // O = P V -> columns h*dk.. of the concat (concat_cols order)
+  smem_mm(n, dk, n, SMat{S, lds, 1}, SMat{V, ldh, 1}, [&](int i, int c, float v) {
+    o[(int64_t)(row0 + i) * d + h * dk + c] = fromf<T>(v);
+  });
+}
+
+template <class T>
+__global__ void attn_bwd_kernel(const int* __restrict__ cu, int H, int dk,
+                                const T* __restrict__ qkv, const T* __restrict__ o,
+                                const T* __restrict__ dO, const float* __restrict__ lse,
+                                T* __restrict__ dqkv, int T_total) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int row0 = cu[b], n = cu[b + 1] - row0;
+  if (n <= 0) return;
+  const int n4 = (n + 3) & ~3, ldh = dk + 1, lds = n4 + 1;
+  const int d = H * dk;
+  const int64_t ldq = 3 * (int64_t)d;
+  float* Q = sm;
+  float* K = Q + n4 * ldh;
+  float* V = K + n4 * ldh;
+  float* G = V + n4 * ldh;  // dO
+  float* S = G + n4 * ldh;
+  float* D = S + n4 * lds;  // rowsum(dO * O)
+  load_head(Q, ldh, n, n4, dk, qkv, row0, ldq, h * dk);
+  load_head(K, ldh, n, n4, dk, qkv, row0, ldq, d + h * dk);
+  load_head(V, ldh, n, n4, dk, qkv, row0, ldq, 2 * d + h * dk);
+  load_head(G, ldh, n, n4, dk, dO, row0, d, h * dk);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = w; i < n; i += nw) {
+    float acc = 0.f;
+    for (int c = lane; c < dk; c += 32)
+      acc += G[i * ldh + c] * tof(o[(int64_t)(row0 + i) * d + h * dk + c]);
+    acc = warp_sum(acc);
+    if (lane == 0) D[i] = acc;
+  }
+  __syncthreads();
+  const float scale = 1.f / sqrtf((float)dk);
+  // P = exp(S*scale - lse)
+  smem_mm(n, n, dk, SMat{Q, ldh, 1}, SMat{K, 1, ldh}, [&](int i, int j, float v) {
+    S[i * lds + j] = expf(v * scale - lse[(int64_t)h * T_total + row0 + i]);
+  });
+  __syncthreads();
+  // dV = P^T dO
+  smem_mm(n, dk, n, SMat{S, 1, lds}, SMat{G, ldh, 1}, [&](int j, int c, float v) {
+    dqkv[(int64_t)(row0 + j) * ldq + 2 * d + h * dk + c] = fromf<T>(v);
+  });
+  __syncthreads();
+  // dS = P * (dO V^T - D)   (tape.hpp:274-286), in place
+  smem_mm(n, n, dk, SMat{G, ldh, 1}, SMat{V, 1, ldh}, [&](int i, int j, float v) {
+    float* p = S + i * lds + j;
+    *p = *p * (v - D[i]) * scale;
+  });
+  __syncthreads();
+  // dQ = dS K ; dK = dS^T Q
+  smem_mm(n, dk, n, SMat{S, lds, 1}, SMat{K, ldh, 1}, [&](int i, int c, float v) {
+    dqkv[(int64_t)(row0 + i) * ldq + h * dk + c] = fromf<T>(v);
+  });
+  smem_mm(n, dk, n, SMat{S, 1, lds}, SMat{Q, ldh, 1}, [&](int j, int c, float v) {
+    dqkv[(int64_t)(row0 + j) * ldq + d + h * dk + c] = fromf<T>(v);
+  });
+}
+
+static size_t attn_smem(int n4, int dk, bool bwd) {
+  const int ldh = dk + 1, lds = n4 + 1;
+  return sizeof(float) * ((size_t)(bwd ? 4 : 3) * n4 * ldh + (size_t)n4 * lds + (bwd ? n4 : 0));
+}
+
+static constexpr int kAttnMaxSeq = 128;
+
+void attention_fwd(const DevBatch& b, int H, int dk, const void* qkv, void* o,
+                   float* lse, DType t, cudaStream_t s) {
+  if (b.B == 0) return;
+  const size_t sm = attn_smem(kAttnMaxSeq, dk, false);
+  DISPATCH1(t, X, {
+    HP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attn_fwd_kernel<X><<<dim3(b.B, H), 256, sm, s>>>(b.cu, H, dk, (const X*)qkv, (X*)o, lse, b.T);
+  });
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+void attention_bwd(const DevBatch& b, int H, int dk, const void* qkv,
+                   const void* o, const void* dO, const float* lse, void* dqkv,
+                   DType t, cudaStream_t s) {
+  if (b.B == 0) return;
+  const size_t sm = attn_smem(kAttnMaxSeq, dk, true);
+  DISPATCH1(t, X, {
+    HP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attn_bwd_kernel<X><<<dim3(b.B, H), 256, sm, s>>>(b.cu, H, dk, (const X*)qkv, (const X*)o,
+                                                    (const X*)dO, lse, (X*)dqkv, b.T);
+  });
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+// ------------------------------------------------------------------ rows
+template <class T>
+__global__ void gather_kernel(int R, int d, const int* __restrict__ idx, const T* __restrict__ src,
+                              T* __restrict__ dst) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= R) return;
+  const int lane = threadIdx.x & 31;
+  const T* s = src + (int64_t)idx[r] * d;
+  for (int c = lane; c < d; c += 32) dst[(int64_t)r * d + c] = s[c];
+}
+template <class T>
+__global__ void scatter_kernel(int R, int d, const int* __restrict__ idx, const T* __restrict__ src,
+                               T* __restrict__ dst) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= R) return;
+  const int lane = threadIdx.x & 31;
+  T* o = dst + (int64_t)idx[r] * d;
+  for (int c = lane; c < d; c += 32) o[c] = src[(int64_t)r * d + c];
+}
+void gather_rows(int R, int d, const int* idx, const void* src, void* dst, DType t,
+                 cudaStream_t s) {
+  if (R == 0) return;
+  DISPATCH1(t, X, gather_kernel<X><<<(R + 7) / 8, 256, 0, s>>>(R, d, idx, (const X*)src, (X*)dst));
+  LAUNCH_CHECK();
+  count_launch();
+}
+void scatter_rows(int R, int d, const int* idx, const void* src, void* dst,
+                  DType t, cudaStream_t s) {
+  if (R == 0) return;
+  DISPATCH1(t, X, scatter_kernel<X><<<(R + 7) / 8, 256, 0, s>>>(R, d, idx, (const X*)src, (X*)dst));
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+// ------------------------------------------------------------------ ls_ce
+template <class DZT>
+__global__ void ls_ce_kernel(int V, const float* __restrict__ z, int64_t ldz,
+                             const int* __restrict__ target, float eps,
+                             float* __restrict__ row_loss, DZT* __restrict__ dz, int64_t ld_dz) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const float* zr = z + (int64_t)r * ldz;
+  float mx = -FLT_MAX, zs = 0.f;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) {
+    const float v = zr[j];
+    mx = fmaxf(mx, v);
+    zs += v;
+  }
+  mx = block_max<256>(mx, red);
+  zs = block_sum<256>(zs, red);
+  float se = 0.f;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) se += expf(zr[j] - mx);
+  se = block_sum<256>(se, red);
+  const int t = target[r];
+  const float invV = eps / (float)V;
+  if (threadIdx.x == 0) {
+    const float lse = mx + logf(se);
+    row_loss[r] = lse - (1.f - eps) * zr[t] - invV * zs;
+  }
+  if (dz) {
+    const float inv_se = 1.f / se;
+    DZT* o = dz + (int64_t)r * ld_dz;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) {
+      float g = expf(zr[j] - mx) * inv_se - invV;
+      if (j == t) g -= 1.f - eps;
+      o[j] = fromf<DZT>(g);
+    }
+  }
+}
+
+void ls_ce(int R, int V, const float* z, int64_t ldz, const int* target,
+           float eps, float* row_loss, void* dz, DType dzt, int64_t ld_dz,
+           cudaStream_t s) {
+  if (R == 0) return;
+  DISPATCH1(dzt, X, ls_ce_kernel<X><<<R, 256, 0, s>>>(V, z, ldz, target, eps, row_loss,
+                                                     (X*)dz, ld_dz));
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+// ------------------------------------------------------------------ NSP head
+template <class HT>
+__global__ void nsp_fwd_bwd_kernel(int B, int d, const int* __restrict__ cu,
+                                   const int* __restrict__ label, const HT* __restrict__ H,
+                                   const float* __restrict__ W, const float* __restrict__ bias,
+                                   float* __restrict__ row_loss, float* __restrict__ dW,
+                                   float* __restrict__ db, HT* __restrict__ dH, int grad) {
+  extern __shared__ float dzs[];  // [B][2]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int b = w; b < B; b += nw) {
+    const HT* h0 = H + (int64_t)cu[b] * d;
+    float z0 = 0.f, z1 = 0.f;
+    for (int c = lane; c < d; c += 32) {
+      const float hv = tof(h0[c]);
+      z0 += hv * W[c * 2 + 0];
+      z1 += hv * W[c * 2 + 1];
+    }
+    z0 = warp_sum(z0) + bias[0];
+    z1 = warp_sum(z1) + bias[1];
+    const float mx = fmaxf(z0, z1);
+    const float e0 = expf(z0 - mx), e1 = expf(z1 - mx);
+    const float se = e0 + e1;
+    const int t = label[b];
+    const float g0 = e0 / se - (t == 0 ? 1.f : 0.f);
+    const float g1 = e1 / se - (t == 1 ? 1.f : 0.f);
+    if (lane == 0) {
+      row_loss[b] = mx + logf(se) - (t == 0 ? z0 : z1);
+      dzs[2 * b + 0] = g0;
+      dzs[2 * b + 1] = g1;
+    }
+    if (grad) {
+      HT* dh = dH + (int64_t)cu[b] * d;
+      for (int c = lane; c < d; c += 32)
+        dh[c] = fromf<HT>(tof(dh[c]) + g0 * W[c * 2 + 0] + g1 * W[c * 2 + 1]);
+    }
+  }
+  if (!grad) return;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * d; e += blockDim.x) {
+    const int c = e >> 1, k = e & 1;
+    float acc = 0.f;
+    for (int b = 0; b < B; ++b) acc += tof(H[(int64_t)cu[b] * d + c]) * dzs[2 * b + k];
+    dW[e] = acc;
+  }
+  if (threadIdx.x < 2) {
+    float acc = 0.f;
+    for (int b = 0; b < B; ++b) acc += dzs[2 * b + threadIdx.x];
+    db[threadIdx.x] = acc;
+  }
+}
+
+void nsp_head(const DevBatch& b, int d, const void* H, DType ht, const float* W,
+              const float* bias, float* row_loss, float* dW, float* db, void* dH,
+              int compute_grad, cudaStream_t s) {
+  if (b.B == 0) return;
+  const size_t sm = sizeof(float) * 2 * b.B;
+  DISPATCH1(ht, X, nsp_fwd_bwd_kernel<X><<<1, 512, sm, s>>>(b.B, d, b.cu, b.label, (const X*)H, W,
+                                                           bias, row_loss, dW, db, (X*)dH,
+                                                           compute_grad));
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+// ------------------------------------------------------------------ scalars
+__global__ void loss_reduce_kernel(const float* __restrict__ a, int na, const float* __restrict__ b,
+                                   int nb, double* __restrict__ out) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < na; i += blockDim.x) acc += (double)a[i];
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) acc += (double)b[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+void loss_reduce(const float* a, int na, const float* b, int nb, double* out,
+                 cudaStream_t s) {
+  loss_reduce_kernel<<<1, 256, 0, s>>>(a, na, b, nb, out);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+__global__ void finalize_weight_kernel(const double* lw, float* inv_w, double* inv_w64, int* flags) {
+  const double l = lw[0], w = lw[1];
+  int f = 0;
+  if (!isfinite(l)) f |= 1;
+  if (!(w > 0.0)) f |= 2;
+  *flags = f;
+  *inv_w64 = w > 0.0 ? 1.0 / w : 0.0;
+  *inv_w = (float)(*inv_w64);
+}
+void finalize_weight(const double* lw, float* inv_w, double* inv_w64, int* flags,
+                     cudaStream_t s) {
+  finalize_weight_kernel<<<1, 1, 0, s>>>(lw, inv_w, inv_w64, flags);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+// ------------------------------------------------------------------ Adam
+__device__ __forceinline__ uint64_t shadow_index(const uint64_t* seg, int nseg, uint64_t i) {
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {  // last segment with offset <= i
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg[4 * mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  const uint64_t off = seg[4 * lo], cols = seg[4 * lo + 1], soff = seg[4 * lo + 2],
+                 pcols = seg[4 * lo + 3];
+  const uint64_t local = i - off;
+  return cols == pcols ? soff + local : soff + (local / cols) * pcols + local % cols;
+}
+
+__global__ void adam_kernel(AdamArgs a) {
+  if (a.flags && *a.flags) return;  // numeric error: leave parameters untouched
+  const double sc = a.inv_w64 ? *a.inv_w64 : 1.0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  bf16* sh = (bf16*)a.shadow;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    // g /= total weight in f64, then cast to T (engine.hpp:151, optim.hpp:135)
+    const float g = a.inv_w64 ? (float)((double)a.g[i] * sc) : a.g[i];
+    if (!isfinite(g)) {
+      *a.bad = 1;
+      continue;
+    }
+    float p = a.p[i];
+    if (a.sgd) {
+      p = __fsub_rn(p, __fmul_rn(a.lr, g));
+    } else {
+      // explicit round-to-nearest ops: no FMA contraction, matching the
+      // reference's -ffp-contract=off scalar loop bit for bit
+      const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(__fsub_rn(1.f, a.b1), g));
+      const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]),
+                                __fmul_rn(__fsub_rn(1.f, a.b2), __fmul_rn(g, g)));
+      a.m[i] = m;
+      a.v[i] = v;
+      const float mh = __fmul_rn(m, a.c1);
+      const float vh = __fmul_rn(v, a.c2);
+      p = __fsub_rn(p, __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
+    }
+    a.p[i] = p;
+    if (sh) sh[shadow_index(a.seg_table, a.nseg, i)] = __float2bfloat16_rn(p);
+  }
+}
+void adam_update(const AdamArgs& a, cudaStream_t s) {
+  if (a.n == 0) return;
+  const int blocks = (int)std::min<uint64_t>((a.n + 255) / 256, 148 * 8);
+  adam_kernel<<<blocks, 256, 0, s>>>(a);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+__global__ void shadow_kernel(const float* p, bf16* sh, const uint64_t* seg, int nseg, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    sh[shadow_index(seg, nseg, i)] = __float2bfloat16_rn(p[i]);
+}
+void refresh_shadow(const float* p, void* shadow, const uint64_t* seg_table,
+                    int nseg, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  shadow_kernel<<<148 * 8, 256, 0, s>>>(p, (bf16*)shadow, seg_table, nseg, n);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+__global__ void fill_kernel(float* p, uint64_t n, float v) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = v;
+}
+void fill_f32(float* p, uint64_t n, float v, cudaStream_t s) {
+  if (n == 0) return;
+  fill_kernel<<<148 * 4, 256, 0, s>>>(p, n, v);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+__global__ void fnv_kernel(const uint8_t* p, uint64_t n, uint64_t* out) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (uint64_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  *out = h;
+}
+void fnv1a(const uint8_t* p, uint64_t n, uint64_t* out, cudaStream_t s) {
+  fnv_kernel<<<1, 1, 0, s>>>(p, n, out);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+// ------------------------------------------------------------------ SIMT GEMM
+template <class T>
+__device__ __forceinline__ float ld_op(const Operand& o, int64_t off) {
+  return tof(static_cast<const T*>(o.p)[off]);
+}
+__device__ __forceinline__ int64_t a_off(const Operand& o, int64_t m, int64_t k) {
+  return o.trans ? k * o.ld + m : m * o.ld + k;
+}
+__device__ __forceinline__ int64_t b_off(const Operand& o, int64_t k, int64_t n) {
+  if (!o.trans) {
+    return o.group ? (n / o.group) * o.gstride + k * o.ld + n % o.group : k * o.ld + n;
+  }
+  return o.group ? (k / o.group) * o.gstride + n * o.ld + k % o.group : n * o.ld + k;
+}
+
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float dgelu_f(float x) {
+  return 0.5f * (1.f + erff(x * 0.70710678118654752f)) +
+         x * 0.39894228040143268f * expf(-0.5f * x * x);
+}
+
+template <class CT>
+__device__ __forceinline__ void epi_store(const GemmArgs& g, int m, int n, float acc) {
+  float v = acc * g.alpha;
+  if (g.bias) v += g.bias[n];
+  const int64_t co = g.c_group ? (n / g.c_group) * g.c_gstride + (int64_t)m * g.ldc + n % g.c_group
+                               : (int64_t)m * g.ldc + n;
+  if (g.act == ACT_GELU) {
+    static_cast<CT*>(g.aux)[co] = fromf<CT>(v);
+    v = gelu_f(v);
+  } else if (g.act == ACT_DGELU) {
+    v *= dgelu_f(tof(static_cast<const CT*>(g.aux)[co]));
+  }
+  if (g.resid) v += tof(static_cast<const CT*>(g.resid)[(int64_t)m * g.ld_resid + n]);
+  CT* c = static_cast<CT*>(g.c);
+  if (g.accumulate) v += tof(c[co]);
+  c[co] = fromf<CT>(v);
+}
+
+template <class ABT, class CT>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < g.K; k0 += BK) {
+    for (int e = threadIdx.x; e < BM * BK; e += 256) {
+      // trans A: m fastest for coalescing, else k fastest
+      int mm, kk;
+      if (g.a.trans) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < g.M && k < g.K) ? ld_op<ABT>(g.a, a_off(g.a, m, k)) : 0.f;
+    }
+    for (int e = threadIdx.x; e < BK * BN; e += 256) {
+      int kk, nn;
+      if (g.b.trans) { kk = e % BK; nn = e / BK; } else { nn = e % BN; kk = e / BN; }
+      const int k = k0 + kk, n = n0 + nn;
+      Bs[kk][nn] = (n < g.N && k < g.K) ? ld_op<ABT>(g.b, b_off(g.b, k, n)) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < g.M && n < g.N) epi_store<CT>(g, m, n, acc[i][j]);
+    }
+}
+
+void gemm_simt(const GemmArgs& g, cudaStream_t s) {
+  if (g.M == 0 || g.N == 0) return;
+  dim3 grid((g.N + 63) / 64, (g.M + 63) / 64);
+  DISPATCH1(g.ab, AB, DISPATCH1(g.ct, C, gemm_simt_kernel<AB, C><<<grid, 256, 0, s>>>(g)));
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+namespace {
+int g_tc_mode = 0;
+}
+void gemm_tc_force(int mode) { g_tc_mode = mode; }
+
+int gemm(const GemmArgs& g, cudaStream_t s) {
+  if (g_tc_mode == 0 && g.ab == DType::bf16 && gemm_tc_supported(g)) {
+    gemm_tc(g, s);
+    return 1;
+  }
+  gemm_simt(g, s);
+  return 0;
+}
+
+}  // namespace hp

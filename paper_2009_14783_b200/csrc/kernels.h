@@ -1,0 +1,151 @@
+// Launch wrappers for the sm_100a kernels of the DP step.  All take an
+// explicit stream; none synchronizes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace hp {
+
+enum class DType : int { f32 = 0, bf16 = 1 };
+
+// Strided operand of a GEMM (row-major everywhere).
+//   A(m,k): trans=0 -> p[m*ld + k];  trans=1 -> p[k*ld + m]
+//   B(k,n): trans=0 -> p[(n/g)*gs + k*ld + n%g];  trans=1 -> p[(k/g)*gs + n*ld + k%g]
+//   C(m,n): p[(n/g)*gs + m*ld + n%g]
+// g == 0 disables grouping.  Grouping describes the per-head projection
+// matrices wq.0..wq.{h-1}, wk.*, wv.* which the canonical layout keeps as
+// separate [d x dk] blocks (model.hpp:103-112).
+struct Operand {
+  const void* p = nullptr;
+  int64_t ld = 0;
+  int trans = 0;
+  int64_t group = 0;
+  int64_t gstride = 0;
+};
+
+// ACT_GELU: store pre-activation to aux, apply GELU.
+// ACT_DGELU: multiply by GELU'(aux) (aux = saved pre-activation, read only).
+enum Act { ACT_NONE = 0, ACT_GELU = 1, ACT_DGELU = 2 };
+
+struct GemmArgs {
+  int M = 0, N = 0, K = 0;
+  DType ab = DType::f32;  // A and B element type
+  Operand a, b;
+  void* c = nullptr;
+  int64_t ldc = 0;
+  int64_t c_group = 0, c_gstride = 0;
+  DType ct = DType::f32;
+  float alpha = 1.f;
+  int accumulate = 0;          // C += result (f32 C only)
+  const float* bias = nullptr; // [N], added before the activation
+  int act = ACT_NONE;
+  void* aux = nullptr;         // pre-activation (ct type), ld = ldc
+  const void* resid = nullptr; // C = epi(...) + R(m,n), R of type ct
+  int64_t ld_resid = 0;
+};
+
+// Dispatch: tcgen05 path for bf16 operands whose layout TMA can describe,
+// fp32 SIMT path otherwise.  Returns the path used (0 SIMT, 1 tcgen05).
+int gemm(const GemmArgs& g, cudaStream_t s);
+void gemm_simt(const GemmArgs& g, cudaStream_t s);
+bool gemm_tc_supported(const GemmArgs& g);
+void gemm_tc(const GemmArgs& g, cudaStream_t s);
+void gemm_tc_force(int mode);  // test hook: 0 auto, 1 never tcgen05
+void gemm_tc_set_bn(int bn);   // test hook: 0 heuristic, 128 or 256
+
+// Device batch (one rank batch, SoA int32), see engine.cpp.
+struct DevBatch {
+  int T = 0, B = 0, M = 0;
+  const int* tok = nullptr;     // [T]
+  const int* seg = nullptr;     // [T]
+  const int* pos = nullptr;     // [T] position within its instance
+  const int* cu = nullptr;      // [B+1] instance token offsets
+  const int* mrow = nullptr;    // [M] global token row of each masked position
+  const int* morig = nullptr;   // [M] original token id (MLM target)
+  const int* label = nullptr;   // [B] NSP label
+};
+
+// x[t] = E[tok] + seg_{s}[.] + PE[pos] ; optional LN afterwards is separate.
+void embed_fwd(const DevBatch& b, int d, const void* E, const void* seg0,
+               const void* seg1, DType wt, const float* pe, void* x, DType xt,
+               cudaStream_t s);
+// dE[tok] += dx (atomics), dseg{0,1} = column sums over the segment's tokens.
+void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
+               float* dseg0, float* dseg1, float* scratch, cudaStream_t s);
+
+void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
+                   const float* bta, void* y, DType yt, float* mean, float* rstd,
+                   cudaStream_t s);
+// dx = LN'(dy); dg/db column sums written (not accumulated) to dg, db.
+void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
+                   DType xt, const float* mean, const float* rstd, const float* g,
+                   void* dx, DType dxt, float* dg, float* db, float* scratch,
+                   cudaStream_t s);
+
+// Varlen multi-head self-attention over packed QKV [T x 3d] (columns:
+// q heads | k heads | v heads, dk each).  O [T x d], lse [H x T].
+void attention_fwd(const DevBatch& b, int H, int dk, const void* qkv, void* o,
+                   float* lse, DType t, cudaStream_t s);
+void attention_bwd(const DevBatch& b, int H, int dk, const void* qkv,
+                   const void* o, const void* dO, const float* lse, void* dqkv,
+                   DType t, cudaStream_t s);
+
+// rows of src selected by idx -> dst (dst[r] = src[idx[r]]).
+void gather_rows(int R, int d, const int* idx, const void* src, void* dst, DType t,
+                 cudaStream_t s);
+// dst[idx[r]] = src[r] (rows unique), other rows untouched.
+void scatter_rows(int R, int d, const int* idx, const void* src, void* dst,
+                  DType t, cudaStream_t s);
+
+// Label-smoothed CE over logits [R x V] (ld), tape.hpp:180-209/302-321.
+// Per-row losses -> row_loss[R]; dz = p - q - eps/V written to dz (ld_dz).
+void ls_ce(int R, int V, const float* z, int64_t ldz, const int* target,
+           float eps, float* row_loss, void* dz, DType dzt, int64_t ld_dz,
+           cudaStream_t s);
+
+// NSP head (model.hpp:381-388): h0 = H[cu[b]], z = h0 W + b, CE(eps=0);
+// writes row losses, dW [d x 2], db [2] (overwrite), and dH[cu[b]] += dz W^T.
+void nsp_head(const DevBatch& b, int d, const void* H, DType ht, const float* W,
+              const float* bias, float* row_loss, float* dW, float* db, void* dH,
+              int compute_grad, cudaStream_t s);
+
+// Column sums of a [R x N] matrix into out[N] (overwrite).
+void col_sum(int R, int N, const void* x, int64_t ld, DType t, float* out,
+             float* scratch, cudaStream_t s);
+
+// out[0] += sum(a[0..na)) + sum(b[0..nb)) in double, deterministic order.
+void loss_reduce(const float* a, int na, const float* b, int nb, double* out,
+                 cudaStream_t s);
+
+// lw = [loss, weight]: finalize after the allreduce; inv_w = 1/weight (f32),
+// flags |= 1 when loss is non-finite, |= 2 when weight <= 0.
+void finalize_weight(const double* lw, float* inv_w, double* inv_w64, int* flags,
+                     cudaStream_t s);
+
+// Adam (kernels_scalar.cpp:74-83) bit-exact in f32 on identical inputs:
+//   g = grad * scale (scale from *inv_w64 when non-null, else 1)
+// shadow: optional bf16 working copy written with the param table's padded
+// layout (see engine.cpp), segs describe [offset, cols, shadow_off, pcols].
+struct AdamArgs {
+  float* p; float* m; float* v; const float* g; uint64_t n;
+  float lr, b1, b2, eps, c1, c2;
+  const double* inv_w64;  // may be null
+  const int* flags;       // skip everything when *flags != 0
+  int* bad;               // set to 1 on a non-finite gradient
+  int sgd;
+  void* shadow; const uint64_t* seg_table; int nseg;
+};
+void adam_update(const AdamArgs& a, cudaStream_t s);
+
+// bf16 shadow refresh from fp32 params (after set_params / broadcast).
+void refresh_shadow(const float* p, void* shadow, const uint64_t* seg_table,
+                    int nseg, uint64_t n, cudaStream_t s);
+void fill_f32(float* p, uint64_t n, float v, cudaStream_t s);
+// FNV-1a over bytes (params_digest) -- single-thread kernel, off the hot path.
+void fnv1a(const uint8_t* p, uint64_t n, uint64_t* out, cudaStream_t s);
+
+uint64_t kernel_launch_count();
+void count_launch(int n = 1);
+
+}  // namespace hp

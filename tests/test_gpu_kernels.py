@@ -1,0 +1,182 @@
+"""Kernel-level numerics on the B200: the tcgen05/TMA GEMM (every operand
+major-ness, grouped per-head operands, tails, fused epilogues) and the SIMT
+fp32 GEMM against a torch fp32 reference; Adam bit-exact against the C
+oracle's restatement of kern::scalar::adam_update<float>."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from helpers import oracle_lib
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _lib():
+    from paper_2009_14783_b200 import _lib
+    return _lib
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def run_gemm(M, N, K, dtype, a_trans, b_trans, path, bn=0, group=0, bias=False, act=0, resid=False,
+             accumulate=False, c_dtype=None, c_group=0, seed=0, b_pad=0):
+    L = _lib()
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    dev = "cuda"
+    c_dtype = c_dtype or dtype
+    A = torch.randn(M, K, generator=g).to(dev, dtype)       # logical A
+    if group:
+        nb = N // group if not b_trans else K // group
+    Bl = torch.randn(K, N, generator=g).to(dev, dtype)      # logical B
+    # storage
+    A_st = A.t().contiguous() if a_trans else A.contiguous()
+    lda = M if a_trans else K
+    if group and not b_trans:      # grouped along N: [N/g][K][g]
+        B_st = Bl.reshape(K, N // group, group).permute(1, 0, 2).contiguous()
+        ldb, gstride = group, K * group
+    elif group and b_trans:        # grouped along K: [K/g][N][g]
+        B_st = Bl.reshape(K // group, group, N).permute(0, 2, 1).contiguous()
+        ldb, gstride = group, N * group
+    elif b_trans:
+        B_st = Bl.t().contiguous()
+        ldb, gstride = K, 0
+    else:
+        B_st = torch.zeros(K, N + b_pad, device=dev, dtype=dtype)
+        B_st[:, :N] = Bl
+        ldb, gstride = N + b_pad, 0
+    ref = A.float() @ Bl.float()
+    bvec = torch.randn(N, generator=g).to(dev) if bias else None
+    if bvec is not None:
+        ref = ref + bvec
+    aux = None
+    if act == 1:
+        aux = torch.zeros(M, N, device=dev, dtype=c_dtype)
+        pre = ref.clone()
+        ref = torch.nn.functional.gelu(ref)
+    elif act == 2:
+        aux = torch.randn(M, N, generator=g).to(dev, c_dtype)
+        x = aux.float()
+        dg = 0.5 * (1 + torch.erf(x / 2**0.5)) + x * torch.exp(-0.5 * x * x) / (2 * np.pi) ** 0.5
+        ref = ref * dg
+    R = torch.randn(M, N, generator=g).to(dev, c_dtype) if resid else None
+    if R is not None:
+        ref = ref + R.float()
+    C0 = torch.randn(M, N, generator=g).to(dev, c_dtype) if accumulate else torch.zeros(M, N, device=dev, dtype=c_dtype)
+    if accumulate:
+        ref = ref + C0.float()
+    if c_group:
+        Cst = C0.reshape(M, N // c_group, c_group).permute(1, 0, 2).contiguous()
+        ldc, cgs = c_group, M * c_group
+    else:
+        Cst = C0.clone()
+        ldc, cgs = N, 0
+    L.call("hp_debug_gemm", M, N, K, int(dtype == torch.bfloat16), _ptr(A_st), lda, int(a_trans),
+           _ptr(B_st), ldb, int(b_trans), group, gstride, _ptr(Cst), ldc,
+           int(c_dtype == torch.bfloat16), c_group, cgs, _ptr(bvec), act, _ptr(aux), _ptr(R),
+           N if resid else 0, int(accumulate), path, bn)
+    L.call("hp_debug_sync")
+    out = Cst.permute(1, 0, 2).reshape(M, N) if c_group else Cst
+    res = {"out": out.float(), "ref": ref}
+    if act == 1:
+        res["aux"] = aux.float()
+        res["pre"] = pre
+    return res
+
+
+def _tol(dtype, K):
+    return (2e-2 if dtype == torch.bfloat16 else 1e-4) * max(1.0, (K / 64) ** 0.5)
+
+
+def _check(res, dtype, K):
+    err = (res["out"] - res["ref"]).abs().max().item()
+    scale = res["ref"].abs().max().item() + 1e-6
+    assert err / scale < _tol(dtype, K), (err, scale)
+
+
+@pytest.mark.parametrize("a_trans", [0, 1])
+@pytest.mark.parametrize("b_trans", [0, 1])
+@pytest.mark.parametrize("bn", [128, 256])
+def test_tc_gemm_layouts(a_trans, b_trans, bn):
+    res = run_gemm(384, 512, 320, torch.bfloat16, a_trans, b_trans, path=2, bn=bn, c_dtype=torch.float32)
+    _check(res, torch.bfloat16, 320)
+
+
+@pytest.mark.parametrize("shape", [(200, 136, 72), (136, 264, 104), (8, 64, 16), (4096, 768, 64)])
+def test_tc_gemm_tails(shape):
+    M, N, K = shape
+    for a_trans, b_trans in ((0, 0), (0, 1), (1, 0)):
+        res = run_gemm(M, N, K, torch.bfloat16, a_trans, b_trans, path=2, c_dtype=torch.float32)
+        _check(res, torch.bfloat16, K)
+
+
+@pytest.mark.parametrize("b_trans", [0, 1])
+def test_tc_gemm_grouped_heads(b_trans):
+    # QKV fwd (grouped N) and dgrad (grouped K), dk = 64
+    res = run_gemm(256, 384, 384, torch.bfloat16, 0, b_trans, path=2, group=64)
+    _check(res, torch.bfloat16, 384)
+
+
+def test_tc_gemm_grouped_output():
+    # QKV wgrad: C scattered into [N/64][M][64] blocks (fp32 flat gradient)
+    res = run_gemm(256, 384, 512, torch.bfloat16, 1, 0, path=2, c_dtype=torch.float32, c_group=64)
+    _check(res, torch.bfloat16, 512)
+
+
+def test_tc_gemm_epilogues():
+    res = run_gemm(256, 512, 256, torch.bfloat16, 0, 0, path=2, bias=True, act=1)
+    _check(res, torch.bfloat16, 256)
+    assert (res["aux"] - res["pre"]).abs().max().item() < 0.05 * res["pre"].abs().max().item()
+    res = run_gemm(256, 512, 256, torch.bfloat16, 0, 1, path=2, act=2)
+    _check(res, torch.bfloat16, 256)
+    res = run_gemm(256, 384, 256, torch.bfloat16, 0, 0, path=2, bias=True, resid=True)
+    _check(res, torch.bfloat16, 256)
+    res = run_gemm(256, 384, 256, torch.bfloat16, 1, 0, path=2, accumulate=True, c_dtype=torch.float32)
+    _check(res, torch.bfloat16, 256)
+
+
+def test_tc_gemm_unaligned_output_rows():
+    # MLM head wgrad: fp32 C with ldc = V = 30522 (rows not 16B aligned)
+    res = run_gemm(128, 1002, 96, torch.bfloat16, 1, 0, path=2, c_dtype=torch.float32, b_pad=6)
+    _check(res, torch.bfloat16, 96)
+
+
+@pytest.mark.parametrize("a_trans,b_trans", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_simt_gemm_fp32(a_trans, b_trans):
+    res = run_gemm(100, 70, 45, torch.float32, a_trans, b_trans, path=1, bias=True)
+    _check(res, torch.float32, 45)
+    res = run_gemm(64, 96, 64, torch.float32, a_trans, b_trans, path=1, group=32 if not a_trans else 0)
+    _check(res, torch.float32, 64)
+
+
+def test_adam_bit_exact_vs_reference_scalar():
+    L = _lib()
+    orc = oracle_lib()
+    rng = np.random.default_rng(1)
+    n = 100003
+    p = rng.standard_normal(n).astype(np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    dp, dm, dv = (torch.from_numpy(x.copy()).cuda() for x in (p, m, v))
+    f = C.c_float
+    pp = lambda a: C.c_void_p(a.ctypes.data)
+    for t in range(1, 6):
+        g = (rng.standard_normal(n) * 10.0 ** rng.integers(-8, 2, n)).astype(np.float32)
+        c1, c2 = 1 / (1 - 0.9**t), 1 / (1 - 0.98**t)
+        args = (f(1e-3), f(0.9), f(0.98), f(1e-9), f(c1), f(c2))
+        orc.orc_adam_update_f32(pp(p), pp(m), pp(v), pp(g), C.c_uint64(n), *args)
+        dg = torch.from_numpy(g).cuda()
+        L.call("hp_debug_adam", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(dg), n, *[a.value for a in args], 0)
+    assert np.array_equal(dp.cpu().numpy().view(np.uint32), p.view(np.uint32))
+    assert np.array_equal(dm.cpu().numpy().view(np.uint32), m.view(np.uint32))
+    assert np.array_equal(dv.cpu().numpy().view(np.uint32), v.view(np.uint32))
+    # SGD
+    g = rng.standard_normal(n).astype(np.float32)
+    orc.orc_sgd_update_f32(pp(p), pp(g), C.c_uint64(n), f(0.1))
+    L.call("hp_debug_adam", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(torch.from_numpy(g).cuda()), n,
+           0.1, 0.9, 0.98, 1e-9, 1.0, 1.0, 1)
+    assert np.array_equal(dp.cpu().numpy().view(np.uint32), p.view(np.uint32))
