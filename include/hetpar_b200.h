@@ -238,7 +238,8 @@ hp_status hp_engine_io_bytes(hp_engine* e, uint64_t* h2d, uint64_t* d2h);
  * Test hooks (used by tests/ only): run one GEMM of the engine's dispatch on
  * caller-owned device buffers.  path: 0 auto, 1 SIMT fp32, 2 tcgen05.
  * act: 0 none, 1 GELU (pre-activation to aux), 2 dGELU (multiply by
- * GELU'(aux)).  bn: tcgen05 tile width (0 = heuristic, 128 or 256).
+ * GELU'(aux)).  bn: tcgen05 tile width (0 = heuristic, 128, 192 or 256),
+ * plus 1000 * s to force an s-way split-K (fp32 C without epilogue ops).
  * ---------------------------------------------------------------------- */
 hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t lda,
                         int a_trans, const void* B, int64_t ldb, int b_trans,
@@ -247,6 +248,12 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
                         const float* bias, int act, void* aux, const void* resid,
                         int64_t ld_resid, int accumulate, int path, int bn);
 hp_status hp_debug_sync(void);
+/* Varlen self-attention on caller-owned device buffers: cu[B+1] (int32,
+ * device), qkv [T x 3*H*dk], o [T x H*dk], lse [H x T], dO, dqkv.  bf16 = 1
+ * selects bf16 I/O; path: 0 auto, 1 SIMT, 2 tensor-core (mma.sync). */
+hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf16,
+                             const void* qkv, void* o, float* lse, const void* dO,
+                             void* dqkv, int path);
 /* One Adam (sgd=0) or SGD (sgd=1) update of the device kernel on caller-owned
  * device fp32 buffers, no scaling: compare with kern::adam_update<float>. */
 hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n,

@@ -385,9 +385,11 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
   if (path == 1) {
     hp::gemm_simt(g, 0);
   } else if (path == 2) {
-    hp::gemm_tc_set_bn(bn);
+    hp::gemm_tc_set_bn(bn % 1000);
+    hp::gemm_tc_set_splits(bn / 1000);
     hp::gemm_tc(g, 0);
     hp::gemm_tc_set_bn(0);
+    hp::gemm_tc_set_splits(0);
   } else {
     hp::gemm(g, 0);
   }
@@ -404,9 +406,39 @@ hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n
   a.p = p; a.m = m; a.v = v; a.g = g; a.n = n;
   a.lr = lr; a.b1 = b1; a.b2 = b2; a.eps = eps; a.c1 = c1; a.c2 = c2;
   a.bad = bad; a.sgd = sgd;
+  std::vector<uint64_t> items;
+  for (uint64_t o = 0; o < n; o += 65536)
+    items.insert(items.end(), {o, std::min<uint64_t>(65536, n - o), o, 1, 1});
+  uint64_t* d_items = nullptr;
+  HP_CUDA(cudaMalloc(&d_items, items.size() * 8 + 8));
+  HP_CUDA(cudaMemcpy(d_items, items.data(), items.size() * 8, cudaMemcpyHostToDevice));
+  a.items = d_items;
+  a.nitems = static_cast<int>(items.size() / 5);
   hp::adam_update(a, 0);
   HP_CUDA(cudaDeviceSynchronize());
   HP_CUDA(cudaFree(bad));
+  HP_CUDA(cudaFree(d_items));
+  HP_API_END
+}
+
+hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf16,
+                             const void* qkv, void* o, float* lse, const void* dO, void* dqkv,
+                             int path) {
+  HP_API_BEGIN
+  hp::DevBatch b;
+  b.B = B;
+  b.T = T;
+  b.cu = cu;
+  const bool mma = path == 2 || (path == 0 && bf16 && hp::attention_mma_supported(dk, 128));
+  if (mma) {
+    hp::attention_fwd_mma(b, H, qkv, o, lse, 0);
+    if (dO) hp::attention_bwd_mma(b, H, qkv, o, dO, lse, dqkv, 0);
+  } else {
+    const hp::DType t = bf16 ? hp::DType::bf16 : hp::DType::f32;
+    hp::attention_fwd(b, H, dk, qkv, o, lse, t, 0);
+    if (dO) hp::attention_bwd(b, H, dk, qkv, o, dO, lse, dqkv, t, 0);
+  }
+  HP_CUDA(cudaDeviceSynchronize());
   HP_API_END
 }
 

@@ -120,6 +120,36 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   }
   seg_table_ = static_cast<uint64_t*>(dalloc(seg.size() * 8));
   HP_CUDA(cudaMemcpy(seg_table_, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice));
+  {
+    // Adam work items: runs of parameters whose working copy is laid out
+    // contiguously are merged; every item is cut to <= 64K elements.
+    constexpr uint64_t kChunk = 65536;
+    std::vector<std::array<uint64_t, 5>> runs;
+    for (size_t i = 0; i < table_.size(); ++i) {
+      const uint64_t lo = table_[i].offset, n = table_[i].size();
+      const uint64_t slo = bf16_ ? shadow_off_[i] : lo;
+      const uint64_t cols = table_[i].cols, pc = bf16_ ? shadow_ld_[i] : cols;
+      if (cols == pc && !runs.empty() && runs.back()[3] == runs.back()[4] &&
+          runs.back()[0] + runs.back()[1] == lo && runs.back()[2] + runs.back()[1] == slo) {
+        runs.back()[1] += n;
+      } else {
+        runs.push_back({lo, n, slo, cols == pc ? 1 : cols, cols == pc ? 1 : pc});
+      }
+    }
+    std::vector<uint64_t> items;
+    for (const auto& r : runs) {
+      const bool contig = r[3] == r[4];
+      const uint64_t step = contig ? kChunk : std::max<uint64_t>(1, kChunk / r[3]) * r[3];
+      for (uint64_t o = 0; o < r[1]; o += step) {
+        const uint64_t cnt = std::min(step, r[1] - o);
+        const uint64_t srow = contig ? o : (o / r[3]) * r[4];
+        items.insert(items.end(), {r[0] + o, cnt, r[2] + srow, r[3], r[4]});
+      }
+    }
+    nitems_ = static_cast<int>(items.size() / 5);
+    adam_items_ = static_cast<uint64_t*>(dalloc(items.size() * 8));
+    HP_CUDA(cudaMemcpy(adam_items_, items.data(), items.size() * 8, cudaMemcpyHostToDevice));
+  }
 
   // sinusoidal positions computed in double then cast (attention.hpp:53-67)
   {
@@ -196,9 +226,9 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   dC_ = dalloc(T * wmax * asz_);
   dU_ = bert_ ? dalloc(T * F_ * asz_) : nullptr;
   dqkv_ = dalloc(T * 3 * d_ * asz_);
-  const size_t chunksT = (T + 63) / 64, chunksM = (Mm + 63) / 64;
-  const size_t scratch = std::max({chunksT * 2 * wmax + 2 * wmax, chunksM * (size_t)Vp_ + Vp_,
-                                   chunksT * 4 * (size_t)d_ + 4 * (size_t)d_});
+  const size_t scratch = std::max({colsum_scratch_floats((int)T, (int)wmax),
+                                   colsum_scratch_floats((int)Mm, Vp_),
+                                   colsum_scratch_floats((int)T, d_)});
   scratch_ = static_cast<float*>(dalloc(scratch * 4));
   d_lw_ = static_cast<double*>(dalloc(4 * 8));
   inv_w_ = static_cast<float*>(dalloc(4));
@@ -491,7 +521,10 @@ void Engine::forward(bool need_grad) {
     q.c = y.qkv; q.ldc = 3 * d_; q.ct = at_;
     gemm_t(q);
     tstart(TM_ATTN);
-    attention_fwd(b, H_, dk_, y.qkv, y.o, y.lse, at_, s_main_);
+    if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
+      attention_fwd_mma(b, H_, y.qkv, y.o, y.lse, s_main_);
+    else
+      attention_fwd(b, H_, dk_, y.qkv, y.o, y.lse, at_, s_main_);
     tstop(TM_ATTN, 4.0 * H_ * dk_ * (double)T * (double)m_.max_seq, 0);
     void* out = (l + 1 < L_) ? layers_[l + 1].x : x_final_;
     if (!bert_) {
@@ -615,8 +648,9 @@ void Engine::backward() {
       const int ibo = iwo + 1, ig1 = iwo + 2, iw1 = iwo + 4, ib1 = iwo + 5, iw2 = iwo + 6,
                 ib2 = iwo + 7, ig2 = iwo + 8;
       tstart(TM_NORM);
+      // LN2' also yields d(ffn.b2) = colsum(dP2) (P2 = G W2 + b2 + X1)
       layernorm_bwd(T, d_, dA_, at_, y.p2, at_, y.mean2, y.rstd2, pp(ig2), dB_, at_, gp(ig2),
-                    gp(ig2 + 1), scratch_, s_main_);
+                    gp(ig2 + 1), gp(ib2), scratch_, s_main_);
       tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
       GemmArgs w2;  // d(ffn.w2) = G^T dP2
       w2.M = F_; w2.N = d_; w2.K = T; w2.ab = at_;
@@ -624,9 +658,6 @@ void Engine::backward() {
       w2.b = Operand{dB_, d_, 0, 0, 0};
       w2.c = gp(iw2); w2.ldc = d_; w2.ct = DType::f32;
       gemm_t(w2);
-      tstart(TM_NORM);
-      col_sum(T, d_, dB_, d_, at_, gp(ib2), scratch_, s_main_);
-      tstop(TM_NORM, 0, 0);
       GemmArgs du;  // dU = (dP2 W2^T) * gelu'(U)
       du.M = T; du.N = F_; du.K = d_; du.ab = at_;
       du.a = Operand{dB_, d_, 0, 0, 0};
@@ -651,9 +682,9 @@ void Engine::backward() {
       dx1.resid = dB_; dx1.ld_resid = d_;
       gemm_t(dx1);
       tstart(TM_NORM);
+      // LN1' also yields d(bo) = colsum(dP1)
       layernorm_bwd(T, d_, dC_, at_, y.p1, at_, y.mean1, y.rstd1, pp(ig1), dB_, at_, gp(ig1),
-                    gp(ig1 + 1), scratch_, s_main_);
-      col_sum(T, d_, dB_, d_, at_, gp(ibo), scratch_, s_main_);
+                    gp(ig1 + 1), gp(ibo), scratch_, s_main_);
       tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
       dP1 = dB_;
     } else {
@@ -672,7 +703,10 @@ void Engine::backward() {
     dO.c = dC_; dO.ldc = d_; dO.ct = at_;
     gemm_t(dO);
     tstart(TM_ATTN);
-    attention_bwd(b, H_, dk_, y.qkv, y.o, dC_, y.lse, dqkv_, at_, s_main_);
+    if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
+      attention_bwd_mma(b, H_, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
+    else
+      attention_bwd(b, H_, dk_, y.qkv, y.o, dC_, y.lse, dqkv_, at_, s_main_);
     tstop(TM_ATTN, 8.0 * H_ * dk_ * (double)T * (double)m_.max_seq, 0);
     const int64_t gstride_w = bf16_ ? (int64_t)(shadow_off_[iq + 1] - shadow_off_[iq])
                                     : (int64_t)(table_[iq + 1].offset - table_[iq].offset);
@@ -703,7 +737,7 @@ void Engine::backward() {
     const int g = pidx("emb_ln.g");
     tstart(TM_NORM);
     layernorm_bwd(T, d_, dA_, at_, p0_, at_, mean0_, rstd0_, pp(g), dB_, at_, gp(g), gp(g + 1),
-                  scratch_, s_main_);
+                  nullptr, scratch_, s_main_);
     tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
     dx0 = dB_;
   }
@@ -778,8 +812,8 @@ void Engine::round_async(int dummy, double lr) {
   a.bad = flags_ + 1;
   a.sgd = o_.kind == HP_OPT_SGD;
   a.shadow = shadow_;
-  a.seg_table = seg_table_;
-  a.nseg = nseg_;
+  a.items = adam_items_;
+  a.nitems = nitems_;
   tstart(TM_ADAM);
   adam_update(a, s_main_);
   tstop(TM_ADAM, 0, 28.0 * (double)n_ + (bf16_ ? 2.0 * (double)n_ : 0.0));

@@ -88,6 +88,8 @@ class Engine {
   float *params_ = nullptr, *grads_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
   void* shadow_ = nullptr;
   uint64_t* seg_table_ = nullptr;
+  uint64_t* adam_items_ = nullptr;
+  int nitems_ = 0;
   int nseg_ = 0;
   float* pe_ = nullptr;
 

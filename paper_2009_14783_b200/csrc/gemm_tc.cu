@@ -1,14 +1,19 @@
 // tcgen05 + TMA + TMEM bf16 GEMM for sm_100a (fp32 accumulation in TMEM).
 //
-// One CTA computes a 128 x BN output tile.  Warp roles:
+// Persistent, warp-specialized: grid = min(#work units, #SMs); a CTA walks
+// work units u = blockIdx.x, += gridDim.x.  A unit is one 128 x BN output tile
+// (BN in {128, 192, 256}) over one K range (split-K for the weight-gradient
+// GEMMs whose output has too few tiles to fill 148 SMs).
 //   warp 0      TMA producer: STAGES-deep ring of (A 128x64, B BNx64) tiles,
-//               128B-swizzled, signalled through full/empty mbarriers
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (UMMA_K=16),
-//               tcgen05.commit frees each smem stage and finally signals the
-//               epilogue
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> bias / GELU /
-//               residual -> vectorized global stores (row r of the tile is TMEM
-//               lane r; warp w may only touch lanes 32*(w%4)..+31)
+//               128B-swizzled, full/empty mbarriers
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (UMMA_K=16)
+//               into one of TWO accumulator buffers, so the epilogue of tile i
+//               overlaps the MMAs of tile i+1
+//   warps 2..9  epilogue: tcgen05.ld 32x32b.x32 -> registers -> bias / GELU /
+//               dGELU / residual -> vectorized global stores (or fp32 vector
+//               reductions for split-K).  Warp w reads TMEM lanes
+//               32*(w%4)..+31; warps 2-5 take the left half of the tile's
+//               columns, warps 6-9 the right half.
 //
 // Operands may be K-major or MN-major (the three GEMMs of a linear layer's
 // training step: fwd X.W, dgrad dY.W^T, wgrad X^T.dY all read the canonical
@@ -34,14 +39,16 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int STAGES = 4;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kATileBytes = BM * BK * 2;  // 16 KB
 
 struct Params {
   int M, N, K;
-  int a_mn;           // A stored MN-major (A^T row-major)
-  int b_mn;           // B stored MN-major (row-major K x N)
-  int b_grouped;      // B uses the 3-D grouped map (group = 64)
+  int a_mn;       // A stored MN-major (A^T row-major)
+  int b_mn;       // B stored MN-major (row-major K x N)
+  int b_grouped;  // B uses the 3-D grouped map (group = 64)
+  int m_tiles, n_tiles, splits, kb_per_split, units;
   void* c;
   int64_t ldc;
   int64_t c_group, c_gstride;
@@ -66,6 +73,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -147,35 +157,73 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+__device__ __forceinline__ void store8_bf16(__nv_bfloat16* dst, const float* v) {
+  *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                                              pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+}
+__device__ __forceinline__ void load8_bf16(const __nv_bfloat16* src, float* v) {
+  const uint4 u = *reinterpret_cast<const uint4*>(src);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(h[e]);
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
 
 // Epilogue for 32 consecutive columns [n, n+32) of row m.
 __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float* v) {
   if (m >= p.M) return;
+  const bool inb = n + 32 <= p.N;
+  const bool full = inb && p.vec;
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
-  const bool full = n + 32 <= p.N && p.vec;
-  const bool inb = n + 32 <= p.N;
-  if (p.bias) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += (inb || n + i < p.N) ? p.bias[n + i] : 0.f;
-  }
   const int64_t co = p.c_group ? (n / p.c_group) * p.c_gstride + (int64_t)m * p.ldc + n % p.c_group
                                : (int64_t)m * p.ldc + n;
+  if (p.splits > 1) {  // split-K partial: reduce into the (zeroed) fp32 output
+    float* c = static_cast<float*>(p.c) + co;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) red_add_v4(c + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (n + i < p.N) atomicAdd(c + i, v[i]);
+    }
+    return;
+  }
+  if (p.bias) {
+    if (inb && (reinterpret_cast<uintptr_t>(p.bias + n) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n) + q);
+        v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += (n + i < p.N) ? p.bias[n + i] : 0.f;
+    }
+  }
   if (p.act == ACT_GELU) {
     // pre-activation kept for the backward pass (same type as C)
     if (p.c_f32) {
       float* a = static_cast<float*>(p.aux) + co;
+#pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (full || n + i < p.N) a[i] = v[i];
+        if (n + i < p.N) a[i] = v[i];
     } else {
       __nv_bfloat16* a = static_cast<__nv_bfloat16*>(p.aux) + co;
       if (full) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          reinterpret_cast<uint4*>(a)[q] =
-              make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                         pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+        for (int q = 0; q < 4; ++q) store8_bf16(a + 8 * q, v + 8 * q);
       } else {
+#pragma unroll
         for (int i = 0; i < 32; ++i)
           if (n + i < p.N) a[i] = __float2bfloat16_rn(v[i]);
       }
@@ -185,23 +233,21 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
   } else if (p.act == ACT_DGELU) {
     if (p.c_f32) {
       const float* a = static_cast<const float*>(p.aux) + co;
+#pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (inb || n + i < p.N) v[i] *= dgelu_f(a[i]);
+        if (n + i < p.N) v[i] *= dgelu_f(a[i]);
     } else {
       const __nv_bfloat16* a = static_cast<const __nv_bfloat16*>(p.aux) + co;
       if (full) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          uint4 u = reinterpret_cast<const uint4*>(a)[q];
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+          float f[8];
+          load8_bf16(a + 8 * q, f);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float2 f = __bfloat1622float2(h[e]);
-            v[8 * q + 2 * e] *= dgelu_f(f.x);
-            v[8 * q + 2 * e + 1] *= dgelu_f(f.y);
-          }
+          for (int e = 0; e < 8; ++e) v[8 * q + e] *= dgelu_f(f[e]);
         }
       } else {
+#pragma unroll
         for (int i = 0; i < 32; ++i)
           if (n + i < p.N) v[i] *= dgelu_f(__bfloat162float(a[i]));
       }
@@ -210,23 +256,21 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
   if (p.resid) {
     if (p.c_f32) {
       const float* r = static_cast<const float*>(p.resid) + (int64_t)m * p.ld_resid + n;
+#pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (full || n + i < p.N) v[i] += r[i];
+        if (n + i < p.N) v[i] += r[i];
     } else {
       const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.resid) + (int64_t)m * p.ld_resid + n;
       if (full) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          uint4 u = reinterpret_cast<const uint4*>(r)[q];
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+          float f[8];
+          load8_bf16(r + 8 * q, f);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float2 f = __bfloat1622float2(h[e]);
-            v[8 * q + 2 * e] += f.x;
-            v[8 * q + 2 * e + 1] += f.y;
-          }
+          for (int e = 0; e < 8; ++e) v[8 * q + e] += f[e];
         }
       } else {
+#pragma unroll
         for (int i = 0; i < 32; ++i)
           if (n + i < p.N) v[i] += __bfloat162float(r[i]);
       }
@@ -239,12 +283,13 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
       for (int q = 0; q < 8; ++q) {
         float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         if (p.accumulate) {
-          float4 old = reinterpret_cast<const float4*>(c)[q];
+          const float4 old = reinterpret_cast<const float4*>(c)[q];
           o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
         }
         reinterpret_cast<float4*>(c)[q] = o;
       }
     } else {
+#pragma unroll
       for (int i = 0; i < 32; ++i)
         if (n + i < p.N) c[i] = p.accumulate ? c[i] + v[i] : v[i];
     }
@@ -252,15 +297,24 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
     __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.c) + co;
     if (full) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        reinterpret_cast<uint4*>(c)[q] =
-            make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+      for (int q = 0; q < 4; ++q) store8_bf16(c + 8 * q, v + 8 * q);
     } else {
+#pragma unroll
       for (int i = 0; i < 32; ++i)
         if (n + i < p.N) c[i] = __float2bfloat16_rn(v[i]);
     }
   }
+}
+
+__device__ __forceinline__ void decode_unit(const Params& p, int u, int& m0, int& n0, int& kb0,
+                                            int& kb1) {
+  const int s = u % p.splits;
+  const int r = u / p.splits;
+  m0 = (r % p.m_tiles) * BM;
+  n0 = (r / p.m_tiles);  // scaled by BN by the caller
+  const int num_kb = (p.K + BK - 1) / BK;
+  kb0 = s * p.kb_per_split;
+  kb1 = min(num_kb, kb0 + p.kb_per_split);
 }
 
 template <int BN>
@@ -269,23 +323,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap map_b, const Params p) {
   constexpr uint32_t kBTileBytes = BN * BK * 2;
   constexpr uint32_t kStageBytes = kATileBytes + kBTileBytes;
+  constexpr uint32_t kAccStride = BN <= 128 ? 128 : 256;  // TMEM columns per accumulator
+  constexpr uint32_t kTmemCols = 2 * kAccStride;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + STAGES;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -293,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -303,33 +361,39 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], kStageBytes);
-        uint8_t* sa = smem + s * kStageBytes;
-        uint8_t* sb = sa + kATileBytes;
-        const int k0 = kb * BK;
-        if (p.a_mn) {
-          tma_2d(&map_a, &full[s], sa, m0, k0);
-          tma_2d(&map_a, &full[s], sa + 8192, m0 + 64, k0);
-        } else {
-          tma_2d(&map_a, &full[s], sa, k0, m0);
-        }
-        if (p.b_mn) {
-#pragma unroll
-          for (int j = 0; j < BN / 64; ++j) {
-            if (p.b_grouped)
-              tma_3d(&map_b, &full[s], sb + j * 8192, 0, k0, n0 / 64 + j);
-            else
-              tma_2d(&map_b, &full[s], sb + j * 8192, n0 + 64 * j, k0);
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        int m0, nt, kb0, kb1;
+        decode_unit(p, u, m0, nt, kb0, kb1);
+        const int n0 = nt * BN;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], kStageBytes);
+          uint8_t* sa = smem + s * kStageBytes;
+          uint8_t* sb = sa + kATileBytes;
+          const int k0 = kb * BK;
+          if (p.a_mn) {
+            tma_2d(&map_a, &full[s], sa, m0, k0);
+            tma_2d(&map_a, &full[s], sa + 8192, m0 + 64, k0);
+          } else {
+            tma_2d(&map_a, &full[s], sa, k0, m0);
           }
-        } else {
-          if (p.b_grouped)
-            tma_3d(&map_b, &full[s], sb, 0, n0, kb);
-          else
-            tma_2d(&map_b, &full[s], sb, k0, n0);
+          if (p.b_mn) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) {
+              if (p.b_grouped)
+                tma_3d(&map_b, &full[s], sb + j * 8192, 0, k0, n0 / 64 + j);
+              else
+                tma_2d(&map_b, &full[s], sb + j * 8192, n0 + 64 * j, k0);
+            }
+          } else {
+            if (p.b_grouped)
+              tma_3d(&map_b, &full[s], sb, 0, n0, kb);
+            else
+              tma_2d(&map_b, &full[s], sb, k0, n0);
+          }
         }
       }
     }
@@ -341,54 +405,74 @@ __global__ void __launch_bounds__(kThreads, 1)
                              (static_cast<uint32_t>(p.b_mn) << 16) |
                              (static_cast<uint32_t>(BN >> 3) << 17) |
                              (static_cast<uint32_t>(BM >> 4) << 24);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      uint32_t it = 0, lt = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++lt) {
+        int m0, nt, kb0, kb1;
+        decode_unit(p, u, m0, nt, kb0, kb1);
+        const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
+        mbar_wait(&tmem_empty[as], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sa = smem_u32(smem + s * kStageBytes);
-        const uint32_t sb = sa + kATileBytes;
+        const uint32_t dacc = tmem_base + as * kAccStride;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + s * kStageBytes);
+          const uint32_t sb = sa + kATileBytes;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          // K-major: 128B rows, 8-row groups 1024B apart, +32B per UMMA_K.
-          // MN-major: 64-wide MN atoms 8KB apart (LBO), 8-row K groups 1024B
-          // apart (SBO), +16 rows (2048B) per UMMA_K.
-          const uint64_t ad = p.a_mn ? umma_desc(sa + k * 2048, 8192, 1024)
-                                     : umma_desc(sa + k * 32, 16, 1024);
-          const uint64_t bd = p.b_mn ? umma_desc(sb + k * 2048, 8192, 1024)
-                                     : umma_desc(sb + k * 32, 16, 1024);
-          umma_bf16(tmem_base, ad, bd, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: 128B rows, 8-row groups 1024B apart, +32B per UMMA_K.
+            // MN-major: 64-wide MN atoms 8KB apart (LBO), 8-row K groups
+            // 1024B apart (SBO), +16 rows (2048B) per UMMA_K.
+            const uint64_t ad = p.a_mn ? umma_desc(sa + k * 2048, 8192, 1024)
+                                       : umma_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = p.b_mn ? umma_desc(sb + k * 2048, 8192, 1024)
+                                       : umma_desc(sb + k * 32, 16, 1024);
+            umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&tmem_full[as]);
       }
-      umma_commit(tmem_full);
     }
     __syncwarp();
   } else {
-    // epilogue warps 2..5
+    // epilogue warps 2..9
     const int quarter = warp & 3;
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int m = m0 + quarter * 32 + lane;
-    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+    const int half = (warp - 2) >> 2;
+    uint32_t lt = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++lt) {
+      int m0, nt, kb0, kb1;
+      decode_unit(p, u, m0, nt, kb0, kb1);
+      const int n0 = nt * BN;
+      const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
+      mbar_wait(&tmem_full[as], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * kAccStride;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      TMEM_LD32(lane_addr + c0, r);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (n0 + c0 < p.N) {
-        float v[32];
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+        uint32_t r[32];
+        TMEM_LD32(taddr + c0, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (n0 + c0 < p.N) {
+          float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        epilogue32(p, m, n0 + c0, v);
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          epilogue32(p, m, n0 + c0, v);
+        }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[as]);
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
   }
 }
 
@@ -439,7 +523,23 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    HP_CUDA(cudaGetDevice(&dev));
+    HP_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+int g_force_bn = 0;
+int g_force_splits = 0;
+
 }  // namespace
+
+void gemm_tc_set_bn(int bn) { g_force_bn = bn; }
+void gemm_tc_set_splits(int s) { g_force_splits = s; }
 
 bool gemm_tc_supported(const GemmArgs& g) {
   if (g.ab != DType::bf16) return false;
@@ -476,20 +576,42 @@ static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Pa
                                  (int)smem));
     attr = true;
   }
-  dim3 grid((p.N + BN - 1) / BN, (p.M + tc::BM - 1) / tc::BM);
+  const int grid = std::min(p.units, num_sms());
   tc::gemm_tc_kernel<BN><<<grid, tc::kThreads, smem, s>>>(ma, mb, p);
   HP_CUDA(cudaGetLastError());
   count_launch();
 }
 
-namespace {
-int g_force_bn = 0;
-}
-void gemm_tc_set_bn(int bn) { g_force_bn = bn; }
-
 void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (!gemm_tc_supported(g)) fail(HP_ECONFIG, "gemm_tc: unsupported operand layout");
-  int bn = g_force_bn ? g_force_bn : (g.N >= 2048 ? 256 : 128);
+  const int nsm = num_sms();
+  const int m_tiles = (g.M + tc::BM - 1) / tc::BM;
+  const int num_kb = (g.K + tc::BK - 1) / tc::BK;
+  const bool can_split = g.ct == DType::f32 && !g.bias && !g.act && !g.resid && !g.accumulate;
+  // Pick the N tile (and split-K factor) maximising SM-wave efficiency;
+  // ties go to the wider tile (more reuse per byte staged).
+  int bn = 256, splits = 1;
+  double best = -1;
+  for (int cand : {256, 192, 128}) {
+    if (g.b.group && !g.b.trans && cand % 64) continue;
+    const int tiles = m_tiles * ((g.N + cand - 1) / cand);
+    int sp = 1;
+    if (can_split && tiles < nsm) sp = std::max(1, std::min(nsm / tiles, num_kb / 4));
+    const int units = tiles * sp;
+    const int waves = (units + nsm - 1) / nsm;
+    const double eff = static_cast<double>(units) / (waves * nsm) * (cand == 256 ? 1.0 : cand == 192 ? 0.97 : 0.93);
+    if (eff > best + 1e-9) {
+      best = eff;
+      bn = cand;
+      splits = sp;
+    }
+  }
+  if (g_force_bn) bn = g_force_bn;
+  if (g_force_splits && can_split) splits = g_force_splits;
+  if (!can_split) splits = 1;
+  const int kb_per_split = (num_kb + splits - 1) / splits;
+  splits = (num_kb + kb_per_split - 1) / kb_per_split;  // no empty splits
+
   CUtensorMap ma, mb;
   {
     uint64_t dims[2], str[1];
@@ -531,13 +653,28 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.a_mn = g.a.trans ? 1 : 0;
   p.b_mn = g.b.trans ? 0 : 1;
   p.b_grouped = g.b.group ? 1 : 0;
+  p.m_tiles = m_tiles;
+  p.n_tiles = (g.N + bn - 1) / bn;
+  p.splits = splits;
+  p.kb_per_split = kb_per_split;
+  p.units = m_tiles * p.n_tiles * splits;
   p.c = g.c; p.ldc = g.ldc; p.c_group = g.c_group; p.c_gstride = g.c_gstride;
   p.c_f32 = g.ct == DType::f32;
   p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias; p.act = g.act;
   p.aux = g.aux; p.resid = g.resid; p.ld_resid = g.ld_resid;
   p.vec = epilogue_vec_ok(g) ? 1 : 0;
+  if (splits > 1) {
+    // partial sums are reduced into C: clear the output region first
+    if (g.c_group) {
+      HP_CUDA(cudaMemsetAsync(g.c, 0, sizeof(float) * (size_t)(g.N / g.c_group) * g.c_gstride, s));
+    } else {
+      HP_CUDA(cudaMemset2DAsync(g.c, sizeof(float) * g.ldc, 0, sizeof(float) * g.N, g.M, s));
+    }
+  }
   if (bn == 256)
     launch_tc<256>(ma, mb, p, s);
+  else if (bn == 192)
+    launch_tc<192>(ma, mb, p, s);
   else
     launch_tc<128>(ma, mb, p, s);
 }

@@ -14,6 +14,7 @@
 #include <atomic>
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 
 #include "hp_common.h"
 #include "kernels.h"
@@ -72,6 +73,24 @@ __device__ float block_max(float v, float* red) {
   __syncthreads();
   return red[0];
 }
+
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 v = __bfloat1622float2(h[e]);
+    f[2 * e] = v.x;
+    f[2 * e + 1] = v.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+  return u;
+}
+
 
 #define DISPATCH1(dt, T, ...)              \
   if ((dt) == DType::f32) {                \
@@ -137,20 +156,76 @@ __global__ void colsum_partial_kernel(int R, int N, const XT* __restrict__ x, in
     if (!sel || sel[r] == want) acc += tof(x[(int64_t)r * ld + c]);
   part[(int64_t)blockIdx.y * N + c] = acc;
 }
+// Final stage of every column reduction: out[c] = sum_k part[k*stride + c].
+// Block (32 columns x 16 chunk-lanes): each lane sums every 16th chunk, then
+// the 16 lane sums are added in a fixed order (deterministic).
+constexpr int kFinY = 16;
+__device__ __forceinline__ float final_sum(int chunks, int stride, const float* __restrict__ part,
+                                           int c, bool ok) {
+  __shared__ float red[kFinY][33];
+  float acc = 0.f;
+  if (ok)
+    for (int k = threadIdx.y; k < chunks; k += kFinY) acc += part[(int64_t)k * stride + c];
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  float s = 0.f;
+  if (threadIdx.y == 0)
+#pragma unroll
+    for (int j = 0; j < kFinY; ++j) s += red[j][threadIdx.x];
+  return s;
+}
+__global__ void colsum_final_strided(int chunks, int stride, int N, const float* __restrict__ part,
+                                     float* __restrict__ out) {
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const float s = final_sum(chunks, stride, part, c, c < N);
+  if (threadIdx.y == 0 && c < N) out[c] = s;
+}
+#define FINAL_LAUNCH(N) dim3(((N) + 31) / 32), dim3(32, kFinY)
 __global__ void colsum_final_kernel(int chunks, int N, const float* __restrict__ part,
                                     float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  float acc = 0.f;
-  for (int k = 0; k < chunks; ++k) acc += part[(int64_t)k * N + c];
-  out[c] = acc;
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const float s = final_sum(chunks, N, part, c, c < N);
+  if (threadIdx.y == 0 && c < N) out[c] = s;
 }
 
 static constexpr int kColRows = 64;
+constexpr int kLnBwdRows = 16;
+
+// bf16 [R x ld] column sums, 8 columns (one 16-byte load) per thread.
+__global__ void colsum_partial_vec(int R, int N8, const bf16* __restrict__ x, int64_t ld,
+                                   int rows_per, float* __restrict__ part) {
+  const int c8 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c8 * 8 >= N8) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(R, r0 + rows_per);
+  float acc[8] = {};
+  for (int r = r0; r < r1; ++r) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + (int64_t)r * ld + 8 * c8), f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += f[e];
+  }
+  float4* o = reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * N8 + 8 * c8);
+  o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
 
 template <class XT>
 static void colsum_launch(int R, int N, const XT* x, int64_t ld, const int* sel,
                           int want, float* out, float* scratch, cudaStream_t s) {
+  if constexpr (std::is_same<XT, bf16>::value) {
+    const int N8 = (N + 7) & ~7;
+    if (!sel && ld % 8 == 0 && ld >= N8 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && R > 0) {
+      const int rows_per = 32;
+      const int chunks = (R + rows_per - 1) / rows_per;
+      dim3 g1((N8 / 8 + 127) / 128, chunks);
+      colsum_partial_vec<<<g1, 128, 0, s>>>(R, N8, x, ld, rows_per, scratch);
+      LAUNCH_CHECK();
+      colsum_final_strided<<<FINAL_LAUNCH(N), 0, s>>>(chunks, N8, N, scratch, out);
+      LAUNCH_CHECK();
+      count_launch(2);
+      return;
+    }
+  }
   const int chunks = (R + kColRows - 1) / kColRows;
   if (chunks == 0) {
     HP_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * N, s));
@@ -159,7 +234,7 @@ static void colsum_launch(int R, int N, const XT* x, int64_t ld, const int* sel,
   dim3 g1((N + 127) / 128, chunks);
   colsum_partial_kernel<XT><<<g1, 128, 0, s>>>(R, N, x, ld, sel, want, kColRows, scratch);
   LAUNCH_CHECK();
-  colsum_final_kernel<<<(N + 127) / 128, 128, 0, s>>>(chunks, N, scratch, out);
+  colsum_final_kernel<<<FINAL_LAUNCH(N), 0, s>>>(chunks, N, scratch, out);
   LAUNCH_CHECK();
   count_launch(2);
 }
@@ -179,6 +254,13 @@ void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
 void col_sum(int R, int N, const void* x, int64_t ld, DType t, float* out,
              float* scratch, cudaStream_t s) {
   DISPATCH1(t, X, colsum_launch<X>(R, N, (const X*)x, ld, nullptr, 0, out, scratch, s));
+}
+
+size_t colsum_scratch_floats(int R, int N) {
+  const size_t a = (size_t)((R + kColRows - 1) / kColRows) * (N + 8) * 2;   // scalar path (+LN 2d)
+  const size_t b = (size_t)((R + 31) / 32) * (((N + 7) & ~7));             // vector path
+  const size_t c = (size_t)((R + kLnBwdRows - 1) / kLnBwdRows) * 3 * N;    // LN bwd partials
+  return std::max(a, std::max(b, c)) + 3 * (size_t)N + 64;
 }
 
 // ------------------------------------------------------------------ LayerNorm
@@ -253,21 +335,176 @@ __global__ void ln_pgrad_partial(int T, int d, const DYT* __restrict__ dy, const
   part[(int64_t)blockIdx.y * 2 * d + d + c] = ab;
 }
 
+// ---- vectorized bf16 LayerNorm (d = 256 * NV): each lane keeps NV x 8
+// elements of its row in registers; 16-byte loads/stores.
+template <int NV>
+__global__ void __launch_bounds__(256) ln_fwd_vec(int T, const bf16* __restrict__ x,
+                                                  const float* __restrict__ g,
+                                                  const float* __restrict__ bta, bf16* __restrict__ y,
+                                                  float* __restrict__ mean, float* __restrict__ rstd) {
+  constexpr int d = 256 * NV;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  float v[NV * 8];
+  const bf16* xr = x + (int64_t)t * d;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) unpack8(*reinterpret_cast<const uint4*>(xr + 8 * lane + 256 * j), v + 8 * j);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV * 8; ++i) s += v[i];
+  const float mu = warp_sum(s) * (1.f / d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV * 8; ++i) q += (v[i] - mu) * (v[i] - mu);
+  const float rs = rsqrtf(warp_sum(q) * (1.f / d) + kLnEps);
+  bf16* yr = y + (int64_t)t * d;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c0 = 8 * lane + 256 * j;
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = (v[8 * j + e] - mu) * rs * __ldg(g + c0 + e) + __ldg(bta + c0 + e);
+    *reinterpret_cast<uint4*>(yr + c0) = pack8(o);
+  }
+  if (lane == 0) {
+    mean[t] = mu;
+    rstd[t] = rs;
+  }
+}
+
+// dx = LN'(dy) plus per-block partial column sums of dy*xhat (dgamma), dy
+// (dbeta) and dx (the bias gradient of the layer that produced x, which the
+// residual makes equal to colsum(dx)).  Deterministic: fixed reduction order.
+template <int NV>
+__global__ void __launch_bounds__(256) ln_bwd_vec(int T, const bf16* __restrict__ dy,
+                                                  const bf16* __restrict__ x,
+                                                  const float* __restrict__ mean,
+                                                  const float* __restrict__ rstd,
+                                                  const float* __restrict__ g, bf16* __restrict__ dx,
+                                                  float* __restrict__ part) {
+  constexpr int d = 256 * NV;
+  extern __shared__ float red[];  // [8 warps][3][d]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float ag[NV * 8], ab[NV * 8], ax[NV * 8];
+#pragma unroll
+  for (int i = 0; i < NV * 8; ++i) ag[i] = ab[i] = ax[i] = 0.f;
+  float gg[NV * 8];
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) gg[8 * j + e] = __ldg(g + 8 * lane + 256 * j + e);
+  for (int rr = w; rr < kLnBwdRows; rr += 8) {
+    const int t = blockIdx.x * kLnBwdRows + rr;
+    if (t >= T) break;
+    const float mu = mean[t], rs = rstd[t];
+    float xh[NV * 8], gy[NV * 8];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      unpack8(*reinterpret_cast<const uint4*>(x + (int64_t)t * d + 8 * lane + 256 * j), xh + 8 * j);
+      unpack8(*reinterpret_cast<const uint4*>(dy + (int64_t)t * d + 8 * lane + 256 * j), gy + 8 * j);
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV * 8; ++i) {
+      xh[i] = (xh[i] - mu) * rs;
+      const float dxh = gy[i] * gg[i];
+      s1 += dxh;
+      s2 += dxh * xh[i];
+      ag[i] += gy[i] * xh[i];
+      ab[i] += gy[i];
+    }
+    s1 = warp_sum(s1) * (1.f / d);
+    s2 = warp_sum(s2) * (1.f / d);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = 8 * j + e;
+        o[e] = rs * (gy[i] * gg[i] - (s1 + xh[i] * s2));
+      }
+      const uint4 u = pack8(o);
+      *reinterpret_cast<uint4*>(dx + (int64_t)t * d + 8 * lane + 256 * j) = u;
+      float r[8];
+      unpack8(u, r);  // sum what the next kernel will read
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ax[8 * j + e] += r[e];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = 8 * lane + 256 * j + e;
+      red[(w * 3 + 0) * d + c] = ag[8 * j + e];
+      red[(w * 3 + 1) * d + c] = ab[8 * j + e];
+      red[(w * 3 + 2) * d + c] = ax[8 * j + e];
+    }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 3 * d; c += blockDim.x) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += red[k * 3 * d + c];
+    part[(int64_t)blockIdx.x * 3 * d + c] = acc;
+  }
+}
+
+// out0/out1/out2 = column sums of the [chunks x 3d] partials
+__global__ void ln_part_final(int chunks, int d, const float* __restrict__ part, float* __restrict__ dg,
+                              float* __restrict__ db, float* __restrict__ dbias) {
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const float acc = final_sum(chunks, 3 * d, part, c, c < 3 * d);
+  if (threadIdx.y != 0 || c >= 3 * d) return;
+  if (c < d) dg[c] = acc;
+  else if (c < 2 * d) db[c - d] = acc;
+  else if (dbias) dbias[c - 2 * d] = acc;
+}
+
 void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
                    const float* bta, void* y, DType yt, float* mean, float* rstd,
                    cudaStream_t s) {
   if (T == 0) return;
-  DISPATCH1(xt, X, DISPATCH1(yt, Y,
-      ln_fwd_kernel<X, Y><<<(T + 7) / 8, 256, 0, s>>>(T, d, (const X*)x, g, bta, (Y*)y, mean, rstd)));
+  const int grid = (T + 7) / 8;
+  if (xt == DType::bf16 && yt == DType::bf16 && d % 256 == 0 && d <= 1024) {
+    switch (d / 256) {
+      case 1: ln_fwd_vec<1><<<grid, 256, 0, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 2: ln_fwd_vec<2><<<grid, 256, 0, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 3: ln_fwd_vec<3><<<grid, 256, 0, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      default: ln_fwd_vec<4><<<grid, 256, 0, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+    }
+  } else {
+    DISPATCH1(xt, X, DISPATCH1(yt, Y,
+        ln_fwd_kernel<X, Y><<<grid, 256, 0, s>>>(T, d, (const X*)x, g, bta, (Y*)y, mean, rstd)));
+  }
   LAUNCH_CHECK();
   count_launch();
 }
 
 void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
                    DType xt, const float* mean, const float* rstd, const float* g,
-                   void* dx, DType dxt, float* dg, float* db, float* scratch,
+                   void* dx, DType dxt, float* dg, float* db, float* dbias, float* scratch,
                    cudaStream_t s) {
   if (T == 0) return;
+  if (dyt == DType::bf16 && xt == DType::bf16 && dxt == DType::bf16 && d % 256 == 0 && d <= 1024) {
+    const int chunks = (T + kLnBwdRows - 1) / kLnBwdRows;
+    const size_t sm = sizeof(float) * 8 * 3 * d;
+    switch (d / 256) {
+#define LNB(NV)                                                                                 \
+  case NV:                                                                                      \
+    HP_CUDA(cudaFuncSetAttribute(ln_bwd_vec<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    ln_bwd_vec<NV><<<chunks, 256, sm, s>>>(T, (const bf16*)dy, (const bf16*)x, mean, rstd, g,   \
+                                          (bf16*)dx, scratch);                                  \
+    break;
+      LNB(1) LNB(2) LNB(3) default: LNB(4)
+#undef LNB
+    }
+    LAUNCH_CHECK();
+    ln_part_final<<<FINAL_LAUNCH(3 * d), 0, s>>>(chunks, d, scratch, dg, db, dbias);
+    LAUNCH_CHECK();
+    count_launch(2);
+    return;
+  }
   DISPATCH1(dyt, DY, DISPATCH1(xt, X, {
     DISPATCH1(dxt, DX, ln_bwd_kernel<DY, X, DX><<<(T + 7) / 8, 256, 0, s>>>(
         T, d, (const DY*)dy, (const X*)x, mean, rstd, g, (DX*)dx));
@@ -277,11 +514,13 @@ void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
         T, d, (const DY*)dy, (const X*)x, mean, rstd, kColRows, scratch);
     LAUNCH_CHECK();
     // final: rows of 2d partials -> dg | db
-    colsum_final_kernel<<<(2 * d + 127) / 128, 128, 0, s>>>(chunks, 2 * d, scratch, scratch + (int64_t)chunks * 2 * d);
+    colsum_final_kernel<<<FINAL_LAUNCH(2 * d), 0, s>>>(chunks, 2 * d, scratch, scratch + (int64_t)chunks * 2 * d);
     LAUNCH_CHECK();
     HP_CUDA(cudaMemcpyAsync(dg, scratch + (int64_t)chunks * 2 * d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
     HP_CUDA(cudaMemcpyAsync(db, scratch + (int64_t)chunks * 2 * d + d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
     count_launch(3);
+    if (dbias)
+      DISPATCH1(dxt, DX, colsum_launch<DX>(T, d, (const DX*)dx, d, nullptr, 0, dbias, scratch, s));
   }));
 }
 
@@ -403,6 +642,7 @@ __global__ void attn_bwd_kernel(const int* __restrict__ cu, int H, int dk,
   load_head(K, ldh, n, n4, dk, qkv, row0, ldq, d + h * dk);
   load_head(V, ldh, n, n4, dk, qkv, row0, ldq, 2 * d + h * dk);
   load_head(G, ldh, n, n4, dk, dO, row0, d, h * dk);
+  __syncthreads();  // D below reads rows other warps loaded
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int i = w; i < n; i += nw) {
     float acc = 0.f;
@@ -665,41 +905,87 @@ __device__ __forceinline__ uint64_t shadow_index(const uint64_t* seg, int nseg, 
   return cols == pcols ? soff + local : soff + (local / cols) * pcols + local % cols;
 }
 
-__global__ void adam_kernel(AdamArgs a) {
-  if (a.flags && *a.flags) return;  // numeric error: leave parameters untouched
-  const double sc = a.inv_w64 ? *a.inv_w64 : 1.0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  bf16* sh = (bf16*)a.shadow;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-    // g /= total weight in f64, then cast to T (engine.hpp:151, optim.hpp:135)
-    const float g = a.inv_w64 ? (float)((double)a.g[i] * sc) : a.g[i];
-    if (!isfinite(g)) {
-      *a.bad = 1;
-      continue;
-    }
-    float p = a.p[i];
-    if (a.sgd) {
-      p = __fsub_rn(p, __fmul_rn(a.lr, g));
-    } else {
-      // explicit round-to-nearest ops: no FMA contraction, matching the
-      // reference's -ffp-contract=off scalar loop bit for bit
-      const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(__fsub_rn(1.f, a.b1), g));
-      const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]),
-                                __fmul_rn(__fsub_rn(1.f, a.b2), __fmul_rn(g, g)));
-      a.m[i] = m;
-      a.v[i] = v;
-      const float mh = __fmul_rn(m, a.c1);
-      const float vh = __fmul_rn(v, a.c2);
-      p = __fsub_rn(p, __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
-    }
-    a.p[i] = p;
-    if (sh) sh[shadow_index(a.seg_table, a.nseg, i)] = __float2bfloat16_rn(p);
+__device__ __forceinline__ void adam_one(const AdamArgs& a, float& p, float& m, float& v, float g) {
+  if (a.sgd) {
+    p = __fsub_rn(p, __fmul_rn(a.lr, g));
+    return;
   }
+  // explicit round-to-nearest ops: no FMA contraction, matching the
+  // reference's -ffp-contract=off scalar loop bit for bit
+  m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(__fsub_rn(1.f, a.b1), g));
+  v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(__fsub_rn(1.f, a.b2), __fmul_rn(g, g)));
+  const float mh = __fmul_rn(m, a.c1);
+  const float vh = __fmul_rn(v, a.c2);
+  p = __fsub_rn(p, __fmul_rn(a.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps))));
+}
+
+// One CTA per work item.  float4 I/O when the item is 16-byte aligned.
+__global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
+  if (a.flags && *a.flags) return;  // numeric error: leave parameters untouched
+  const uint64_t* it = a.items + 5 * blockIdx.x;
+  const uint64_t lo = it[0], n = it[1], slo = it[2], cols = it[3], pcols = it[4];
+  const bool scale = a.inv_w64 != nullptr;
+  const double sc = scale ? *a.inv_w64 : 1.0;
+  bf16* sh = (bf16*)a.shadow;
+  const bool contig = cols == pcols;
+  auto sidx = [&](uint64_t local) {
+    return contig ? slo + local : slo + (local / cols) * pcols + local % cols;
+  };
+  int bad = 0;
+  if ((lo & 3) == 0 && (!sh || !contig || (slo & 3) == 0)) {
+    const uint64_t n4 = n & ~uint64_t(3);
+    for (uint64_t i = 4 * threadIdx.x; i < n4; i += 4 * blockDim.x) {
+      float4 p = *reinterpret_cast<const float4*>(a.p + lo + i);
+      float4 m = *reinterpret_cast<const float4*>(a.m + lo + i);
+      float4 v = *reinterpret_cast<const float4*>(a.v + lo + i);
+      float4 g = *reinterpret_cast<const float4*>(a.g + lo + i);
+      float* pp = &p.x; float* mm = &m.x; float* vv = &v.x; float* gg = &g.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        // g /= total weight in f64, then cast to T (engine.hpp:151, optim.hpp:135)
+        const float ge = scale ? (float)((double)gg[e] * sc) : gg[e];
+        if (!isfinite(ge)) { bad = 1; continue; }
+        adam_one(a, pp[e], mm[e], vv[e], ge);
+      }
+      *reinterpret_cast<float4*>(a.p + lo + i) = p;
+      *reinterpret_cast<float4*>(a.m + lo + i) = m;
+      *reinterpret_cast<float4*>(a.v + lo + i) = v;
+      if (sh) {
+        if (contig) {
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(p.x, p.y), h1 = __floats2bfloat162_rn(p.z, p.w);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&h0);
+          u.y = *reinterpret_cast<uint32_t*>(&h1);
+          *reinterpret_cast<uint2*>(sh + slo + i) = u;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sh[sidx(i + e)] = __float2bfloat16_rn(pp[e]);
+        }
+      }
+    }
+    for (uint64_t i = n4 + threadIdx.x; i < n; i += blockDim.x) {
+      const float ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+      if (!isfinite(ge)) { bad = 1; continue; }
+      float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
+      adam_one(a, p, m, v, ge);
+      a.p[lo + i] = p; a.m[lo + i] = m; a.v[lo + i] = v;
+      if (sh) sh[sidx(i)] = __float2bfloat16_rn(p);
+    }
+  } else {
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const float ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+      if (!isfinite(ge)) { bad = 1; continue; }
+      float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
+      adam_one(a, p, m, v, ge);
+      a.p[lo + i] = p; a.m[lo + i] = m; a.v[lo + i] = v;
+      if (sh) sh[sidx(i)] = __float2bfloat16_rn(p);
+    }
+  }
+  if (bad) *a.bad = 1;
 }
 void adam_update(const AdamArgs& a, cudaStream_t s) {
-  if (a.n == 0) return;
-  const int blocks = (int)std::min<uint64_t>((a.n + 255) / 256, 148 * 8);
-  adam_kernel<<<blocks, 256, 0, s>>>(a);
+  if (a.nitems == 0) return;
+  adam_kernel<<<a.nitems, 256, 0, s>>>(a);
   LAUNCH_CHECK();
   count_launch();
 }

@@ -52,7 +52,8 @@ void gemm_simt(const GemmArgs& g, cudaStream_t s);
 bool gemm_tc_supported(const GemmArgs& g);
 void gemm_tc(const GemmArgs& g, cudaStream_t s);
 void gemm_tc_force(int mode);  // test hook: 0 auto, 1 never tcgen05
-void gemm_tc_set_bn(int bn);   // test hook: 0 heuristic, 128 or 256
+void gemm_tc_set_bn(int bn);   // test hook: 0 heuristic, 128, 192 or 256
+void gemm_tc_set_splits(int s);  // test hook: 0 heuristic, else forced split-K
 
 // Device batch (one rank batch, SoA int32), see engine.cpp.
 struct DevBatch {
@@ -77,11 +78,15 @@ void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
 void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
                    const float* bta, void* y, DType yt, float* mean, float* rstd,
                    cudaStream_t s);
-// dx = LN'(dy); dg/db column sums written (not accumulated) to dg, db.
+// dx = LN'(dy); dg/db column sums written (not accumulated) to dg, db; when
+// dbias is given it receives colsum(dx) (the bias gradient of the linear whose
+// output, through the residual, fed this LayerNorm).
 void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
                    DType xt, const float* mean, const float* rstd, const float* g,
-                   void* dx, DType dxt, float* dg, float* db, float* scratch,
+                   void* dx, DType dxt, float* dg, float* db, float* dbias, float* scratch,
                    cudaStream_t s);
+// scratch floats the column-sum kernels need for an R x N reduction
+size_t colsum_scratch_floats(int R, int N);
 
 // Varlen multi-head self-attention over packed QKV [T x 3d] (columns:
 // q heads | k heads | v heads, dk each).  O [T x d], lse [H x T].
@@ -90,6 +95,13 @@ void attention_fwd(const DevBatch& b, int H, int dk, const void* qkv, void* o,
 void attention_bwd(const DevBatch& b, int H, int dk, const void* qkv,
                    const void* o, const void* dO, const float* lse, void* dqkv,
                    DType t, cudaStream_t s);
+
+// Tensor-core (mma.sync bf16) attention for dk == 64, sequences <= 128.
+bool attention_mma_supported(int dk, int max_seq);
+void attention_fwd_mma(const DevBatch& b, int H, const void* qkv, void* o, float* lse,
+                       cudaStream_t s);
+void attention_bwd_mma(const DevBatch& b, int H, const void* qkv, const void* o, const void* dO,
+                       const float* lse, void* dqkv, cudaStream_t s);
 
 // rows of src selected by idx -> dst (dst[r] = src[idx[r]]).
 void gather_rows(int R, int d, const int* idx, const void* src, void* dst, DType t,
@@ -134,7 +146,10 @@ struct AdamArgs {
   const int* flags;       // skip everything when *flags != 0
   int* bad;               // set to 1 on a non-finite gradient
   int sgd;
-  void* shadow; const uint64_t* seg_table; int nseg;
+  void* shadow;
+  // work items [nitems][5] = {flat_lo, count, shadow_lo, cols, pcols}; one
+  // CTA per item (see Engine: contiguous runs merged, <= 64K elements each)
+  const uint64_t* items; int nitems;
 };
 void adam_update(const AdamArgs& a, cudaStream_t s);
 

@@ -100,7 +100,7 @@ def _check(res, dtype, K):
 
 @pytest.mark.parametrize("a_trans", [0, 1])
 @pytest.mark.parametrize("b_trans", [0, 1])
-@pytest.mark.parametrize("bn", [128, 256])
+@pytest.mark.parametrize("bn", [128, 192, 256])
 def test_tc_gemm_layouts(a_trans, b_trans, bn):
     res = run_gemm(384, 512, 320, torch.bfloat16, a_trans, b_trans, path=2, bn=bn, c_dtype=torch.float32)
     _check(res, torch.bfloat16, 320)
@@ -180,3 +180,66 @@ def test_adam_bit_exact_vs_reference_scalar():
     L.call("hp_debug_adam", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(torch.from_numpy(g).cuda()), n,
            0.1, 0.9, 0.98, 1e-9, 1.0, 1.0, 1)
     assert np.array_equal(dp.cpu().numpy().view(np.uint32), p.view(np.uint32))
+
+
+def _attn_ref(qkv, cu, H, dk):
+    """torch fp32 reference of the varlen attention forward/backward."""
+    T = qkv.shape[0]
+    d = H * dk
+    q = qkv[:, :d].float().reshape(T, H, dk).requires_grad_(True)
+    k = qkv[:, d:2 * d].float().reshape(T, H, dk).requires_grad_(True)
+    v = qkv[:, 2 * d:].float().reshape(T, H, dk).requires_grad_(True)
+    outs = []
+    for i in range(len(cu) - 1):
+        a, b = cu[i], cu[i + 1]
+        s = torch.einsum("qhd,khd->hqk", q[a:b], k[a:b]) / dk ** 0.5
+        p = torch.softmax(s, dim=-1)
+        outs.append(torch.einsum("hqk,khd->qhd", p, v[a:b]))
+    o = torch.cat(outs).reshape(T, d)
+    return o, (q, k, v)
+
+
+@pytest.mark.parametrize("path,dtype,dk", [(2, torch.bfloat16, 64), (1, torch.bfloat16, 64),
+                                           (1, torch.float32, 32), (1, torch.float32, 64),
+                                           (1, torch.bfloat16, 32)])
+def test_attention_varlen_fwd_bwd(path, dtype, dk):
+    L = _lib()
+    H = 3
+    lens = [128, 1, 17, 63, 64, 100, 5]
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(cu[-1])
+    g = torch.Generator(device="cpu").manual_seed(1)
+    qkv = (torch.randn(T, 3 * H * dk, generator=g) * 1.5).to("cuda", dtype)
+    dO = torch.randn(T, H * dk, generator=g).to("cuda", dtype)
+    o = torch.zeros(T, H * dk, device="cuda", dtype=dtype)
+    lse = torch.zeros(H, T, device="cuda")
+    dqkv = torch.zeros_like(qkv)
+    dcu = torch.from_numpy(cu).cuda()
+    L.call("hp_debug_attention", len(lens), _ptr(dcu), T, H, dk, int(dtype == torch.bfloat16),
+           _ptr(qkv), _ptr(o), _ptr(lse), _ptr(dO), _ptr(dqkv), path)
+    ref, (q, k, v) = _attn_ref(qkv, cu.tolist(), H, dk)
+    ref.backward(dO.float())
+    dref = torch.cat([q.grad.reshape(T, -1), k.grad.reshape(T, -1), v.grad.reshape(T, -1)], 1)
+    tol = 3e-2 if dtype == torch.bfloat16 else 1e-4
+    eo = (o.float() - ref).abs().max().item() / ref.abs().max().item()
+    eg = (dqkv.float() - dref).abs().max().item() / dref.abs().max().item()
+    assert eo < tol and eg < tol, (eo, eg)
+
+
+@pytest.mark.parametrize("splits", [2, 3, 8])
+def test_tc_gemm_split_k(splits):
+    # weight-gradient shape: few output tiles, long K -> split-K reductions
+    res = run_gemm(256, 384, 2048, torch.bfloat16, 1, 0, path=2, bn=128 + 1000 * splits,
+                   c_dtype=torch.float32)
+    _check(res, torch.bfloat16, 2048)
+    res = run_gemm(128, 192, 1024, torch.bfloat16, 1, 0, path=2, bn=192 + 1000 * splits,
+                   c_dtype=torch.float32, c_group=64)
+    _check(res, torch.bfloat16, 1024)
+
+
+def test_tc_gemm_auto_heuristic_shapes():
+    # the engine's shapes at small scale: auto BN / split choice
+    for (M, N, K, at, bt, ct) in [(512, 768, 768, 0, 0, torch.bfloat16), (768, 768, 512, 1, 0, torch.float32),
+                                  (512, 2304, 768, 0, 0, torch.bfloat16), (512, 768, 2304, 0, 1, torch.bfloat16)]:
+        res = run_gemm(M, N, K, torch.bfloat16, at, bt, path=2, c_dtype=ct)
+        _check(res, torch.bfloat16, K)
