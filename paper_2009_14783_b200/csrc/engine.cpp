@@ -98,8 +98,12 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   }
   nseg_ = static_cast<int>(table_.size());
 
-  HP_CUDA(cudaStreamCreateWithFlags(&s_main_, cudaStreamNonBlocking));
-  HP_CUDA(cudaStreamCreateWithFlags(&s_comm_, cudaStreamNonBlocking));
+  // compute stream at the highest priority: the side stream's collectives and
+  // per-bucket updates fill in behind the backward GEMMs
+  int prio_lo = 0, prio_hi = 0;
+  HP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  HP_CUDA(cudaStreamCreateWithPriority(&s_main_, cudaStreamNonBlocking, prio_hi));
+  HP_CUDA(cudaStreamCreateWithPriority(&s_comm_, cudaStreamNonBlocking, prio_lo));
   HP_CUDA(cudaEventCreateWithFlags(&ev_fwd_, cudaEventDisableTiming));
   HP_CUDA(cudaEventCreateWithFlags(&ev_comm_done_, cudaEventDisableTiming));
   HP_CUDA(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming));
@@ -121,30 +125,36 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   seg_table_ = static_cast<uint64_t*>(dalloc(seg.size() * 8));
   HP_CUDA(cudaMemcpy(seg_table_, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice));
   {
-    // Adam work items: runs of parameters whose working copy is laid out
-    // contiguously are merged; every item is cut to <= 64K elements.
+    // Adam work items, per gradient bucket (each bucket is updated as soon as
+    // its reduced gradient is final): runs of parameters whose working copy
+    // is laid out contiguously are merged; every item is cut to <= 64K.
     constexpr uint64_t kChunk = 65536;
-    std::vector<std::array<uint64_t, 5>> runs;
-    for (size_t i = 0; i < table_.size(); ++i) {
-      const uint64_t lo = table_[i].offset, n = table_[i].size();
-      const uint64_t slo = bf16_ ? shadow_off_[i] : lo;
-      const uint64_t cols = table_[i].cols, pc = bf16_ ? shadow_ld_[i] : cols;
-      if (cols == pc && !runs.empty() && runs.back()[3] == runs.back()[4] &&
-          runs.back()[0] + runs.back()[1] == lo && runs.back()[2] + runs.back()[1] == slo) {
-        runs.back()[1] += n;
-      } else {
-        runs.push_back({lo, n, slo, cols == pc ? 1 : cols, cols == pc ? 1 : pc});
-      }
-    }
     std::vector<uint64_t> items;
-    for (const auto& r : runs) {
-      const bool contig = r[3] == r[4];
-      const uint64_t step = contig ? kChunk : std::max<uint64_t>(1, kChunk / r[3]) * r[3];
-      for (uint64_t o = 0; o < r[1]; o += step) {
-        const uint64_t cnt = std::min(step, r[1] - o);
-        const uint64_t srow = contig ? o : (o / r[3]) * r[4];
-        items.insert(items.end(), {r[0] + o, cnt, r[2] + srow, r[3], r[4]});
+    bucket_items_.clear();
+    for (const Bucket& bk : buckets_) {
+      std::vector<std::array<uint64_t, 5>> runs;
+      for (size_t i = bk.first_param; i <= bk.last_param; ++i) {
+        const uint64_t lo = table_[i].offset, n = table_[i].size();
+        const uint64_t slo = bf16_ ? shadow_off_[i] : lo;
+        const uint64_t cols = table_[i].cols, pc = bf16_ ? shadow_ld_[i] : cols;
+        if (cols == pc && !runs.empty() && runs.back()[3] == runs.back()[4] &&
+            runs.back()[0] + runs.back()[1] == lo && runs.back()[2] + runs.back()[1] == slo) {
+          runs.back()[1] += n;
+        } else {
+          runs.push_back({lo, n, slo, cols == pc ? 1 : cols, cols == pc ? 1 : pc});
+        }
       }
+      const int first = static_cast<int>(items.size() / 5);
+      for (const auto& r : runs) {
+        const bool contig = r[3] == r[4];
+        const uint64_t step = contig ? kChunk : std::max<uint64_t>(1, kChunk / r[3]) * r[3];
+        for (uint64_t o = 0; o < r[1]; o += step) {
+          const uint64_t cnt = std::min(step, r[1] - o);
+          const uint64_t srow = contig ? o : (o / r[3]) * r[4];
+          items.insert(items.end(), {r[0] + o, cnt, r[2] + srow, r[3], r[4]});
+        }
+      }
+      bucket_items_.push_back({first, static_cast<int>(items.size() / 5) - first});
     }
     nitems_ = static_cast<int>(items.size() / 5);
     adam_items_ = static_cast<uint64_t*>(dalloc(items.size() * 8));
@@ -215,7 +225,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     rstd0_ = static_cast<float*>(dalloc(T * 4));
   }
   hm_ = dalloc(Mm * d_ * asz_);
-  dhm_ = dalloc(Mm * d_ * asz_);
+  dhm_ = dalloc(Mm * d_ * 4);  // fp32: the vocab-long dgrad runs split-K
   z_ = static_cast<float*>(dalloc(Mm * Vp_ * 4));
   dz_ = dalloc(Mm * Vp_ * asz_);
   HP_CUDA(cudaMemset(dz_, 0, Mm * Vp_ * asz_));
@@ -444,7 +454,7 @@ void Engine::synchronize() {
   HP_CUDA(cudaStreamSynchronize(s_comm_));
 }
 
-void Engine::tstart(int cls) {
+void Engine::tstart(int cls, cudaStream_t st) {
   if (!timers_on_) return;
   TimerAcc& t = tm_[cls];
   if (t.used == t.ev.size()) {
@@ -453,12 +463,12 @@ void Engine::tstart(int cls) {
     HP_CUDA(cudaEventCreate(&b));
     t.ev.emplace_back(a, b);
   }
-  HP_CUDA(cudaEventRecord(t.ev[t.used].first, s_main_));
+  HP_CUDA(cudaEventRecord(t.ev[t.used].first, st ? st : s_main_));
 }
-void Engine::tstop(int cls, double flops, double bytes) {
+void Engine::tstop(int cls, double flops, double bytes, cudaStream_t st) {
   if (!timers_on_) return;
   TimerAcc& t = tm_[cls];
-  HP_CUDA(cudaEventRecord(t.ev[t.used].second, s_main_));
+  HP_CUDA(cudaEventRecord(t.ev[t.used].second, st ? st : s_main_));
   ++t.used;
   t.flops += flops;
   t.bytes += bytes;
@@ -601,12 +611,21 @@ void Engine::grads_ready(int first_done) {
 }
 
 void Engine::issue_bucket(size_t k) {
-  if (!comm_) return;
   const Bucket& bk = buckets_[k];
   HP_CUDA(cudaEventRecord(ev_bucket_[k], s_main_));
   HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_bucket_[k], 0));
-  HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, premul_,
-                        comm_->nccl, s_comm_));
+  if (comm_)
+    HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, premul_,
+                          comm_->nccl, s_comm_));
+  // the bucket's update runs behind the rest of backward (engine.hpp:147-153:
+  // every rank applies the identical update to the identical reduced sum)
+  AdamArgs a = adam_args_;
+  a.items = adam_items_ + 5 * static_cast<size_t>(bucket_items_[k].first);
+  a.nitems = bucket_items_[k].second;
+  tstart(TM_ADAM, s_comm_);
+  adam_update(a, s_comm_);
+  tstop(TM_ADAM, 0, 28.0 * (double)(bk.hi - bk.lo) + (bf16_ ? 2.0 * (double)(bk.hi - bk.lo) : 0.0),
+        s_comm_);
 }
 
 void Engine::backward() {
@@ -628,9 +647,9 @@ void Engine::backward() {
     gd.M = b.M; gd.N = d_; gd.K = V_; gd.ab = at_;
     gd.a = Operand{dz_, Vp_, 0, 0, 0};
     gd.b = Operand{w(iw), wld(iw), 1, 0, 0};
-    gd.c = dhm_; gd.ldc = d_; gd.ct = at_;
+    gd.c = dhm_; gd.ldc = d_; gd.ct = DType::f32;
     gemm_t(gd);
-    scatter_rows(b.M, d_, b.mrow, dhm_, dA_, at_, s_main_);
+    scatter_rows_f32(b.M, d_, b.mrow, static_cast<const float*>(dhm_), dA_, at_, s_main_);
   } else {
     HP_CUDA(cudaMemsetAsync(gp(iw), 0, sizeof(float) * (size_t)(d_ + 1) * V_, s_main_));
   }
@@ -776,6 +795,26 @@ void Engine::round_async(int dummy, double lr) {
   }
   finalize_weight(d_lw_, inv_w_, inv_w64_, flags_, sw);
 
+  // one identical update on every rank (engine.hpp:147-153, optim.hpp:107-146),
+  // issued per bucket on the side stream as the buckets complete
+  ++adam_t_;
+  const double c1 = 1.0 / (1.0 - std::pow(o_.beta1, static_cast<double>(adam_t_)));
+  const double c2 = 1.0 / (1.0 - std::pow(o_.beta2, static_cast<double>(adam_t_)));
+  AdamArgs& a = adam_args_;
+  a = AdamArgs{};
+  a.p = params_; a.m = adam_m_; a.v = adam_v_; a.g = grads_; a.n = n_;
+  a.lr = static_cast<float>(lr);
+  a.b1 = static_cast<float>(o_.beta1);
+  a.b2 = static_cast<float>(o_.beta2);
+  a.eps = static_cast<float>(o_.eps);
+  a.c1 = static_cast<float>(c1);
+  a.c2 = static_cast<float>(c2);
+  a.inv_w64 = comm_ ? nullptr : inv_w64_;  // with NCCL the scale rode PreMulSum
+  a.flags = flags_;
+  a.bad = flags_ + 1;
+  a.sgd = o_.kind == HP_OPT_SGD;
+  a.shadow = shadow_;
+
   next_bucket_ = 0;
   if (dummy) {
     // zero loss, weight and gradient (engine.hpp:141-142)
@@ -791,32 +830,9 @@ void Engine::round_async(int dummy, double lr) {
     grads_ready(0);
     capture_ = true;
   }
-  if (comm_) {
-    HP_CUDA(cudaEventRecord(ev_comm_done_, s_comm_));
-    HP_CUDA(cudaStreamWaitEvent(s_main_, ev_comm_done_, 0));
-  }
-  // one identical update on every rank (engine.hpp:147-153, optim.hpp:107-146)
-  ++adam_t_;
-  const double c1 = 1.0 / (1.0 - std::pow(o_.beta1, static_cast<double>(adam_t_)));
-  const double c2 = 1.0 / (1.0 - std::pow(o_.beta2, static_cast<double>(adam_t_)));
-  AdamArgs a{};
-  a.p = params_; a.m = adam_m_; a.v = adam_v_; a.g = grads_; a.n = n_;
-  a.lr = static_cast<float>(lr);
-  a.b1 = static_cast<float>(o_.beta1);
-  a.b2 = static_cast<float>(o_.beta2);
-  a.eps = static_cast<float>(o_.eps);
-  a.c1 = static_cast<float>(c1);
-  a.c2 = static_cast<float>(c2);
-  a.inv_w64 = comm_ ? nullptr : inv_w64_;  // with NCCL the scale rode PreMulSum
-  a.flags = flags_;
-  a.bad = flags_ + 1;
-  a.sgd = o_.kind == HP_OPT_SGD;
-  a.shadow = shadow_;
-  a.items = adam_items_;
-  a.nitems = nitems_;
-  tstart(TM_ADAM);
-  adam_update(a, s_main_);
-  tstop(TM_ADAM, 0, 28.0 * (double)n_ + (bf16_ ? 2.0 * (double)n_ : 0.0));
+  // the round ends when the last bucket's update has landed
+  HP_CUDA(cudaEventRecord(ev_comm_done_, s_comm_));
+  HP_CUDA(cudaStreamWaitEvent(s_main_, ev_comm_done_, 0));
   ++step_;
   HP_CUDA(cudaMemcpyAsync(h_lw_, d_lw_, 4 * 8, cudaMemcpyDeviceToHost, s_main_));
   HP_CUDA(cudaMemcpyAsync(h_flags_, flags_, 2 * 4, cudaMemcpyDeviceToHost, s_main_));

@@ -63,8 +63,8 @@ class Engine {
   float* pp(int idx) const { return params_ + table_[idx].offset; }
   int pidx(const std::string& name) const;
   void gemm_t(const GemmArgs& g);
-  void tstart(int cls);
-  void tstop(int cls, double flops, double bytes);
+  void tstart(int cls, cudaStream_t st = nullptr);
+  void tstop(int cls, double flops, double bytes, cudaStream_t st = nullptr);
   void forward(bool need_grad_state);
   void backward();
   void grads_ready(int first_done_param);
@@ -150,6 +150,8 @@ class Engine {
   };
   std::array<TimerAcc, TM_COUNT> tm_;
   std::array<cudaEvent_t, 8> marks_{};
+  AdamArgs adam_args_{};
+  std::vector<std::pair<int, int>> bucket_items_;  // [first item, count] per bucket
 };
 
 }  // namespace hp

@@ -181,7 +181,7 @@ __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c
 __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float* v) {
   if (m >= p.M) return;
   const bool inb = n + 32 <= p.N;
-  const bool full = inb && p.vec;
+  const bool full = inb && p.vec == 1;
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
   const int64_t co = p.c_group ? (n / p.c_group) * p.c_gstride + (int64_t)m * p.ldc + n % p.c_group
@@ -287,6 +287,20 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
           o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
         }
         reinterpret_cast<float4*>(c)[q] = o;
+      }
+    } else if (inb && p.vec == 2 && !p.accumulate) {
+      // rows only 8-byte aligned (e.g. d(mlm.w) with ld = V = 30522)
+      if ((reinterpret_cast<uintptr_t>(c) & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          reinterpret_cast<float4*>(c)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      } else {
+        reinterpret_cast<float2*>(c)[0] = make_float2(v[0], v[1]);
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+          reinterpret_cast<float4*>(c + 2)[q] =
+              make_float4(v[2 + 4 * q], v[3 + 4 * q], v[4 + 4 * q], v[5 + 4 * q]);
+        reinterpret_cast<float2*>(c + 30)[0] = make_float2(v[30], v[31]);
       }
     } else {
 #pragma unroll
@@ -557,13 +571,18 @@ bool gemm_tc_supported(const GemmArgs& g) {
   return true;
 }
 
-static bool epilogue_vec_ok(const GemmArgs& g) {
+// 1: every output row 16-byte aligned (full vector epilogue); 2: fp32 rows
+// only 8-byte aligned (float2 + float4 stores, plain stores only); 0: scalar.
+static int epilogue_vec_ok(const GemmArgs& g) {
   const int64_t elem = g.ct == DType::f32 ? 4 : 2;
-  if (!aligned16(g.c) || (g.ldc * elem) % 16) return false;
-  if (g.c_group && (g.c_gstride * elem) % 16) return false;
-  if (g.resid && ((g.ld_resid * elem) % 16 || !aligned16(g.resid))) return false;
-  if (g.aux && !aligned16(g.aux)) return false;
-  return true;
+  if (g.resid && ((g.ld_resid * elem) % 16 || !aligned16(g.resid))) return 0;
+  if (g.aux && !aligned16(g.aux)) return 0;
+  if (g.c_group && (g.c_gstride * elem) % 16) return 0;
+  if (aligned16(g.c) && (g.ldc * elem) % 16 == 0) return 1;
+  if (g.ct == DType::f32 && !g.c_group && (reinterpret_cast<uintptr_t>(g.c) & 7) == 0 &&
+      g.ldc % 2 == 0)
+    return 2;
+  return 0;
 }
 
 template <int BN>
@@ -662,7 +681,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.c_f32 = g.ct == DType::f32;
   p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias; p.act = g.act;
   p.aux = g.aux; p.resid = g.resid; p.ld_resid = g.ld_resid;
-  p.vec = epilogue_vec_ok(g) ? 1 : 0;
+  p.vec = epilogue_vec_ok(g);
   if (splits > 1) {
     // partial sums are reduced into C: clear the output region first
     if (g.c_group) {

@@ -189,7 +189,7 @@ __global__ void colsum_final_kernel(int chunks, int N, const float* __restrict__
 }
 
 static constexpr int kColRows = 64;
-constexpr int kLnBwdRows = 16;
+constexpr int kLnBwdRows = 32;
 
 // bf16 [R x ld] column sums, 8 columns (one 16-byte load) per thread.
 __global__ void colsum_partial_vec(int R, int N8, const bf16* __restrict__ x, int64_t ld,
@@ -198,7 +198,20 @@ __global__ void colsum_partial_vec(int R, int N8, const bf16* __restrict__ x, in
   if (c8 * 8 >= N8) return;
   const int r0 = blockIdx.y * rows_per, r1 = min(R, r0 + rows_per);
   float acc[8] = {};
-  for (int r = r0; r < r1; ++r) {
+  int r = r0;
+  for (; r + 4 <= r1; r += 4) {  // four independent 16-byte loads in flight
+    uint4 u[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) u[q] = *reinterpret_cast<const uint4*>(x + (int64_t)(r + q) * ld + 8 * c8);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float f[8];
+      unpack8(u[q], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += f[e];
+    }
+  }
+  for (; r < r1; ++r) {
     float f[8];
     unpack8(*reinterpret_cast<const uint4*>(x + (int64_t)r * ld + 8 * c8), f);
 #pragma unroll
@@ -348,8 +361,15 @@ __global__ void __launch_bounds__(256) ln_fwd_vec(int T, const bf16* __restrict_
   const int lane = threadIdx.x & 31;
   float v[NV * 8];
   const bf16* xr = x + (int64_t)t * d;
+  float4 gq[NV * 2], bq[NV * 2];  // gamma/beta issued with the row loads
 #pragma unroll
-  for (int j = 0; j < NV; ++j) unpack8(*reinterpret_cast<const uint4*>(xr + 8 * lane + 256 * j), v + 8 * j);
+  for (int j = 0; j < NV; ++j) {
+    unpack8(*reinterpret_cast<const uint4*>(xr + 8 * lane + 256 * j), v + 8 * j);
+    gq[2 * j] = __ldg(reinterpret_cast<const float4*>(g + 8 * lane + 256 * j));
+    gq[2 * j + 1] = __ldg(reinterpret_cast<const float4*>(g + 8 * lane + 256 * j) + 1);
+    bq[2 * j] = __ldg(reinterpret_cast<const float4*>(bta + 8 * lane + 256 * j));
+    bq[2 * j + 1] = __ldg(reinterpret_cast<const float4*>(bta + 8 * lane + 256 * j) + 1);
+  }
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < NV * 8; ++i) s += v[i];
@@ -362,9 +382,11 @@ __global__ void __launch_bounds__(256) ln_fwd_vec(int T, const bf16* __restrict_
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int c0 = 8 * lane + 256 * j;
+    const float* gg = reinterpret_cast<const float*>(&gq[2 * j]);
+    const float* bb = reinterpret_cast<const float*>(&bq[2 * j]);
     float o[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = (v[8 * j + e] - mu) * rs * __ldg(g + c0 + e) + __ldg(bta + c0 + e);
+    for (int e = 0; e < 8; ++e) o[e] = (v[8 * j + e] - mu) * rs * gg[e] + bb[e];
     *reinterpret_cast<uint4*>(yr + c0) = pack8(o);
   }
   if (lane == 0) {
@@ -391,9 +413,12 @@ __global__ void __launch_bounds__(256) ln_bwd_vec(int T, const bf16* __restrict_
   for (int i = 0; i < NV * 8; ++i) ag[i] = ab[i] = ax[i] = 0.f;
   float gg[NV * 8];
 #pragma unroll
-  for (int j = 0; j < NV; ++j)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) gg[8 * j + e] = __ldg(g + 8 * lane + 256 * j + e);
+  for (int j = 0; j < NV; ++j) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(g + 8 * lane + 256 * j));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(g + 8 * lane + 256 * j) + 1);
+    gg[8 * j + 0] = a.x; gg[8 * j + 1] = a.y; gg[8 * j + 2] = a.z; gg[8 * j + 3] = a.w;
+    gg[8 * j + 4] = b.x; gg[8 * j + 5] = b.y; gg[8 * j + 6] = b.z; gg[8 * j + 7] = b.w;
+  }
   for (int rr = w; rr < kLnBwdRows; rr += 8) {
     const int t = blockIdx.x * kLnBwdRows + rr;
     if (t >= T) break;
@@ -737,6 +762,22 @@ void gather_rows(int R, int d, const int* idx, const void* src, void* dst, DType
   LAUNCH_CHECK();
   count_launch();
 }
+template <class T>
+__global__ void scatter_f32_kernel(int R, int d, const int* __restrict__ idx,
+                                   const float* __restrict__ src, T* __restrict__ dst) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= R) return;
+  const int lane = threadIdx.x & 31;
+  T* o = dst + (int64_t)idx[r] * d;
+  for (int c = lane; c < d; c += 32) o[c] = fromf<T>(src[(int64_t)r * d + c]);
+}
+void scatter_rows_f32(int R, int d, const int* idx, const float* src, void* dst, DType t,
+                      cudaStream_t s) {
+  if (R == 0) return;
+  DISPATCH1(t, X, scatter_f32_kernel<X><<<(R + 7) / 8, 256, 0, s>>>(R, d, idx, src, (X*)dst));
+  LAUNCH_CHECK();
+  count_launch();
+}
 void scatter_rows(int R, int d, const int* idx, const void* src, void* dst,
                   DType t, cudaStream_t s) {
   if (R == 0) return;
@@ -747,23 +788,40 @@ void scatter_rows(int R, int d, const int* idx, const void* src, void* dst,
 
 // ------------------------------------------------------------------ ls_ce
 template <class DZT>
-__global__ void ls_ce_kernel(int V, const float* __restrict__ z, int64_t ldz,
+__global__ void __launch_bounds__(512) ls_ce_kernel(int V, const float* __restrict__ z, int64_t ldz,
                              const int* __restrict__ target, float eps,
                              float* __restrict__ row_loss, DZT* __restrict__ dz, int64_t ld_dz) {
   __shared__ float red[32];
   const int r = blockIdx.x;
   const float* zr = z + (int64_t)r * ldz;
-  float mx = -FLT_MAX, zs = 0.f;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) {
+  // one pass: running max, rescaled sum of exp, and the plain sum (for eps)
+  // fp32 parity path: accurate expf; bf16 path: fast __expf
+  auto ex = [](float x) { return std::is_same<DZT, float>::value ? expf(x) : __expf(x); };
+  float mx = -FLT_MAX, se = 0.f, zs = 0.f;
+  const int V4 = (reinterpret_cast<uintptr_t>(zr) & 15) == 0 ? (V & ~3) : 0;
+  for (int j = 4 * threadIdx.x; j < V4; j += 4 * blockDim.x) {
+    const float4 q = *reinterpret_cast<const float4*>(zr + j);
+    const float m4 = fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w));
+    if (m4 > mx) {
+      se *= ex(mx - m4);
+      mx = m4;
+    }
+    se += ex(q.x - mx) + ex(q.y - mx) + ex(q.z - mx) + ex(q.w - mx);
+    zs += (q.x + q.y) + (q.z + q.w);
+  }
+  for (int j = V4 + threadIdx.x; j < V; j += blockDim.x) {
     const float v = zr[j];
-    mx = fmaxf(mx, v);
+    if (v > mx) {
+      se *= ex(mx - v);
+      mx = v;
+    }
+    se += ex(v - mx);
     zs += v;
   }
-  mx = block_max<256>(mx, red);
-  zs = block_sum<256>(zs, red);
-  float se = 0.f;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) se += expf(zr[j] - mx);
-  se = block_sum<256>(se, red);
+  const float gmx = block_max<512>(mx, red);
+  se = block_sum<512>(mx == -FLT_MAX ? 0.f : se * ex(mx - gmx), red);
+  zs = block_sum<512>(zs, red);
+  mx = gmx;
   const int t = target[r];
   const float invV = eps / (float)V;
   if (threadIdx.x == 0) {
@@ -773,7 +831,21 @@ __global__ void ls_ce_kernel(int V, const float* __restrict__ z, int64_t ldz,
   if (dz) {
     const float inv_se = 1.f / se;
     DZT* o = dz + (int64_t)r * ld_dz;
-    for (int j = threadIdx.x; j < V; j += blockDim.x) {
+    const int V4w = (std::is_same<DZT, bf16>::value && (reinterpret_cast<uintptr_t>(o) & 7) == 0) ? V4 : 0;
+    for (int j = 4 * threadIdx.x; j < V4w; j += 4 * blockDim.x) {
+      const float4 q = *reinterpret_cast<const float4*>(zr + j);
+      float g[4] = {__expf(q.x - mx) * inv_se - invV, __expf(q.y - mx) * inv_se - invV,
+                    __expf(q.z - mx) * inv_se - invV, __expf(q.w - mx) * inv_se - invV};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (j + e == t) g[e] -= 1.f - eps;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(g[0], g[1]), h1 = __floats2bfloat162_rn(g[2], g[3]);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&h0);
+      u.y = *reinterpret_cast<uint32_t*>(&h1);
+      *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(o) + j) = u;
+    }
+    for (int j = V4w + threadIdx.x; j < V; j += blockDim.x) {
       float g = expf(zr[j] - mx) * inv_se - invV;
       if (j == t) g -= 1.f - eps;
       o[j] = fromf<DZT>(g);
@@ -785,7 +857,7 @@ void ls_ce(int R, int V, const float* z, int64_t ldz, const int* target,
            float eps, float* row_loss, void* dz, DType dzt, int64_t ld_dz,
            cudaStream_t s) {
   if (R == 0) return;
-  DISPATCH1(dzt, X, ls_ce_kernel<X><<<R, 256, 0, s>>>(V, z, ldz, target, eps, row_loss,
+  DISPATCH1(dzt, X, ls_ce_kernel<X><<<R, 512, 0, s>>>(V, z, ldz, target, eps, row_loss,
                                                      (X*)dz, ld_dz));
   LAUNCH_CHECK();
   count_launch();

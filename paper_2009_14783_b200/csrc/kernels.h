@@ -109,6 +109,9 @@ void gather_rows(int R, int d, const int* idx, const void* src, void* dst, DType
 // dst[idx[r]] = src[r] (rows unique), other rows untouched.
 void scatter_rows(int R, int d, const int* idx, const void* src, void* dst,
                   DType t, cudaStream_t s);
+// same with an fp32 source converted to the destination type
+void scatter_rows_f32(int R, int d, const int* idx, const float* src, void* dst, DType t,
+                      cudaStream_t s);
 
 // Label-smoothed CE over logits [R x V] (ld), tape.hpp:180-209/302-321.
 // Per-row losses -> row_loss[R]; dz = p - q - eps/V written to dz (ld_dz).
