@@ -9,11 +9,11 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (UMMA_K=16)
 //               into one of TWO accumulator buffers, so the epilogue of tile i
 //               overlaps the MMAs of tile i+1
-//   warps 2..9  epilogue: tcgen05.ld 32x32b.x32 -> registers -> bias / GELU /
-//               dGELU / residual -> vectorized global stores (or fp32 vector
-//               reductions for split-K).  Warp w reads TMEM lanes
-//               32*(w%4)..+31; warps 2-5 take the left half of the tile's
-//               columns, warps 6-9 the right half.
+//   warps 2..17 epilogue: tcgen05.ld 32x32b.x32 -> registers -> bias / GELU /
+//               dGELU / residual -> global, staged through a swizzled 2 KB
+//               smem tile per warp so every global access is a full row
+//               segment (coalesced; split-K uses fp32 vector reductions).
+//               Warp w reads TMEM lanes 32*(w%4)..+31, every 4th 32-col chunk.
 //
 // Operands may be K-major or MN-major (the three GEMMs of a linear layer's
 // training step: fwd X.W, dgrad dY.W^T, wgrad X^T.dY all read the canonical
@@ -39,7 +39,7 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int STAGES = 4;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kATileBytes = BM * BK * 2;  // 16 KB
 
@@ -134,6 +134,15 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+#define TMEM_LD16(taddr, r)                                                                      \
+  asm volatile(                                                                                  \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+      "%15}, [%16];"                                                                             \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),      \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),  \
+        "=r"(r[14]), "=r"(r[15])                                                                 \
+      : "r"(taddr))
+
 #define TMEM_LD32(taddr, r)                                                                      \
   asm volatile(                                                                                  \
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
@@ -151,6 +160,29 @@ __device__ __forceinline__ float gelu_f(float x) {
 __device__ __forceinline__ float dgelu_f(float x) {
   return 0.5f * (1.f + erff(x * 0.70710678118654752f)) +
          x * 0.39894228040143268f * expf(-0.5f * x * x);
+}
+// Branch-free normal CDF / PDF for the bf16 epilogues: erf by Abramowitz &
+// Stegun 7.1.26 (|error| <= 1.5e-7, far below bf16 rounding); exp(-x^2/2) is
+// shared between Phi and phi.  2 MUFU ops + ~10 FMA per element.
+__device__ __forceinline__ float phi_cdf(float x, float& pdf) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
+  const float e = __expf(-z * z);
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
+               0.254829592f);
+  const float erf_abs = fmaf(-poly, e, 1.f);
+  pdf = e * 0.39894228040143268f;
+  return 0.5f * (1.f + copysignf(erf_abs, x));
+}
+__device__ __forceinline__ float gelu_fast(float x) {
+  float pdf;
+  return x * phi_cdf(x, pdf);
+}
+__device__ __forceinline__ float dgelu_fast(float x) {
+  float pdf;
+  const float c = phi_cdf(x, pdf);
+  return fmaf(x, pdf, c);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -177,23 +209,24 @@ __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c
                : "memory");
 }
 
-// Epilogue for 32 consecutive columns [n, n+32) of row m.
-__device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float* v) {
+// Epilogue for NC consecutive columns [n, n+NC) of row m.
+template <int NC>
+__device__ __forceinline__ void epilogue_cols(const Params& p, int m, int n, float* v) {
   if (m >= p.M) return;
-  const bool inb = n + 32 <= p.N;
+  const bool inb = n + NC <= p.N;
   const bool full = inb && p.vec == 1;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+  for (int i = 0; i < NC; ++i) v[i] *= p.alpha;
   const int64_t co = p.c_group ? (n / p.c_group) * p.c_gstride + (int64_t)m * p.ldc + n % p.c_group
                                : (int64_t)m * p.ldc + n;
   if (p.splits > 1) {  // split-K partial: reduce into the (zeroed) fp32 output
     float* c = static_cast<float*>(p.c) + co;
     if (full) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) red_add_v4(c + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      for (int q = 0; q < NC / 4; ++q) red_add_v4(c + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     } else {
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
+      for (int i = 0; i < NC; ++i)
         if (n + i < p.N) atomicAdd(c + i, v[i]);
     }
     return;
@@ -201,13 +234,13 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
   if (p.bias) {
     if (inb && (reinterpret_cast<uintptr_t>(p.bias + n) & 15) == 0) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NC / 4; ++q) {
         const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n) + q);
         v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += (n + i < p.N) ? p.bias[n + i] : 0.f;
+      for (int i = 0; i < NC; ++i) v[i] += (n + i < p.N) ? p.bias[n + i] : 0.f;
     }
   }
   if (p.act == ACT_GELU) {
@@ -215,41 +248,41 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
     if (p.c_f32) {
       float* a = static_cast<float*>(p.aux) + co;
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
+      for (int i = 0; i < NC; ++i)
         if (n + i < p.N) a[i] = v[i];
     } else {
       __nv_bfloat16* a = static_cast<__nv_bfloat16*>(p.aux) + co;
       if (full) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) store8_bf16(a + 8 * q, v + 8 * q);
+        for (int q = 0; q < NC / 8; ++q) store8_bf16(a + 8 * q, v + 8 * q);
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
+        for (int i = 0; i < NC; ++i)
           if (n + i < p.N) a[i] = __float2bfloat16_rn(v[i]);
       }
     }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+    for (int i = 0; i < NC; ++i) v[i] = gelu_fast(v[i]);
   } else if (p.act == ACT_DGELU) {
     if (p.c_f32) {
       const float* a = static_cast<const float*>(p.aux) + co;
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (n + i < p.N) v[i] *= dgelu_f(a[i]);
+      for (int i = 0; i < NC; ++i)
+        if (n + i < p.N) v[i] *= dgelu_fast(a[i]);
     } else {
       const __nv_bfloat16* a = static_cast<const __nv_bfloat16*>(p.aux) + co;
       if (full) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < NC / 8; ++q) {
           float f[8];
           load8_bf16(a + 8 * q, f);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[8 * q + e] *= dgelu_f(f[e]);
+          for (int e = 0; e < 8; ++e) v[8 * q + e] *= dgelu_fast(f[e]);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (n + i < p.N) v[i] *= dgelu_f(__bfloat162float(a[i]));
+        for (int i = 0; i < NC; ++i)
+          if (n + i < p.N) v[i] *= dgelu_fast(__bfloat162float(a[i]));
       }
     }
   }
@@ -257,13 +290,13 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
     if (p.c_f32) {
       const float* r = static_cast<const float*>(p.resid) + (int64_t)m * p.ld_resid + n;
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
+      for (int i = 0; i < NC; ++i)
         if (n + i < p.N) v[i] += r[i];
     } else {
       const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.resid) + (int64_t)m * p.ld_resid + n;
       if (full) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < NC / 8; ++q) {
           float f[8];
           load8_bf16(r + 8 * q, f);
 #pragma unroll
@@ -271,7 +304,7 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
+        for (int i = 0; i < NC; ++i)
           if (n + i < p.N) v[i] += __bfloat162float(r[i]);
       }
     }
@@ -280,7 +313,7 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
     float* c = static_cast<float*>(p.c) + co;
     if (full) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NC / 4; ++q) {
         float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         if (p.accumulate) {
           const float4 old = reinterpret_cast<const float4*>(c)[q];
@@ -292,32 +325,201 @@ __device__ __forceinline__ void epilogue32(const Params& p, int m, int n, float*
       // rows only 8-byte aligned (e.g. d(mlm.w) with ld = V = 30522)
       if ((reinterpret_cast<uintptr_t>(c) & 15) == 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < NC / 4; ++q)
           reinterpret_cast<float4*>(c)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       } else {
         reinterpret_cast<float2*>(c)[0] = make_float2(v[0], v[1]);
 #pragma unroll
-        for (int q = 0; q < 7; ++q)
+        for (int q = 0; q < NC / 4 - 1; ++q)
           reinterpret_cast<float4*>(c + 2)[q] =
               make_float4(v[2 + 4 * q], v[3 + 4 * q], v[4 + 4 * q], v[5 + 4 * q]);
-        reinterpret_cast<float2*>(c + 30)[0] = make_float2(v[30], v[31]);
+        reinterpret_cast<float2*>(c + NC - 2)[0] = make_float2(v[NC - 2], v[NC - 1]);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
+      for (int i = 0; i < NC; ++i)
         if (n + i < p.N) c[i] = p.accumulate ? c[i] + v[i] : v[i];
     }
   } else {
     __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.c) + co;
     if (full) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) store8_bf16(c + 8 * q, v + 8 * q);
+      for (int q = 0; q < NC / 8; ++q) store8_bf16(c + 8 * q, v + 8 * q);
     } else {
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
+      for (int i = 0; i < NC; ++i)
         if (n + i < p.N) c[i] = __float2bfloat16_rn(v[i]);
     }
   }
+}
+
+// ---- coalesced epilogue through a per-warp smem staging buffer ------------
+// A warp owns 32 output rows (its TMEM lane quarter) x 32 columns per chunk.
+// Thread r holds row r in registers; global traffic instead goes row-segment
+// by row-segment (4 or 8 lanes per row, full 64/128-byte segments), through a
+// swizzled [32 rows][32 x elem] staging tile that is conflict-free both when a
+// thread writes its own row and when a warp reads a row segment.
+// Staging tile: 32 rows x 64 bytes (32 bf16, or 16 fp32 = half a chunk).
+template <int ES>  // element size: 2 (bf16) or 4 (fp32)
+struct Stage {
+  static constexpr int RB = 64;        // row bytes
+  static constexpr int CPR = 4;        // 16-byte pieces per row
+  static constexpr int RPI = 8;        // rows per warp instruction
+  static constexpr int NE = 64 / ES;   // elements per staged row (32 or 16)
+  __device__ static __forceinline__ int off(int r, int j) {
+    return r * RB + ((j ^ ((r >> 1) & 3)) * 16);  // conflict-free both ways
+  }
+};
+
+// thread `lane` writes its NE values (row lane) into the staging tile
+template <int ES>
+__device__ __forceinline__ void stage_put(uint8_t* st, int lane, const float* v) {
+  if constexpr (ES == 2) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<uint4*>(st + Stage<2>::off(lane, j)) =
+          make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                     pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<float4*>(st + Stage<4>::off(lane, j)) =
+          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  }
+}
+// thread `lane` reads its row back as floats
+template <int ES>
+__device__ __forceinline__ void stage_get(const uint8_t* st, int lane, float* v) {
+  if constexpr (ES == 2) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) load8_bf16(reinterpret_cast<const __nv_bfloat16*>(st + Stage<2>::off(lane, j)), v + 8 * j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 q = *reinterpret_cast<const float4*>(st + Stage<4>::off(lane, j));
+      v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    }
+  }
+}
+// staging tile -> global rows [row0, row0+32) (rows >= M skipped); mode 0
+// store, 1 fp32 vector reduction (split-K), 2 fp32 read-add-store (accumulate)
+template <int ES>
+__device__ __forceinline__ void stage_store(const uint8_t* st, int lane, char* g0, int64_t ld_bytes,
+                                            int rows_left, int mode) {
+  using S = Stage<ES>;
+#pragma unroll
+  for (int i = 0; i < S::CPR; ++i) {
+    const int r = i * S::RPI + lane / S::CPR, j = lane % S::CPR;
+    if (r < rows_left) {
+      const uint4 u = *reinterpret_cast<const uint4*>(st + S::off(r, j));
+      char* g = g0 + r * ld_bytes + j * 16;
+      if (mode == 0) {
+        *reinterpret_cast<uint4*>(g) = u;
+      } else if (mode == 1) {
+        red_add_v4(reinterpret_cast<float*>(g), __uint_as_float(u.x), __uint_as_float(u.y),
+                   __uint_as_float(u.z), __uint_as_float(u.w));
+      } else {
+        float4 o = *reinterpret_cast<float4*>(g);
+        o.x += __uint_as_float(u.x); o.y += __uint_as_float(u.y);
+        o.z += __uint_as_float(u.z); o.w += __uint_as_float(u.w);
+        *reinterpret_cast<float4*>(g) = o;
+      }
+    }
+  }
+}
+// global rows -> staging tile (coalesced), for the residual / aux operands
+template <int ES>
+__device__ __forceinline__ void stage_load(uint8_t* st, int lane, const char* g0, int64_t ld_bytes,
+                                           int rows_left) {
+  using S = Stage<ES>;
+#pragma unroll
+  for (int i = 0; i < S::CPR; ++i) {
+    const int r = i * S::RPI + lane / S::CPR, j = lane % S::CPR;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (r < rows_left) u = *reinterpret_cast<const uint4*>(g0 + r * ld_bytes + j * 16);
+    *reinterpret_cast<uint4*>(st + S::off(r, j)) = u;
+  }
+}
+
+// 32 register values of row `lane` -> 32 columns of rows [row0, row0+32) at
+// g (byte address of the first row's first column), via the staging tile.
+__device__ __forceinline__ void staged_out(bool f32, uint8_t* st, int lane, const float* v, char* g,
+                                           int64_t ld_bytes, int rows_left, int mode) {
+  if (f32) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      stage_put<4>(st, lane, v + 16 * h);
+      __syncwarp();
+      stage_store<4>(st, lane, g + 64 * h, ld_bytes, rows_left, mode);
+      __syncwarp();
+    }
+  } else {
+    stage_put<2>(st, lane, v);
+    __syncwarp();
+    stage_store<2>(st, lane, g, ld_bytes, rows_left, mode);
+    __syncwarp();
+  }
+}
+__device__ __forceinline__ void staged_in(bool f32, uint8_t* st, int lane, float* v, const char* g,
+                                          int64_t ld_bytes, int rows_left) {
+  if (f32) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      stage_load<4>(st, lane, g + 64 * h, ld_bytes, rows_left);
+      __syncwarp();
+      stage_get<4>(st, lane, v + 16 * h);
+      __syncwarp();
+    }
+  } else {
+    stage_load<2>(st, lane, g, ld_bytes, rows_left);
+    __syncwarp();
+    stage_get<2>(st, lane, v);
+    __syncwarp();
+  }
+}
+
+// Full 32-column chunk [n, n+32) of the warp's 32 rows starting at row0.
+// Preconditions (checked by the caller): n + 32 <= N, p.vec == 1.
+__device__ __forceinline__ void epilogue_staged(const Params& p, uint8_t* st, int lane, int row0,
+                                                int n, float* v) {
+  const int rows_left = p.M - row0;
+  const int64_t co0 = p.c_group ? (n / p.c_group) * p.c_gstride + (int64_t)row0 * p.ldc + n % p.c_group
+                                : (int64_t)row0 * p.ldc + n;
+  const bool f32 = p.c_f32;
+  const int cs = f32 ? 4 : 2;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+  if (p.splits > 1) {
+    staged_out(true, st, lane, v, static_cast<char*>(p.c) + co0 * 4, p.ldc * 4, rows_left, 1);
+    return;
+  }
+  if (p.bias) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n) + q);
+      v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
+    }
+  }
+  if (p.act == ACT_GELU) {  // pre-activation to aux (same type and layout as C)
+    staged_out(f32, st, lane, v, static_cast<char*>(p.aux) + co0 * cs, p.ldc * cs, rows_left, 0);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_fast(v[i]);
+  } else if (p.act == ACT_DGELU) {
+    float a[32];
+    staged_in(f32, st, lane, a, static_cast<const char*>(p.aux) + co0 * cs, p.ldc * cs, rows_left);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(a[i]);
+  }
+  if (p.resid) {
+    float r[32];
+    const int64_t ro = (int64_t)row0 * p.ld_resid + n;
+    staged_in(f32, st, lane, r, static_cast<const char*>(p.resid) + ro * cs, p.ld_resid * cs,
+              rows_left);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += r[i];
+  }
+  staged_out(f32, st, lane, v, static_cast<char*>(p.c) + co0 * cs, p.ldc * cs, rows_left,
+             f32 && p.accumulate ? 2 : 0);
 }
 
 __device__ __forceinline__ void decode_unit(const Params& p, int u, int& m0, int& n0, int& kb0,
@@ -452,9 +654,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else {
-    // epilogue warps 2..9
+    // epilogue warps 2..17: lane quarter = warp % 4 (the TMEM lanes a warp
+    // may access); the tile's 32-column chunks are dealt round-robin to the
+    // four warps of a quarter; each chunk is staged through the warp's own
+    // 2 KB smem tile for coalesced global traffic
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int slice = (warp - 2) >> 2;
+    uint8_t* st = smem + STAGES * kStageBytes + 1024 + (warp - 2) * 2048;
     uint32_t lt = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++lt) {
       int m0, nt, kb0, kb1;
@@ -463,18 +669,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
       mbar_wait(&tmem_full[as], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int m = m0 + quarter * 32 + lane;
+      const int row0 = m0 + quarter * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * kAccStride;
 #pragma unroll 1
-      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+      for (int c0 = slice * 32; c0 < BN; c0 += 128) {
         uint32_t r[32];
         TMEM_LD32(taddr + c0, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (n0 + c0 < p.N) {
+        const int n = n0 + c0;
+        if (n < p.N && row0 < p.M) {
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          epilogue32(p, m, n0 + c0, v);
+          if (n + 32 <= p.N && p.vec == 1)
+            epilogue_staged(p, st, lane, row0, n, v);
+          else
+            epilogue_cols<32>(p, row0 + lane, n, v);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -588,7 +798,9 @@ static int epilogue_vec_ok(const GemmArgs& g) {
 template <int BN>
 static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Params& p,
                       cudaStream_t s) {
-  constexpr size_t smem = tc::STAGES * (tc::kATileBytes + BN * tc::BK * 2) + 1024 + 256;
+  // stages + barriers (1 KB) + 16 epilogue staging tiles (2 KB) + alignment slack
+  constexpr size_t smem = tc::STAGES * (tc::kATileBytes + BN * tc::BK * 2) + 1024 +
+                          tc::kEpiWarps * 2048 + 1024;
   static bool attr = false;
   if (!attr) {
     HP_CUDA(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -38,9 +38,18 @@ SHAPES = [
     ("dmlm_w", D, 30522, 608, 1, 0, 1, 0, 0, 0, 0),
     ("dhm", 608, D, 30522, 0, 1, 1, 0, 0, 0, 0),
 ]
-PER_STEP = {"qkv_fwd": 12, "wo_fwd": 12, "ffn1_fwd_gelu": 12, "ffn2_fwd": 12, "dW2": 12,
+VARIANTS = [
+    ("v_plain_bf16", T, F, D, 0, 0, 0, 0, 0, 0, 0),
+    ("v_bias_bf16", T, F, D, 0, 0, 0, 1, 0, 0, 0),
+    ("v_gelu_aux", T, F, D, 0, 0, 0, 1, 1, 0, 0),
+    ("v_plain_f32", T, F, D, 0, 0, 1, 0, 0, 0, 0),
+    ("v_kmajor_b", T, F, D, 0, 1, 0, 0, 0, 0, 0),
+    ("v_long_k", T, D, F, 0, 0, 0, 0, 0, 0, 0),
+]
+PER_STEP = {v[0]: 0 for v in VARIANTS}
+PER_STEP.update({"qkv_fwd": 12, "wo_fwd": 12, "ffn1_fwd_gelu": 12, "ffn2_fwd": 12, "dW2": 12,
             "dU_dgelu": 12, "dW1": 12, "dX1": 12, "dWo": 12, "dO": 12, "dWqkv": 12, "dX": 12,
-            "mlm_logits": 1, "dmlm_w": 1, "dhm": 1}
+            "mlm_logits": 1, "dmlm_w": 1, "dhm": 1})
 
 
 def p(t):
@@ -108,15 +117,19 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--only", default=None, help="comma-separated shape names")
     a = ap.parse_args()
-    res = [run(s, a.iters, a.bn) for s in SHAPES]
+    shapes = [s for s in SHAPES + VARIANTS if (not a.only and s in SHAPES) or
+              (a.only and (s[0] in a.only.split(",") or (a.only == "variants" and s in VARIANTS)))]
+    res = [run(s, a.iters, a.bn) for s in shapes]
     tot = sum(r["us"] * r["per_step"] for r in res)
     tot_cb = sum(r["cublas_us"] * r["per_step"] for r in res)
     fl = sum(2.0 * r["M"] * r["N"] * r["K"] * r["per_step"] for r in res)
     for r in res:
         print(f"{r['name']:>14} {r['M']:5d}x{r['N']:5d}x{r['K']:5d}  {r['us']:8.1f} us {r['tflops']:7.1f} TF/s"
               f"   cuBLAS {r['cublas_us']:8.1f} us {r['cublas_tflops']:7.1f} TF/s")
-    print(f"step GEMM total: ours {tot/1e3:.3f} ms ({fl/tot/1e6:.0f} TF/s)  cuBLAS {tot_cb/1e3:.3f} ms ({fl/tot_cb/1e6:.0f} TF/s)")
+    if tot > 0:
+        print(f"step GEMM total: ours {tot/1e3:.3f} ms ({fl/tot/1e6:.0f} TF/s)  cuBLAS {tot_cb/1e3:.3f} ms ({fl/tot_cb/1e6:.0f} TF/s)")
     if a.json:
         with open(a.json, "w") as f:
             json.dump({"shapes": res, "total_ms": tot / 1e3, "cublas_total_ms": tot_cb / 1e3}, f, indent=1)
