@@ -238,8 +238,9 @@ hp_status hp_engine_io_bytes(hp_engine* e, uint64_t* h2d, uint64_t* d2h);
  * Test hooks (used by tests/ only): run one GEMM of the engine's dispatch on
  * caller-owned device buffers.  path: 0 auto, 1 SIMT fp32, 2 tcgen05.
  * act: 0 none, 1 GELU (pre-activation to aux), 2 dGELU (multiply by
- * GELU'(aux)).  bn: tcgen05 tile width (0 = heuristic, 128, 192 or 256),
- * plus 1000 * s to force an s-way split-K (fp32 C without epilogue ops).
+ * GELU'(aux)).  bn = 10000 * s + 1000 * cg + tile: tile width (0 = heuristic,
+ * 128, 192 or 256), cg CTA group (0 heuristic, 1 single CTA, 2 CTA pair), s a
+ * forced s-way split-K (fp32 C without epilogue ops).
  * ---------------------------------------------------------------------- */
 hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t lda,
                         int a_trans, const void* B, int64_t ldb, int b_trans,
@@ -248,6 +249,12 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
                         const float* bias, int act, void* aux, const void* resid,
                         int64_t ld_resid, int accumulate, int path, int bn);
 hp_status hp_debug_sync(void);
+/* Profiling hook: when buf (device, >= 1024 u64) is non-null, CTA 0 of every
+ * following tcgen05 GEMM writes a clock64 timeline into it; null disables. */
+hp_status hp_debug_gemm_trace(unsigned long long* buf);
+/* Test hook: 1 forces every tcgen05 GEMM onto the generic epilogue kernel
+ * (all epilogue flags at run time) instead of the per-kind specialisation. */
+hp_status hp_debug_gemm_generic(int on);
 /* Varlen self-attention on caller-owned device buffers: cu[B+1] (int32,
  * device), qkv [T x 3*H*dk], o [T x H*dk], lse [H x T], dO, dqkv.  bf16 = 1
  * selects bf16 I/O; path: 0 auto, 1 SIMT, 2 tensor-core (mma.sync). */

@@ -140,6 +140,8 @@ _SIGS = {
     "hp_debug_gemm": [I, I, I, I, P, I64, I, P, I64, I, I64, I64, P, I64, I, I64, I64, P, I, P, P,
                       I64, I, I, I],
     "hp_debug_sync": [],
+    "hp_debug_gemm_trace": [P],
+    "hp_debug_gemm_generic": [I],
     "hp_debug_attention": [I, P, I, I, I, I, P, P, P, P, P, I],
     "hp_debug_adam": [P, P, P, P, U64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float,
                       C.c_float, I],

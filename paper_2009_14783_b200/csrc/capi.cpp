@@ -386,9 +386,13 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
     hp::gemm_simt(g, 0);
   } else if (path == 2) {
     hp::gemm_tc_set_bn(bn % 1000);
-    hp::gemm_tc_set_splits(bn / 1000);
+    hp::gemm_tc_set_cg((bn / 1000) % 10);
+    hp::gemm_tc_set_splits((bn / 10000) % 10);
+    hp::gemm_tc_set_debug(bn / 100000);
     hp::gemm_tc(g, 0);
+    hp::gemm_tc_set_debug(0);
     hp::gemm_tc_set_bn(0);
+    hp::gemm_tc_set_cg(0);
     hp::gemm_tc_set_splits(0);
   } else {
     hp::gemm(g, 0);
@@ -445,6 +449,18 @@ hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf1
 hp_status hp_debug_sync(void) {
   HP_API_BEGIN
   HP_CUDA(cudaDeviceSynchronize());
+  HP_API_END
+}
+
+hp_status hp_debug_gemm_trace(unsigned long long* buf) {
+  HP_API_BEGIN
+  hp::gemm_tc_set_trace(buf);
+  HP_API_END
+}
+
+hp_status hp_debug_gemm_generic(int on) {
+  HP_API_BEGIN
+  hp::gemm_tc_set_generic(on);
   HP_API_END
 }
 

@@ -127,8 +127,9 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   {
     // Adam work items, per gradient bucket (each bucket is updated as soon as
     // its reduced gradient is final): runs of parameters whose working copy
-    // is laid out contiguously are merged; every item is cut to <= 64K.
-    constexpr uint64_t kChunk = 65536;
+    // is laid out contiguously are merged; every item is cut to <= 8K elements
+    // so even one 25 MB bucket spreads over ~800 CTAs.
+    constexpr uint64_t kChunk = 8192;
     std::vector<uint64_t> items;
     bucket_items_.clear();
     for (const Bucket& bk : buckets_) {

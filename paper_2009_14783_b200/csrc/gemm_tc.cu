@@ -38,8 +38,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
-constexpr int STAGES = 4;
-constexpr int kEpiWarps = 16;
+constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kATileBytes = BM * BK * 2;  // 16 KB
 
@@ -48,10 +47,12 @@ struct Params {
   int a_mn;       // A stored MN-major (A^T row-major)
   int b_mn;       // B stored MN-major (row-major K x N)
   int b_grouped;  // B uses the 3-D grouped map (group = 64)
+  int a_atoms, b_atoms;  // MN-major operand loaded through the 3-D atom map
   int m_tiles, n_tiles, splits, kb_per_split, units;
   void* c;
   int64_t ldc;
-  int64_t c_group, c_gstride;
+  int c_group;  // 32-bit: divided per chunk in the epilogue
+  int64_t c_gstride;
   int c_f32;
   float alpha;
   int accumulate;
@@ -61,7 +62,17 @@ struct Params {
   const void* resid;
   int64_t ld_resid;
   int vec;  // C / aux / resid rows are 16-byte aligned
+  int debug;  // profiling only: 0 normal, 1 skip TMA loads, 2 skip MMAs, 3 skip epilogue
+  unsigned long long* trace;  // profiling only: CTA 0 clock64 timeline (see kTr*)
 };
+// trace slots (CTA 0): [0] entry, [1] after prologue sync, [2] exit;
+// [16+it] producer got empty slot, [16+256+it] MMA got full stage,
+// [16+512+it] MMA committed, [16+768+2*t] epilogue tile t start / +1 end
+constexpr int kTrP = 16, kTrF = 16 + 256, kTrC = 16 + 512, kTrE = 16 + 768, kTrSlots = 16 + 768 + 64;
+constexpr int kTrX = 900;  // tile 0, warp 2: per chunk [before tcgen05.ld, after wait, after epilogue]
+__device__ __forceinline__ void trace_at(const Params& p, int slot, int lim = 1 << 30) {
+  if (p.trace && blockIdx.x == 0 && slot < lim) p.trace[slot] = clock64();
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -90,6 +101,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Wait for threads that have nothing else to do (the epilogue warps while a
+// tile's mainloop runs): the suspend-time hint parks the warp in the barrier
+// unit until the phase completes instead of re-polling, so 16 idle warps do not
+// compete with the producer / MMA threads' barrier traffic and issue slots.
+__device__ __forceinline__ void mbar_wait_parked(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(200);
+  }
+}
 __device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
                                        int c1) {
   asm volatile(
@@ -104,6 +148,64 @@ __device__ __forceinline__ void tma_3d(const CUtensorMap* map, uint64_t* bar, vo
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem location in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA load into this CTA's smem, completing bytes on the (leader's) barrier
+__device__ __forceinline__ void tma_2d_cg2(const CUtensorMap* map, uint32_t bar_cluster, void* dst,
+                                           int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_cg2(const CUtensorMap* map, uint32_t bar_cluster, void* dst,
+                                           int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_cg2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+// commit the pair's MMAs to the same barrier in both CTAs
+__device__ __forceinline__ void umma_commit_cg2(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+      "}\n" ::"r"(smem_u32(bar))
       : "memory");
 }
 
@@ -154,35 +256,29 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
       : "r"(taddr))
 
-__device__ __forceinline__ float gelu_f(float x) {
-  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
-}
-__device__ __forceinline__ float dgelu_f(float x) {
-  return 0.5f * (1.f + erff(x * 0.70710678118654752f)) +
-         x * 0.39894228040143268f * expf(-0.5f * x * x);
-}
-// Branch-free normal CDF / PDF for the bf16 epilogues: erf by Abramowitz &
-// Stegun 7.1.26 (|error| <= 1.5e-7, far below bf16 rounding); exp(-x^2/2) is
-// shared between Phi and phi.  2 MUFU ops + ~10 FMA per element.
-__device__ __forceinline__ float phi_cdf(float x, float& pdf) {
-  const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
-  const float e = __expf(-z * z);
-  const float poly =
-      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
-               0.254829592f);
-  const float erf_abs = fmaf(-poly, e, 1.f);
-  pdf = e * 0.39894228040143268f;
-  return 0.5f * (1.f + copysignf(erf_abs, x));
+// bf16 epilogues use the tanh form of GELU, 0.5 x (1 + tanh(sqrt(2/pi) (x +
+// 0.044715 x^3))), on the MUFU tanh unit: |GELU_tanh - GELU_erf| <= 4.8e-4,
+// under 1/16 of a bf16 half-ulp where it peaks (x ~ 2.7), at ~6 instructions
+// per element instead of ~20 for an erf polynomial.  The backward multiplies
+// by the exact derivative of the same tanh form, so gradients stay consistent
+// with the loss the forward computed.  (The fp32 engine path keeps exact erf,
+// kernels.cu.)
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 __device__ __forceinline__ float gelu_fast(float x) {
-  float pdf;
-  return x * phi_cdf(x, pdf);
+  const float u = x * fmaf(0.0356774081363001f, x * x, 0.7978845608028654f);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_approx(u), hx);
 }
 __device__ __forceinline__ float dgelu_fast(float x) {
-  float pdf;
-  const float c = phi_cdf(x, pdf);
-  return fmaf(x, pdf, c);
+  const float x2 = x * x;
+  const float t = tanh_approx(x * fmaf(0.0356774081363001f, x2, 0.7978845608028654f));
+  const float du = fmaf(0.1070322244089f, x2, 0.7978845608028654f);
+  const float hx = 0.5f * x;
+  return fmaf(hx * fmaf(-t, t, 1.f), du, fmaf(0.5f, t, 0.5f));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -371,47 +467,75 @@ struct Stage {
   }
 };
 
+// Staging-tile accesses use explicit shared-space instructions on a 32-bit
+// shared address: generic (flat) ld/st here would be ordered behind the
+// warp's in-flight global stores, serialising every chunk.
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void unpack8_bf16(const uint4 u, float* v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(h[e]);
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
+}
+
 // thread `lane` writes its NE values (row lane) into the staging tile
 template <int ES>
-__device__ __forceinline__ void stage_put(uint8_t* st, int lane, const float* v) {
+__device__ __forceinline__ void stage_put(uint32_t st, int lane, const float* v) {
   if constexpr (ES == 2) {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      *reinterpret_cast<uint4*>(st + Stage<2>::off(lane, j)) =
-          make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
-                     pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+      sts128(st + Stage<2>::off(lane, j),
+             make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                        pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7])));
   } else {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      *reinterpret_cast<float4*>(st + Stage<4>::off(lane, j)) =
-          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      sts128(st + Stage<4>::off(lane, j),
+             make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                        __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3])));
   }
 }
 // thread `lane` reads its row back as floats
 template <int ES>
-__device__ __forceinline__ void stage_get(const uint8_t* st, int lane, float* v) {
+__device__ __forceinline__ void stage_get(uint32_t st, int lane, float* v) {
   if constexpr (ES == 2) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) load8_bf16(reinterpret_cast<const __nv_bfloat16*>(st + Stage<2>::off(lane, j)), v + 8 * j);
+    for (int j = 0; j < 4; ++j) unpack8_bf16(lds128(st + Stage<2>::off(lane, j)), v + 8 * j);
   } else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float4 q = *reinterpret_cast<const float4*>(st + Stage<4>::off(lane, j));
-      v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+      const uint4 q = lds128(st + Stage<4>::off(lane, j));
+      v[4 * j] = __uint_as_float(q.x); v[4 * j + 1] = __uint_as_float(q.y);
+      v[4 * j + 2] = __uint_as_float(q.z); v[4 * j + 3] = __uint_as_float(q.w);
     }
   }
 }
 // staging tile -> global rows [row0, row0+32) (rows >= M skipped); mode 0
 // store, 1 fp32 vector reduction (split-K), 2 fp32 read-add-store (accumulate)
 template <int ES>
-__device__ __forceinline__ void stage_store(const uint8_t* st, int lane, char* g0, int64_t ld_bytes,
+__device__ __forceinline__ void stage_store(uint32_t st, int lane, char* g0, int64_t ld_bytes,
                                             int rows_left, int mode) {
   using S = Stage<ES>;
 #pragma unroll
   for (int i = 0; i < S::CPR; ++i) {
     const int r = i * S::RPI + lane / S::CPR, j = lane % S::CPR;
     if (r < rows_left) {
-      const uint4 u = *reinterpret_cast<const uint4*>(st + S::off(r, j));
+      const uint4 u = lds128(st + S::off(r, j));
       char* g = g0 + r * ld_bytes + j * 16;
       if (mode == 0) {
         *reinterpret_cast<uint4*>(g) = u;
@@ -429,7 +553,7 @@ __device__ __forceinline__ void stage_store(const uint8_t* st, int lane, char* g
 }
 // global rows -> staging tile (coalesced), for the residual / aux operands
 template <int ES>
-__device__ __forceinline__ void stage_load(uint8_t* st, int lane, const char* g0, int64_t ld_bytes,
+__device__ __forceinline__ void stage_load(uint32_t st, int lane, const char* g0, int64_t ld_bytes,
                                            int rows_left) {
   using S = Stage<ES>;
 #pragma unroll
@@ -437,13 +561,13 @@ __device__ __forceinline__ void stage_load(uint8_t* st, int lane, const char* g0
     const int r = i * S::RPI + lane / S::CPR, j = lane % S::CPR;
     uint4 u = make_uint4(0, 0, 0, 0);
     if (r < rows_left) u = *reinterpret_cast<const uint4*>(g0 + r * ld_bytes + j * 16);
-    *reinterpret_cast<uint4*>(st + S::off(r, j)) = u;
+    sts128(st + S::off(r, j), u);
   }
 }
 
 // 32 register values of row `lane` -> 32 columns of rows [row0, row0+32) at
 // g (byte address of the first row's first column), via the staging tile.
-__device__ __forceinline__ void staged_out(bool f32, uint8_t* st, int lane, const float* v, char* g,
+__device__ __forceinline__ void staged_out(bool f32, uint32_t st, int lane, const float* v, char* g,
                                            int64_t ld_bytes, int rows_left, int mode) {
   if (f32) {
 #pragma unroll
@@ -460,7 +584,7 @@ __device__ __forceinline__ void staged_out(bool f32, uint8_t* st, int lane, cons
     __syncwarp();
   }
 }
-__device__ __forceinline__ void staged_in(bool f32, uint8_t* st, int lane, float* v, const char* g,
+__device__ __forceinline__ void staged_in(bool f32, uint32_t st, int lane, float* v, const char* g,
                                           int64_t ld_bytes, int rows_left) {
   if (f32) {
 #pragma unroll
@@ -478,67 +602,164 @@ __device__ __forceinline__ void staged_in(bool f32, uint8_t* st, int lane, float
   }
 }
 
-// Full 32-column chunk [n, n+32) of the warp's 32 rows starting at row0.
-// Preconditions (checked by the caller): n + 32 <= N, p.vec == 1.
-__device__ __forceinline__ void epilogue_staged(const Params& p, uint8_t* st, int lane, int row0,
-                                                int n, float* v) {
-  const int rows_left = p.M - row0;
-  const int64_t co0 = p.c_group ? (n / p.c_group) * p.c_gstride + (int64_t)row0 * p.ldc + n % p.c_group
-                                : (int64_t)row0 * p.ldc + n;
-  const bool f32 = p.c_f32;
-  const int cs = f32 ? 4 : 2;
+// Prefetch of a bf16 [32 rows x 32 cols] operand chunk (the dGELU
+// pre-activation or the residual) into registers, coalesced like
+// stage_load<2>: lane reads 16-byte piece (lane % 4) of rows i*8 + lane/4.
+// Issued one chunk ahead (and for a tile's first chunk before its accumulator
+// is ready) so the epilogue never waits on global-load latency.
+__device__ __forceinline__ void pre_issue(const char* g0, int64_t ld_bytes, int rows_left, int lane,
+                                          uint4 (&q)[4]) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
-  if (p.splits > 1) {
-    staged_out(true, st, lane, v, static_cast<char*>(p.c) + co0 * 4, p.ldc * 4, rows_left, 1);
-    return;
+  for (int i = 0; i < 4; ++i) {
+    const int r = i * 8 + lane / 4, j = lane % 4;
+    q[i] = r < rows_left ? __ldg(reinterpret_cast<const uint4*>(g0 + r * ld_bytes + j * 16))
+                         : make_uint4(0, 0, 0, 0);
   }
-  if (p.bias) {
+}
+// prefetched pieces -> staging tile -> row `lane` as floats
+__device__ __forceinline__ void pre_consume(uint32_t st, int lane, const uint4 (&q)[4], float* out) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n) + q);
-      v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
+  for (int i = 0; i < 4; ++i) sts128(st + Stage<2>::off(i * 8 + lane / 4, lane % 4), q[i]);
+  __syncwarp();
+  stage_get<2>(st, lane, out);
+  __syncwarp();
+}
+
+// Epilogue kinds: each kernel instantiation carries only its own path (a
+// single kernel with every variant behind runtime flags was ~7.5k SASS
+// instructions, and its epilogue warps stalled on instruction fetch).
+enum EpiKind : int {
+  EK_GENERIC = 0,  // any flags; unaligned / partial chunks via epilogue_cols
+  EK_BF16 = 1,     // bf16 C (+ bias) (+ residual, prefetched)
+  EK_GELU = 2,     // bf16 C = GELU(acc + bias), pre-activation -> aux
+  EK_DGELU = 3,    // bf16 C = acc * GELU'(aux), aux prefetched
+  EK_F32 = 4,      // fp32 C (+ bias) (accumulate | split-K reduction), grouped C
+};
+
+// Full 32-column chunk [n, n+32) of the warp's 32 rows starting at row0.
+// Preconditions (checked by the caller): n + 32 <= N, p.vec == 1.  `pre`:
+// the prefetched aux (pre_kind 1, dGELU) or residual (pre_kind 2) chunk.
+template <int EK>
+__device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, int lane, int row0,
+                                                int n, float* v, const float* pre, int pre_kind) {
+  constexpr bool kAnyF32 = EK == EK_GENERIC || EK == EK_F32;
+  const int rows_left = p.M - row0;
+  int64_t co0 = (int64_t)row0 * p.ldc + n;
+  if constexpr (kAnyF32) {
+    if (p.c_group) co0 = (n / p.c_group) * p.c_gstride + (int64_t)row0 * p.ldc + n % p.c_group;
+  }
+  const bool f32 = EK == EK_F32 || (EK == EK_GENERIC && p.c_f32);
+  const int cs = f32 ? 4 : 2;
+  if (p.alpha != 1.f) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+  }
+  if constexpr (kAnyF32) {
+    if (p.splits > 1) {
+      staged_out(true, st, lane, v, static_cast<char*>(p.c) + co0 * 4, p.ldc * 4, rows_left, 1);
+      return;
     }
   }
-  if (p.act == ACT_GELU) {  // pre-activation to aux (same type and layout as C)
+  if constexpr (EK != EK_DGELU) {
+    if (p.bias) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n) + q);
+        v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
+      }
+    }
+  }
+  if (EK == EK_GELU || (EK == EK_GENERIC && p.act == ACT_GELU)) {
+    // pre-activation to aux (same type and layout as C)
     staged_out(f32, st, lane, v, static_cast<char*>(p.aux) + co0 * cs, p.ldc * cs, rows_left, 0);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = gelu_fast(v[i]);
-  } else if (p.act == ACT_DGELU) {
-    float a[32];
-    staged_in(f32, st, lane, a, static_cast<const char*>(p.aux) + co0 * cs, p.ldc * cs, rows_left);
+  } else if (EK == EK_DGELU || (EK == EK_GENERIC && p.act == ACT_DGELU)) {
+    if (EK == EK_DGELU || pre_kind == 1) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(a[i]);
-  }
-  if (p.resid) {
-    float r[32];
-    const int64_t ro = (int64_t)row0 * p.ld_resid + n;
-    staged_in(f32, st, lane, r, static_cast<const char*>(p.resid) + ro * cs, p.ld_resid * cs,
-              rows_left);
+      for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(pre[i]);
+    } else if constexpr (EK == EK_GENERIC) {
+      float a[32];
+      staged_in(f32, st, lane, a, static_cast<const char*>(p.aux) + co0 * cs, p.ldc * cs, rows_left);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += r[i];
+      for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(a[i]);
+    }
   }
-  staged_out(f32, st, lane, v, static_cast<char*>(p.c) + co0 * cs, p.ldc * cs, rows_left,
-             f32 && p.accumulate ? 2 : 0);
+  if constexpr (EK == EK_BF16 || EK == EK_GENERIC) {
+    if (p.resid) {
+      if (pre_kind == 2) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += pre[i];
+      } else if constexpr (EK == EK_GENERIC) {
+        float r[32];
+        const int64_t ro = (int64_t)row0 * p.ld_resid + n;
+        staged_in(f32, st, lane, r, static_cast<const char*>(p.resid) + ro * cs, p.ld_resid * cs,
+                  rows_left);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += r[i];
+      }
+    }
+  }
+  int mode = 0;
+  if constexpr (kAnyF32) mode = f32 && p.accumulate ? 2 : 0;
+  staged_out(f32, st, lane, v, static_cast<char*>(p.c) + co0 * cs, p.ldc * cs, rows_left, mode);
 }
 
-__device__ __forceinline__ void decode_unit(const Params& p, int u, int& m0, int& n0, int& kb0,
-                                            int& kb1) {
+__device__ __forceinline__ void decode_unit(const Params& p, int u, int mt_rows, int& m0, int& n0,
+                                            int& kb0, int& kb1) {
   const int s = u % p.splits;
   const int r = u / p.splits;
-  m0 = (r % p.m_tiles) * BM;
+  m0 = (r % p.m_tiles) * mt_rows;
   n0 = (r / p.m_tiles);  // scaled by BN by the caller
   const int num_kb = (p.K + BK - 1) / BK;
   kb0 = s * p.kb_per_split;
   kb1 = min(num_kb, kb0 + p.kb_per_split);
 }
 
-template <int BN>
+// Shared-memory plan of one (BN, CG) instantiation: as many pipeline stages
+// as fit next to the barriers and the epilogue staging tiles (4 for a 128x256
+// tile, 6 for 128x128 or a CTA pair's 128x128 half of 256x256).
+constexpr int kSmemBudget = 232448;  // 227 KB opt-in per CTA
+constexpr int kEpiStageBytes = 2048;  // per epilogue warp
+template <int BN, int CG>
+struct Tile {
+  static constexpr int BNL = BN / CG;  // B columns staged by this CTA
+  static constexpr uint32_t kBTileBytes = BNL * BK * 2;
+  static constexpr uint32_t kStageBytes = kATileBytes + kBTileBytes;
+  static constexpr int kFit = (kSmemBudget - 2048 - kEpiWarps * kEpiStageBytes) / kStageBytes;
+  static constexpr int kStages = kFit < 8 ? kFit : 8;
+  static constexpr size_t kSmem = kStages * kStageBytes + 1024 + kEpiWarps * kEpiStageBytes + 1024;
+  static_assert(kStages >= 3, "pipeline too shallow");
+  static_assert(kSmem <= kSmemBudget, "smem plan over budget");
+};
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// CG = 1: one CTA computes a 128 x BN tile.
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with
+//   tcgen05.mma.cta_group::2 (UMMA M = 256) issued by the leader; each CTA
+//   stages its own 128 rows of A and half (BN/2 columns) of B, so per-SM smem
+//   traffic per FLOP drops by a third.  Both CTAs' TMA complete on the
+//   leader's full barrier; commits multicast to both CTAs' empty / tmem_full
+//   barriers; both CTAs' epilogues release the leader's tmem_empty barrier.
+template <int BN, int CG, int EK>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const Params p) {
-  constexpr uint32_t kBTileBytes = BN * BK * 2;
-  constexpr uint32_t kStageBytes = kATileBytes + kBTileBytes;
+  using TL = Tile<BN, CG>;
+  constexpr int BNL = TL::BNL;
+  constexpr int STAGES = TL::kStages;
+  constexpr uint32_t kStageBytes = TL::kStageBytes;
   constexpr uint32_t kAccStride = BN <= 128 ? 128 : 256;  // TMEM columns per accumulator
   constexpr uint32_t kTmemCols = 2 * kAccStride;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -550,6 +771,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace_at(p, 0);
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const int unit0 = blockIdx.x / CG, unit_step = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -558,73 +782,119 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], kEpiWarps);
+      mbar_init(&tmem_empty[a], CG * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before use
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) trace_at(p, 1);
 
   if (warp == 0) {
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        int m0, nt, kb0, kb1;
-        decode_unit(p, u, m0, nt, kb0, kb1);
-        const int n0 = nt * BN;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], kStageBytes);
-          uint8_t* sa = smem + s * kStageBytes;
-          uint8_t* sb = sa + kATileBytes;
-          const int k0 = kb * BK;
-          if (p.a_mn) {
-            tma_2d(&map_a, &full[s], sa, m0, k0);
-            tma_2d(&map_a, &full[s], sa + 8192, m0 + 64, k0);
-          } else {
-            tma_2d(&map_a, &full[s], sa, k0, m0);
-          }
-          if (p.b_mn) {
+    // TMA producer (whole warp walks the ring, one elected lane issues).  An
+    // MN-major operand tile is BNL/64 (or 2 for A) 8 KB swizzle atoms; with
+    // the 3-D "atom" map (64 cols, K, col-block) it is ONE bulk-tensor load.
+    uint32_t it = 0;
+    for (int u = unit0; u < p.units; u += unit_step) {
+      int m0, nt, kb0, kb1;
+      decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
+      const int am0 = m0 + static_cast<int>(rank) * BM;       // this CTA's A rows
+      const int bn0 = nt * BN + static_cast<int>(rank) * BNL;  // this CTA's B columns
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        if (lane == 0) trace_at(p, kTrP + it, kTrF);
+        uint8_t* sa = smem + s * kStageBytes;
+        uint8_t* sb = sa + kATileBytes;
+        const int k0 = kb * BK;
+        if (elect_one()) {
+          if (p.debug & 1) {  // profiling mode: no loads, MMA on stale smem
+            if (rank == 0) mbar_arrive(&full[s]);
+          } else if constexpr (CG == 1) {
+            uint64_t* bar = &full[s];
+            mbar_expect_tx(bar, kStageBytes);
+            if (!p.a_mn) tma_2d(&map_a, bar, sa, k0, am0);
+            else if (p.a_atoms) tma_3d(&map_a, bar, sa, 0, k0, am0 / 64);
+            else {
+              tma_2d(&map_a, bar, sa, am0, k0);
+              tma_2d(&map_a, bar, sa + 8192, am0 + 64, k0);
+            }
+            if (!p.b_mn) {
+              if (p.b_grouped) tma_3d(&map_b, bar, sb, 0, bn0, kb);
+              else tma_2d(&map_b, bar, sb, k0, bn0);
+            } else if (p.b_atoms) {
+              tma_3d(&map_b, bar, sb, 0, k0, bn0 / 64);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
-              if (p.b_grouped)
-                tma_3d(&map_b, &full[s], sb + j * 8192, 0, k0, n0 / 64 + j);
-              else
-                tma_2d(&map_b, &full[s], sb + j * 8192, n0 + 64 * j, k0);
+              for (int j = 0; j < BNL / 64; ++j) tma_2d(&map_b, bar, sb + j * 8192, bn0 + 64 * j, k0);
             }
           } else {
-            if (p.b_grouped)
-              tma_3d(&map_b, &full[s], sb, 0, n0, kb);
-            else
-              tma_2d(&map_b, &full[s], sb, k0, n0);
+            // both CTAs' bytes land on the leader's full barrier
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * kStageBytes);
+            const uint32_t bar = mapa_shared(smem_u32(&full[s]), 0);
+            if (!p.a_mn) tma_2d_cg2(&map_a, bar, sa, k0, am0);
+            else if (p.a_atoms) tma_3d_cg2(&map_a, bar, sa, 0, k0, am0 / 64);
+            else {
+              tma_2d_cg2(&map_a, bar, sa, am0, k0);
+              tma_2d_cg2(&map_a, bar, sa + 8192, am0 + 64, k0);
+            }
+            if (!p.b_mn) {
+              if (p.b_grouped) tma_3d_cg2(&map_b, bar, sb, 0, bn0, kb);
+              else tma_2d_cg2(&map_b, bar, sb, k0, bn0);
+            } else if (p.b_atoms) {
+              tma_3d_cg2(&map_b, bar, sb, 0, k0, bn0 / 64);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BNL / 64; ++j) tma_2d_cg2(&map_b, bar, sb + j * 8192, bn0 + 64 * j, k0);
+            }
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // The whole warp walks the pipeline (so every value feeding tcgen05.mma is
+    // warp-uniform); one elected lane issues the MMAs and their commit.
+    if (rank == 0) {
       // kind::f16 instruction descriptor: D f32, A/B bf16, majors, N>>3, M>>4
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
                              (static_cast<uint32_t>(p.a_mn) << 15) |
                              (static_cast<uint32_t>(p.b_mn) << 16) |
                              (static_cast<uint32_t>(BN >> 3) << 17) |
-                             (static_cast<uint32_t>(BM >> 4) << 24);
+                             (static_cast<uint32_t>((BM * CG) >> 4) << 24);
+      // Descriptors of stage 0, k-step 0; stage s / k-step k add plain offsets
+      // to the 14-bit start-address field (smem < 256 KB: no carry out).
+      // K-major: 128B rows, 8-row groups 1024B apart, +32B per UMMA_K.
+      // MN-major: 64-wide MN atoms 8KB apart (LBO), 8-row K groups 1024B
+      // apart (SBO), +16 rows (2048B) per UMMA_K.
+      const uint32_t s0 = smem_u32(smem);
+      const uint64_t da0 = umma_desc(s0, p.a_mn ? 8192 : 16, 1024);
+      const uint64_t db0 = umma_desc(s0 + kATileBytes, p.b_mn ? 8192 : 16, 1024);
+      const uint64_t dak = p.a_mn ? (2048 >> 4) : (32 >> 4);
+      const uint64_t dbk = p.b_mn ? (2048 >> 4) : (32 >> 4);
       uint32_t it = 0, lt = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++lt) {
+      for (int u = unit0; u < p.units; u += unit_step, ++lt) {
         int m0, nt, kb0, kb1;
-        decode_unit(p, u, m0, nt, kb0, kb1);
+        decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
         const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
         mbar_wait(&tmem_empty[as], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -633,70 +903,124 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
+          if (lane == 0) trace_at(p, kTrF + it, kTrC);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa = smem_u32(smem + s * kStageBytes);
-          const uint32_t sb = sa + kATileBytes;
+          const uint64_t soff = static_cast<uint64_t>(s) * (kStageBytes >> 4);
+          if (elect_one()) {
+            if (!(p.debug & 2)) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: 128B rows, 8-row groups 1024B apart, +32B per UMMA_K.
-            // MN-major: 64-wide MN atoms 8KB apart (LBO), 8-row K groups
-            // 1024B apart (SBO), +16 rows (2048B) per UMMA_K.
-            const uint64_t ad = p.a_mn ? umma_desc(sa + k * 2048, 8192, 1024)
-                                       : umma_desc(sa + k * 32, 16, 1024);
-            const uint64_t bd = p.b_mn ? umma_desc(sb + k * 2048, 8192, 1024)
-                                       : umma_desc(sb + k * 32, 16, 1024);
-            umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < BK / 16; ++k) {
+                const uint64_t ad = da0 + soff + k * dak, bd = db0 + soff + k * dbk;
+                if constexpr (CG == 2)
+                  umma_bf16_cg2(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                else
+                  umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              }
+            }
+            if constexpr (CG == 2) umma_commit_cg2(&empty[s]); else umma_commit(&empty[s]);
           }
-          umma_commit(&empty[s]);
+          __syncwarp();
+          if (lane == 0) trace_at(p, kTrC + it, kTrE);
         }
-        umma_commit(&tmem_full[as]);
+        if (elect_one()) {
+          if constexpr (CG == 2) umma_commit_cg2(&tmem_full[as]); else umma_commit(&tmem_full[as]);
+        }
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else {
-    // epilogue warps 2..17: lane quarter = warp % 4 (the TMEM lanes a warp
-    // may access); the tile's 32-column chunks are dealt round-robin to the
-    // four warps of a quarter; each chunk is staged through the warp's own
-    // 2 KB smem tile for coalesced global traffic
+    // epilogue warps 2..kEpiWarps+1: lane quarter = warp % 4 (the TMEM lanes
+    // a warp may access); a quarter's 32-column chunks are dealt round-robin
+    // to its kEpiWarps/4 warps; each chunk is staged through the warp's own
+    // 2 KB smem tile for coalesced global traffic.
+    constexpr int kChunkStep = 32 * (kEpiWarps / 4);
+    const int ew = warp - 2;
     const int quarter = warp & 3;
-    const int slice = (warp - 2) >> 2;
-    uint8_t* st = smem + STAGES * kStageBytes + 1024 + (warp - 2) * 2048;
+    const int first = (ew >> 2) * 32;
+    const uint32_t st = smem_u32(smem + STAGES * kStageBytes + 1024 + ew * kEpiStageBytes);
+    // operand prefetched a chunk ahead: 1 = dGELU pre-activation, 2 = residual
+    int pre_kind = 0;
+    if constexpr (EK == EK_DGELU) pre_kind = 1;
+    if constexpr (EK == EK_BF16) pre_kind = p.resid ? 2 : 0;
+    if constexpr (EK == EK_GENERIC)
+      pre_kind = (!p.c_f32 && p.vec == 1 && p.splits == 1) ? (p.act == ACT_DGELU ? 1 : (p.resid ? 2 : 0)) : 0;
+    const char* pre_base = static_cast<const char*>(pre_kind == 1 ? p.aux : p.resid);
+    const int64_t pre_ld = pre_kind == 1 ? p.ldc : p.ld_resid;
     uint32_t lt = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++lt) {
+    const uint32_t empty_leader[2] = {CG == 2 ? mapa_shared(smem_u32(&tmem_empty[0]), 0) : 0u,
+                                      CG == 2 ? mapa_shared(smem_u32(&tmem_empty[1]), 0) : 0u};
+    for (int u = unit0; u < p.units; u += unit_step, ++lt) {
       int m0, nt, kb0, kb1;
-      decode_unit(p, u, m0, nt, kb0, kb1);
+      decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
       const int n0 = nt * BN;
       const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
+      const int row0 = m0 + static_cast<int>(rank) * BM + quarter * 32;
+      const int rows_left = p.M - row0;
+      // chunk at tile column c takes the staged path with a prefetched operand
+      auto pre_ok = [&](int c) { return pre_kind != 0 && c < BN && n0 + c + 32 <= p.N && rows_left > 0; };
+      auto pre_src = [&](int c) {
+        const int n = n0 + c;
+        const int64_t o = (EK == EK_GENERIC && pre_kind == 1 && p.c_group)
+                              ? (n / p.c_group) * p.c_gstride + (int64_t)row0 * p.ldc + n % p.c_group
+                              : (int64_t)row0 * pre_ld + n;
+        return pre_base + o * 2;
+      };
+      uint4 cur[4], nxt[4];
+      if (pre_ok(first)) pre_issue(pre_src(first), pre_ld * 2, rows_left, lane, cur);
       mbar_wait(&tmem_full[as], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row0 = m0 + quarter * 32;
+      if (warp == 2 && lane == 0) trace_at(p, kTrE + 2 * lt, kTrSlots);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * kAccStride;
 #pragma unroll 1
-      for (int c0 = slice * 32; c0 < BN; c0 += 128) {
+      for (int c = first; c < BN; c += kChunkStep) {
+        if (pre_ok(c + kChunkStep)) pre_issue(pre_src(c + kChunkStep), pre_ld * 2, rows_left, lane, nxt);
+        const bool tr = warp == 2 && lane == 0 && lt == 0;
+        const int tslot = kTrX + 3 * ((c - first) / kChunkStep);
+        if (tr) trace_at(p, tslot, 1024);
         uint32_t r[32];
-        TMEM_LD32(taddr + c0, r);
+        TMEM_LD32(taddr + c, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const int n = n0 + c0;
-        if (n < p.N && row0 < p.M) {
+        if (tr) trace_at(p, tslot + 1, 1024);
+        const int n = n0 + c;
+        if (n < p.N && rows_left > 0 && !(p.debug & 4)) {
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (n + 32 <= p.N && p.vec == 1)
-            epilogue_staged(p, st, lane, row0, n, v);
-          else
+          // specialised kinds are only launched with N % 32 == 0, vec == 1
+          if (EK != EK_GENERIC || (n + 32 <= p.N && p.vec == 1)) {
+            float a[32];
+            if (pre_kind) pre_consume(st, lane, cur, a);
+            epilogue_staged<EK>(p, st, lane, row0, n, v, a, pre_kind);
+          } else if constexpr (EK == EK_GENERIC) {
             epilogue_cols<32>(p, row0 + lane, n, v);
+          }
         }
+        if (tr) trace_at(p, tslot + 2, 1024);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[as]);
+      if (warp == 2 && lane == 0) trace_at(p, kTrE + 2 * lt + 1, kTrSlots);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(empty_leader[as]);
+        else
+          mbar_arrive(&tmem_empty[as]);
+      }
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_at(p, 2);
+  if constexpr (CG == 2) cluster_sync_all();  // both CTAs done before the pair frees TMEM
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols));
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols));
   }
 }
 
@@ -759,6 +1083,8 @@ int num_sms() {
 
 int g_force_bn = 0;
 int g_force_splits = 0;
+int g_debug_mode = 0;
+unsigned long long* g_trace = nullptr;
 
 }  // namespace
 
@@ -795,76 +1121,138 @@ static int epilogue_vec_ok(const GemmArgs& g) {
   return 0;
 }
 
-template <int BN>
+template <int BN, int CG, int EK>
 static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Params& p,
                       cudaStream_t s) {
-  // stages + barriers (1 KB) + 16 epilogue staging tiles (2 KB) + alignment slack
-  constexpr size_t smem = tc::STAGES * (tc::kATileBytes + BN * tc::BK * 2) + 1024 +
-                          tc::kEpiWarps * 2048 + 1024;
+  // stages + barriers (1 KB) + epilogue staging tiles + alignment slack
+  constexpr size_t smem = tc::Tile<BN, CG>::kSmem;
   static bool attr = false;
   if (!attr) {
-    HP_CUDA(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    HP_CUDA(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, CG, EK>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int grid = std::min(p.units, num_sms());
-  tc::gemm_tc_kernel<BN><<<grid, tc::kThreads, smem, s>>>(ma, mb, p);
+  const int grid = CG * std::min(p.units, num_sms() / CG);
+  if constexpr (CG == 1) {
+    tc::gemm_tc_kernel<BN, 1, EK><<<grid, tc::kThreads, smem, s>>>(ma, mb, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HP_CUDA(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BN, 2, EK>, ma, mb, p));
+  }
   HP_CUDA(cudaGetLastError());
   count_launch();
 }
 
+namespace {
+int g_force_cg = 0;
+int g_generic_only = 0;
+}
+void gemm_tc_set_generic(int on) { g_generic_only = on; }
+
+template <int EK>
+static void launch_ek(int cg, int bn, const CUtensorMap& ma, const CUtensorMap& mb,
+                      const tc::Params& p, cudaStream_t s) {
+  if (cg == 2) {
+    if (bn == 256) launch_tc<256, 2, EK>(ma, mb, p, s);
+    else launch_tc<128, 2, EK>(ma, mb, p, s);
+  } else {
+    if (bn == 256) launch_tc<256, 1, EK>(ma, mb, p, s);
+    else if (bn == 192) launch_tc<192, 1, EK>(ma, mb, p, s);
+    else launch_tc<128, 1, EK>(ma, mb, p, s);
+  }
+}
+void gemm_tc_set_cg(int cg) { g_force_cg = cg; }
+void gemm_tc_set_debug(int mode) { g_debug_mode = mode; }
+void gemm_tc_set_trace(unsigned long long* buf) { g_trace = buf; }
+
 void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (!gemm_tc_supported(g)) fail(HP_ECONFIG, "gemm_tc: unsupported operand layout");
   const int nsm = num_sms();
-  const int m_tiles = (g.M + tc::BM - 1) / tc::BM;
   const int num_kb = (g.K + tc::BK - 1) / tc::BK;
   const bool can_split = g.ct == DType::f32 && !g.bias && !g.act && !g.resid && !g.accumulate;
-  // Pick the N tile (and split-K factor) maximising SM-wave efficiency;
-  // ties go to the wider tile (more reuse per byte staged).
-  int bn = 256, splits = 1;
+  // Pick (CTA group, N tile, split-K) maximising SM-wave efficiency weighted
+  // by the tile's operand reuse: a CTA pair with a 256-wide tile stages the
+  // fewest bytes per FLOP, one CTA with a 128-wide tile the most.
+  int bn = 256, cg = 2, splits = 1;
   double best = -1;
-  for (int cand : {256, 192, 128}) {
-    if (g.b.group && !g.b.trans && cand % 64) continue;
-    const int tiles = m_tiles * ((g.N + cand - 1) / cand);
+  const int cands[5][3] = {{2, 256, 118}, {2, 128, 100}, {1, 256, 100}, {1, 192, 97}, {1, 128, 90}};
+  for (const auto& c : cands) {
+    const int ccg = c[0], cbn = c[1];
+    if (g_force_cg && ccg != g_force_cg) continue;
+    if (g_force_bn && cbn != g_force_bn) continue;
+    if (g.b.group && !g.b.trans && (cbn / ccg) % 64) continue;
+    const int mt = (g.M + tc::BM * ccg - 1) / (tc::BM * ccg);
+    const int tiles = mt * ((g.N + cbn - 1) / cbn);
+    const int slots = nsm / ccg;
     int sp = 1;
-    if (can_split && tiles < nsm) sp = std::max(1, std::min(nsm / tiles, num_kb / 4));
+    if (can_split && tiles < slots) sp = std::max(1, std::min(slots / tiles, num_kb / 4));
     const int units = tiles * sp;
-    const int waves = (units + nsm - 1) / nsm;
-    const double eff = static_cast<double>(units) / (waves * nsm) * (cand == 256 ? 1.0 : cand == 192 ? 0.97 : 0.93);
+    const int waves = (units + slots - 1) / slots;
+    const double eff = static_cast<double>(units) / (waves * slots) * c[2] / 100.0;
     if (eff > best + 1e-9) {
       best = eff;
-      bn = cand;
+      bn = cbn;
+      cg = ccg;
       splits = sp;
     }
   }
-  if (g_force_bn) bn = g_force_bn;
   if (g_force_splits && can_split) splits = g_force_splits;
   if (!can_split) splits = 1;
+  const int m_tiles = (g.M + tc::BM * cg - 1) / (tc::BM * cg);
   const int kb_per_split = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per_split - 1) / kb_per_split;  // no empty splits
+  const int bnl = bn / cg;  // B columns per CTA
 
+  // MN-major operands: "atom" maps view the row-major [K][MN] matrix as
+  // (64 cols, K rows, MN/64 col-blocks) so one box brings every 8 KB swizzle
+  // atom of a tile.  The last col-block may read past column MN (garbage in
+  // discarded output rows / cols) but never past the row pitch.
+  const int a_blocks = (g.M + 63) / 64, b_blocks = (g.N + 63) / 64;
+  const bool a_atoms = g.a.trans && 64LL * a_blocks <= g.a.ld;
+  const bool b_atoms = !g.b.trans && (g.b.group || 64LL * b_blocks <= g.b.ld);
   CUtensorMap ma, mb;
   {
-    uint64_t dims[2], str[1];
-    uint32_t box[2];
-    if (g.a.trans) {  // memory [K rows][M cols]
+    uint64_t dims[3], str[2];
+    uint32_t box[3];
+    int rank = 2;
+    if (g.a.trans && a_atoms) {  // memory [K rows][M cols], atom view
+      rank = 3;
+      dims[0] = 64; dims[1] = g.K; dims[2] = a_blocks;
+      str[0] = g.a.ld; str[1] = 64;
+      box[0] = 64; box[1] = 64; box[2] = tc::BM / 64;
+    } else if (g.a.trans) {
       dims[0] = g.M; dims[1] = g.K; str[0] = g.a.ld; box[0] = 64; box[1] = 64;
     } else {          // memory [M rows][K cols]
       dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = tc::BM;
     }
-    ma = make_map(g.a.p, 2, dims, str, box);
+    ma = make_map(g.a.p, rank, dims, str, box);
   }
   {
     uint64_t dims[3], str[2];
     uint32_t box[3];
     int rank = 2;
     if (!g.b.trans) {  // MN-major: memory [K rows][N cols] (or grouped blocks)
+      rank = 3;
+      box[0] = 64; box[1] = 64; box[2] = (uint32_t)(bnl / 64);
       if (g.b.group) {
-        rank = 3;
         dims[0] = 64; dims[1] = g.K; dims[2] = g.N / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
-        box[0] = 64; box[1] = 64; box[2] = 1;
+      } else if (b_atoms) {
+        dims[0] = 64; dims[1] = g.K; dims[2] = b_blocks;
+        str[0] = g.b.ld; str[1] = 64;
       } else {
+        rank = 2;
         dims[0] = g.N; dims[1] = g.K; str[0] = g.b.ld; box[0] = 64; box[1] = 64;
       }
     } else {           // K-major: memory [N rows][K cols] (or grouped along K)
@@ -872,9 +1260,9 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         rank = 3;
         dims[0] = 64; dims[1] = g.N; dims[2] = g.K / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
-        box[0] = 64; box[1] = (uint32_t)bn; box[2] = 1;
+        box[0] = 64; box[1] = (uint32_t)bnl; box[2] = 1;
       } else {
-        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64; box[1] = (uint32_t)bn;
+        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64; box[1] = (uint32_t)bnl;
       }
     }
     mb = make_map(g.b.p, rank, dims, str, box);
@@ -884,16 +1272,20 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.a_mn = g.a.trans ? 1 : 0;
   p.b_mn = g.b.trans ? 0 : 1;
   p.b_grouped = g.b.group ? 1 : 0;
+  p.a_atoms = a_atoms ? 1 : 0;
+  p.b_atoms = b_atoms ? 1 : 0;
   p.m_tiles = m_tiles;
   p.n_tiles = (g.N + bn - 1) / bn;
   p.splits = splits;
   p.kb_per_split = kb_per_split;
   p.units = m_tiles * p.n_tiles * splits;
-  p.c = g.c; p.ldc = g.ldc; p.c_group = g.c_group; p.c_gstride = g.c_gstride;
+  p.c = g.c; p.ldc = g.ldc; p.c_group = static_cast<int>(g.c_group); p.c_gstride = g.c_gstride;
   p.c_f32 = g.ct == DType::f32;
   p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias; p.act = g.act;
   p.aux = g.aux; p.resid = g.resid; p.ld_resid = g.ld_resid;
   p.vec = epilogue_vec_ok(g);
+  p.debug = g_debug_mode;
+  p.trace = g_trace;
   if (splits > 1) {
     // partial sums are reduced into C: clear the output region first
     if (g.c_group) {
@@ -902,12 +1294,25 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
       HP_CUDA(cudaMemset2DAsync(g.c, sizeof(float) * g.ldc, 0, sizeof(float) * g.N, g.M, s));
     }
   }
-  if (bn == 256)
-    launch_tc<256>(ma, mb, p, s);
-  else if (bn == 192)
-    launch_tc<192>(ma, mb, p, s);
-  else
-    launch_tc<128>(ma, mb, p, s);
+  // epilogue kind (see tc::EpiKind); specialised kinds need whole 32-column
+  // chunks and 16-byte aligned rows
+  int ek = tc::EK_GENERIC;
+  if (p.vec == 1 && g.N % 32 == 0 && !g_generic_only) {
+    if (g.ct == DType::bf16 && !g.c_group && splits == 1) {
+      if (g.act == ACT_NONE) ek = tc::EK_BF16;
+      else if (g.act == ACT_GELU && !g.resid) ek = tc::EK_GELU;
+      else if (g.act == ACT_DGELU && !g.resid && !g.bias) ek = tc::EK_DGELU;
+    } else if (g.ct == DType::f32 && g.act == ACT_NONE && !g.resid) {
+      ek = tc::EK_F32;
+    }
+  }
+  switch (ek) {
+    case tc::EK_BF16: launch_ek<tc::EK_BF16>(cg, bn, ma, mb, p, s); break;
+    case tc::EK_GELU: launch_ek<tc::EK_GELU>(cg, bn, ma, mb, p, s); break;
+    case tc::EK_DGELU: launch_ek<tc::EK_DGELU>(cg, bn, ma, mb, p, s); break;
+    case tc::EK_F32: launch_ek<tc::EK_F32>(cg, bn, ma, mb, p, s); break;
+    default: launch_ek<tc::EK_GENERIC>(cg, bn, ma, mb, p, s); break;
+  }
 }
 
 }  // namespace hp

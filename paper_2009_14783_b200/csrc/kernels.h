@@ -54,6 +54,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s);
 void gemm_tc_force(int mode);  // test hook: 0 auto, 1 never tcgen05
 void gemm_tc_set_bn(int bn);   // test hook: 0 heuristic, 128, 192 or 256
 void gemm_tc_set_splits(int s);  // test hook: 0 heuristic, else forced split-K
+void gemm_tc_set_cg(int cg);     // test hook: 0 heuristic, 1 single CTA, 2 CTA pair
+void gemm_tc_set_debug(int mode);  // profiling hook: bits 1 no loads, 2 no MMA, 4 no epilogue
+void gemm_tc_set_trace(unsigned long long* buf);  // profiling hook: CTA 0 clock64 timeline
+void gemm_tc_set_generic(int on);  // test hook: 1 forces the generic (all-flags) epilogue
 
 // Device batch (one rank batch, SoA int32), see engine.cpp.
 struct DevBatch {

@@ -88,6 +88,16 @@ def run_gemm(M, N, K, dtype, a_trans, b_trans, path, bn=0, group=0, bias=False, 
     return res
 
 
+@pytest.fixture(params=[0, 1], ids=["specialised", "generic"])
+def epi_kind(request):
+    """Run a test with the per-kind specialised epilogue kernels (default
+    selection) and again with every launch forced onto the generic one."""
+    L = _lib()
+    L.call("hp_debug_gemm_generic", request.param)
+    yield request.param
+    L.call("hp_debug_gemm_generic", 0)
+
+
 def _tol(dtype, K):
     return (2e-2 if dtype == torch.bfloat16 else 1e-4) * max(1.0, (K / 64) ** 0.5)
 
@@ -100,7 +110,7 @@ def _check(res, dtype, K):
 
 @pytest.mark.parametrize("a_trans", [0, 1])
 @pytest.mark.parametrize("b_trans", [0, 1])
-@pytest.mark.parametrize("bn", [128, 192, 256])
+@pytest.mark.parametrize("bn", [1128, 1192, 1256, 2128, 2256])
 def test_tc_gemm_layouts(a_trans, b_trans, bn):
     res = run_gemm(384, 512, 320, torch.bfloat16, a_trans, b_trans, path=2, bn=bn, c_dtype=torch.float32)
     _check(res, torch.bfloat16, 320)
@@ -121,13 +131,13 @@ def test_tc_gemm_grouped_heads(b_trans):
     _check(res, torch.bfloat16, 384)
 
 
-def test_tc_gemm_grouped_output():
+def test_tc_gemm_grouped_output(epi_kind):
     # QKV wgrad: C scattered into [N/64][M][64] blocks (fp32 flat gradient)
     res = run_gemm(256, 384, 512, torch.bfloat16, 1, 0, path=2, c_dtype=torch.float32, c_group=64)
     _check(res, torch.bfloat16, 512)
 
 
-def test_tc_gemm_epilogues():
+def test_tc_gemm_epilogues(epi_kind):
     res = run_gemm(256, 512, 256, torch.bfloat16, 0, 0, path=2, bias=True, act=1)
     _check(res, torch.bfloat16, 256)
     assert (res["aux"] - res["pre"]).abs().max().item() < 0.05 * res["pre"].abs().max().item()
@@ -227,19 +237,42 @@ def test_attention_varlen_fwd_bwd(path, dtype, dk):
 
 
 @pytest.mark.parametrize("splits", [2, 3, 8])
-def test_tc_gemm_split_k(splits):
+def test_tc_gemm_split_k(splits, epi_kind):
     # weight-gradient shape: few output tiles, long K -> split-K reductions
-    res = run_gemm(256, 384, 2048, torch.bfloat16, 1, 0, path=2, bn=128 + 1000 * splits,
+    res = run_gemm(256, 384, 2048, torch.bfloat16, 1, 0, path=2, bn=128 + 1000 + 10000 * splits,
                    c_dtype=torch.float32)
     _check(res, torch.bfloat16, 2048)
-    res = run_gemm(128, 192, 1024, torch.bfloat16, 1, 0, path=2, bn=192 + 1000 * splits,
+    res = run_gemm(128, 192, 1024, torch.bfloat16, 1, 0, path=2, bn=192 + 1000 + 10000 * splits,
                    c_dtype=torch.float32, c_group=64)
     _check(res, torch.bfloat16, 1024)
+    # CTA-pair split-K
+    res = run_gemm(512, 512, 2048, torch.bfloat16, 1, 0, path=2, bn=256 + 2000 + 10000 * splits,
+                   c_dtype=torch.float32)
+    _check(res, torch.bfloat16, 2048)
 
 
-def test_tc_gemm_auto_heuristic_shapes():
+def test_tc_gemm_auto_heuristic_shapes(epi_kind):
     # the engine's shapes at small scale: auto BN / split choice
     for (M, N, K, at, bt, ct) in [(512, 768, 768, 0, 0, torch.bfloat16), (768, 768, 512, 1, 0, torch.float32),
                                   (512, 2304, 768, 0, 0, torch.bfloat16), (512, 768, 2304, 0, 1, torch.bfloat16)]:
         res = run_gemm(M, N, K, torch.bfloat16, at, bt, path=2, c_dtype=ct)
         _check(res, torch.bfloat16, K)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_tc_gemm_pair_and_single_edge_cases(cg, epi_kind):
+    tile = 256
+    code = cg * 1000 + tile
+    for (M, N, K, at, bt) in [(600, 1000, 200, 0, 0), (130, 264, 104, 0, 1), (512, 384, 64, 1, 0)]:
+        res = run_gemm(M, N, K, torch.bfloat16, at, bt, path=2, bn=code, c_dtype=torch.float32)
+        _check(res, torch.bfloat16, K)
+    res = run_gemm(512, 384, 384, torch.bfloat16, 0, 0, path=2, bn=code, group=64)
+    _check(res, torch.bfloat16, 384)
+    res = run_gemm(512, 384, 384, torch.bfloat16, 0, 1, path=2, bn=code, group=64)
+    _check(res, torch.bfloat16, 384)
+    res = run_gemm(512, 512, 256, torch.bfloat16, 0, 0, path=2, bn=code, bias=True, act=1)
+    _check(res, torch.bfloat16, 256)
+    res = run_gemm(512, 512, 256, torch.bfloat16, 0, 1, path=2, bn=code, act=2, resid=True)
+    _check(res, torch.bfloat16, 256)
+    res = run_gemm(256, 384, 512, torch.bfloat16, 1, 0, path=2, bn=code, c_dtype=torch.float32, c_group=64)
+    _check(res, torch.bfloat16, 512)

@@ -87,6 +87,9 @@ def run(shape, iters, bn):
         _lib.call("hp_debug_gemm", *args)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # keep the GPU busy while the host enqueues, so the timed launches run
+    # back to back (device time, not host launch overhead)
+    torch.cuda._sleep(100_000_000)
     e0.record()
     for _ in range(iters):
         _lib.call("hp_debug_gemm", *args)
@@ -101,6 +104,7 @@ def run(shape, iters, bn):
     for _ in range(3):
         torch.matmul(x, y)
     torch.cuda.synchronize()
+    torch.cuda._sleep(100_000_000)
     e0.record()
     for _ in range(iters):
         torch.matmul(x, y)
