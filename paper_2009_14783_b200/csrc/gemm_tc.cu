@@ -70,8 +70,22 @@ struct Params {
 // [16+512+it] MMA committed, [16+768+2*t] epilogue tile t start / +1 end
 constexpr int kTrP = 16, kTrF = 16 + 256, kTrC = 16 + 512, kTrE = 16 + 768, kTrSlots = 16 + 768 + 64;
 constexpr int kTrX = 900;  // tile 0, warp 2: per chunk [before tcgen05.ld, after wait, after epilogue]
+// Profiling hooks (timeline trace, debug bits) exist only in builds with
+// HP_GEMM_PROFILE defined (HP_GEMM_PROFILE=1 tools/build_native.py); they cost
+// registers the production kernels need.
+#ifdef HP_GEMM_PROFILE
+constexpr bool kProfile = true;
+#else
+constexpr bool kProfile = false;
+#endif
 __device__ __forceinline__ void trace_at(const Params& p, int slot, int lim = 1 << 30) {
-  if (p.trace && blockIdx.x == 0 && slot < lim) p.trace[slot] = clock64();
+  if constexpr (kProfile) {
+    if (p.trace && blockIdx.x == 0 && slot < lim) p.trace[slot] = clock64();
+  }
+}
+__device__ __forceinline__ bool debug_bit(const Params& p, int bit) {
+  if constexpr (kProfile) return (p.debug & bit) != 0;
+  return false;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -167,8 +181,12 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
+// Epilogue -> leader "accumulator drained" arrive.  Relaxed: the TMEM reads it
+// publishes are ordered by tcgen05.wait::ld + tcgen05.fence::before_thread_sync,
+// and a release here would stall on every outstanding global store
+// (MEMBAR.ALL.GPU) at each tile end.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
 // TMA load into this CTA's smem, completing bytes on the (leader's) barrier
@@ -616,12 +634,13 @@ __device__ __forceinline__ void pre_issue(const char* g0, int64_t ld_bytes, int 
                          : make_uint4(0, 0, 0, 0);
   }
 }
-// prefetched pieces -> staging tile -> row `lane` as floats
-__device__ __forceinline__ void pre_consume(uint32_t st, int lane, const uint4 (&q)[4], float* out) {
+// prefetched pieces -> staging tile -> row `lane` (32 bf16, kept packed)
+__device__ __forceinline__ void pre_consume(uint32_t st, int lane, const uint4 (&q)[4], uint4 (&row)[4]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) sts128(st + Stage<2>::off(i * 8 + lane / 4, lane % 4), q[i]);
   __syncwarp();
-  stage_get<2>(st, lane, out);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) row[j] = lds128(st + Stage<2>::off(lane, j));
   __syncwarp();
 }
 
@@ -641,7 +660,7 @@ enum EpiKind : int {
 // the prefetched aux (pre_kind 1, dGELU) or residual (pre_kind 2) chunk.
 template <int EK>
 __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, int lane, int row0,
-                                                int n, float* v, const float* pre, int pre_kind) {
+                                                int n, float* v, const uint4 (&pre)[4], int pre_kind) {
   constexpr bool kAnyF32 = EK == EK_GENERIC || EK == EK_F32;
   const int rows_left = p.M - row0;
   int64_t co0 = (int64_t)row0 * p.ldc + n;
@@ -677,7 +696,12 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, in
   } else if (EK == EK_DGELU || (EK == EK_GENERIC && p.act == ACT_DGELU)) {
     if (EK == EK_DGELU || pre_kind == 1) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(pre[i]);
+      for (int j = 0; j < 4; ++j) {
+        float f[8];
+        unpack8_bf16(pre[j], f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[8 * j + e] *= dgelu_fast(f[e]);
+      }
     } else if constexpr (EK == EK_GENERIC) {
       float a[32];
       staged_in(f32, st, lane, a, static_cast<const char*>(p.aux) + co0 * cs, p.ldc * cs, rows_left);
@@ -689,7 +713,12 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, in
     if (p.resid) {
       if (pre_kind == 2) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] += pre[i];
+        for (int j = 0; j < 4; ++j) {
+          float f[8];
+          unpack8_bf16(pre[j], f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[8 * j + e] += f[e];
+        }
       } else if constexpr (EK == EK_GENERIC) {
         float r[32];
         const int64_t ro = (int64_t)row0 * p.ld_resid + n;
@@ -827,7 +856,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* sb = sa + kATileBytes;
         const int k0 = kb * BK;
         if (elect_one()) {
-          if (p.debug & 1) {  // profiling mode: no loads, MMA on stale smem
+          if (debug_bit(p, 1)) {  // profiling mode: no loads, MMA on stale smem
             if (rank == 0) mbar_arrive(&full[s]);
           } else if constexpr (CG == 1) {
             uint64_t* bar = &full[s];
@@ -907,7 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t soff = static_cast<uint64_t>(s) * (kStageBytes >> 4);
           if (elect_one()) {
-            if (!(p.debug & 2)) {
+            if (!debug_bit(p, 2)) {
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k) {
                 const uint64_t ad = da0 + soff + k * dak, bd = db0 + soff + k * dbk;
@@ -974,7 +1003,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = first; c < BN; c += kChunkStep) {
         if (pre_ok(c + kChunkStep)) pre_issue(pre_src(c + kChunkStep), pre_ld * 2, rows_left, lane, nxt);
-        const bool tr = warp == 2 && lane == 0 && lt == 0;
+        const bool tr = kProfile && warp == 2 && lane == 0 && lt == 0;
         const int tslot = kTrX + 3 * ((c - first) / kChunkStep);
         if (tr) trace_at(p, tslot, 1024);
         uint32_t r[32];
@@ -982,15 +1011,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (tr) trace_at(p, tslot + 1, 1024);
         const int n = n0 + c;
-        if (n < p.N && rows_left > 0 && !(p.debug & 4)) {
+        if (n < p.N && rows_left > 0 && !debug_bit(p, 4)) {
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           // specialised kinds are only launched with N % 32 == 0, vec == 1
           if (EK != EK_GENERIC || (n + 32 <= p.N && p.vec == 1)) {
-            float a[32];
-            if (pre_kind) pre_consume(st, lane, cur, a);
-            epilogue_staged<EK>(p, st, lane, row0, n, v, a, pre_kind);
+            uint4 pre[4];
+            if (pre_kind) pre_consume(st, lane, cur, pre);
+            epilogue_staged<EK>(p, st, lane, row0, n, v, pre, pre_kind);
           } else if constexpr (EK == EK_GENERIC) {
             epilogue_cols<32>(p, row0 + lane, n, v);
           }

@@ -31,17 +31,21 @@ def nccl_dir() -> str:
 
 
 def build(verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+    # HP_GEMM_PROFILE=1: compile the GEMM's timeline trace / debug hooks in
+    # (tools/gemm_trace.py); separate object dir so builds never mix
+    profile = os.environ.get("HP_GEMM_PROFILE") == "1"
+    obj_dir = OBJ + ("_profile" if profile else "")
+    os.makedirs(obj_dir, exist_ok=True)
     nd = nccl_dir()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include")]
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-                    "--expt-relaxed-constexpr"] + inc
+                    "--expt-relaxed-constexpr"] + inc + (["-DHP_GEMM_PROFILE"] if profile else [])
     srcs = sorted(glob.glob(os.path.join(SRC, "*.cu")) + glob.glob(os.path.join(SRC, "*.cpp")))
     hdrs = glob.glob(os.path.join(SRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
 
     def compile_one(src: str) -> str:
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), newest_hdr):
             return obj
         cmd = [NVCC] + flags + ["-c", src, "-o", obj]
