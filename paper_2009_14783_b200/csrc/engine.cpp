@@ -18,6 +18,8 @@
 //     refreshes the bf16 working copy the tcgen05 GEMMs read.
 #include "engine.h"
 
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -27,6 +29,8 @@
 #include "hp_common.h"
 
 namespace hp {
+
+constexpr int kEmbHotTokens = 32;  // = kEmbHot in kernels.cu
 
 namespace {
 uint64_t pad8(uint64_t v) { return (v + 7) & ~uint64_t(7); }
@@ -176,9 +180,17 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     HP_CUDA(cudaMemcpy(pe_, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice));
   }
 
+  // masked positions are padded to a multiple of mpad_ (index -1 rows: no
+  // loss, no gradient) so CUDA graphs keyed by the padded count get reused
+  mpad_ = bf16_ ? 64 : 1;
+  {
+    const char* e = std::getenv("HP_GRAPHS");
+    graphs_on_ = !(e && std::string(e) == "0");
+  }
   // staged batch block (fixed layout at capacity)
-  const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch, Mm = std::max<uint64_t>(x_.max_masks, 1);
-  const size_t ints = 3 * Tm + (Bm + 1) + 2 * Mm + Bm;
+  const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch,
+                 Mm = (std::max<uint64_t>(x_.max_masks, 1) + mpad_ - 1) / mpad_ * mpad_;
+  const size_t ints = 3 * Tm + (Bm + 1) + 2 * Mm + Bm + (4 * Tm + 3);
   stage_bytes_ = ((ints * 4 + 7) & ~size_t(7)) + 8;
   for (int i = 0; i < kStageBufs; ++i) {
     HP_CUDA(cudaMallocHost(&h_stage_[i], stage_bytes_));
@@ -195,6 +207,11 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     batch_.mrow = base + 3 * Tm + Bm + 1;
     batch_.morig = batch_.mrow + Mm;
     batch_.label = batch_.morig + Mm;
+    batch_.perm = batch_.label + Bm;
+    batch_.uid = batch_.perm + Tm;
+    batch_.useg = batch_.uid + Tm;
+    batch_.ulist = batch_.useg + Tm + 1;
+    batch_.ucount = batch_.ulist + Tm;
     d_weight_ = reinterpret_cast<double*>(static_cast<char*>(d_stage_) + stage_bytes_ - 8);
   }
 
@@ -245,6 +262,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   inv_w_ = static_cast<float*>(dalloc(4));
   inv_w64_ = static_cast<double*>(dalloc(8));
   flags_ = static_cast<int*>(dalloc(2 * 4));
+  d_hyper_ = static_cast<float*>(dalloc(4 * 4));
   HP_CUDA(cudaMallocHost(&h_lw_, 4 * 8));
   HP_CUDA(cudaMallocHost(&h_flags_, 2 * 4));
   HP_CUDA(cudaMemset(flags_, 0, 8));
@@ -259,6 +277,8 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
 Engine::~Engine() {
   if (s_main_) cudaStreamSynchronize(s_main_);
   if (s_comm_) cudaStreamSynchronize(s_comm_);
+  for (auto& kv : graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (have_premul_ && comm_) ncclRedOpDestroy(premul_, comm_->nccl);
   for (auto& t : tm_)
     for (auto& pr : t.ev) {
@@ -367,12 +387,14 @@ void Engine::stage_batch(const hp_batch& b) {
   if (B > x_.max_batch || T > x_.max_tokens || M > std::max<uint64_t>(x_.max_masks, 1))
     fail(HP_ECONFIG, "batch exceeds the engine capacity (tokens " + std::to_string(T) +
                          ", instances " + std::to_string(B) + ", masks " + std::to_string(M) + ")");
-  const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch, Mm = std::max<uint64_t>(x_.max_masks, 1);
+  const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch,
+                 Mm = (std::max<uint64_t>(x_.max_masks, 1) + mpad_ - 1) / mpad_ * mpad_;
   // wait until the previous copy out of this pinned buffer finished
   HP_CUDA(cudaEventSynchronize(ev_stage_[stage_idx_]));
   int* h = static_cast<int*>(h_stage_[stage_idx_]);
   int *tok = h, *seg = h + Tm, *pos = h + 2 * Tm, *cu = h + 3 * Tm, *mrow = cu + Bm + 1,
-      *morig = mrow + Mm, *label = morig + Mm;
+      *morig = mrow + Mm, *label = morig + Mm, *perm = label + Bm, *uid = perm + Tm,
+      *useg = uid + Tm, *ulist = useg + Tm + 1, *ucount = ulist + Tm;
   double weight = 0.0;
   for (uint64_t i = 0; i < B; ++i) {
     const uint64_t t0 = b.tok_off[i], t1 = b.tok_off[i + 1];
@@ -415,6 +437,40 @@ void Engine::stage_batch(const hp_batch& b) {
     weight += x_.policy == HP_POLICY_SENTENCES ? 1.0 : inst_w;
   }
   cu[B] = static_cast<int>(T);
+  // embedding-gradient plan: token positions grouped by id, position order
+  // inside each group (embed_grad_kernel)
+  {
+    auto& order = sort_buf_;
+    order.resize(T);
+    for (uint64_t t = 0; t < T; ++t) order[t] = (static_cast<uint64_t>(tok[t]) << 32) | t;
+    std::sort(order.begin(), order.end());
+    int U = 0;
+    for (uint64_t k = 0; k < T; ++k) {
+      const int id = static_cast<int>(order[k] >> 32);
+      perm[k] = static_cast<int>(order[k] & 0xffffffffu);
+      if (k == 0 || id != uid[U - 1]) {
+        uid[U] = id;
+        useg[U] = static_cast<int>(k);
+        ++U;
+      }
+    }
+    useg[U] = static_cast<int>(T);
+    int ns = 0;
+    for (int u = 0; u < U; ++u)
+      if (useg[u + 1] - useg[u] <= kEmbHotTokens) ulist[ns++] = u;
+    int nh = 0;
+    for (int u = 0; u < U; ++u)
+      if (useg[u + 1] - useg[u] > kEmbHotTokens) ulist[ns + nh++] = u;
+    ucount[0] = ns;
+    ucount[1] = nh;
+  }
+  // padding rows up to a multiple of mpad_ (gathered as zeros, no loss, no
+  // gradient: the weight above counts only real targets)
+  const uint64_t Mp = M == 0 ? 0 : (M + mpad_ - 1) / mpad_ * mpad_;
+  for (uint64_t k = M; k < Mp; ++k) {
+    mrow[k] = -1;
+    morig[k] = -1;
+  }
   *reinterpret_cast<double*>(static_cast<char*>(h_stage_[stage_idx_]) + stage_bytes_ - 8) = weight;
   HP_CUDA(cudaMemcpyAsync(d_stage_, h_stage_[stage_idx_], stage_bytes_, cudaMemcpyHostToDevice,
                           s_main_));
@@ -422,7 +478,7 @@ void Engine::stage_batch(const hp_batch& b) {
   stage_idx_ = (stage_idx_ + 1) % kStageBufs;
   batch_.T = static_cast<int>(T);
   batch_.B = static_cast<int>(B);
-  batch_.M = static_cast<int>(M);
+  batch_.M = static_cast<int>(Mp);
   local_weight_ = weight;
   staged_ = true;
 }
@@ -772,6 +828,67 @@ void Engine::backward() {
 void Engine::round_async(int dummy, double lr) {
   if (!staged_) fail(HP_ECONFIG, "round: no batch staged");
   HP_CUDA(cudaSetDevice(x_.device));
+  // one identical update on every rank (engine.hpp:147-153, optim.hpp:107-146),
+  // issued per bucket on the side stream as the buckets complete
+  ++adam_t_;
+  const double c1 = 1.0 / (1.0 - std::pow(o_.beta1, static_cast<double>(adam_t_)));
+  const double c2 = 1.0 / (1.0 - std::pow(o_.beta2, static_cast<double>(adam_t_)));
+  AdamArgs& a = adam_args_;
+  a = AdamArgs{};
+  a.p = params_; a.m = adam_m_; a.v = adam_v_; a.g = grads_; a.n = n_;
+  a.lr = static_cast<float>(lr);
+  a.b1 = static_cast<float>(o_.beta1);
+  a.b2 = static_cast<float>(o_.beta2);
+  a.eps = static_cast<float>(o_.eps);
+  a.c1 = static_cast<float>(c1);
+  a.c2 = static_cast<float>(c2);
+  a.hyper = d_hyper_;  // the same three values, read on the device
+  a.inv_w64 = comm_ ? nullptr : inv_w64_;  // with NCCL the scale rode PreMulSum
+  a.flags = flags_;
+  a.bad = flags_ + 1;
+  a.sgd = o_.kind == HP_OPT_SGD;
+  a.shadow = shadow_;
+  // pageable source: staged by the driver at the call, so the host array can
+  // be reused at once; ordered before the round on s_main_
+  const float hyper[4] = {a.lr, a.c1, a.c2, 0.f};
+  HP_CUDA(cudaMemcpyAsync(d_hyper_, hyper, sizeof(hyper), cudaMemcpyHostToDevice, s_main_));
+
+  if (graphs_on_ && !timers_on_ && !capture_) {
+    GraphEntry& e = graphs_[std::make_tuple(batch_.T, batch_.B, batch_.M, dummy ? 1 : 0)];
+    if (e.exec) {
+      HP_CUDA(cudaGraphLaunch(e.exec, s_main_));
+      count_launch(static_cast<int>(e.launches));
+    } else if (e.seen++ == 0) {
+      round_body(dummy);
+    } else {
+      const uint64_t k0 = kernel_launch_count();
+      HP_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeThreadLocal));
+      try {
+        round_body(dummy);
+      } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(s_main_, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      cudaGraph_t g = nullptr;
+      HP_CUDA(cudaStreamEndCapture(s_main_, &g));
+      e.launches = kernel_launch_count() - k0;
+      const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) fail(HP_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+      HP_CUDA(cudaGraphLaunch(e.exec, s_main_));
+    }
+  } else {
+    round_body(dummy);
+  }
+  ++step_;
+  HP_CUDA(cudaEventRecord(ev_done_, s_main_));
+  in_flight_ = true;
+  last_dummy_ = dummy != 0;
+}
+
+void Engine::round_body(int dummy) {
   HP_CUDA(cudaMemsetAsync(flags_, 0, 8, s_main_));
   // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
   forward(!dummy);
@@ -793,28 +910,11 @@ void Engine::round_async(int dummy, double lr) {
     HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_fwd_, 0));
     HP_NCCL(ncclAllReduce(d_lw_, d_lw_, 2, ncclDouble, ncclSum, comm_->nccl, s_comm_));
     sw = s_comm_;
+  } else {
+    // the side stream joins here (updates depend on the weight finalised below)
+    HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_fwd_, 0));
   }
   finalize_weight(d_lw_, inv_w_, inv_w64_, flags_, sw);
-
-  // one identical update on every rank (engine.hpp:147-153, optim.hpp:107-146),
-  // issued per bucket on the side stream as the buckets complete
-  ++adam_t_;
-  const double c1 = 1.0 / (1.0 - std::pow(o_.beta1, static_cast<double>(adam_t_)));
-  const double c2 = 1.0 / (1.0 - std::pow(o_.beta2, static_cast<double>(adam_t_)));
-  AdamArgs& a = adam_args_;
-  a = AdamArgs{};
-  a.p = params_; a.m = adam_m_; a.v = adam_v_; a.g = grads_; a.n = n_;
-  a.lr = static_cast<float>(lr);
-  a.b1 = static_cast<float>(o_.beta1);
-  a.b2 = static_cast<float>(o_.beta2);
-  a.eps = static_cast<float>(o_.eps);
-  a.c1 = static_cast<float>(c1);
-  a.c2 = static_cast<float>(c2);
-  a.inv_w64 = comm_ ? nullptr : inv_w64_;  // with NCCL the scale rode PreMulSum
-  a.flags = flags_;
-  a.bad = flags_ + 1;
-  a.sgd = o_.kind == HP_OPT_SGD;
-  a.shadow = shadow_;
 
   next_bucket_ = 0;
   if (dummy) {
@@ -834,12 +934,8 @@ void Engine::round_async(int dummy, double lr) {
   // the round ends when the last bucket's update has landed
   HP_CUDA(cudaEventRecord(ev_comm_done_, s_comm_));
   HP_CUDA(cudaStreamWaitEvent(s_main_, ev_comm_done_, 0));
-  ++step_;
   HP_CUDA(cudaMemcpyAsync(h_lw_, d_lw_, 4 * 8, cudaMemcpyDeviceToHost, s_main_));
   HP_CUDA(cudaMemcpyAsync(h_flags_, flags_, 2 * 4, cudaMemcpyDeviceToHost, s_main_));
-  HP_CUDA(cudaEventRecord(ev_done_, s_main_));
-  in_flight_ = true;
-  last_dummy_ = dummy != 0;
 }
 
 void Engine::round_sync(hp_round_out* out) {

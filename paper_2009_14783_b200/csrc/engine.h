@@ -6,7 +6,9 @@
 #include <nccl.h>
 
 #include <array>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "hetpar_b200.h"
@@ -69,6 +71,7 @@ class Engine {
   void backward();
   void grads_ready(int first_done_param);
   void issue_bucket(size_t b);
+  void round_body(int dummy);  // the device work of one round (eager or captured)
 
   hp_model_desc m_;
   hp_optim_desc o_;
@@ -104,6 +107,7 @@ class Engine {
   double* d_weight_ = nullptr;  // inside the staged block
   double local_weight_ = 0;
   bool staged_ = false;
+  std::vector<uint64_t> sort_buf_;
 
   // activations
   struct Layer {
@@ -149,6 +153,19 @@ class Engine {
     cudaEvent_t cur = nullptr;
   };
   std::array<TimerAcc, TM_COUNT> tm_;
+
+  // CUDA graphs of round_body, keyed by batch shape (T, B, padded M, dummy):
+  // first sighting runs eagerly, the second is captured, later ones replay
+  // (one graph launch instead of ~300 kernel launches per round).
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;  // kernels inside, for kernel_launch_count()
+    int seen = 0;
+  };
+  std::map<std::tuple<int, int, int, int>, GraphEntry> graphs_;
+  bool graphs_on_ = true;
+  float* d_hyper_ = nullptr;  // [lr, c1, c2, 0] of the current round (device)
+  int mpad_ = 1;              // masked positions padded to a multiple (bf16: 64)
   std::array<cudaEvent_t, 8> marks_{};
   AdamArgs adam_args_{};
   std::vector<std::pair<int, int>> bucket_items_;  // [first item, count] per bucket

@@ -132,14 +132,102 @@ void embed_fwd(const DevBatch& b, int d, const void* E, const void* seg0,
   count_launch();
 }
 
+// dE rows of the batch's distinct token ids: row id = sum of dx over the
+// tokens with that id -- no atomics, fixed summation order, so the round is
+// deterministic.  Engine::stage_batch groups token positions by id (perm,
+// useg) and lists the ids with <= kEmbHot tokens first (ulist[0, n_small)),
+// the hot ones (e.g. [MASK], [CLS]) after (ulist[n_small, n_small + n_hot)).
+//   small id: one warp, rows summed in position order (the reference's
+//             accumulation order), loads issued 8 rows ahead
+//   hot id:   one 1024-thread CTA; warp w sums rows w, w+32, ... in order,
+//             the 32 partials are added in warp order through smem
+// Fixed grids, counts read on the device (CUDA-graph stable).
+constexpr int kEmbHot = 32;
+
 template <class XT>
-__global__ void embed_scatter_kernel(int T, int d, const int* __restrict__ tok,
-                                     const XT* __restrict__ dx, float* __restrict__ dE) {
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= T) return;
-  const int lane = threadIdx.x & 31;
-  float* row = dE + (int64_t)tok[t] * d;
-  for (int c = lane; c < d; c += 32) atomicAdd(row + c, tof(dx[(int64_t)t * d + c]));
+__device__ __forceinline__ void emb_load8(const XT* p, float* f) {
+  if constexpr (std::is_same<XT, bf16>::value) {
+    unpack8(*reinterpret_cast<const uint4*>(p), f);
+  } else {
+    const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+}
+
+template <class XT>
+__global__ void __launch_bounds__(256) embed_grad_small(const int* __restrict__ counts,
+                                                        const int* __restrict__ ulist,
+                                                        const int* __restrict__ uid,
+                                                        const int* __restrict__ useg,
+                                                        const int* __restrict__ perm, int d,
+                                                        const XT* __restrict__ dx,
+                                                        float* __restrict__ dE) {
+  const int n_small = counts[0];
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const int d8 = d / 8;
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_small; i += gridDim.x * wpb) {
+    const int u = ulist[i];
+    const int k0 = useg[u], k1 = useg[u + 1];
+    float* o = dE + (int64_t)uid[u] * d;
+    for (int c8 = lane; c8 < d8; c8 += 32) {
+      float acc[8] = {};
+      for (int k = k0; k < k1; k += 8) {
+        float f[8][8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (k + j < k1) emb_load8(dx + (int64_t)perm[k + j] * d + 8 * c8, f[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (k + j < k1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += f[j][e];
+      }
+      reinterpret_cast<float4*>(o + 8 * c8)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      reinterpret_cast<float4*>(o + 8 * c8)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+}
+
+template <class XT>
+__global__ void __launch_bounds__(1024) embed_grad_hot(const int* __restrict__ counts,
+                                                       const int* __restrict__ ulist,
+                                                       const int* __restrict__ uid,
+                                                       const int* __restrict__ useg,
+                                                       const int* __restrict__ perm, int d,
+                                                       const XT* __restrict__ dx,
+                                                       float* __restrict__ dE) {
+  extern __shared__ float part[];  // [32 warps][d]
+  const int n_small = counts[0], n_hot = counts[1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d8 = d / 8;
+  for (int i = blockIdx.x; i < n_hot; i += gridDim.x) {
+    const int u = ulist[n_small + i];
+    const int k0 = useg[u], k1 = useg[u + 1];
+    for (int c8 = lane; c8 < d8; c8 += 32) {
+      float acc[8] = {};
+      for (int k = k0 + w; k < k1; k += 32 * 4) {
+        float f[4][8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (k + 32 * j < k1) emb_load8(dx + (int64_t)perm[k + 32 * j] * d + 8 * c8, f[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (k + 32 * j < k1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += f[j][e];
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) part[w * d + 8 * c8 + e] = acc[e];
+    }
+    __syncthreads();
+    float* o = dE + (int64_t)uid[u] * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      float acc = 0.f;
+      for (int j = 0; j < 32; ++j) acc += part[j * d + c];
+      o[c] = acc;
+    }
+    __syncthreads();
+  }
 }
 
 // column sums over row chunks; sel (optional) keeps rows with sel[r] == want
@@ -256,9 +344,22 @@ void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
                float* dseg0, float* dseg1, float* scratch, cudaStream_t s) {
   if (b.T == 0) return;
   DISPATCH1(xt, X, {
-    embed_scatter_kernel<X><<<(b.T + 7) / 8, 256, 0, s>>>(b.T, d, b.tok, (const X*)dx, dE);
+    if (d % 8) fail(HP_ECONFIG, "embedding gradient: d_model must be a multiple of 8");
+    embed_grad_small<X><<<148 * 4, 256, 0, s>>>(b.ucount, b.ulist, b.uid, b.useg, b.perm, d,
+                                                (const X*)dx, dE);
     LAUNCH_CHECK();
-    count_launch();
+    {
+      const int sm = 32 * d * (int)sizeof(float);
+      static int set_for = 0;
+      if (sm > 48 * 1024 && sm > set_for) {
+        HP_CUDA(cudaFuncSetAttribute(embed_grad_hot<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        set_for = sm;
+      }
+      embed_grad_hot<X><<<64, 1024, sm, s>>>(b.ucount, b.ulist, b.uid, b.useg, b.perm, d,
+                                             (const X*)dx, dE);
+      LAUNCH_CHECK();
+    }
+    count_launch(2);
     colsum_launch<X>(b.T, d, (const X*)dx, d, b.seg, 0, dseg0, scratch, s);
     colsum_launch<X>(b.T, d, (const X*)dx, d, b.seg, 1, dseg1, scratch, s);
   });
@@ -743,7 +844,12 @@ __global__ void gather_kernel(int R, int d, const int* __restrict__ idx, const T
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= R) return;
   const int lane = threadIdx.x & 31;
-  const T* s = src + (int64_t)idx[r] * d;
+  const int i = idx[r];
+  if (i < 0) {  // padding row (see Engine::stage_batch): zeros
+    for (int c = lane; c < d; c += 32) dst[(int64_t)r * d + c] = fromf<T>(0.f);
+    return;
+  }
+  const T* s = src + (int64_t)i * d;
   for (int c = lane; c < d; c += 32) dst[(int64_t)r * d + c] = s[c];
 }
 template <class T>
@@ -752,6 +858,7 @@ __global__ void scatter_kernel(int R, int d, const int* __restrict__ idx, const 
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= R) return;
   const int lane = threadIdx.x & 31;
+  if (idx[r] < 0) return;  // padding row
   T* o = dst + (int64_t)idx[r] * d;
   for (int c = lane; c < d; c += 32) o[c] = src[(int64_t)r * d + c];
 }
@@ -768,6 +875,7 @@ __global__ void scatter_f32_kernel(int R, int d, const int* __restrict__ idx,
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= R) return;
   const int lane = threadIdx.x & 31;
+  if (idx[r] < 0) return;  // padding row
   T* o = dst + (int64_t)idx[r] * d;
   for (int c = lane; c < d; c += 32) o[c] = fromf<T>(src[(int64_t)r * d + c]);
 }
@@ -793,6 +901,12 @@ __global__ void __launch_bounds__(512) ls_ce_kernel(int V, const float* __restri
                              float* __restrict__ row_loss, DZT* __restrict__ dz, int64_t ld_dz) {
   __shared__ float red[32];
   const int r = blockIdx.x;
+  if (target[r] < 0) {  // padding row (see Engine::stage_batch): no loss, no gradient
+    if (threadIdx.x == 0) row_loss[r] = 0.f;
+    if (dz)
+      for (int j = threadIdx.x; j < V; j += blockDim.x) dz[(int64_t)r * ld_dz + j] = fromf<DZT>(0.f);
+    return;
+  }
   const float* zr = z + (int64_t)r * ldz;
   // one pass: running max, rescaled sum of exp, and the plain sum (for eps)
   // fp32 parity path: accurate expf; bf16 path: fast __expf
@@ -992,8 +1106,14 @@ __device__ __forceinline__ void adam_one(const AdamArgs& a, float& p, float& m, 
 }
 
 // One CTA per work item.  float4 I/O when the item is 16-byte aligned.
-__global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
-  if (a.flags && *a.flags) return;  // numeric error: leave parameters untouched
+__global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a0) {
+  if (a0.flags && *a0.flags) return;  // numeric error: leave parameters untouched
+  AdamArgs a = a0;
+  if (a.hyper) {  // per-step scalars from device memory (graph replays)
+    a.lr = a.hyper[0];
+    a.c1 = a.hyper[1];
+    a.c2 = a.hyper[2];
+  }
   const uint64_t* it = a.items + 5 * blockIdx.x;
   const uint64_t lo = it[0], n = it[1], slo = it[2], cols = it[3], pcols = it[4];
   const bool scale = a.inv_w64 != nullptr;

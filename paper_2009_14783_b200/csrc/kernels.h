@@ -69,13 +69,22 @@ struct DevBatch {
   const int* mrow = nullptr;    // [M] global token row of each masked position
   const int* morig = nullptr;   // [M] original token id (MLM target)
   const int* label = nullptr;   // [B] NSP label
+  // distinct token ids for the embedding gradient: uid[u], its tokens
+  // perm[useg[u] .. useg[u+1]) in position order; ulist = the u's with few
+  // tokens (ucount[0] of them), then the hot ones (ucount[1])
+  const int* perm = nullptr;    // [T]
+  const int* uid = nullptr;     // [T]
+  const int* useg = nullptr;    // [T+1]
+  const int* ulist = nullptr;   // [T]
+  const int* ucount = nullptr;  // [2]
 };
 
 // x[t] = E[tok] + seg_{s}[.] + PE[pos] ; optional LN afterwards is separate.
 void embed_fwd(const DevBatch& b, int d, const void* E, const void* seg0,
                const void* seg1, DType wt, const float* pe, void* x, DType xt,
                cudaStream_t s);
-// dE[tok] += dx (atomics), dseg{0,1} = column sums over the segment's tokens.
+// dE[id] = sum of dx over the tokens with that id (dE zeroed by the caller;
+// deterministic, position order), dseg{0,1} = column sums over the segment's tokens.
 void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
                float* dseg0, float* dseg1, float* scratch, cudaStream_t s);
 
@@ -107,7 +116,8 @@ void attention_fwd_mma(const DevBatch& b, int H, const void* qkv, void* o, float
 void attention_bwd_mma(const DevBatch& b, int H, const void* qkv, const void* o, const void* dO,
                        const float* lse, void* dqkv, cudaStream_t s);
 
-// rows of src selected by idx -> dst (dst[r] = src[idx[r]]).
+// rows of src selected by idx -> dst (dst[r] = src[idx[r]]); idx < 0 marks a
+// padding row (zeros here, skipped by the scatters, no loss in ls_ce).
 void gather_rows(int R, int d, const int* idx, const void* src, void* dst, DType t,
                  cudaStream_t s);
 // dst[idx[r]] = src[r] (rows unique), other rows untouched.
@@ -149,6 +159,7 @@ void finalize_weight(const double* lw, float* inv_w, double* inv_w64, int* flags
 struct AdamArgs {
   float* p; float* m; float* v; const float* g; uint64_t n;
   float lr, b1, b2, eps, c1, c2;
+  const float* hyper;     // device [lr, c1, c2]; overrides the scalars when non-null
   const double* inv_w64;  // may be null
   const int* flags;       // skip everything when *flags != 0
   int* bad;               // set to 1 on a non-finite gradient
