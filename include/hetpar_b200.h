@@ -257,7 +257,7 @@ hp_status hp_debug_gemm_trace(unsigned long long* buf);
 hp_status hp_debug_gemm_generic(int on);
 /* Varlen self-attention on caller-owned device buffers: cu[B+1] (int32,
  * device), qkv [T x 3*H*dk], o [T x H*dk], lse [H x T], dO, dqkv.  bf16 = 1
- * selects bf16 I/O; path: 0 auto, 1 SIMT, 2 tensor-core (mma.sync). */
+ * selects bf16 I/O; path: 0 auto, 1 SIMT, 2 tensor-core (mma.sync), 3 tcgen05. */
 hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf16,
                              const void* qkv, void* o, float* lse, const void* dO,
                              void* dqkv, int path);

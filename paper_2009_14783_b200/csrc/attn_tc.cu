@@ -1,0 +1,456 @@
+// tcgen05 multi-head self-attention for the bf16 path (dk = 64, varlen
+// sequences of <= 128 tokens).  One CTA per (instance, head); every matrix of
+// the head fits one UMMA tile, so the whole head is a handful of tcgen05.mma
+// instructions with fp32 accumulators in TMEM:
+//
+//   forward   S = Q K^T                (M 128 q,   N 128 keys, K 64)
+//             P = softmax(S / sqrt(dk)) over the instance's keys (registers)
+//             O = P V                  (M 128 q,   N 64,       K 128 keys)
+//   backward  S = Q K^T, dP = dO V^T   (recompute, as tape.hpp:274-286)
+//             P = exp(S / sqrt(dk) - lse), dS = P (dP - D) / sqrt(dk),
+//             D = rowsum(dO * O)
+//             dV = P^T dO, dK = dS^T Q (M 128 keys, N 64, K 128 q)
+//             dQ = dS K                (M 128 q,    N 64, K 128 keys)
+//
+// Warps: 0 TMA producer (Q, K, V [, dO] as 128 x 64 SWIZZLE_128B boxes of the
+// packed [T x 3d] QKV activations -- rows past the instance are other
+// instances' tokens or TMA zero fill, masked below), 1 TMEM allocator + MMA
+// issuer, 2..5 softmax / epilogue (thread = TMEM lane = one query or key row).
+// P and dS are written by the softmax threads as bf16 into smem in the same
+// 128B-swizzled [rows][64] sub-tile layout TMA produces; the one [q][key]
+// buffer is read as a K-major A operand (O = P V, dQ = dS K) and as an
+// MN-major A operand (dV = P^T dO, dK = dS^T Q) through different UMMA
+// descriptors, so no transposes are materialised.
+// Semantics: attention.hpp:15-26 (softmax over the instance's own tokens).
+#include <cuda_bf16.h>
+
+#include <cfloat>
+
+#include "hp_common.h"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace hp {
+namespace attn_tc {
+
+using namespace hp::tc;
+using bf16 = __nv_bfloat16;
+constexpr int DK = 64;
+constexpr int NQ = 128;                   // rows of every tile (queries / keys)
+constexpr uint32_t kTile = NQ * DK * 2;   // [128][64] bf16, 16 KB
+constexpr int kSoftWarps = 8;  // 2 per TMEM lane quarter, 64 key columns each
+constexpr int kThreads = 64 + 32 * kSoftWarps;
+
+// byte offset of 16-byte chunk j (8 bf16) of row r in a [128][64] SW128 tile
+__device__ __forceinline__ uint32_t sw128(int r, int j) {
+  return static_cast<uint32_t>(r * 128 + ((j ^ (r & 7)) << 4));
+}
+// kind::f16 instruction descriptor, M = 128: D f32, A/B bf16
+__device__ __forceinline__ uint32_t idesc(int n, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(128 >> 4) << 24);
+}
+// descriptors: K-major [128][64] tile (K-step +32 B); MN-major operand whose
+// K rows are the tile rows (K-step of 16 rows = +2048 B), atom columns
+// (64 MN elements) 16 KB apart
+__device__ __forceinline__ uint64_t kmaj(uint32_t base) { return umma_desc(base, 16, 1024); }
+__device__ __forceinline__ uint64_t mnmaj(uint32_t base) { return umma_desc(base, kTile, 1024); }
+// A operand = [128 rows][128 k] stored as two K-major [128][64] sub-tiles
+__device__ __forceinline__ uint64_t kmaj2(uint32_t base, int kk) {
+  return kmaj(base + (kk >> 2) * kTile + (kk & 3) * 32);
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w)
+               : "memory");
+}
+// 32 consecutive values of row r (columns 32c .. 32c+31 of a [128][128]
+// operand held as two [128][64] sub-tiles) -> bf16 in smem
+__device__ __forceinline__ void put_row32(uint32_t base, int r, int c, const float* v) {
+  const uint32_t sub = base + (c >> 1) * kTile;
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const float* q = v + 8 * jj;
+    sts128(sub + sw128(r, (c & 1) * 4 + jj), pack2(q[0], q[1]), pack2(q[2], q[3]), pack2(q[4], q[5]),
+           pack2(q[6], q[7]));
+  }
+}
+// 32 fp32 TMEM columns of this thread's row -> 32 bf16 (64 B) at dst
+__device__ __forceinline__ void tmem_row32_to_global(uint32_t taddr, float scale, bf16* dst, bool store) {
+  uint32_t v[32];
+  TMEM_LD32(taddr, v);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  if (store) {
+    uint4* o = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[q] = make_uint4(pack2(__uint_as_float(v[8 * q]) * scale, __uint_as_float(v[8 * q + 1]) * scale),
+                        pack2(__uint_as_float(v[8 * q + 2]) * scale, __uint_as_float(v[8 * q + 3]) * scale),
+                        pack2(__uint_as_float(v[8 * q + 4]) * scale, __uint_as_float(v[8 * q + 5]) * scale),
+                        pack2(__uint_as_float(v[8 * q + 6]) * scale, __uint_as_float(v[8 * q + 7]) * scale));
+  }
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// the two warps sharing a TMEM lane quarter (64 threads, barrier 1 + quarter)
+__device__ __forceinline__ void pair_sync(int quarter) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+}
+
+template <int NTILE, int NP>
+struct Smem {
+  uint8_t tile[NTILE][kTile];  // Q, K, V [, dO]
+  uint8_t pbuf[NP][2 * kTile];  // P [, dS]: [128 q][128 keys]
+  float red[2][2][NQ];  // [max | sum][column half][row]: the two warps of a row pair
+  uint64_t full, s_done, p_ready, o_done;
+  uint32_t tmem;
+};
+using FwdSmem = Smem<3, 1>;
+using BwdSmem = Smem<4, 2>;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// profiling: CTA (0,0) clock64 timeline (tools/gemm_trace.py style), null off
+__device__ __forceinline__ void atr(unsigned long long* tr, int slot) {
+  if (tr && blockIdx.x == 0 && blockIdx.y == 0) tr[slot] = clock64();
+}
+
+// ------------------------------------------------------------------ forward
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_tc(const __grid_constant__ CUtensorMap map_qkv, const int* __restrict__ cu, int H,
+                bf16* __restrict__ o, float* __restrict__ lse, int T_total,
+                unsigned long long* tr) {
+  if (threadIdx.x == 0) atr(tr, 0);
+  extern __shared__ __align__(1024) uint8_t raw[];
+  FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(raw));
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int row0 = cu[b], n = cu[b + 1] - row0;
+  if (n <= 0) return;
+  if (threadIdx.x == 0) atr(tr, 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = H * DK;
+  constexpr uint32_t kCols = 256;  // S [0,128), O [128,192)
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.full, 1);
+    mbar_init(&sm.s_done, 1);
+    mbar_init(&sm.p_ready, 32 * kSoftWarps);
+    mbar_init(&sm.o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem)), "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem = sm.tmem;
+  if (threadIdx.x == 0) atr(tr, 2);
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_expect_tx(&sm.full, 3 * kTile);
+      tma_2d(&map_qkv, &sm.full, sm.tile[0], h * DK, row0);
+      tma_2d(&map_qkv, &sm.full, sm.tile[1], d + h * DK, row0);
+      tma_2d(&map_qkv, &sm.full, sm.tile[2], 2 * d + h * DK, row0);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    mbar_wait(&sm.full, 0);
+    if (lane == 0) atr(tr, 3);
+    tmem_fence_after();
+    if (elect_one()) {
+      const uint32_t id = idesc(128, 0, 0);
+      const uint64_t aq = kmaj(smem_u32(sm.tile[0])), bk = kmaj(smem_u32(sm.tile[1]));
+#pragma unroll
+      for (int kk = 0; kk < DK / 16; ++kk) umma_bf16(tmem, aq + 2 * kk, bk + 2 * kk, id, kk > 0);
+      umma_commit(&sm.s_done);
+    }
+    __syncwarp();
+    mbar_wait(&sm.p_ready, 0);
+    if (lane == 0) atr(tr, 6);
+    tmem_fence_after();
+    if (elect_one()) {
+      const uint32_t id = idesc(64, 0, 1);
+      const uint32_t pb = smem_u32(sm.pbuf[0]);
+      const uint64_t bv = mnmaj(smem_u32(sm.tile[2]));
+#pragma unroll
+      for (int kk = 0; kk < NQ / 16; ++kk)
+        umma_bf16(tmem + 128, kmaj2(pb, kk), bv + kk * (2048 >> 4), id, kk > 0);
+      umma_commit(&sm.o_done);
+    }
+    __syncwarp();
+  } else {
+    // softmax warps: row r = 32 * quarter + lane, key columns [64 half, +64)
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int r = 32 * quarter + lane;  // query row
+    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
+    const float scale = rsqrtf(static_cast<float>(DK));
+    const float sl2 = scale * 1.4426950408889634f;
+    mbar_wait(&sm.s_done, 0);
+    if (r == 0 && half == 0) atr(tr, 4);
+    tmem_fence_after();
+    uint32_t va[32], vb[32];
+    TMEM_LD32(trow + 64 * half, va);
+    TMEM_LD32(trow + 64 * half + 32, vb);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float v[64];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      v[i] = __uint_as_float(va[i]);
+      v[32 + i] = __uint_as_float(vb[i]);
+    }
+    float m4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      if (64 * half + i < n) m4[i & 3] = fmaxf(m4[i & 3], v[i]);
+    sm.red[0][half][r] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    pair_sync(quarter);
+    const float mx = fmaxf(sm.red[0][0][r], sm.red[0][1][r]);
+    const float mo = -mx * sl2;
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+    float p[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      p[i] = (64 * half + i < n) ? ex2(fmaf(v[i], sl2, mo)) : 0.f;
+      s4[i & 3] += p[i];
+    }
+    const uint32_t pb = smem_u32(sm.pbuf[0]);
+    put_row32(pb, r, 2 * half, p);
+    put_row32(pb, r, 2 * half + 1, p + 32);
+    sm.red[1][half][r] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    if (r == 0 && half == 0) atr(tr, 5);
+    fence_async_smem();
+    tmem_fence_before();
+    mbar_arrive(&sm.p_ready);
+    pair_sync(quarter);
+    const float sum = sm.red[1][0][r] + sm.red[1][1][r];
+    mbar_wait(&sm.o_done, 0);
+    if (r == 0 && half == 0) atr(tr, 7);
+    tmem_fence_after();
+    const bool ok = r < n;
+    tmem_row32_to_global(trow + 128 + 32 * half, 1.f / sum, o + (int64_t)(row0 + r) * d + h * DK + 32 * half,
+                         ok);
+    if (ok && half == 0) lse[(int64_t)h * T_total + row0 + r] = mx * scale + logf(sum);
+    if (r == 0 && half == 0) atr(tr, 8);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tmem_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+  }
+  if (threadIdx.x == 0) atr(tr, 9);
+}
+
+// ------------------------------------------------------------------ backward
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_tc(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                const int* __restrict__ cu, int H, const bf16* __restrict__ o,
+                const bf16* __restrict__ dO, const float* __restrict__ lse, bf16* __restrict__ dqkv,
+                int T_total) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  BwdSmem& sm = *reinterpret_cast<BwdSmem*>(align1024(raw));
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int row0 = cu[b], n = cu[b + 1] - row0;
+  if (n <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = H * DK;
+  // TMEM: S [0,128), dP [128,256), dV [256,320), dK [320,384), dQ [384,448)
+  constexpr uint32_t kCols = 512;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.full, 1);
+    mbar_init(&sm.s_done, 1);
+    mbar_init(&sm.p_ready, 32 * kSoftWarps);
+    mbar_init(&sm.o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem)), "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_expect_tx(&sm.full, 4 * kTile);
+      tma_2d(&map_qkv, &sm.full, sm.tile[0], h * DK, row0);
+      tma_2d(&map_qkv, &sm.full, sm.tile[1], d + h * DK, row0);
+      tma_2d(&map_qkv, &sm.full, sm.tile[2], 2 * d + h * DK, row0);
+      tma_2d(&map_do, &sm.full, sm.tile[3], h * DK, row0);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    mbar_wait(&sm.full, 0);
+    tmem_fence_after();
+    const uint32_t tq = smem_u32(sm.tile[0]), tk = smem_u32(sm.tile[1]), tv = smem_u32(sm.tile[2]),
+                   tdo = smem_u32(sm.tile[3]);
+    if (elect_one()) {
+      const uint32_t id = idesc(128, 0, 0);
+#pragma unroll
+      for (int kk = 0; kk < DK / 16; ++kk) {
+        umma_bf16(tmem, kmaj(tq) + 2 * kk, kmaj(tk) + 2 * kk, id, kk > 0);         // S
+        umma_bf16(tmem + 128, kmaj(tdo) + 2 * kk, kmaj(tv) + 2 * kk, id, kk > 0);  // dP
+      }
+      umma_commit(&sm.s_done);
+    }
+    __syncwarp();
+    mbar_wait(&sm.p_ready, 0);
+    tmem_fence_after();
+    if (elect_one()) {
+      const uint32_t pb = smem_u32(sm.pbuf[0]), sb = smem_u32(sm.pbuf[1]);
+      const uint32_t id_t = idesc(64, 1, 1), id_q = idesc(64, 0, 1);
+#pragma unroll
+      for (int kk = 0; kk < NQ / 16; ++kk) {
+        const uint64_t step = kk * (2048 >> 4);  // 16 rows of the K (row) dimension
+        umma_bf16(tmem + 256, mnmaj(pb) + step, mnmaj(tdo) + step, id_t, kk > 0);  // dV = P^T dO
+        umma_bf16(tmem + 320, mnmaj(sb) + step, mnmaj(tq) + step, id_t, kk > 0);   // dK = dS^T Q
+        umma_bf16(tmem + 384, kmaj2(sb, kk), mnmaj(tk) + step, id_q, kk > 0);     // dQ = dS K
+      }
+      umma_commit(&sm.o_done);
+    }
+    __syncwarp();
+  } else {
+    // softmax warps: row r = 32 * quarter + lane, columns [64 half, +64)
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int r = 32 * quarter + lane;  // query row (S, dP, dQ) / key row (dK, dV)
+    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
+    const float scale = rsqrtf(static_cast<float>(DK));
+    const float l2e = 1.4426950408889634f;
+    const bool rok = r < n;
+    // D_r = rowsum(dO * O), lse_r -- while the MMAs run
+    float Dr = 0.f, lr = 0.f;
+    if (rok) {
+      const uint4* po = reinterpret_cast<const uint4*>(o + (int64_t)(row0 + r) * d + h * DK);
+      const uint4* pg = reinterpret_cast<const uint4*>(dO + (int64_t)(row0 + r) * d + h * DK);
+      float d4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 a = po[q], g = pg[q];
+        const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+        const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 af = __bfloat1622float2(ah[e]), gf = __bfloat1622float2(gh[e]);
+          d4[e] = fmaf(af.x, gf.x, d4[e]);
+          d4[e] = fmaf(af.y, gf.y, d4[e]);
+        }
+      }
+      Dr = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+      lr = lse[(int64_t)h * T_total + row0 + r];
+    }
+    const float sl2 = scale * l2e, lo = -lr * l2e;
+    mbar_wait(&sm.s_done, 0);
+    tmem_fence_after();
+    const uint32_t pb = smem_u32(sm.pbuf[0]), sb = smem_u32(sm.pbuf[1]);
+#pragma unroll 1
+    for (int c2 = 0; c2 < 2; ++c2) {
+      const int c = 2 * half + c2;
+      uint32_t sv[32], dv[32];
+      TMEM_LD32(trow + 32 * c, sv);
+      TMEM_LD32(trow + 128 + 32 * c, dv);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float p[32], ds[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const bool ok = rok && (32 * c + i < n);
+        p[i] = ok ? ex2(fmaf(__uint_as_float(sv[i]), sl2, lo)) : 0.f;
+        ds[i] = p[i] * (__uint_as_float(dv[i]) - Dr) * scale;
+      }
+      put_row32(pb, r, c, p);
+      put_row32(sb, r, c, ds);
+    }
+    fence_async_smem();
+    tmem_fence_before();
+    mbar_arrive(&sm.p_ready);
+    mbar_wait(&sm.o_done, 0);
+    tmem_fence_after();
+    bf16* row = dqkv + (int64_t)(row0 + r) * 3 * d + h * DK + 32 * half;
+    tmem_row32_to_global(trow + 384 + 32 * half, 1.f, row, rok);          // dQ
+    tmem_row32_to_global(trow + 320 + 32 * half, 1.f, row + d, rok);      // dK
+    tmem_row32_to_global(trow + 256 + 32 * half, 1.f, row + 2 * d, rok);  // dV
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tmem_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+  }
+}
+
+}  // namespace attn_tc
+
+bool attention_tc_supported(int dk, int max_seq) { return dk == attn_tc::DK && max_seq <= attn_tc::NQ; }
+
+static unsigned long long* g_attn_trace = nullptr;
+void attention_tc_set_trace(unsigned long long* buf) { g_attn_trace = buf; }
+
+namespace {
+// [rows][cols] bf16 row-major activations as a 128 x 64 box map
+CUtensorMap act_map(const void* base, int rows, int cols) {
+  const uint64_t dims[2] = {static_cast<uint64_t>(cols), static_cast<uint64_t>(rows)};
+  const uint64_t str[1] = {static_cast<uint64_t>(cols)};
+  const uint32_t box[2] = {64, 128};
+  return make_map(base, 2, dims, str, box);
+}
+}  // namespace
+
+void attention_fwd_tc(const DevBatch& b, int H, const void* qkv, void* o, float* lse, cudaStream_t s) {
+  if (b.B == 0) return;
+  const int d = H * attn_tc::DK;
+  const CUtensorMap mq = act_map(qkv, b.T, 3 * d);
+  const int sm = static_cast<int>(sizeof(attn_tc::FwdSmem)) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    attr = true;
+  }
+  attn_tc::attn_fwd_tc<<<dim3(b.B, H), attn_tc::kThreads, sm, s>>>(
+      mq, b.cu, H, static_cast<attn_tc::bf16*>(o), lse, b.T, g_attn_trace);
+  HP_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void attention_bwd_tc(const DevBatch& b, int H, const void* qkv, const void* o, const void* dO,
+                      const float* lse, void* dqkv, cudaStream_t s) {
+  if (b.B == 0) return;
+  const int d = H * attn_tc::DK;
+  const CUtensorMap mq = act_map(qkv, b.T, 3 * d);
+  const CUtensorMap mg = act_map(dO, b.T, d);
+  const int sm = static_cast<int>(sizeof(attn_tc::BwdSmem)) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    attr = true;
+  }
+  attn_tc::attn_bwd_tc<<<dim3(b.B, H), attn_tc::kThreads, sm, s>>>(
+      mq, mg, b.cu, H, static_cast<const attn_tc::bf16*>(o), static_cast<const attn_tc::bf16*>(dO), lse,
+      static_cast<attn_tc::bf16*>(dqkv), b.T);
+  HP_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace hp

@@ -433,8 +433,12 @@ hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf1
   b.B = B;
   b.T = T;
   b.cu = cu;
-  const bool mma = path == 2 || (path == 0 && bf16 && hp::attention_mma_supported(dk, 128));
-  if (mma) {
+  const bool tcp = path == 3 || (path == 0 && bf16 && hp::attention_tc_supported(dk, 128));
+  const bool mma = !tcp && (path == 2 || (path == 0 && bf16 && hp::attention_mma_supported(dk, 128)));
+  if (tcp) {
+    hp::attention_fwd_tc(b, H, qkv, o, lse, 0);
+    if (dO) hp::attention_bwd_tc(b, H, qkv, o, dO, lse, dqkv, 0);
+  } else if (mma) {
     hp::attention_fwd_mma(b, H, qkv, o, lse, 0);
     if (dO) hp::attention_bwd_mma(b, H, qkv, o, dO, lse, dqkv, 0);
   } else {
@@ -455,6 +459,7 @@ hp_status hp_debug_sync(void) {
 hp_status hp_debug_gemm_trace(unsigned long long* buf) {
   HP_API_BEGIN
   hp::gemm_tc_set_trace(buf);
+  hp::attention_tc_set_trace(buf ? buf + 1008 : nullptr);  // slots 1008.. (attention)
   HP_API_END
 }
 

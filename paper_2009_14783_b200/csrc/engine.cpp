@@ -186,6 +186,10 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   {
     const char* e = std::getenv("HP_GRAPHS");
     graphs_on_ = !(e && std::string(e) == "0");
+    // attention: tcgen05 kernels when the shape allows (HP_ATTN=mma selects
+    // the mma.sync kernels, for A/B comparisons)
+    const char* a = std::getenv("HP_ATTN");
+    attn_tc_ = bf16_ && attention_tc_supported(dk_, (int)m_.max_seq) && !(a && std::string(a) == "mma");
   }
   // staged batch block (fixed layout at capacity)
   const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch,
@@ -588,7 +592,9 @@ void Engine::forward(bool need_grad) {
     q.c = y.qkv; q.ldc = 3 * d_; q.ct = at_;
     gemm_t(q);
     tstart(TM_ATTN);
-    if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
+    if (attn_tc_)
+      attention_fwd_tc(b, H_, y.qkv, y.o, y.lse, s_main_);
+    else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
       attention_fwd_mma(b, H_, y.qkv, y.o, y.lse, s_main_);
     else
       attention_fwd(b, H_, dk_, y.qkv, y.o, y.lse, at_, s_main_);
@@ -779,7 +785,9 @@ void Engine::backward() {
     dO.c = dC_; dO.ldc = d_; dO.ct = at_;
     gemm_t(dO);
     tstart(TM_ATTN);
-    if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
+    if (attn_tc_)
+      attention_bwd_tc(b, H_, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
+    else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
       attention_bwd_mma(b, H_, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
     else
       attention_bwd(b, H_, dk_, y.qkv, y.o, dC_, y.lse, dqkv_, at_, s_main_);

@@ -164,6 +164,7 @@ class Engine {
   };
   std::map<std::tuple<int, int, int, int>, GraphEntry> graphs_;
   bool graphs_on_ = true;
+  bool attn_tc_ = false;      // tcgen05 attention kernels (attn_tc.cu)
   float* d_hyper_ = nullptr;  // [lr, c1, c2, 0] of the current round (device)
   int mpad_ = 1;              // masked positions padded to a multiple (bf16: 64)
   std::array<cudaEvent_t, 8> marks_{};

@@ -116,6 +116,14 @@ void attention_fwd_mma(const DevBatch& b, int H, const void* qkv, void* o, float
 void attention_bwd_mma(const DevBatch& b, int H, const void* qkv, const void* o, const void* dO,
                        const float* lse, void* dqkv, cudaStream_t s);
 
+// tcgen05 attention (attn_tc.cu): dk == 64, sequences <= 128, bf16.
+bool attention_tc_supported(int dk, int max_seq);
+void attention_tc_set_trace(unsigned long long* buf);  // profiling: CTA (0,0) timeline
+void attention_fwd_tc(const DevBatch& b, int H, const void* qkv, void* o, float* lse,
+                      cudaStream_t s);
+void attention_bwd_tc(const DevBatch& b, int H, const void* qkv, const void* o, const void* dO,
+                      const float* lse, void* dqkv, cudaStream_t s);
+
 // rows of src selected by idx -> dst (dst[r] = src[idx[r]]); idx < 0 marks a
 // padding row (zeros here, skipped by the scatters, no loss in ls_ce).
 void gather_rows(int R, int d, const int* idx, const void* src, void* dst, DType t,

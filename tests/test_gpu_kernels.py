@@ -209,7 +209,8 @@ def _attn_ref(qkv, cu, H, dk):
     return o, (q, k, v)
 
 
-@pytest.mark.parametrize("path,dtype,dk", [(2, torch.bfloat16, 64), (1, torch.bfloat16, 64),
+@pytest.mark.parametrize("path,dtype,dk", [(3, torch.bfloat16, 64), (2, torch.bfloat16, 64),
+                                           (1, torch.bfloat16, 64),
                                            (1, torch.float32, 32), (1, torch.float32, 64),
                                            (1, torch.bfloat16, 32)])
 def test_attention_varlen_fwd_bwd(path, dtype, dk):

@@ -41,7 +41,8 @@ def build(verbose: bool = False) -> str:
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                     "--expt-relaxed-constexpr"] + inc + (["-DHP_GEMM_PROFILE"] if profile else [])
     srcs = sorted(glob.glob(os.path.join(SRC, "*.cu")) + glob.glob(os.path.join(SRC, "*.cpp")))
-    hdrs = glob.glob(os.path.join(SRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+    hdrs = (glob.glob(os.path.join(SRC, "*.h")) + glob.glob(os.path.join(SRC, "*.cuh")) +
+            glob.glob(os.path.join(ROOT, "include", "*.h")))
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
 
     def compile_one(src: str) -> str:
