@@ -38,8 +38,10 @@ using bf16 = __nv_bfloat16;
 constexpr int DK = 64;
 constexpr int NQ = 128;                   // rows of every tile (queries / keys)
 constexpr uint32_t kTile = NQ * DK * 2;   // [128][64] bf16, 16 KB
-constexpr int kSoftWarps = 8;  // 2 per TMEM lane quarter, 64 key columns each
-constexpr int kThreads = 64 + 32 * kSoftWarps;
+// forward: 4 softmax warps (one per TMEM lane quarter, whole rows), 4 CTAs per
+// SM; backward: 8 (two per quarter, 64 columns each), 2 CTAs per SM
+constexpr int kSoftWarpsF = 4, kThreadsF = 64 + 32 * kSoftWarpsF;
+constexpr int kSoftWarpsB = 8, kThreadsB = 64 + 32 * kSoftWarpsB;
 
 // byte offset of 16-byte chunk j (8 bf16) of row r in a [128][64] SW128 tile
 __device__ __forceinline__ uint32_t sw128(int r, int j) {
@@ -56,9 +58,14 @@ __device__ __forceinline__ uint32_t idesc(int n, int a_mn, int b_mn) {
 // (64 MN elements) 16 KB apart
 __device__ __forceinline__ uint64_t kmaj(uint32_t base) { return umma_desc(base, 16, 1024); }
 __device__ __forceinline__ uint64_t mnmaj(uint32_t base) { return umma_desc(base, kTile, 1024); }
-// A operand = [128 rows][128 k] stored as two K-major [128][64] sub-tiles
-__device__ __forceinline__ uint64_t kmaj2(uint32_t base, int kk) {
-  return kmaj(base + (kk >> 2) * kTile + (kk & 3) * 32);
+// [128 rows][128 cols] operand stored as two [128][64] sub-tiles `stride`
+// bytes apart: as a K-major A (K = the 128 columns) at k-step kk, or as an
+// MN-major A (M = the 128 columns, K = the rows; atom columns = sub-tiles)
+__device__ __forceinline__ uint64_t kmaj2(uint32_t base, int kk, uint32_t stride) {
+  return kmaj(base + (kk >> 2) * stride + (kk & 3) * 32);
+}
+__device__ __forceinline__ uint64_t mnmaj2(uint32_t base, uint32_t stride) {
+  return umma_desc(base, stride, 1024);
 }
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -78,9 +85,10 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
                : "memory");
 }
 // 32 consecutive values of row r (columns 32c .. 32c+31 of a [128][128]
-// operand held as two [128][64] sub-tiles) -> bf16 in smem
-__device__ __forceinline__ void put_row32(uint32_t base, int r, int c, const float* v) {
-  const uint32_t sub = base + (c >> 1) * kTile;
+// operand held as two [128][64] sub-tiles `stride` bytes apart) -> bf16 in smem
+__device__ __forceinline__ void put_row32(uint32_t base, int r, int c, const float* v,
+                                          uint32_t stride = kTile) {
+  const uint32_t sub = base + (c >> 1) * stride;
 #pragma unroll
   for (int jj = 0; jj < 4; ++jj) {
     const float* q = v + 8 * jj;
@@ -108,21 +116,41 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// the two warps sharing a TMEM lane quarter (64 threads, barrier 1 + quarter)
-__device__ __forceinline__ void pair_sync(int quarter) {
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+// 32 bf16 of row r, columns 32c .. 32c+31 (layout of put_row32) -> floats
+__device__ __forceinline__ void get_row32(uint32_t base, int r, int c, float* v, uint32_t stride) {
+  const uint32_t sub = base + (c >> 1) * stride;
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    uint4 u;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                 : "r"(sub + sw128(r, (c & 1) * 4 + jj))
+                 : "memory");
+    const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(hh[e]);
+      v[8 * jj + 2 * e] = f.x;
+      v[8 * jj + 2 * e + 1] = f.y;
+    }
+  }
 }
 
-template <int NTILE, int NP>
-struct Smem {
-  uint8_t tile[NTILE][kTile];  // Q, K, V [, dO]
-  uint8_t pbuf[NP][2 * kTile];  // P [, dS]: [128 q][128 keys]
-  float red[2][2][NQ];  // [max | sum][column half][row]: the two warps of a row pair
+// Forward: Q, K, V; P (32 KB) overwrites Q and K once S is computed.  48 KB
+// + TMEM 128 columns (S, then O in its first 64) -> 4 CTAs per SM.
+struct FwdSmem {
+  uint8_t tile[3][kTile];
   uint64_t full, s_done, p_ready, o_done;
   uint32_t tmem;
 };
-using FwdSmem = Smem<3, 1>;
-using BwdSmem = Smem<4, 2>;
+// Backward: Q, K, V, dO, X; the [q][key] buffer is {V, X} (V is dead once dP
+// is computed): P first, then -- after dV = P^T dO has read it -- dS.  80 KB
+// + TMEM 256 (S | dP, then dV | dK | dQ) -> 2 CTAs per SM.
+struct BwdSmem {
+  uint8_t tile[5][kTile];
+  uint64_t full, s_done, p_ready, pv_done, ds_ready, o_done;
+  uint32_t tmem;
+};
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -134,7 +162,7 @@ __device__ __forceinline__ void atr(unsigned long long* tr, int slot) {
 }
 
 // ------------------------------------------------------------------ forward
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsF, 4)
     attn_fwd_tc(const __grid_constant__ CUtensorMap map_qkv, const int* __restrict__ cu, int H,
                 bf16* __restrict__ o, float* __restrict__ lse, int T_total,
                 unsigned long long* tr) {
@@ -147,11 +175,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) atr(tr, 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = H * DK;
-  constexpr uint32_t kCols = 256;  // S [0,128), O [128,192)
+  constexpr uint32_t kCols = 128;  // S [0,128), then O [0,64)
   if (threadIdx.x == 0) {
     mbar_init(&sm.full, 1);
     mbar_init(&sm.s_done, 1);
-    mbar_init(&sm.p_ready, 32 * kSoftWarps);
+    mbar_init(&sm.p_ready, 32 * kSoftWarpsF);
     mbar_init(&sm.o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -191,67 +219,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_fence_after();
     if (elect_one()) {
       const uint32_t id = idesc(64, 0, 1);
-      const uint32_t pb = smem_u32(sm.pbuf[0]);
+      const uint32_t pb = smem_u32(sm.tile[0]);
       const uint64_t bv = mnmaj(smem_u32(sm.tile[2]));
 #pragma unroll
       for (int kk = 0; kk < NQ / 16; ++kk)
-        umma_bf16(tmem + 128, kmaj2(pb, kk), bv + kk * (2048 >> 4), id, kk > 0);
+        umma_bf16(tmem, kmaj2(pb, kk, kTile), bv + kk * (2048 >> 4), id, kk > 0);
       umma_commit(&sm.o_done);
     }
     __syncwarp();
   } else {
-    // softmax warps: row r = 32 * quarter + lane, key columns [64 half, +64)
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    // softmax warps 2..5: row r = 32 * quarter + lane (the whole row: 4
+    // chunks of 32 keys, a max pass and an exp pass over TMEM)
+    const int quarter = warp & 3;
     const int r = 32 * quarter + lane;  // query row
     const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
     const float scale = rsqrtf(static_cast<float>(DK));
     const float sl2 = scale * 1.4426950408889634f;
     mbar_wait(&sm.s_done, 0);
-    if (r == 0 && half == 0) atr(tr, 4);
+    if (r == 0) atr(tr, 4);
     tmem_fence_after();
-    uint32_t va[32], vb[32];
-    TMEM_LD32(trow + 64 * half, va);
-    TMEM_LD32(trow + 64 * half + 32, vb);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    float v[64];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      v[i] = __uint_as_float(va[i]);
-      v[32 + i] = __uint_as_float(vb[i]);
-    }
     float m4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
 #pragma unroll
-    for (int i = 0; i < 64; ++i)
-      if (64 * half + i < n) m4[i & 3] = fmaxf(m4[i & 3], v[i]);
-    sm.red[0][half][r] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-    pair_sync(quarter);
-    const float mx = fmaxf(sm.red[0][0][r], sm.red[0][1][r]);
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[32];
+      TMEM_LD32(trow + 32 * c, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (32 * c + i < n) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(v[i]));
+    }
+    const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     const float mo = -mx * sl2;
     float s4[4] = {0.f, 0.f, 0.f, 0.f};
-    float p[64];
+    const uint32_t pb = smem_u32(sm.tile[0]);  // P over Q and K (S is final)
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      p[i] = (64 * half + i < n) ? ex2(fmaf(v[i], sl2, mo)) : 0.f;
-      s4[i & 3] += p[i];
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[32];
+      TMEM_LD32(trow + 32 * c, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float p[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        p[i] = (32 * c + i < n) ? ex2(fmaf(__uint_as_float(v[i]), sl2, mo)) : 0.f;
+        s4[i & 3] += p[i];
+      }
+      put_row32(pb, r, c, p);
     }
-    const uint32_t pb = smem_u32(sm.pbuf[0]);
-    put_row32(pb, r, 2 * half, p);
-    put_row32(pb, r, 2 * half + 1, p + 32);
-    sm.red[1][half][r] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-    if (r == 0 && half == 0) atr(tr, 5);
+    const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    if (r == 0) atr(tr, 5);
     fence_async_smem();
     tmem_fence_before();
     mbar_arrive(&sm.p_ready);
-    pair_sync(quarter);
-    const float sum = sm.red[1][0][r] + sm.red[1][1][r];
     mbar_wait(&sm.o_done, 0);
-    if (r == 0 && half == 0) atr(tr, 7);
+    if (r == 0) atr(tr, 7);
     tmem_fence_after();
     const bool ok = r < n;
-    tmem_row32_to_global(trow + 128 + 32 * half, 1.f / sum, o + (int64_t)(row0 + r) * d + h * DK + 32 * half,
-                         ok);
-    if (ok && half == 0) lse[(int64_t)h * T_total + row0 + r] = mx * scale + logf(sum);
-    if (r == 0 && half == 0) atr(tr, 8);
+    bf16* orow = o + (int64_t)(row0 + r) * d + h * DK;
+    tmem_row32_to_global(trow, 1.f / sum, orow, ok);
+    tmem_row32_to_global(trow + 32, 1.f / sum, orow + 32, ok);
+    if (ok) lse[(int64_t)h * T_total + row0 + r] = mx * scale + logf(sum);
+    if (r == 0) atr(tr, 8);
   }
   tmem_fence_before();
   __syncthreads();
@@ -263,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------ backward
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsB, 2)
     attn_bwd_tc(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                 const int* __restrict__ cu, int H, const bf16* __restrict__ o,
                 const bf16* __restrict__ dO, const float* __restrict__ lse, bf16* __restrict__ dqkv,
@@ -275,12 +302,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (n <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = H * DK;
-  // TMEM: S [0,128), dP [128,256), dV [256,320), dK [320,384), dQ [384,448)
-  constexpr uint32_t kCols = 512;
+  // TMEM: S [0,128), dP [128,256); then dV [0,64), dK [64,128), dQ [128,192)
+  constexpr uint32_t kCols = 256;
   if (threadIdx.x == 0) {
     mbar_init(&sm.full, 1);
     mbar_init(&sm.s_done, 1);
-    mbar_init(&sm.p_ready, 32 * kSoftWarps);
+    mbar_init(&sm.p_ready, 32 * kSoftWarpsB);
+    mbar_init(&sm.pv_done, 1);
+    mbar_init(&sm.ds_ready, 32 * kSoftWarpsB);
     mbar_init(&sm.o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -318,17 +347,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&sm.s_done);
     }
     __syncwarp();
+    const uint32_t xb = tv;  // {V, X}: P, then dS
+    constexpr uint32_t kXs = 2 * kTile;
     mbar_wait(&sm.p_ready, 0);
     tmem_fence_after();
     if (elect_one()) {
-      const uint32_t pb = smem_u32(sm.pbuf[0]), sb = smem_u32(sm.pbuf[1]);
-      const uint32_t id_t = idesc(64, 1, 1), id_q = idesc(64, 0, 1);
+      const uint32_t id_t = idesc(64, 1, 1);
 #pragma unroll
       for (int kk = 0; kk < NQ / 16; ++kk) {
         const uint64_t step = kk * (2048 >> 4);  // 16 rows of the K (row) dimension
-        umma_bf16(tmem + 256, mnmaj(pb) + step, mnmaj(tdo) + step, id_t, kk > 0);  // dV = P^T dO
-        umma_bf16(tmem + 320, mnmaj(sb) + step, mnmaj(tq) + step, id_t, kk > 0);   // dK = dS^T Q
-        umma_bf16(tmem + 384, kmaj2(sb, kk), mnmaj(tk) + step, id_q, kk > 0);     // dQ = dS K
+        umma_bf16(tmem, mnmaj2(xb, kXs) + step, mnmaj(tdo) + step, id_t, kk > 0);  // dV = P^T dO
+      }
+      umma_commit(&sm.pv_done);
+    }
+    __syncwarp();
+    mbar_wait(&sm.ds_ready, 0);
+    tmem_fence_after();
+    if (elect_one()) {
+      const uint32_t id_t = idesc(64, 1, 1), id_q = idesc(64, 0, 1);
+#pragma unroll
+      for (int kk = 0; kk < NQ / 16; ++kk) {
+        const uint64_t step = kk * (2048 >> 4);
+        umma_bf16(tmem + 64, mnmaj2(xb, kXs) + step, mnmaj(tq) + step, id_t, kk > 0);  // dK = dS^T Q
+        umma_bf16(tmem + 128, kmaj2(xb, kk, kXs), mnmaj(tk) + step, id_q, kk > 0);    // dQ = dS K
       }
       umma_commit(&sm.o_done);
     }
@@ -365,33 +406,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = scale * l2e, lo = -lr * l2e;
     mbar_wait(&sm.s_done, 0);
     tmem_fence_after();
-    const uint32_t pb = smem_u32(sm.pbuf[0]), sb = smem_u32(sm.pbuf[1]);
+    const uint32_t xb = smem_u32(sm.tile[2]);  // {V, X}: P, then dS
+    constexpr uint32_t kXs = 2 * kTile;
 #pragma unroll 1
     for (int c2 = 0; c2 < 2; ++c2) {
       const int c = 2 * half + c2;
-      uint32_t sv[32], dv[32];
+      uint32_t sv[32];
       TMEM_LD32(trow + 32 * c, sv);
-      TMEM_LD32(trow + 128 + 32 * c, dv);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      float p[32], ds[32];
+      float p[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const bool ok = rok && (32 * c + i < n);
         p[i] = ok ? ex2(fmaf(__uint_as_float(sv[i]), sl2, lo)) : 0.f;
-        ds[i] = p[i] * (__uint_as_float(dv[i]) - Dr) * scale;
       }
-      put_row32(pb, r, c, p);
-      put_row32(sb, r, c, ds);
+      put_row32(xb, r, c, p, kXs);
     }
     fence_async_smem();
     tmem_fence_before();
     mbar_arrive(&sm.p_ready);
+    // once dV = P^T dO has read P, the buffer takes dS = P (dP - D) / sqrt(dk)
+    // (P as stored, bf16; this thread rewrites only its own row)
+    mbar_wait(&sm.pv_done, 0);
+    tmem_fence_after();
+#pragma unroll 1
+    for (int c2 = 0; c2 < 2; ++c2) {
+      const int c = 2 * half + c2;
+      uint32_t dv[32];
+      TMEM_LD32(trow + 128 + 32 * c, dv);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float pd[32];
+      get_row32(xb, r, c, pd, kXs);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) pd[i] = pd[i] * (__uint_as_float(dv[i]) - Dr) * scale;
+      put_row32(xb, r, c, pd, kXs);
+    }
+    fence_async_smem();
+    tmem_fence_before();
+    mbar_arrive(&sm.ds_ready);
     mbar_wait(&sm.o_done, 0);
     tmem_fence_after();
     bf16* row = dqkv + (int64_t)(row0 + r) * 3 * d + h * DK + 32 * half;
-    tmem_row32_to_global(trow + 384 + 32 * half, 1.f, row, rok);          // dQ
-    tmem_row32_to_global(trow + 320 + 32 * half, 1.f, row + d, rok);      // dK
-    tmem_row32_to_global(trow + 256 + 32 * half, 1.f, row + 2 * d, rok);  // dV
+    tmem_row32_to_global(trow + 128 + 32 * half, 1.f, row, rok);        // dQ
+    tmem_row32_to_global(trow + 64 + 32 * half, 1.f, row + d, rok);     // dK
+    tmem_row32_to_global(trow + 32 * half, 1.f, row + 2 * d, rok);      // dV
   }
   tmem_fence_before();
   __syncthreads();
@@ -428,7 +486,7 @@ void attention_fwd_tc(const DevBatch& b, int H, const void* qkv, void* o, float*
     HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr = true;
   }
-  attn_tc::attn_fwd_tc<<<dim3(b.B, H), attn_tc::kThreads, sm, s>>>(
+  attn_tc::attn_fwd_tc<<<dim3(b.B, H), attn_tc::kThreadsF, sm, s>>>(
       mq, b.cu, H, static_cast<attn_tc::bf16*>(o), lse, b.T, g_attn_trace);
   HP_CUDA(cudaGetLastError());
   count_launch();
@@ -446,7 +504,7 @@ void attention_bwd_tc(const DevBatch& b, int H, const void* qkv, const void* o, 
     HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr = true;
   }
-  attn_tc::attn_bwd_tc<<<dim3(b.B, H), attn_tc::kThreads, sm, s>>>(
+  attn_tc::attn_bwd_tc<<<dim3(b.B, H), attn_tc::kThreadsB, sm, s>>>(
       mq, mg, b.cu, H, static_cast<const attn_tc::bf16*>(o), static_cast<const attn_tc::bf16*>(dO), lse,
       static_cast<attn_tc::bf16*>(dqkv), b.T);
   HP_CUDA(cudaGetLastError());
