@@ -298,6 +298,7 @@ Engine::~Engine() {
   if (h_flags_) cudaFreeHost(h_flags_);
   if (h_params_) cudaFreeHost(h_params_);
   for (auto& e : ev_bucket_) cudaEventDestroy(e);
+  for (auto& e : final_evs_) cudaEventDestroy(e);
   for (auto& e : marks_)
     if (e) cudaEventDestroy(e);
   if (ev_fwd_) cudaEventDestroy(ev_fwd_);
@@ -704,7 +705,12 @@ void Engine::backward() {
     gw.c = gp(iw); gw.ldc = V_; gw.ct = DType::f32;
     gemm_t(gw);
     tstart(TM_HEAD);
-    col_sum(b.M, V_, dz_, Vp_, at_, gp(iw + 1), scratch_, s_main_);
+    {
+      const uint64_t Mm = (std::max<uint64_t>(x_.max_masks, 1) + mpad_ - 1) / mpad_ * mpad_;
+      DeferredFinal f = final_slot(colsum_part_floats((int)Mm, Vp_));
+      col_sum(b.M, V_, dz_, Vp_, at_, gp(iw + 1), scratch_, s_main_, &f);
+      issue_final(f);
+    }
     tstop(TM_HEAD, 0, 0);
     GemmArgs gd;
     gd.M = b.M; gd.N = d_; gd.K = V_; gd.ab = at_;
@@ -731,8 +737,12 @@ void Engine::backward() {
                 ib2 = iwo + 7, ig2 = iwo + 8;
       tstart(TM_NORM);
       // LN2' also yields d(ffn.b2) = colsum(dP2) (P2 = G W2 + b2 + X1)
-      layernorm_bwd(T, d_, dA_, at_, y.p2, at_, y.mean2, y.rstd2, pp(ig2), dB_, at_, gp(ig2),
-                    gp(ig2 + 1), gp(ib2), scratch_, s_main_);
+      {
+        DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, d_));
+        layernorm_bwd(T, d_, dA_, at_, y.p2, at_, y.mean2, y.rstd2, pp(ig2), dB_, at_, gp(ig2),
+                      gp(ig2 + 1), gp(ib2), scratch_, s_main_, &f);
+        issue_final(f);
+      }
       tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
       GemmArgs w2;  // d(ffn.w2) = G^T dP2
       w2.M = F_; w2.N = d_; w2.K = T; w2.ab = at_;
@@ -754,7 +764,11 @@ void Engine::backward() {
       w1.c = gp(iw1); w1.ldc = F_; w1.ct = DType::f32;
       gemm_t(w1);
       tstart(TM_NORM);
-      col_sum(T, F_, dU_, F_, at_, gp(ib1), scratch_, s_main_);
+      {
+        DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, F_));
+        col_sum(T, F_, dU_, F_, at_, gp(ib1), scratch_, s_main_, &f);
+        issue_final(f);
+      }
       tstop(TM_NORM, 0, 0);
       GemmArgs dx1;  // dX1 = dU W1^T + dP2
       dx1.M = T; dx1.N = d_; dx1.K = F_; dx1.ab = at_;
@@ -765,8 +779,12 @@ void Engine::backward() {
       gemm_t(dx1);
       tstart(TM_NORM);
       // LN1' also yields d(bo) = colsum(dP1)
-      layernorm_bwd(T, d_, dC_, at_, y.p1, at_, y.mean1, y.rstd1, pp(ig1), dB_, at_, gp(ig1),
-                    gp(ig1 + 1), gp(ibo), scratch_, s_main_);
+      {
+        DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, d_));
+        layernorm_bwd(T, d_, dC_, at_, y.p1, at_, y.mean1, y.rstd1, pp(ig1), dB_, at_, gp(ig1),
+                      gp(ig1 + 1), gp(ibo), scratch_, s_main_, &f);
+        issue_final(f);
+      }
       tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
       dP1 = dB_;
     } else {
@@ -820,8 +838,12 @@ void Engine::backward() {
   if (bert_) {
     const int g = pidx("emb_ln.g");
     tstart(TM_NORM);
-    layernorm_bwd(T, d_, dA_, at_, p0_, at_, mean0_, rstd0_, pp(g), dB_, at_, gp(g), gp(g + 1),
-                  nullptr, scratch_, s_main_);
+    {
+      DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, d_));
+      layernorm_bwd(T, d_, dA_, at_, p0_, at_, mean0_, rstd0_, pp(g), dB_, at_, gp(g), gp(g + 1),
+                    nullptr, scratch_, s_main_, &f);
+      issue_final(f);
+    }
     tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
     dx0 = dB_;
   }
@@ -896,7 +918,34 @@ void Engine::round_async(int dummy, double lr) {
   last_dummy_ = dummy != 0;
 }
 
+DeferredFinal Engine::final_slot(size_t floats) {
+  if (final_n_ == final_bufs_.size()) {
+    final_bufs_.emplace_back(static_cast<float*>(dalloc(floats * 4)), floats);
+    cudaEvent_t e;
+    HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    final_evs_.push_back(e);
+  }
+  if (final_bufs_[final_n_].second < floats) {
+    // a new job sequence (e.g. a round without masked positions shifts the
+    // slots): grow -- only ever on a shape's first, eager round; the old
+    // buffer stays alive for graphs captured with it
+    final_bufs_[final_n_] = {static_cast<float*>(dalloc(floats * 4)), floats};
+  }
+  DeferredFinal f;
+  f.part = final_bufs_[final_n_].first;
+  return f;
+}
+
+void Engine::issue_final(DeferredFinal& f) {
+  if (!f.queued) return;
+  HP_CUDA(cudaEventRecord(final_evs_[final_n_], s_main_));
+  HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[final_n_], 0));
+  launch_final(f, s_comm_);
+  ++final_n_;
+}
+
 void Engine::round_body(int dummy) {
+  final_n_ = 0;
   HP_CUDA(cudaMemsetAsync(flags_, 0, 8, s_main_));
   // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
   forward(!dummy);

@@ -72,6 +72,8 @@ class Engine {
   void grads_ready(int first_done_param);
   void issue_bucket(size_t b);
   void round_body(int dummy);  // the device work of one round (eager or captured)
+  DeferredFinal final_slot(size_t floats);  // partial buffer for the next deferred final
+  void issue_final(DeferredFinal& f);        // its final on the side stream
 
   hp_model_desc m_;
   hp_optim_desc o_;
@@ -166,6 +168,11 @@ class Engine {
   bool graphs_on_ = true;
   bool attn_tc_ = false;      // tcgen05 attention kernels (attn_tc.cu)
   float* d_hyper_ = nullptr;  // [lr, c1, c2, 0] of the current round (device)
+  // deferred column-reduction finals: one partial buffer + event per job of a
+  // round (the job sequence is fixed by the model), allocated on first use
+  std::vector<std::pair<float*, size_t>> final_bufs_;
+  std::vector<cudaEvent_t> final_evs_;
+  size_t final_n_ = 0;
   int mpad_ = 1;              // masked positions padded to a multiple (bf16: 64)
   std::array<cudaEvent_t, 8> marks_{};
   AdamArgs adam_args_{};

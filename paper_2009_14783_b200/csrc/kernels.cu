@@ -18,6 +18,7 @@
 
 #include "hp_common.h"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace hp {
 
@@ -312,13 +313,26 @@ __global__ void colsum_partial_vec(int R, int N8, const bf16* __restrict__ x, in
 
 template <class XT>
 static void colsum_launch(int R, int N, const XT* x, int64_t ld, const int* sel,
-                          int want, float* out, float* scratch, cudaStream_t s) {
+                          int want, float* out, float* scratch, cudaStream_t s,
+                          DeferredFinal* df = nullptr) {
   if constexpr (std::is_same<XT, bf16>::value) {
     const int N8 = (N + 7) & ~7;
     if (!sel && ld % 8 == 0 && ld >= N8 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && R > 0) {
       const int rows_per = 32;
       const int chunks = (R + rows_per - 1) / rows_per;
       dim3 g1((N8 / 8 + 127) / 128, chunks);
+      if (df) {
+        colsum_partial_vec<<<g1, 128, 0, s>>>(R, N8, x, ld, rows_per, df->part);
+        LAUNCH_CHECK();
+        count_launch();
+        df->queued = true;
+        df->kind = 1;
+        df->chunks = chunks;
+        df->stride = N8;
+        df->n = N;
+        df->o0 = out;
+        return;
+      }
       colsum_partial_vec<<<g1, 128, 0, s>>>(R, N8, x, ld, rows_per, scratch);
       LAUNCH_CHECK();
       colsum_final_strided<<<FINAL_LAUNCH(N), 0, s>>>(chunks, N8, N, scratch, out);
@@ -366,8 +380,14 @@ void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
 }
 
 void col_sum(int R, int N, const void* x, int64_t ld, DType t, float* out,
-             float* scratch, cudaStream_t s) {
-  DISPATCH1(t, X, colsum_launch<X>(R, N, (const X*)x, ld, nullptr, 0, out, scratch, s));
+             float* scratch, cudaStream_t s, DeferredFinal* df) {
+  if (df) df->queued = false;
+  DISPATCH1(t, X, colsum_launch<X>(R, N, (const X*)x, ld, nullptr, 0, out, scratch, s, df));
+}
+
+size_t colsum_part_floats(int R, int N) {
+  const size_t chunks = (size_t)((R + 31) / 32);
+  return chunks * std::max<size_t>(3 * (size_t)N, (size_t)((N + 7) & ~7)) + 64;
 }
 
 size_t colsum_scratch_floats(int R, int N) {
@@ -576,6 +596,180 @@ __global__ void __launch_bounds__(256) ln_bwd_vec(int T, const bf16* __restrict_
   }
 }
 
+// ---- bulk-fed bf16 LayerNorm (d = 256 * NV).  Each warp owns RPW
+// consecutive rows and fetches them with ONE 1-D bulk copy per operand
+// (cp.async.bulk, completion on the warp's mbarrier), so a CTA's whole row
+// block is in flight at once and the load latency is paid once; the math then
+// reads shared memory.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+// warp-private mbarrier: lane 0 initialises and arms it, every lane waits
+__device__ __forceinline__ void warp_bar_init(uint64_t* bar, int lane) {
+  if (lane == 0) {
+    tc::mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+
+constexpr int kLnFwdRpw = 2;  // rows per warp (16 per CTA)
+template <int NV>
+__global__ void __launch_bounds__(256) ln_fwd_bulk(int T, const bf16* __restrict__ x,
+                                                   const float* __restrict__ g,
+                                                   const float* __restrict__ bta, bf16* __restrict__ y,
+                                                   float* __restrict__ mean, float* __restrict__ rstd) {
+  constexpr int d = 256 * NV;
+  extern __shared__ __align__(128) uint8_t lsm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(lsm);
+  bf16* xs = reinterpret_cast<bf16*>(lsm + 128);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = (blockIdx.x * 8 + w) * kLnFwdRpw;
+  const int nr = min(kLnFwdRpw, T - row0);
+  if (nr <= 0) return;
+  bf16* xw = xs + w * kLnFwdRpw * d;
+  warp_bar_init(&bar[w], lane);
+  if (lane == 0) {
+    tc::mbar_expect_tx(&bar[w], nr * d * 2);
+    bulk_g2s(xw, x + (int64_t)row0 * d, nr * d * 2, &bar[w]);
+  }
+  float4 gq[NV * 2], bq[NV * 2];  // gamma / beta: loaded once for the warp's rows
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    gq[2 * j] = __ldg(reinterpret_cast<const float4*>(g + 8 * lane + 256 * j));
+    gq[2 * j + 1] = __ldg(reinterpret_cast<const float4*>(g + 8 * lane + 256 * j) + 1);
+    bq[2 * j] = __ldg(reinterpret_cast<const float4*>(bta + 8 * lane + 256 * j));
+    bq[2 * j + 1] = __ldg(reinterpret_cast<const float4*>(bta + 8 * lane + 256 * j) + 1);
+  }
+  tc::mbar_wait(&bar[w], 0);
+  for (int i = 0; i < nr; ++i) {
+    const int t = row0 + i;
+    float v[NV * 8];
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      unpack8(*reinterpret_cast<const uint4*>(xw + i * d + 8 * lane + 256 * j), v + 8 * j);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV * 8; ++k) s += v[k];
+    const float mu = warp_sum(s) * (1.f / d);
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV * 8; ++k) q += (v[k] - mu) * (v[k] - mu);
+    const float rs = rsqrtf(warp_sum(q) * (1.f / d) + kLnEps);
+    bf16* yr = y + (int64_t)t * d;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const float* gg = reinterpret_cast<const float*>(&gq[2 * j]);
+      const float* bb = reinterpret_cast<const float*>(&bq[2 * j]);
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = (v[8 * j + e] - mu) * rs * gg[e] + bb[e];
+      *reinterpret_cast<uint4*>(yr + 8 * lane + 256 * j) = pack8(o);
+    }
+    if (lane == 0) {
+      mean[t] = mu;
+      rstd[t] = rs;
+    }
+  }
+}
+
+// Backward, kLnBwdRows rows per CTA (4 per warp), x and dy bulk-copied; the
+// cross-warp partial reduction reuses the row buffers.
+template <int NV>
+__global__ void __launch_bounds__(256, 1) ln_bwd_bulk(int T, const bf16* __restrict__ dy,
+                                                      const bf16* __restrict__ x,
+                                                      const float* __restrict__ mean,
+                                                      const float* __restrict__ rstd,
+                                                      const float* __restrict__ g,
+                                                      bf16* __restrict__ dx, float* __restrict__ part) {
+  constexpr int d = 256 * NV;
+  constexpr int RPW = kLnBwdRows / 8;
+  extern __shared__ __align__(128) uint8_t lsm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(lsm);
+  bf16* xs = reinterpret_cast<bf16*>(lsm + 128);
+  bf16* ys = xs + kLnBwdRows * d;
+  float* red = reinterpret_cast<float*>(lsm + 128);  // [8 warps][3][d], after the rows are consumed
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = blockIdx.x * kLnBwdRows + w * RPW;
+  const int nr = max(0, min(RPW, T - row0));
+  warp_bar_init(&bar[w], lane);
+  if (lane == 0 && nr > 0) {
+    tc::mbar_expect_tx(&bar[w], 2 * nr * d * 2);
+    bulk_g2s(xs + w * RPW * d, x + (int64_t)row0 * d, nr * d * 2, &bar[w]);
+    bulk_g2s(ys + w * RPW * d, dy + (int64_t)row0 * d, nr * d * 2, &bar[w]);
+  }
+  float ag[NV * 8], ab[NV * 8], ax[NV * 8];
+#pragma unroll
+  for (int i = 0; i < NV * 8; ++i) ag[i] = ab[i] = ax[i] = 0.f;
+  float gg[NV * 8];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(g + 8 * lane + 256 * j));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(g + 8 * lane + 256 * j) + 1);
+    gg[8 * j + 0] = a.x; gg[8 * j + 1] = a.y; gg[8 * j + 2] = a.z; gg[8 * j + 3] = a.w;
+    gg[8 * j + 4] = b.x; gg[8 * j + 5] = b.y; gg[8 * j + 6] = b.z; gg[8 * j + 7] = b.w;
+  }
+  if (nr > 0) tc::mbar_wait(&bar[w], 0);
+  for (int i = 0; i < nr; ++i) {
+    const int t = row0 + i;
+    const float mu = mean[t], rs = rstd[t];
+    float xh[NV * 8], gy[NV * 8];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      unpack8(*reinterpret_cast<const uint4*>(xs + (w * RPW + i) * d + 8 * lane + 256 * j), xh + 8 * j);
+      unpack8(*reinterpret_cast<const uint4*>(ys + (w * RPW + i) * d + 8 * lane + 256 * j), gy + 8 * j);
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV * 8; ++k) {
+      xh[k] = (xh[k] - mu) * rs;
+      const float dxh = gy[k] * gg[k];
+      s1 += dxh;
+      s2 += dxh * xh[k];
+      ag[k] += gy[k] * xh[k];
+      ab[k] += gy[k];
+    }
+    s1 = warp_sum(s1) * (1.f / d);
+    s2 = warp_sum(s2) * (1.f / d);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int k = 8 * j + e;
+        o[e] = rs * (gy[k] * gg[k] - (s1 + xh[k] * s2));
+      }
+      const uint4 u = pack8(o);
+      *reinterpret_cast<uint4*>(dx + (int64_t)t * d + 8 * lane + 256 * j) = u;
+      float r[8];
+      unpack8(u, r);  // sum what the next kernel will read
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ax[8 * j + e] += r[e];
+    }
+  }
+  __syncthreads();  // every warp is done with the row buffers
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = 8 * lane + 256 * j + e;
+      red[(w * 3 + 0) * d + c] = ag[8 * j + e];
+      red[(w * 3 + 1) * d + c] = ab[8 * j + e];
+      red[(w * 3 + 2) * d + c] = ax[8 * j + e];
+    }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 3 * d; c += blockDim.x) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += red[k * 3 * d + c];
+    part[(int64_t)blockIdx.x * 3 * d + c] = acc;
+  }
+}
+
 // out0/out1/out2 = column sums of the [chunks x 3d] partials
 __global__ void ln_part_final(int chunks, int d, const float* __restrict__ part, float* __restrict__ dg,
                               float* __restrict__ db, float* __restrict__ dbias) {
@@ -593,11 +787,14 @@ void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
   if (T == 0) return;
   const int grid = (T + 7) / 8;
   if (xt == DType::bf16 && yt == DType::bf16 && d % 256 == 0 && d <= 1024) {
+    const int rows_cta = 8 * kLnFwdRpw;
+    const int gb = (T + rows_cta - 1) / rows_cta;
+    const size_t sm = 128 + (size_t)rows_cta * d * 2;
     switch (d / 256) {
-      case 1: ln_fwd_vec<1><<<grid, 256, 0, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      case 2: ln_fwd_vec<2><<<grid, 256, 0, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      case 3: ln_fwd_vec<3><<<grid, 256, 0, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      default: ln_fwd_vec<4><<<grid, 256, 0, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 1: ln_fwd_bulk<1><<<gb, 256, sm, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 2: ln_fwd_bulk<2><<<gb, 256, sm, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 3: ln_fwd_bulk<3><<<gb, 256, sm, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      default: ln_fwd_bulk<4><<<gb, 256, sm, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
     }
   } else {
     DISPATCH1(xt, X, DISPATCH1(yt, Y,
@@ -610,22 +807,40 @@ void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
 void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
                    DType xt, const float* mean, const float* rstd, const float* g,
                    void* dx, DType dxt, float* dg, float* db, float* dbias, float* scratch,
-                   cudaStream_t s) {
+                   cudaStream_t s, DeferredFinal* df) {
+  if (df) df->queued = false;
   if (T == 0) return;
+  float* part = df ? df->part : scratch;
   if (dyt == DType::bf16 && xt == DType::bf16 && dxt == DType::bf16 && d % 256 == 0 && d <= 1024) {
     const int chunks = (T + kLnBwdRows - 1) / kLnBwdRows;
-    const size_t sm = sizeof(float) * 8 * 3 * d;
+    // rows (x, dy) and, later, the [8][3][d] reduction share the buffer
+    const size_t sm = 128 + std::max(sizeof(float) * 8 * 3 * d, (size_t)2 * kLnBwdRows * d * 2);
     switch (d / 256) {
 #define LNB(NV)                                                                                 \
-  case NV:                                                                                      \
-    HP_CUDA(cudaFuncSetAttribute(ln_bwd_vec<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    ln_bwd_vec<NV><<<chunks, 256, sm, s>>>(T, (const bf16*)dy, (const bf16*)x, mean, rstd, g,   \
-                                          (bf16*)dx, scratch);                                  \
-    break;
+  case NV: {                                                                                    \
+    static size_t attr_##NV = 0;                                                                \
+    if (attr_##NV < sm) {                                                                       \
+      HP_CUDA(cudaFuncSetAttribute(ln_bwd_bulk<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+      attr_##NV = sm;                                                                           \
+    }                                                                                           \
+    ln_bwd_bulk<NV><<<chunks, 256, sm, s>>>(T, (const bf16*)dy, (const bf16*)x, mean, rstd, g,  \
+                                           (bf16*)dx, part);                                    \
+  } break;
       LNB(1) LNB(2) LNB(3) default: LNB(4)
 #undef LNB
     }
     LAUNCH_CHECK();
+    if (df) {
+      count_launch();
+      df->queued = true;
+      df->kind = 0;
+      df->chunks = chunks;
+      df->d = d;
+      df->o0 = dg;
+      df->o1 = db;
+      df->o2 = dbias;
+      return;
+    }
     ln_part_final<<<FINAL_LAUNCH(3 * d), 0, s>>>(chunks, d, scratch, dg, db, dbias);
     LAUNCH_CHECK();
     count_launch(2);
@@ -648,6 +863,17 @@ void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
     if (dbias)
       DISPATCH1(dxt, DX, colsum_launch<DX>(T, d, (const DX*)dx, d, nullptr, 0, dbias, scratch, s));
   }));
+}
+
+void launch_final(const DeferredFinal& f, cudaStream_t s) {
+  if (!f.queued) return;
+  if (f.kind == 0) {
+    ln_part_final<<<FINAL_LAUNCH(3 * f.d), 0, s>>>(f.chunks, f.d, f.part, f.o0, f.o1, f.o2);
+  } else {
+    colsum_final_strided<<<FINAL_LAUNCH(f.n), 0, s>>>(f.chunks, f.stride, f.n, f.part, f.o0);
+  }
+  LAUNCH_CHECK();
+  count_launch();
 }
 
 // ------------------------------------------------------------------ attention

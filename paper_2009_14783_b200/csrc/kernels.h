@@ -88,6 +88,21 @@ void embed_fwd(const DevBatch& b, int d, const void* E, const void* seg0,
 void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
                float* dseg0, float* dseg1, float* scratch, cudaStream_t s);
 
+// Deferred final of a column reduction (LayerNorm-backward dgamma/dbeta/dbias,
+// bias column sums): when the caller passes one, the bf16 partial kernel writes
+// its [chunks x N] partial rows into `part` (caller-owned, colsum_part_floats
+// floats) and leaves the last, tiny reduction to launch_final() -- which the
+// engine issues on its side stream, off the backward's critical path (the
+// results are only read by the bucket's allreduce / update on that stream).
+struct DeferredFinal {
+  float* part = nullptr;  // in
+  bool queued = false;    // out: launch_final() must run
+  int kind = 0, chunks = 0, d = 0, stride = 0, n = 0;
+  float *o0 = nullptr, *o1 = nullptr, *o2 = nullptr;
+};
+void launch_final(const DeferredFinal& f, cudaStream_t s);
+size_t colsum_part_floats(int R, int N);
+
 void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
                    const float* bta, void* y, DType yt, float* mean, float* rstd,
                    cudaStream_t s);
@@ -97,7 +112,7 @@ void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
 void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
                    DType xt, const float* mean, const float* rstd, const float* g,
                    void* dx, DType dxt, float* dg, float* db, float* dbias, float* scratch,
-                   cudaStream_t s);
+                   cudaStream_t s, DeferredFinal* df = nullptr);
 // scratch floats the column-sum kernels need for an R x N reduction
 size_t colsum_scratch_floats(int R, int N);
 
@@ -149,7 +164,7 @@ void nsp_head(const DevBatch& b, int d, const void* H, DType ht, const float* W,
 
 // Column sums of a [R x N] matrix into out[N] (overwrite).
 void col_sum(int R, int N, const void* x, int64_t ld, DType t, float* out,
-             float* scratch, cudaStream_t s);
+             float* scratch, cudaStream_t s, DeferredFinal* df = nullptr);
 
 // out[0] += sum(a[0..na)) + sum(b[0..nb)) in double, deterministic order.
 void loss_reduce(const float* a, int na, const float* b, int nb, double* out,
