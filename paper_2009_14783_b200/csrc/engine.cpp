@@ -272,8 +272,10 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   HP_CUDA(cudaMemset(flags_, 0, 8));
 
   if (comm_) {
-    HP_NCCL(ncclRedOpCreatePreMulSum(&premul_, inv_w_, ncclFloat, ncclScalarDevice, comm_->nccl));
-    have_premul_ = true;
+    // gradient buckets reduce with plain ncclSum (NVLS-eligible: the NVSwitch
+    // does the reduction and NCCL needs few SMs); the 1/total-weight scale is
+    // applied in f64 inside the update, the reference's own order
+    // (all_reduce_sum, then g /= weight; engine.hpp:145-151)
   }
   HP_CUDA(cudaDeviceSynchronize());
 }
@@ -679,7 +681,7 @@ void Engine::issue_bucket(size_t k) {
   HP_CUDA(cudaEventRecord(ev_bucket_[k], s_main_));
   HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_bucket_[k], 0));
   if (comm_)
-    HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, premul_,
+    HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, ncclSum,
                           comm_->nccl, s_comm_));
   // the bucket's update runs behind the rest of backward (engine.hpp:147-153:
   // every rank applies the identical update to the identical reduced sum)
@@ -873,7 +875,7 @@ void Engine::round_async(int dummy, double lr) {
   a.c1 = static_cast<float>(c1);
   a.c2 = static_cast<float>(c2);
   a.hyper = d_hyper_;  // the same three values, read on the device
-  a.inv_w64 = comm_ ? nullptr : inv_w64_;  // with NCCL the scale rode PreMulSum
+  a.inv_w64 = inv_w64_;  // g = (float)((double)sum * (1 / total weight))
   a.flags = flags_;
   a.bad = flags_ + 1;
   a.sgd = o_.kind == HP_OPT_SGD;

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <array>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -40,6 +41,7 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int kEpiWarps = 8;
+constexpr int kSch = 4;  // dynamic-scheduler unit ring depth
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kATileBytes = BM * BK * 2;  // 16 KB
 
@@ -63,6 +65,7 @@ struct Params {
   const void* resid;
   int64_t ld_resid;
   int vec;  // C / aux / resid rows are 16-byte aligned
+  int* sched;  // dynamic tile scheduler: unit claim counter (self-resetting); null: static
   int debug;  // profiling only: 0 normal, 1 skip TMA loads, 2 skip MMAs, 3 skip epilogue
   unsigned long long* trace;  // profiling only: CTA 0 clock64 timeline (see kTr*)
 };
@@ -82,6 +85,16 @@ constexpr bool kProfile = false;
 __device__ __forceinline__ void trace_at(const Params& p, int slot, int lim = 1 << 30) {
   if constexpr (kProfile) {
     if (p.trace && blockIdx.x == 0 && slot < lim) p.trace[slot] = clock64();
+  }
+}
+// per-CTA [start, end] globaltimer (ns) at trace[1024 + 2 * blockIdx.x]
+__device__ __forceinline__ void trace_cta(const Params& p, int which) {
+  if constexpr (kProfile) {
+    if (p.trace) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.trace[1024 + 2 * blockIdx.x + which] = t;
+    }
   }
 }
 __device__ __forceinline__ bool debug_bit(const Params& p, int bit) {
@@ -601,10 +614,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* sch_full = tmem_empty + 2;   // [kSch] unit ring (dynamic scheduler)
+  uint64_t* sch_empty = sch_full + kSch;  // [kSch] (leader's counts every consumer)
+  int* sch_unit = reinterpret_cast<int*>(sch_empty + kSch);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sch_unit + kSch);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) trace_at(p, 0);
+  if (threadIdx.x == 0) {
+    trace_at(p, 0);
+    trace_cta(p, 0);
+  }
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const int unit0 = blockIdx.x / CG, unit_step = gridDim.x / CG;
 
@@ -616,6 +635,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
       mbar_init(&tmem_empty[a], CG * kEpiWarps);
+    }
+    for (int i = 0; i < kSch; ++i) {
+      mbar_init(&sch_full[i], 1);
+      // consumers of a slot: the MMA warp and the epilogue warps of the
+      // leader, plus (pair) the peer's producer and epilogue warps
+      mbar_init(&sch_empty[i], CG == 2 ? 2 * (1 + kEpiWarps) : 1 + kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -641,12 +666,71 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_at(p, 1);
 
+  // Work units: with p.sched the leader's producer draws them from a global
+  // counter (CTAs that start late -- SMs held by a concurrent NCCL or update
+  // kernel -- simply take fewer units) and hands them to this CTA's MMA and
+  // epilogue warps (and the peer CTA of a pair) through a kSch-slot ring; the
+  // last unit drawn is the -1 sentinel.  Without p.sched: static striding.
+  const uint32_t sch_empty_leader = CG == 2 ? mapa_shared(smem_u32(sch_empty), 0) : smem_u32(sch_empty);
+  auto take_unit = [&](uint32_t i) -> int {  // consumer side, whole warp
+    if (!p.sched) {
+      const int u = unit0 + static_cast<int>(i) * unit_step;
+      return u < p.units ? u : -1;
+    }
+    const uint32_t slot = i % kSch, ph = (i / kSch) & 1;
+    if (CG == 2 && rank != 0)
+      mbar_wait_cluster(&sch_full[slot], ph);
+    else
+      mbar_wait(&sch_full[slot], ph);
+    const int u = *reinterpret_cast<volatile int*>(&sch_unit[slot]);
+    __syncwarp();
+    if (lane == 0) {
+      if (CG == 2 && rank != 0)
+        mbar_arrive_release_cluster(sch_empty_leader + slot * 8);  // read before release
+      else
+        mbar_arrive(&sch_empty[slot]);
+    }
+    return u;
+  };
+  // leader producer, whole warp.  A CTA's first unit is static (blockIdx);
+  // later ones are claimed from the counter (offset by the grid's units), one
+  // iteration ahead, so neither the claim's L2 round trip nor the start-of-
+  // kernel burst of same-address atomics ever stalls a load
+  int claimed = 0;
+  auto draw_unit = [&](uint32_t i) -> int {
+    if (!p.sched) return take_unit(i);
+    const uint32_t slot = i % kSch, ph = (i / kSch) & 1;
+    mbar_wait(&sch_empty[slot], ph ^ 1);
+    int u = 0;
+    if (lane == 0) {
+      const int c = i == 0 ? unit0 : claimed;
+      u = c < p.units ? c : -1;
+      sch_unit[slot] = u;
+      if constexpr (CG == 2) {
+        const uint32_t ru = mapa_shared(smem_u32(&sch_unit[slot]), 1);
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ru), "r"(u) : "memory");
+        mbar_arrive_release_cluster(mapa_shared(smem_u32(&sch_full[slot]), 1));
+      }
+      mbar_arrive(&sch_full[slot]);
+      if (u >= 0) {
+        // every published unit makes exactly one claim, so a launch makes
+        // exactly p.units of them: the claim that returns p.units - 1 is the
+        // last, and resets the counter for the next launch
+        const int c2 = atomicAdd(p.sched, 1);
+        if (c2 == p.units - 1) *p.sched = 0;
+        claimed = unit_step + c2;
+      }
+    }
+    return __shfl_sync(0xffffffffu, u, 0);
+  };
   if (warp == 0) {
     // TMA producer (whole warp walks the ring, one elected lane issues).  An
     // MN-major operand tile is BNL/64 (or 2 for A) 8 KB swizzle atoms; with
     // the 3-D "atom" map (64 cols, K, col-block) it is ONE bulk-tensor load.
     uint32_t it = 0;
-    for (int u = unit0; u < p.units; u += unit_step) {
+    for (uint32_t ui = 0;; ++ui) {
+      const int u = rank == 0 ? draw_unit(ui) : take_unit(ui);
+      if (u < 0) break;
       int m0, nt, kb0, kb1;
       decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
       const int am0 = m0 + static_cast<int>(rank) * BM;       // this CTA's A rows
@@ -725,7 +809,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dak = p.a_mn ? (2048 >> 4) : (32 >> 4);
       const uint64_t dbk = p.b_mn ? (2048 >> 4) : (32 >> 4);
       uint32_t it = 0, lt = 0;
-      for (int u = unit0; u < p.units; u += unit_step, ++lt) {
+      for (;; ++lt) {
+        const int u = take_unit(lt);
+        if (u < 0) break;
         int m0, nt, kb0, kb1;
         decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
         const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
@@ -782,7 +868,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t lt = 0;
     const uint32_t empty_leader[2] = {CG == 2 ? mapa_shared(smem_u32(&tmem_empty[0]), 0) : 0u,
                                       CG == 2 ? mapa_shared(smem_u32(&tmem_empty[1]), 0) : 0u};
-    for (int u = unit0; u < p.units; u += unit_step, ++lt) {
+    for (;; ++lt) {
+      const int u = take_unit(lt);
+      if (u < 0) break;
       int m0, nt, kb0, kb1;
       decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
       const int n0 = nt * BN;
@@ -844,7 +932,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) trace_at(p, 2);
+  if (threadIdx.x == 0) {
+    trace_at(p, 2);
+    trace_cta(p, 1);
+  }
   if constexpr (CG == 2) cluster_sync_all();  // both CTAs done before the pair frees TMEM
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -995,6 +1086,21 @@ static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Pa
 namespace {
 int g_force_cg = 0;
 int g_generic_only = 0;
+int g_static_sched = -1;
+// scheduler counters: a pool of {next, done} pairs handed out round robin so
+// consecutive launches never share one (each launch resets its own at exit)
+int* next_sched() {
+  static int* pool = nullptr;
+  static int next = 0;
+  constexpr int kPool = 64;
+  if (!pool) {
+    HP_CUDA(cudaMalloc(&pool, sizeof(int) * 2 * kPool));
+    HP_CUDA(cudaMemset(pool, 0, sizeof(int) * 2 * kPool));
+  }
+  int* c = pool + 2 * next;
+  next = (next + 1) % kPool;
+  return c;
+}
 }
 void gemm_tc_set_generic(int on) { g_generic_only = on; }
 
@@ -1124,6 +1230,15 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.vec = epilogue_vec_ok(g);
   p.debug = g_debug_mode;
   p.trace = g_trace;
+  if (g_static_sched < 0) {
+    // Static unit striding by default.  HP_GEMM_DYNAMIC=1 turns on the
+    // dynamic tile scheduler -- measured ~1 us slower per launch on the C2
+    // shapes at N=1 (3.19 vs 3.00 ms per step of GEMMs) and no better at N=4
+    // under concurrent NCCL rings (5.96 vs 5.85 ms per step), so it stays opt-in.
+    const char* e = std::getenv("HP_GEMM_DYNAMIC");
+    g_static_sched = (e && e[0] == '1') ? 0 : 1;
+  }
+  p.sched = g_static_sched ? nullptr : next_sched();
   if (splits > 1) {
     // partial sums are reduced into C: clear the output region first
     if (g.c_group) {

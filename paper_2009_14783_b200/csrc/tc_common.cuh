@@ -47,6 +47,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // tile's mainloop runs): the suspend-time hint parks the warp in the barrier
 // unit until the phase completes instead of re-polling, so 16 idle warps do not
 // compete with the producer / MMA threads' barrier traffic and issue slots.
+// wait with cluster-scope acquire (the phase was completed by a peer CTA's
+// release arrive, e.g. after it wrote into this CTA's shared memory)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait_parked(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
