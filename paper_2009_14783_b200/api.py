@@ -398,6 +398,7 @@ class StepReport:
     rank_seconds: list = field(default_factory=list)
     local_loss_sum: float = 0.0
     local_weight: float = 0.0
+    updated: bool = True
 
 
 class Communicator:
@@ -455,6 +456,7 @@ class StepEngine:
         if params is not None:
             self.set_params(params)
         self.last_h2d_bytes = 0
+        self._group_t0 = None  # start of the pending update group (K > 1)
 
     def close(self):
         if self._h:
@@ -523,14 +525,23 @@ class StepEngine:
     def round_sync(self) -> StepReport:
         o = _lib.RoundOut()
         call("hp_engine_round_sync", self._h, C.byref(o))
-        return StepReport(o.step, o.loss, o.weight, 0.0, [], o.local_loss_sum, o.local_weight)
+        return StepReport(o.step, o.loss, o.weight, 0.0, [], o.local_loss_sum, o.local_weight,
+                          bool(o.updated))
 
-    def round(self, batch, dummy: bool = False, lr: float = 1e-3) -> StepReport:
+    def round(self, batch, dummy: bool = False, lr: float = 1e-3) -> Optional[StepReport]:
+        """StepEngine::round (engine.hpp:125-165): None on the first K-1 rounds
+        of an update group (update_freq = K), the report on the K-th; seconds
+        run from the group's first round, as the reference's group_start_."""
         t0 = time.perf_counter()
+        if self._group_t0 is None:
+            self._group_t0 = t0
         self.stage(batch)
         self.round_async(dummy, lr)
         rep = self.round_sync()
-        rep.seconds = time.perf_counter() - t0
+        if not rep.updated:
+            return None
+        rep.seconds = time.perf_counter() - self._group_t0
+        self._group_t0 = None
         return rep
 
     # -- instrumentation

@@ -62,8 +62,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
                hp_comm* comm)
     : m_(m), o_(o), x_(x), comm_(comm) {
   table_ = param_table(m_);
-  if (x_.update_freq != 1)
-    fail(HP_ECONFIG, "update_freq > 1 is not implemented on the device engine yet");
+  if (x_.update_freq == 0) fail(HP_ECONFIG, "update_freq must be >= 1");
   if (x_.max_tokens == 0 || x_.max_batch == 0)
     fail(HP_ECONFIG, "exec capacities max_tokens/max_batch must be > 0");
   if (m_.max_seq > static_cast<uint64_t>(kAttnMaxSeq))
@@ -262,12 +261,20 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
                                    colsum_scratch_floats((int)Mm, Vp_),
                                    colsum_scratch_floats((int)T, d_)});
   scratch_ = static_cast<float*>(dalloc(scratch * 4));
-  d_lw_ = static_cast<double*>(dalloc(4 * 8));
+  // [round loss, round weight, local loss, local weight, K-total loss, K-total weight]
+  d_lw_ = static_cast<double*>(dalloc(6 * 8));
+  HP_CUDA(cudaMemset(d_lw_, 0, 6 * 8));
+  if (x_.update_freq > 1) {
+    acc_grads_ = static_cast<float*>(dalloc(n_ * 4));
+    HP_CUDA(cudaMemset(acc_grads_, 0, n_ * 4));
+    d_acc_lw_ = static_cast<double*>(dalloc(2 * 8));
+    HP_CUDA(cudaMemset(d_acc_lw_, 0, 2 * 8));
+  }
   inv_w_ = static_cast<float*>(dalloc(4));
   inv_w64_ = static_cast<double*>(dalloc(8));
   flags_ = static_cast<int*>(dalloc(2 * 4));
   d_hyper_ = static_cast<float*>(dalloc(4 * 4));
-  HP_CUDA(cudaMallocHost(&h_lw_, 4 * 8));
+  HP_CUDA(cudaMallocHost(&h_lw_, 6 * 8));
   HP_CUDA(cudaMallocHost(&h_flags_, 2 * 4));
   HP_CUDA(cudaMemset(flags_, 0, 8));
 
@@ -683,9 +690,15 @@ void Engine::issue_bucket(size_t k) {
   if (comm_)
     HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, ncclSum,
                           comm_->nccl, s_comm_));
+  if (phase_ == 1) {
+    // a non-final round of K: the reduced bucket joins the accumulator
+    accumulate_grad(acc_grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, s_comm_);
+    return;
+  }
   // the bucket's update runs behind the rest of backward (engine.hpp:147-153:
   // every rank applies the identical update to the identical reduced sum)
   AdamArgs a = adam_args_;
+  a.g2 = phase_ == 2 ? acc_grads_ : nullptr;
   a.items = adam_items_ + 5 * static_cast<size_t>(bucket_items_[k].first);
   a.nitems = bucket_items_[k].second;
   tstart(TM_ADAM, s_comm_);
@@ -860,9 +873,14 @@ void Engine::backward() {
 void Engine::round_async(int dummy, double lr) {
   if (!staged_) fail(HP_ECONFIG, "round: no batch staged");
   HP_CUDA(cudaSetDevice(x_.device));
+  // K micro rounds per update (Accumulator, optim.hpp:154-202): rounds 1..K-1
+  // accumulate the reduced gradients, the K-th updates with the totals
+  const uint64_t K = x_.update_freq;
+  const bool final_round = K == 1 || acc_count_ + 1 == K;
+  phase_ = K == 1 ? 0 : (final_round ? 2 : 1);
   // one identical update on every rank (engine.hpp:147-153, optim.hpp:107-146),
   // issued per bucket on the side stream as the buckets complete
-  ++adam_t_;
+  if (final_round) ++adam_t_;
   const double c1 = 1.0 / (1.0 - std::pow(o_.beta1, static_cast<double>(adam_t_)));
   const double c2 = 1.0 / (1.0 - std::pow(o_.beta2, static_cast<double>(adam_t_)));
   AdamArgs& a = adam_args_;
@@ -886,7 +904,7 @@ void Engine::round_async(int dummy, double lr) {
   HP_CUDA(cudaMemcpyAsync(d_hyper_, hyper, sizeof(hyper), cudaMemcpyHostToDevice, s_main_));
 
   if (graphs_on_ && !timers_on_ && !capture_) {
-    GraphEntry& e = graphs_[std::make_tuple(batch_.T, batch_.B, batch_.M, dummy ? 1 : 0)];
+    GraphEntry& e = graphs_[std::make_tuple(batch_.T, batch_.B, batch_.M, (dummy ? 1 : 0) | (phase_ << 1))];
     if (e.exec) {
       HP_CUDA(cudaGraphLaunch(e.exec, s_main_));
       count_launch(static_cast<int>(e.launches));
@@ -914,7 +932,9 @@ void Engine::round_async(int dummy, double lr) {
   } else {
     round_body(dummy);
   }
-  ++step_;
+  acc_count_ = final_round ? 0 : acc_count_ + 1;
+  last_final_ = final_round;
+  if (final_round) ++step_;
   HP_CUDA(cudaEventRecord(ev_done_, s_main_));
   in_flight_ = true;
   last_dummy_ = dummy != 0;
@@ -955,7 +975,7 @@ void Engine::round_body(int dummy) {
               s_main_);
   // d_lw_ = [loss, weight, local loss, local weight]
   if (dummy) {
-    HP_CUDA(cudaMemsetAsync(d_lw_, 0, 4 * 8, s_main_));
+    HP_CUDA(cudaMemsetAsync(d_lw_, 0, 4 * 8, s_main_));  // (K-totals untouched)
   } else {
     HP_CUDA(cudaMemcpyAsync(d_lw_ + 2, d_lw_, 8, cudaMemcpyDeviceToDevice, s_main_));
     HP_CUDA(cudaMemcpyAsync(d_lw_ + 1, d_weight_, 8, cudaMemcpyDeviceToDevice, s_main_));
@@ -974,6 +994,9 @@ void Engine::round_body(int dummy) {
     HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_fwd_, 0));
   }
   finalize_weight(d_lw_, inv_w_, inv_w64_, flags_, sw);
+  // K > 1: running [loss, weight] totals; the K-th round's update divides by
+  // the total weight (engine.hpp:147-151)
+  if (phase_ != 0) accumulate_weight(d_lw_, d_acc_lw_, d_lw_ + 4, inv_w64_, phase_ == 2, sw);
 
   next_bucket_ = 0;
   if (dummy) {
@@ -993,7 +1016,7 @@ void Engine::round_body(int dummy) {
   // the round ends when the last bucket's update has landed
   HP_CUDA(cudaEventRecord(ev_comm_done_, s_comm_));
   HP_CUDA(cudaStreamWaitEvent(s_main_, ev_comm_done_, 0));
-  HP_CUDA(cudaMemcpyAsync(h_lw_, d_lw_, 4 * 8, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaMemcpyAsync(h_lw_, d_lw_, 6 * 8, cudaMemcpyDeviceToHost, s_main_));
   HP_CUDA(cudaMemcpyAsync(h_flags_, flags_, 2 * 4, cudaMemcpyDeviceToHost, s_main_));
 }
 
@@ -1001,20 +1024,27 @@ void Engine::round_sync(hp_round_out* out) {
   if (!in_flight_) fail(HP_ECONFIG, "round_sync without a round in flight");
   HP_CUDA(cudaEventSynchronize(ev_done_));
   in_flight_ = false;
-  const double loss = h_lw_[0], weight = h_lw_[1];
+  // per-round checks on the aggregated [loss, weight] (engine.hpp:134-137)
   if (h_flags_[0] & 1) {
-    --step_;
-    --adam_t_;
+    if (last_final_) {
+      --step_;
+      --adam_t_;
+    }
     fail(HP_ENUMERIC, "non-finite aggregated loss after step " + std::to_string(step_));
   }
   if (h_flags_[0] & 2) {
-    --step_;
-    --adam_t_;
+    if (last_final_) {
+      --step_;
+      --adam_t_;
+    }
     fail(HP_ENUMERIC, "total batch weight is zero: every rank was dummy");
   }
   if (h_flags_[1]) fail(HP_ENUMERIC, "non-finite gradient at step " + std::to_string(step_));
   if (out) {
-    out->updated = 1;
+    // K > 1: the report covers the K rounds (loss_sum / weight of the flush)
+    const bool totals = last_final_ && x_.update_freq > 1;
+    const double loss = totals ? h_lw_[4] : h_lw_[0], weight = totals ? h_lw_[5] : h_lw_[1];
+    out->updated = last_final_ ? 1 : 0;
     out->step = step_;
     out->loss = loss / weight;
     out->weight = weight;

@@ -49,7 +49,7 @@ class Engine {
   double elapsed(int a, int b);
   void synchronize();
   uint64_t stage_bytes() const { return stage_bytes_; }
-  uint64_t readback_bytes() const { return 4 * 8 + 2 * 4; }
+  uint64_t readback_bytes() const { return 6 * 8 + 2 * 4; }
   void timer_read(int which, std::string* name, double* ms, uint64_t* launches, double* bytes,
                   double* flops);
 
@@ -144,6 +144,12 @@ class Engine {
   uint64_t step_ = 0, adam_t_ = 0;
   bool in_flight_ = false;
   bool last_dummy_ = false;
+  // K > 1 accumulation state (Accumulator, optim.hpp:154-202)
+  float* acc_grads_ = nullptr;   // reduced gradient sums of the pending rounds
+  double* d_acc_lw_ = nullptr;   // their [loss, weight] totals
+  uint64_t acc_count_ = 0;       // rounds accumulated since the last update
+  int phase_ = 0;                // current round: 0 K=1, 1 accumulate, 2 final of K
+  bool last_final_ = true;
 
   bool timers_on_ = false;
   struct TimerAcc {

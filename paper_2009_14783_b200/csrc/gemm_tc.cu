@@ -41,7 +41,6 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int kEpiWarps = 8;
-constexpr int kSch = 4;  // dynamic-scheduler unit ring depth
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kATileBytes = BM * BK * 2;  // 16 KB
 
@@ -65,7 +64,6 @@ struct Params {
   const void* resid;
   int64_t ld_resid;
   int vec;  // C / aux / resid rows are 16-byte aligned
-  int* sched;  // dynamic tile scheduler: unit claim counter (self-resetting); null: static
   int debug;  // profiling only: 0 normal, 1 skip TMA loads, 2 skip MMAs, 3 skip epilogue
   unsigned long long* trace;  // profiling only: CTA 0 clock64 timeline (see kTr*)
 };
@@ -614,10 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
-  uint64_t* sch_full = tmem_empty + 2;   // [kSch] unit ring (dynamic scheduler)
-  uint64_t* sch_empty = sch_full + kSch;  // [kSch] (leader's counts every consumer)
-  int* sch_unit = reinterpret_cast<int*>(sch_empty + kSch);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sch_unit + kSch);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -636,12 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_full[a], 1);
       mbar_init(&tmem_empty[a], CG * kEpiWarps);
     }
-    for (int i = 0; i < kSch; ++i) {
-      mbar_init(&sch_full[i], 1);
-      // consumers of a slot: the MMA warp and the epilogue warps of the
-      // leader, plus (pair) the peer's producer and epilogue warps
-      mbar_init(&sch_empty[i], CG == 2 ? 2 * (1 + kEpiWarps) : 1 + kEpiWarps);
-    }
+
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -666,70 +656,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_at(p, 1);
 
-  // Work units: with p.sched the leader's producer draws them from a global
-  // counter (CTAs that start late -- SMs held by a concurrent NCCL or update
-  // kernel -- simply take fewer units) and hands them to this CTA's MMA and
-  // epilogue warps (and the peer CTA of a pair) through a kSch-slot ring; the
-  // last unit drawn is the -1 sentinel.  Without p.sched: static striding.
-  const uint32_t sch_empty_leader = CG == 2 ? mapa_shared(smem_u32(sch_empty), 0) : smem_u32(sch_empty);
-  auto take_unit = [&](uint32_t i) -> int {  // consumer side, whole warp
-    if (!p.sched) {
-      const int u = unit0 + static_cast<int>(i) * unit_step;
-      return u < p.units ? u : -1;
-    }
-    const uint32_t slot = i % kSch, ph = (i / kSch) & 1;
-    if (CG == 2 && rank != 0)
-      mbar_wait_cluster(&sch_full[slot], ph);
-    else
-      mbar_wait(&sch_full[slot], ph);
-    const int u = *reinterpret_cast<volatile int*>(&sch_unit[slot]);
-    __syncwarp();
-    if (lane == 0) {
-      if (CG == 2 && rank != 0)
-        mbar_arrive_release_cluster(sch_empty_leader + slot * 8);  // read before release
-      else
-        mbar_arrive(&sch_empty[slot]);
-    }
-    return u;
+  // Work units: static striding, unit u = blockIdx / CG + i * (gridDim / CG).
+  // (A dynamic scheduler -- units claimed from a global counter one unit
+  // ahead and handed to the MMA / epilogue warps and the peer CTA through an
+  // smem ring -- was measured and removed: ~1 us slower per launch at N=1
+  // and no gain at N=4 under concurrent NCCL rings.)
+  auto take_unit = [&](uint32_t i) -> int {
+    const int u = unit0 + static_cast<int>(i) * unit_step;
+    return u < p.units ? u : -1;
   };
-  // leader producer, whole warp.  A CTA's first unit is static (blockIdx);
-  // later ones are claimed from the counter (offset by the grid's units), one
-  // iteration ahead, so neither the claim's L2 round trip nor the start-of-
-  // kernel burst of same-address atomics ever stalls a load
-  int claimed = 0;
-  auto draw_unit = [&](uint32_t i) -> int {
-    if (!p.sched) return take_unit(i);
-    const uint32_t slot = i % kSch, ph = (i / kSch) & 1;
-    mbar_wait(&sch_empty[slot], ph ^ 1);
-    int u = 0;
-    if (lane == 0) {
-      const int c = i == 0 ? unit0 : claimed;
-      u = c < p.units ? c : -1;
-      sch_unit[slot] = u;
-      if constexpr (CG == 2) {
-        const uint32_t ru = mapa_shared(smem_u32(&sch_unit[slot]), 1);
-        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ru), "r"(u) : "memory");
-        mbar_arrive_release_cluster(mapa_shared(smem_u32(&sch_full[slot]), 1));
-      }
-      mbar_arrive(&sch_full[slot]);
-      if (u >= 0) {
-        // every published unit makes exactly one claim, so a launch makes
-        // exactly p.units of them: the claim that returns p.units - 1 is the
-        // last, and resets the counter for the next launch
-        const int c2 = atomicAdd(p.sched, 1);
-        if (c2 == p.units - 1) *p.sched = 0;
-        claimed = unit_step + c2;
-      }
-    }
-    return __shfl_sync(0xffffffffu, u, 0);
-  };
+
   if (warp == 0) {
     // TMA producer (whole warp walks the ring, one elected lane issues).  An
     // MN-major operand tile is BNL/64 (or 2 for A) 8 KB swizzle atoms; with
     // the 3-D "atom" map (64 cols, K, col-block) it is ONE bulk-tensor load.
     uint32_t it = 0;
     for (uint32_t ui = 0;; ++ui) {
-      const int u = rank == 0 ? draw_unit(ui) : take_unit(ui);
+      const int u = take_unit(ui);
       if (u < 0) break;
       int m0, nt, kb0, kb1;
       decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
@@ -1086,21 +1029,7 @@ static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Pa
 namespace {
 int g_force_cg = 0;
 int g_generic_only = 0;
-int g_static_sched = -1;
-// scheduler counters: a pool of {next, done} pairs handed out round robin so
-// consecutive launches never share one (each launch resets its own at exit)
-int* next_sched() {
-  static int* pool = nullptr;
-  static int next = 0;
-  constexpr int kPool = 64;
-  if (!pool) {
-    HP_CUDA(cudaMalloc(&pool, sizeof(int) * 2 * kPool));
-    HP_CUDA(cudaMemset(pool, 0, sizeof(int) * 2 * kPool));
-  }
-  int* c = pool + 2 * next;
-  next = (next + 1) % kPool;
-  return c;
-}
+
 }
 void gemm_tc_set_generic(int on) { g_generic_only = on; }
 
@@ -1230,15 +1159,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.vec = epilogue_vec_ok(g);
   p.debug = g_debug_mode;
   p.trace = g_trace;
-  if (g_static_sched < 0) {
-    // Static unit striding by default.  HP_GEMM_DYNAMIC=1 turns on the
-    // dynamic tile scheduler -- measured ~1 us slower per launch on the C2
-    // shapes at N=1 (3.19 vs 3.00 ms per step of GEMMs) and no better at N=4
-    // under concurrent NCCL rings (5.96 vs 5.85 ms per step), so it stays opt-in.
-    const char* e = std::getenv("HP_GEMM_DYNAMIC");
-    g_static_sched = (e && e[0] == '1') ? 0 : 1;
-  }
-  p.sched = g_static_sched ? nullptr : next_sched();
+
   if (splits > 1) {
     // partial sums are reduced into C: clear the output region first
     if (g.c_group) {

@@ -1204,17 +1204,22 @@ void ls_ce(int R, int V, const float* z, int64_t ldz, const int* target,
 }
 
 // ------------------------------------------------------------------ NSP head
+// Every CTA recomputes the B x 2 logit gradients (tiny) into smem; CTA 0
+// alone writes the row losses and the dH rows; dW's 2d entries are spread
+// over the grid, each a fixed-order sum over the batch (deterministic).
 template <class HT>
-__global__ void nsp_fwd_bwd_kernel(int B, int d, const int* __restrict__ cu,
-                                   const int* __restrict__ label, const HT* __restrict__ H,
-                                   const float* __restrict__ W, const float* __restrict__ bias,
-                                   float* __restrict__ row_loss, float* __restrict__ dW,
-                                   float* __restrict__ db, HT* __restrict__ dH, int grad) {
+__global__ void __launch_bounds__(1024) nsp_fwd_bwd_kernel(
+    int B, int d, const int* __restrict__ cu, const int* __restrict__ label,
+    const HT* __restrict__ H, const float* __restrict__ W, const float* __restrict__ bias,
+    float* __restrict__ row_loss, float* __restrict__ dW, float* __restrict__ db,
+    HT* __restrict__ dH, int grad) {
   extern __shared__ float dzs[];  // [B][2]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool lead = blockIdx.x == 0;
   for (int b = w; b < B; b += nw) {
     const HT* h0 = H + (int64_t)cu[b] * d;
     float z0 = 0.f, z1 = 0.f;
+#pragma unroll 8
     for (int c = lane; c < d; c += 32) {
       const float hv = tof(h0[c]);
       z0 += hv * W[c * 2 + 0];
@@ -1229,25 +1234,27 @@ __global__ void nsp_fwd_bwd_kernel(int B, int d, const int* __restrict__ cu,
     const float g0 = e0 / se - (t == 0 ? 1.f : 0.f);
     const float g1 = e1 / se - (t == 1 ? 1.f : 0.f);
     if (lane == 0) {
-      row_loss[b] = mx + logf(se) - (t == 0 ? z0 : z1);
+      if (lead) row_loss[b] = mx + logf(se) - (t == 0 ? z0 : z1);
       dzs[2 * b + 0] = g0;
       dzs[2 * b + 1] = g1;
     }
-    if (grad) {
+    if (grad && lead) {
       HT* dh = dH + (int64_t)cu[b] * d;
+#pragma unroll 8
       for (int c = lane; c < d; c += 32)
         dh[c] = fromf<HT>(tof(dh[c]) + g0 * W[c * 2 + 0] + g1 * W[c * 2 + 1]);
     }
   }
   if (!grad) return;
   __syncthreads();
-  for (int e = threadIdx.x; e < 2 * d; e += blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * d; e += gridDim.x * blockDim.x) {
     const int c = e >> 1, k = e & 1;
     float acc = 0.f;
+#pragma unroll 8
     for (int b = 0; b < B; ++b) acc += tof(H[(int64_t)cu[b] * d + c]) * dzs[2 * b + k];
     dW[e] = acc;
   }
-  if (threadIdx.x < 2) {
+  if (lead && threadIdx.x < 2) {
     float acc = 0.f;
     for (int b = 0; b < B; ++b) acc += dzs[2 * b + threadIdx.x];
     db[threadIdx.x] = acc;
@@ -1259,9 +1266,11 @@ void nsp_head(const DevBatch& b, int d, const void* H, DType ht, const float* W,
               int compute_grad, cudaStream_t s) {
   if (b.B == 0) return;
   const size_t sm = sizeof(float) * 2 * b.B;
-  DISPATCH1(ht, X, nsp_fwd_bwd_kernel<X><<<1, 512, sm, s>>>(b.B, d, b.cu, b.label, (const X*)H, W,
-                                                           bias, row_loss, dW, db, (X*)dH,
-                                                           compute_grad));
+  // one warp per row (B <= 32 per CTA pass); dW's 2d sums over 2 CTAs
+  const int grid = compute_grad ? 2 : 1;
+  DISPATCH1(ht, X, nsp_fwd_bwd_kernel<X><<<grid, 1024, sm, s>>>(b.B, d, b.cu, b.label, (const X*)H, W,
+                                                              bias, row_loss, dW, db, (X*)dH,
+                                                              compute_grad));
   LAUNCH_CHECK();
   count_launch();
 }
@@ -1304,6 +1313,57 @@ void finalize_weight(const double* lw, float* inv_w, double* inv_w64, int* flags
   count_launch();
 }
 
+__global__ void fill_add_kernel_scalar(float* __restrict__ acc, const float* __restrict__ g, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) acc[i] += g[i];
+}
+// K > 1 (Accumulator, optim.hpp:154-202): the round's [loss, weight] joins the
+// running totals; on the K-th round the totals become the report (lw[4..5])
+// and 1/total weight the update's scale, and the totals restart.
+__global__ void accumulate_weight_kernel(const double* lw, double* acc, double* out,
+                                         double* inv_w64, int final_round) {
+  acc[0] += lw[0];
+  acc[1] += lw[1];
+  if (final_round) {
+    out[0] = acc[0];
+    out[1] = acc[1];
+    *inv_w64 = acc[1] > 0.0 ? 1.0 / acc[1] : 0.0;
+    acc[0] = 0.0;
+    acc[1] = 0.0;
+  }
+}
+void accumulate_weight(const double* lw, double* acc, double* out, double* inv_w64, int final_round,
+                       cudaStream_t s) {
+  accumulate_weight_kernel<<<1, 1, 0, s>>>(lw, acc, out, inv_w64, final_round);
+  LAUNCH_CHECK();
+  count_launch();
+}
+// acc[lo, lo+n) += g[lo, lo+n) (a reduced gradient bucket of a non-final round)
+__global__ void accumulate_grad_kernel(float* __restrict__ acc, const float* __restrict__ g, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+    if (i + 4 <= n) {
+      float4 a = *reinterpret_cast<const float4*>(acc + i);
+      const float4 b = *reinterpret_cast<const float4*>(g + i);
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      *reinterpret_cast<float4*>(acc + i) = a;
+    } else {
+      for (uint64_t j = i; j < n; ++j) acc[j] += g[j];
+    }
+  }
+}
+void accumulate_grad(float* acc, const float* g, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  // float4 path needs 16-byte alignment of both ranges
+  if (((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(g)) & 15) == 0) {
+    accumulate_grad_kernel<<<148 * 8, 256, 0, s>>>(acc, g, n);
+  } else {
+    fill_add_kernel_scalar<<<148 * 8, 256, 0, s>>>(acc, g, n);
+  }
+  LAUNCH_CHECK();
+  count_launch();
+}
+
 // ------------------------------------------------------------------ Adam
 __device__ __forceinline__ uint64_t shadow_index(const uint64_t* seg, int nseg, uint64_t i) {
   int lo = 0, hi = nseg - 1;
@@ -1332,7 +1392,10 @@ __device__ __forceinline__ void adam_one(const AdamArgs& a, float& p, float& m, 
 }
 
 // One CTA per work item.  float4 I/O when the item is 16-byte aligned.
-__global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a0) {
+// Memory-bound: 6 CTAs (48 warps) per SM keep enough loads in flight, so the
+// register budget is pinned (<= 42).
+template <bool ACC>  // ACC: add (then zero) the K > 1 accumulator a.g2
+__global__ void __launch_bounds__(256, 6) adam_kernel(const AdamArgs a0) {
   if (a0.flags && *a0.flags) return;  // numeric error: leave parameters untouched
   AdamArgs a = a0;
   if (a.hyper) {  // per-step scalars from device memory (graph replays)
@@ -1357,11 +1420,25 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a0) {
       float4 m = *reinterpret_cast<const float4*>(a.m + lo + i);
       float4 v = *reinterpret_cast<const float4*>(a.v + lo + i);
       float4 g = *reinterpret_cast<const float4*>(a.g + lo + i);
-      float* pp = &p.x; float* mm = &m.x; float* vv = &v.x; float* gg = &g.x;
+      float* pp = &p.x; float* mm = &m.x; float* vv = &v.x; const float* gg = &g.x;
+      // g /= total weight in f64, then cast to T (engine.hpp:151, optim.hpp:135)
+      float gs[4];
+      if constexpr (ACC) {  // K > 1: earlier rounds' sums, consumed (zeroed) here
+        const float4 q = *reinterpret_cast<const float4*>(a.g2 + lo + i);
+        *reinterpret_cast<float4*>(a.g2 + lo + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float* qq = &q.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double gd = (double)gg[e] + (double)qq[e];
+          gs[e] = scale ? (float)(gd * sc) : (float)gd;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) gs[e] = scale ? (float)((double)gg[e] * sc) : gg[e];
+      }
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        // g /= total weight in f64, then cast to T (engine.hpp:151, optim.hpp:135)
-        const float ge = scale ? (float)((double)gg[e] * sc) : gg[e];
+        const float ge = gs[e];
         if (!isfinite(ge)) { bad = 1; continue; }
         adam_one(a, pp[e], mm[e], vv[e], ge);
       }
@@ -1382,7 +1459,14 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a0) {
       }
     }
     for (uint64_t i = n4 + threadIdx.x; i < n; i += blockDim.x) {
-      const float ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+      float ge;
+      if constexpr (ACC) {
+        const double gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
+        a.g2[lo + i] = 0.f;
+        ge = scale ? (float)(gd * sc) : (float)gd;
+      } else {
+        ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+      }
       if (!isfinite(ge)) { bad = 1; continue; }
       float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
       adam_one(a, p, m, v, ge);
@@ -1391,7 +1475,14 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a0) {
     }
   } else {
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const float ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+      float ge;
+      if constexpr (ACC) {
+        const double gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
+        a.g2[lo + i] = 0.f;
+        ge = scale ? (float)(gd * sc) : (float)gd;
+      } else {
+        ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+      }
       if (!isfinite(ge)) { bad = 1; continue; }
       float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
       adam_one(a, p, m, v, ge);
@@ -1403,7 +1494,10 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs a0) {
 }
 void adam_update(const AdamArgs& a, cudaStream_t s) {
   if (a.nitems == 0) return;
-  adam_kernel<<<a.nitems, 256, 0, s>>>(a);
+  if (a.g2)
+    adam_kernel<true><<<a.nitems, 256, 0, s>>>(a);
+  else
+    adam_kernel<false><<<a.nitems, 256, 0, s>>>(a);
   LAUNCH_CHECK();
   count_launch();
 }

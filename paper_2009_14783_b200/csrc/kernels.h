@@ -183,6 +183,7 @@ struct AdamArgs {
   float* p; float* m; float* v; const float* g; uint64_t n;
   float lr, b1, b2, eps, c1, c2;
   const float* hyper;     // device [lr, c1, c2]; overrides the scalars when non-null
+  float* g2;              // K > 1: earlier rounds' gradient sums, added then zeroed (or null)
   const double* inv_w64;  // may be null
   const int* flags;       // skip everything when *flags != 0
   int* bad;               // set to 1 on a non-finite gradient
@@ -193,6 +194,10 @@ struct AdamArgs {
   const uint64_t* items; int nitems;
 };
 void adam_update(const AdamArgs& a, cudaStream_t s);
+// K > 1 gradient accumulation (Accumulator, optim.hpp:154-202)
+void accumulate_weight(const double* lw, double* acc, double* out, double* inv_w64, int final_round,
+                       cudaStream_t s);
+void accumulate_grad(float* acc, const float* g, uint64_t n, cudaStream_t s);
 
 // bf16 shadow refresh from fp32 params (after set_params / broadcast).
 void refresh_shadow(const float* p, void* shadow, const uint64_t* seg_table,

@@ -207,3 +207,44 @@ def test_graph_replay_bit_identical_to_eager(monkeypatch, compute):
     assert np.array_equal(lg, le)
     assert dg == de
     assert ng == ne  # replays account for the kernels inside the graph
+
+
+def test_c1_k2_accumulation_matches_reference_w2():
+    # W*K equivalence (test_engine.cpp:237-294, acceptance criterion 2): one
+    # rank with update_freq = 2 fed rank 0's then rank 1's batch reproduces the
+    # reference's W = 2, K = 1 trajectory; the first round of each group
+    # returns no report and does not advance the step.
+    rec, plan = c1_batches()
+    t = golden("c1_ref_train.npz")
+    eng = c1_engine(update_freq=2)
+    losses = []
+    for step in range(10):
+        r0 = hp.partition_for_rank(plan, 2, 0)[step]
+        r1 = hp.partition_for_rank(plan, 2, 1)[step]
+        assert eng.round(rec.batch(plan.batches[r0.batch_index]), lr=1e-3) is None
+        rep = eng.round(rec.batch(plan.batches[r1.batch_index]), lr=1e-3)
+        assert rep is not None and rep.step == step + 1
+        assert rep.weight == 16.0
+        losses.append(rep.loss)
+    losses = np.array(losses)
+    assert np.max(np.abs(losses - t["losses_f64"]) / np.abs(t["losses_f64"])) <= 1e-4
+    assert rel_norm(eng.get_params(), t["params_f64_as_f32"]) <= 1e-4
+
+
+@pytest.mark.parametrize("compute", ["f32", "bf16"])
+def test_k3_accumulation_equals_combined_batch(compute):
+    # K = 3 rounds over batches a, b, c == one K = 1 round over a + b + c
+    # (sums stay raw until the flush; the update divides by the total weight)
+    spec, ospec, rec = _bert_case(d=128, heads=2, dff=256, vocab=203, n=24)
+    mk = lambda k: hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(
+        compute=compute, max_tokens=1024, max_batch=24, max_masks=256, update_freq=k), seed=9)
+    parts = [np.arange(0, 6), np.arange(6, 14), np.arange(14, 20)]
+    ek, e1 = mk(3), mk(1)
+    for rnd in range(2):
+        reps = [ek.round(rec.batch(p), lr=1e-3) for p in parts]
+        assert reps[0] is None and reps[1] is None and reps[2].step == rnd + 1
+        ref = e1.round(rec.batch(np.concatenate(parts)), lr=1e-3)
+        assert abs(reps[2].weight - ref.weight) == 0
+        assert abs(reps[2].loss - ref.loss) <= (1e-6 if compute == "f32" else 2e-2) * abs(ref.loss)
+    tol = 1e-5 if compute == "f32" else 2e-2
+    assert rel_norm(ek.get_params(), e1.get_params()) <= tol
