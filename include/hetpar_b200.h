@@ -197,6 +197,46 @@ hp_status hp_engine_broadcast_params(hp_engine* e, int root);
 /* Adam state (for HCK1): m, v in canonical order, t. */
 hp_status hp_engine_get_adam(hp_engine* e, float* m, float* v, uint64_t* t);
 hp_status hp_engine_set_adam(hp_engine* e, const float* m, const float* v, uint64_t t);
+
+/* ------------------------------------------------------------------------
+ * HCK1 checkpoints (src/checkpoint.cpp:165-302) and resume fast-forward
+ * (include/hetpar/engine.hpp:211-245).  Files are byte-compatible with the
+ * reference's save_checkpoint<float> / load_checkpoint<float>.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  uint64_t epoch, step, seed;  /* TrainState (checkpoint.hpp:15-37) */
+  int policy;                  /* HP_POLICY_* */
+  uint64_t world_size, update_freq;
+  int sched_kind;              /* SchedulerKind: 0 fixed, 1 inverse_sqrt, 2 linear */
+  double peak_lr;
+  uint64_t sched_d_model, warmup_steps, total_steps;
+  int opt_kind;                /* HP_OPT_* */
+  double beta1, beta2, eps;
+  uint64_t opt_t;              /* Adam step counter */
+} hp_ckpt_desc;
+/* Host-side writer / reader of one f32 checkpoint; params, m, v are flat
+ * canonical vectors (m, v read/written only for Adam).  hp_checkpoint_read
+ * validates magic, digest, version, policy, dtype, names and shapes; the
+ * output pointers may be null for a metadata-only read (n = their capacity). */
+hp_status hp_checkpoint_write(const char* path, const hp_model_desc* m, const hp_ckpt_desc* c,
+                              const float* params, const float* adam_m, const float* adam_v);
+hp_status hp_checkpoint_read(const char* path, hp_model_desc* m, hp_ckpt_desc* c, float* params,
+                             float* adam_m, float* adam_v, uint64_t n);
+/* save_checkpoint from device state (master rank): c supplies epoch, seed,
+ * policy, world, update_freq and the scheduler; step, the optimizer and its
+ * moments come from the engine.  Refused while an update group (K > 1) is
+ * partially accumulated -- the format has no accumulator block. */
+hp_status hp_engine_save_checkpoint(hp_engine* e, const char* path, const hp_ckpt_desc* c);
+/* load_checkpoint into device state: parameters, Adam moments and t, step;
+ * the file's model must equal the engine's.  c (may be null) receives the
+ * file's metadata. */
+hp_status hp_engine_load_checkpoint(hp_engine* e, const char* path, hp_ckpt_desc* c);
+/* Epoch and rounds to skip after `step` updates of world x update_freq
+ * lockstep rounds (engine.hpp:225-244). */
+hp_status hp_resume_position(const uint32_t* lens, uint64_t n, uint64_t max_sentences,
+                             uint64_t max_tokens, uint64_t seed, uint64_t world,
+                             uint64_t update_freq, uint64_t step, uint64_t* epoch,
+                             uint64_t* skip_rounds);
 /* local (pre-reduce) gradient of the last round, canonical order; valid after
  * hp_engine_round_sync when debug capture is on. */
 hp_status hp_engine_set_capture(hp_engine* e, int on);

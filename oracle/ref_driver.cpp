@@ -198,6 +198,7 @@ int cmd_train_t(const Args& a) {
   generate_mlm_shards(data, gen_cfg(a));
   EngineConfig cfg = engine_cfg(a, data);
   cfg.checkpoint_dir = out + "/ckpt";
+  cfg.checkpoint_interval = argu(a, "ckpt_every", 0);
   const size_t world = argu(a, "world", 2);
   auto hub = make_inproc_hub(world, 600000);
   std::vector<RunReport> reports(world);
@@ -240,6 +241,12 @@ int cmd_train_t(const Args& a) {
   dump(out + "/adam_m" + suf, m);
   dump(out + "/adam_v" + suf, v);
   fs::remove_all(data);
+  if (argu(a, "keep_ckpt", 0)) {
+    // keep the reference-written HCK1 files (golden fixtures, tools/make_golden.py)
+    for (const auto& f : fs::directory_iterator(cfg.checkpoint_dir))
+      fs::copy_file(f.path(), out + "/" + f.path().filename().string(),
+                    fs::copy_options::overwrite_existing);
+  }
   fs::remove_all(cfg.checkpoint_dir);
   std::printf("steps=%zu final_loss=%.17g params=%zu\n", losses.size(),
               losses.empty() ? 0.0 : losses.back(), flat.size());

@@ -88,6 +88,15 @@ class BatchDesc(C.Structure):
                 ("mask_orig", C.c_void_p), ("label", C.c_void_p)]
 
 
+class CkptDesc(C.Structure):
+    _fields_ = [("epoch", C.c_uint64), ("step", C.c_uint64), ("seed", C.c_uint64),
+                ("policy", C.c_int), ("world_size", C.c_uint64), ("update_freq", C.c_uint64),
+                ("sched_kind", C.c_int), ("peak_lr", C.c_double), ("sched_d_model", C.c_uint64),
+                ("warmup_steps", C.c_uint64), ("total_steps", C.c_uint64), ("opt_kind", C.c_int),
+                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("opt_t", C.c_uint64)]
+
+
 class RoundOut(C.Structure):
     _fields_ = [("updated", C.c_int), ("step", C.c_uint64), ("loss", C.c_double),
                 ("weight", C.c_double), ("local_loss_sum", C.c_double),
@@ -122,6 +131,11 @@ _SIGS = {
     "hp_engine_broadcast_params": [P, I],
     "hp_engine_get_adam": [P, P, P, P],
     "hp_engine_set_adam": [P, P, P, U64],
+    "hp_checkpoint_write": [C.c_char_p, P, P, P, P, P],
+    "hp_checkpoint_read": [C.c_char_p, P, P, P, P, P, U64],
+    "hp_engine_save_checkpoint": [P, C.c_char_p, P],
+    "hp_engine_load_checkpoint": [P, C.c_char_p, P],
+    "hp_resume_position": [P, U64, U64, U64, U64, U64, U64, U64, P, P],
     "hp_engine_set_capture": [P, I],
     "hp_engine_get_local_grads": [P, P, U64],
     "hp_engine_stage_batch": [P, P],

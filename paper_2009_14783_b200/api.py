@@ -57,6 +57,7 @@ def shuffle_iota(seed: int, n: int) -> np.ndarray:
 # --------------------------------------------------------------------- model
 _ARCH = {"masked_token_model": _lib.HP_ARCH_MASKED_TOKEN_MODEL,
          "bert_encoder": _lib.HP_ARCH_BERT_ENCODER}
+_POLICY = {"sentences": _lib.HP_POLICY_SENTENCES, "tokens": _lib.HP_POLICY_TOKENS}
 
 
 @dataclass
@@ -401,6 +402,85 @@ class StepReport:
     updated: bool = True
 
 
+@dataclass
+class CheckpointMeta:
+    """TrainState fields an HCK1 file carries besides the tensors
+    (checkpoint.hpp:15-37, checkpoint.cpp:54-79).  ``step`` and the optimizer
+    fields are filled from the engine on save and from the file on load."""
+    epoch: int = 0
+    step: int = 0
+    seed: int = 0
+    policy: str = "sentences"
+    world_size: int = 1
+    update_freq: int = 1
+    scheduler: SchedulerConfig = field(default_factory=SchedulerConfig)
+    optimizer: str = "adam"
+    beta1: float = 0.9
+    beta2: float = 0.98
+    eps: float = 1e-9
+    opt_t: int = 0
+
+    def desc(self) -> _lib.CkptDesc:
+        sk = {"fixed": 0, "inverse_sqrt": 1, "linear": 2}[self.scheduler.kind]
+        return _lib.CkptDesc(self.epoch, self.step, self.seed, _POLICY[self.policy],
+                             self.world_size, self.update_freq, sk, self.scheduler.peak_lr,
+                             self.scheduler.d_model, self.scheduler.warmup_steps,
+                             self.scheduler.total_steps, 1 if self.optimizer == "adam" else 0,
+                             self.beta1, self.beta2, self.eps, self.opt_t)
+
+    @staticmethod
+    def from_desc(d: _lib.CkptDesc) -> "CheckpointMeta":
+        sched = SchedulerConfig(kind=("fixed", "inverse_sqrt", "linear")[d.sched_kind],
+                                peak_lr=d.peak_lr, d_model=d.sched_d_model,
+                                warmup_steps=d.warmup_steps, total_steps=d.total_steps)
+        return CheckpointMeta(d.epoch, d.step, d.seed, "tokens" if d.policy == 2 else "sentences",
+                              d.world_size, d.update_freq, sched,
+                              "adam" if d.opt_kind == 1 else "sgd", d.beta1, d.beta2, d.eps, d.opt_t)
+
+
+_ARCH_NAME = {v: k for k, v in _ARCH.items()}
+
+
+def write_checkpoint(path: str, spec: ModelSpec, meta: CheckpointMeta, params: np.ndarray,
+                     adam_m: Optional[np.ndarray] = None, adam_v: Optional[np.ndarray] = None) -> None:
+    """save_checkpoint<float> (checkpoint.cpp:165-212): one HCK1 file, written
+    atomically; byte-identical to the reference writer for the same state."""
+    p = np.ascontiguousarray(params, np.float32)
+    m = None if adam_m is None else np.ascontiguousarray(adam_m, np.float32)
+    v = None if adam_v is None else np.ascontiguousarray(adam_v, np.float32)
+    md, cd = spec.desc(), meta.desc()
+    call("hp_checkpoint_write", path.encode(), C.byref(md), C.byref(cd), _p(p),
+         None if m is None else _p(m), None if v is None else _p(v))
+
+
+def read_checkpoint(path: str):
+    """load_checkpoint<float> (checkpoint.cpp:214-287) -> (spec, meta, params,
+    adam_m, adam_v); digest, version, dtype, names and shapes validated."""
+    md, cd = _lib.ModelDesc(), _lib.CkptDesc()
+    call("hp_checkpoint_read", path.encode(), C.byref(md), C.byref(cd), None, None, None, 0)
+    spec = ModelSpec(_ARCH_NAME[md.arch], md.d_model, md.heads, md.vocab, md.max_seq,
+                     md.layers if md.arch == _ARCH["bert_encoder"] else 1, md.d_ff,
+                     bool(md.with_nsp), md.label_smooth_eps)
+    n = flat_size(spec)
+    p, m, v = (np.empty(n, np.float32) for _ in range(3))
+    call("hp_checkpoint_read", path.encode(), None, None, _p(p), _p(m), _p(v), n)
+    meta = CheckpointMeta.from_desc(cd)
+    if meta.optimizer != "adam":
+        m = v = None
+    return spec, meta, p, m, v
+
+
+def resume_position(token_lengths, max_sentences: int, max_tokens: int, seed: int, world: int,
+                    update_freq: int, step: int) -> tuple[int, int]:
+    """Epoch and rounds to skip when resuming after ``step`` updates
+    (engine.hpp:225-244: P updates consumed exactly P*K lockstep rounds)."""
+    lens = np.ascontiguousarray(token_lengths, np.uint32)
+    e, k = C.c_uint64(), C.c_uint64()
+    call("hp_resume_position", _p(lens), len(lens), max_sentences, max_tokens, seed, world,
+         update_freq, step, C.byref(e), C.byref(k))
+    return e.value, k.value
+
+
 class Communicator:
     """NCCL communicator over NVLink/NVSwitch, one process per GPU.  The
     ncclUniqueId is created on rank 0 and shipped with a torch.distributed
@@ -491,6 +571,23 @@ class StepEngine:
         t = C.c_uint64()
         call("hp_engine_get_adam", self._h, _p(m), _p(v), C.byref(t))
         return m, v, t.value
+
+    def save_checkpoint(self, path: str, meta: CheckpointMeta) -> None:
+        """HCK1 from device state (master rank; checkpoint.cpp:165-212).  The
+        engine supplies step, optimizer kind / hyper-parameters and moments."""
+        cd = meta.desc()
+        call("hp_engine_save_checkpoint", self._h, path.encode(), C.byref(cd))
+
+    def load_checkpoint(self, path: str) -> CheckpointMeta:
+        """HCK1 into device state: parameters, Adam m / v / t, step."""
+        cd = _lib.CkptDesc()
+        call("hp_engine_load_checkpoint", self._h, path.encode(), C.byref(cd))
+        return CheckpointMeta.from_desc(cd)
+
+    def step_count(self) -> int:
+        s = C.c_uint64()
+        call("hp_engine_step_count", self._h, C.byref(s))
+        return s.value
 
     def set_capture(self, on: bool):
         call("hp_engine_set_capture", self._h, int(on))

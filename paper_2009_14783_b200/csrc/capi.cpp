@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 
+#include "checkpoint.h"
 #include "engine.h"
 #include "hetpar_b200.h"
 #include "hostdata.h"
@@ -447,6 +448,47 @@ hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf1
     if (dO) hp::attention_bwd(b, H, dk, qkv, o, dO, lse, dqkv, t, 0);
   }
   HP_CUDA(cudaDeviceSynchronize());
+  HP_API_END
+}
+
+hp_status hp_checkpoint_write(const char* path, const hp_model_desc* m, const hp_ckpt_desc* c,
+                              const float* params, const float* adam_m, const float* adam_v) {
+  HP_API_BEGIN
+  if (!path || !m || !c || !params) hp::fail(HP_ECONFIG, "hp_checkpoint_write: null argument");
+  hp::write_file_atomic(path, hp::hck1_serialize(*m, *c, params, adam_m, adam_v));
+  HP_API_END
+}
+
+hp_status hp_checkpoint_read(const char* path, hp_model_desc* m, hp_ckpt_desc* c, float* params,
+                             float* adam_m, float* adam_v, uint64_t n) {
+  HP_API_BEGIN
+  if (!path) hp::fail(HP_ECONFIG, "hp_checkpoint_read: null path");
+  hp::hck1_parse(hp::read_file(path), m, c, params, adam_m, adam_v, n);
+  HP_API_END
+}
+
+hp_status hp_engine_save_checkpoint(hp_engine* e, const char* path, const hp_ckpt_desc* c) {
+  HP_API_BEGIN
+  if (!e || !path || !c) hp::fail(HP_ECONFIG, "hp_engine_save_checkpoint: null argument");
+  e->e->save_checkpoint(path, *c);
+  HP_API_END
+}
+
+hp_status hp_engine_load_checkpoint(hp_engine* e, const char* path, hp_ckpt_desc* c) {
+  HP_API_BEGIN
+  if (!e || !path) hp::fail(HP_ECONFIG, "hp_engine_load_checkpoint: null argument");
+  e->e->load_checkpoint(path, c);
+  HP_API_END
+}
+
+hp_status hp_resume_position(const uint32_t* lens, uint64_t n, uint64_t max_sentences,
+                             uint64_t max_tokens, uint64_t seed, uint64_t world,
+                             uint64_t update_freq, uint64_t step, uint64_t* epoch,
+                             uint64_t* skip_rounds) {
+  HP_API_BEGIN
+  if (!lens || !epoch || !skip_rounds) hp::fail(HP_ECONFIG, "hp_resume_position: null argument");
+  hp::resume_position(std::vector<uint32_t>(lens, lens + n), max_sentences, max_tokens, seed, world,
+                      update_freq, step, epoch, skip_rounds);
   HP_API_END
 }
 

@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "checkpoint.h"
 #include "hp_common.h"
 
 namespace hp {
@@ -367,6 +368,50 @@ void Engine::set_adam(const float* m, const float* v, uint64_t t) {
   HP_CUDA(cudaMemcpyAsync(adam_v_, v, n_ * 4, cudaMemcpyHostToDevice, s_main_));
   HP_CUDA(cudaStreamSynchronize(s_main_));
   adam_t_ = t;
+}
+
+// ------------------------------------------------------------------ HCK1
+// save_checkpoint / load_checkpoint (checkpoint.cpp:165-302) from / into the
+// device state; the byte format lives in checkpoint.cpp.
+void Engine::save_checkpoint(const std::string& path, const hp_ckpt_desc& c) {
+  if (in_flight_) fail(HP_ECONFIG, "save_checkpoint while a round is in flight");
+  if (acc_count_ != 0)
+    fail(HP_ECONFIG, "save_checkpoint inside a partially accumulated update group (update_freq > 1)");
+  std::vector<float> p(n_), m(n_), v(n_);
+  synchronize();
+  HP_CUDA(cudaMemcpy(p.data(), params_, n_ * 4, cudaMemcpyDeviceToHost));
+  HP_CUDA(cudaMemcpy(m.data(), adam_m_, n_ * 4, cudaMemcpyDeviceToHost));
+  HP_CUDA(cudaMemcpy(v.data(), adam_v_, n_ * 4, cudaMemcpyDeviceToHost));
+  hp_ckpt_desc d = c;
+  d.step = step_;
+  d.opt_kind = o_.kind;
+  d.beta1 = o_.beta1;
+  d.beta2 = o_.beta2;
+  d.eps = o_.eps;
+  d.opt_t = adam_t_;
+  write_file_atomic(path, hck1_serialize(m_, d, p.data(), m.data(), v.data()));
+}
+
+void Engine::load_checkpoint(const std::string& path, hp_ckpt_desc* out) {
+  if (in_flight_) fail(HP_ECONFIG, "load_checkpoint while a round is in flight");
+  hp_model_desc md{};
+  hp_ckpt_desc d{};
+  std::vector<float> p(n_), m(n_), v(n_);
+  hck1_parse(read_file(path), &md, &d, nullptr, nullptr, nullptr, 0);  // metadata first
+  const auto ft = param_table(md);
+  if (md.arch != m_.arch || ft.size() != table_.size() ||
+      md.label_smooth_eps != m_.label_smooth_eps || md.with_nsp != m_.with_nsp)
+    fail(HP_ECONFIG, "resume model spec does not match the checkpoint");
+  for (size_t i = 0; i < ft.size(); ++i)
+    if (ft[i].name != table_[i].name || ft[i].rows != table_[i].rows || ft[i].cols != table_[i].cols)
+      fail(HP_ECONFIG, "resume model spec does not match the checkpoint");
+  if (d.opt_kind != o_.kind) fail(HP_ECONFIG, "checkpoint optimizer kind differs from the engine's");
+  hck1_parse(read_file(path), nullptr, nullptr, p.data(), m.data(), v.data(), n_);
+  set_params(p.data(), n_, 0);
+  if (d.opt_kind == HP_OPT_ADAM) set_adam(m.data(), v.data(), d.opt_t);
+  step_ = d.step;
+  acc_count_ = 0;
+  if (out) *out = d;
 }
 
 void Engine::get_local_grads(float* flat, uint64_t n) {

@@ -37,6 +37,8 @@ class Engine {
   void broadcast_params(int root);
   void get_adam(float* m, float* v, uint64_t* t);
   void set_adam(const float* m, const float* v, uint64_t t);
+  void save_checkpoint(const std::string& path, const hp_ckpt_desc& c);
+  void load_checkpoint(const std::string& path, hp_ckpt_desc* out);
   void set_capture(bool on) { capture_ = on; }
   void get_local_grads(float* flat, uint64_t n);
   void stage_batch(const hp_batch& b);

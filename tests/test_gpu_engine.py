@@ -248,3 +248,74 @@ def test_k3_accumulation_equals_combined_batch(compute):
         assert abs(reps[2].loss - ref.loss) <= (1e-6 if compute == "f32" else 2e-2) * abs(ref.loss)
     tol = 1e-5 if compute == "f32" else 2e-2
     assert rel_norm(ek.get_params(), e1.get_params()) <= tol
+
+
+def _hck1_run():
+    import json
+    import os
+    d = os.path.join(os.path.dirname(__file__), "golden", "hck1")
+    run = json.load(open(os.path.join(d, "run.json")))
+    c = run["config"]
+    rec = hp.generate_mlm_records(hp.MlmGenConfig(
+        n=c["n"], vocab=c["vocab"], docs=c["docs"], sentences_per_doc=c["spd"],
+        min_sentence_words=c["min_words"], max_sentence_words=c["max_words"], seed=c["data_seed"]))
+    plan = hp.build_epoch_batches(rec.token_lengths(), c["max_sentences"], 0, c["seed"], 0)
+    return d, run, c, rec, plan
+
+
+def test_resume_from_reference_checkpoint():
+    # load the reference's step-2 HCK1 into device state, run updates 3-4 of
+    # the same W=2 schedule (both ranks' batches in one round), and land on
+    # the reference's final checkpoint; then save and read back.
+    import os
+    from paper_2009_14783_b200.api import read_checkpoint
+    d, run, c, rec, plan = _hck1_run()
+    spec, meta, p2, _, _ = read_checkpoint(os.path.join(d, "checkpoint_000002.hck"))
+    eng = hp.StepEngine(spec, hp.OptimConfig("adam", 0.9, 0.98, 1e-9), hp.ExecConfig(
+        compute="f32", max_tokens=2048, max_batch=16, max_masks=512))
+    m = eng.load_checkpoint(os.path.join(d, "checkpoint_000002.hck"))
+    assert m.step == 2 and m.opt_t == 2 and eng.step_count() == 2
+    assert np.array_equal(eng.get_params(), p2)
+    e, skip = hp.api.resume_position(rec.token_lengths(), c["max_sentences"], 0, c["seed"], 2, 1, 2)
+    assert (e, skip) == (0, 2)
+    losses = []
+    for rnd in range(skip, skip + 2):
+        r0 = hp.partition_for_rank(plan, 2, 0)[rnd]
+        r1 = hp.partition_for_rank(plan, 2, 1)[rnd]
+        ids = np.concatenate([plan.batches[r0.batch_index], plan.batches[r1.batch_index]])
+        losses.append(eng.round(rec.batch(ids), lr=c["lr"]).loss)
+    assert np.max(np.abs(np.array(losses) - run["losses"][2:]) / np.abs(run["losses"][2:])) <= 1e-4
+    _, mf, pf, _, _ = read_checkpoint(os.path.join(d, "checkpoint_final.hck"))
+    assert rel_norm(eng.get_params(), pf) <= 1e-4
+    out = os.path.join(os.environ.get("TMPDIR", "/tmp"), "hp_resume_test.hck")
+    eng.save_checkpoint(out, hp.api.CheckpointMeta(epoch=0, seed=c["seed"], world_size=2))
+    _, ms, ps, mm, vv = read_checkpoint(out)
+    assert ms.step == 4 and ms.opt_t == 4 and np.array_equal(ps, eng.get_params())
+    em, ev, et = eng.get_adam()
+    assert np.array_equal(mm, em) and np.array_equal(vv, ev) and et == 4
+
+
+@pytest.mark.parametrize("compute", ["f32", "bf16"])
+def test_save_load_resume_is_bit_exact(compute):
+    # acceptance criterion 4 (resume determinism): 4 updates straight ==
+    # 2 updates, save, a fresh engine loads, 2 more updates -- same bytes
+    import os
+    spec, ospec, rec = _bert_case(d=128, heads=2, dff=256, vocab=203, n=16)
+    mk = lambda: hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(
+        compute=compute, max_tokens=512, max_batch=16, max_masks=128), seed=9)
+    batches = [rec.batch(np.arange(k, k + 8)) for k in (0, 4, 8, 2)]
+    a = mk()
+    for b in batches:
+        a.round(b, lr=1e-3)
+    f = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"hp_resume_{compute}.hck")
+    b1 = mk()
+    for b in batches[:2]:
+        b1.round(b, lr=1e-3)
+    b1.save_checkpoint(f, hp.api.CheckpointMeta(seed=9))
+    b2 = hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(
+        compute=compute, max_tokens=512, max_batch=16, max_masks=128))
+    assert b2.load_checkpoint(f).step == 2
+    for b in batches[2:]:
+        rep = b2.round(b, lr=1e-3)
+    assert rep.step == 4
+    assert b2.digest() == a.digest()

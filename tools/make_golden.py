@@ -37,8 +37,38 @@ def rd(path, dt):
     return np.fromfile(path, dtype=dt)
 
 
+# HCK1: a small reference run whose checkpoints the repo must read and
+# re-serialise byte for byte (tests/test_checkpoint.py) and resume from
+# (tests/test_gpu_engine.py); W=2, checkpoint every 2 updates, 4 updates.
+HCK1 = dict(n=32, vocab=64, min_words=8, max_words=12, docs=4, spd=4, data_seed=3, shards=2,
+            d=16, heads=2, max_seq=40, eps_ls=0.1, seed=5, max_sentences=4,
+            world=2, steps=4, lr=1e-3, opt="adam", ckpt_every=2)
+
+
+def hck1_golden():
+    import json
+    import shutil
+    out = os.path.join(GOLD, "hck1")
+    os.makedirs(out, exist_ok=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        t = os.path.join(tmp, "t")
+        run("train", out=t, dtype="f32", keep_ckpt=1, **HCK1)
+        for f in ("checkpoint_000002.hck", "checkpoint_final.hck"):
+            shutil.copy(os.path.join(t, f), os.path.join(out, f))
+        losses = rd(os.path.join(t, "losses.f64"), np.float64)
+    with open(os.path.join(out, "run.json"), "w") as f:
+        json.dump({"config": HCK1, "losses": losses.tolist(),
+                   "note": "reference train_run<float>, 2 in-process ranks (oracle/_ref/hetpar_ref)"},
+                  f, indent=1)
+
+
 def main():
+    import sys
+    if "--only-hck1" in sys.argv:
+        hck1_golden()
+        return
     os.makedirs(GOLD, exist_ok=True)
+    hck1_golden()
     with tempfile.TemporaryDirectory() as tmp:
         # records of the reference generator, read back through its index
         g = os.path.join(tmp, "gen")
