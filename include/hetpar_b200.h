@@ -199,6 +199,38 @@ hp_status hp_engine_get_adam(hp_engine* e, float* m, float* v, uint64_t* t);
 hp_status hp_engine_set_adam(hp_engine* e, const float* m, const float* v, uint64_t t);
 
 /* ------------------------------------------------------------------------
+ * HSD1 shard read path (src/shard.cpp:126-218, dataset.cpp:10-50,
+ * loader.cpp:80-139): shards of a directory memory-mapped as one global
+ * record space; a loader assembles one rank's schedule into hp_batch CSR
+ * arrays on a prefetch thread (prefetch_depth batches ahead; 0 = on demand).
+ * ---------------------------------------------------------------------- */
+typedef struct hp_shards hp_shards;
+typedef struct hp_loader hp_loader;
+hp_status hp_shards_open(const char* dir, hp_shards** out);
+hp_status hp_shards_info(hp_shards* s, uint64_t* total, uint64_t* nshards);
+hp_status hp_shards_token_lengths(hp_shards* s, uint32_t* out, uint64_t n);
+hp_status hp_shards_close(hp_shards* s);
+/* generate_mlm_shards' files (datagen.cpp:71-127) for n records in CSR form */
+hp_status hp_mlm_write_shards(const char* dir, uint64_t n, uint64_t shards, const uint64_t* tok_off,
+                              const int64_t* tokens, const int64_t* segments,
+                              const uint64_t* mask_off, const int64_t* mask_pos,
+                              const int64_t* mask_orig, const int64_t* label);
+/* The epoch plan (batch_order = concatenated global ids, batch_sizes) and one
+ * rank's schedule (partition_for_rank) to serve, in order. */
+hp_status hp_loader_create(hp_shards* s, const uint64_t* batch_order, const uint64_t* batch_sizes,
+                           uint64_t nbatches, const uint64_t* sched_batch,
+                           const uint8_t* sched_dummy, uint64_t nsched, uint64_t prefetch_depth,
+                           hp_loader** out);
+typedef struct {
+  uint64_t batch_index;
+  int dummy;
+  hp_batch batch; /* arrays owned by the loader, valid until the next call */
+} hp_loaded_batch;
+/* *has = 0 (and out untouched) once the schedule is exhausted */
+hp_status hp_loader_next(hp_loader* l, hp_loaded_batch* out, int* has);
+hp_status hp_loader_destroy(hp_loader* l);
+
+/* ------------------------------------------------------------------------
  * HCK1 checkpoints (src/checkpoint.cpp:165-302) and resume fast-forward
  * (include/hetpar/engine.hpp:211-245).  Files are byte-compatible with the
  * reference's save_checkpoint<float> / load_checkpoint<float>.

@@ -149,6 +149,13 @@ int cmd_gen(const Args& a) {
   dump(out + "/mask_orig.i64", morig);
   dump(out + "/label.i64", label);
   dump(out + "/lens.u32", lens);
+  if (argu(a, "keep_shards", 0)) {
+    // keep the reference-written HSD1 files (golden fixtures, tools/make_golden.py)
+    fs::create_directories(out + "/kept_shards");
+    for (const auto& f : fs::directory_iterator(data))
+      fs::copy_file(f.path(), out + "/kept_shards/" + f.path().filename().string(),
+                    fs::copy_options::overwrite_existing);
+  }
   fs::remove_all(data);
   std::printf("records=%" PRIu64 "\n", idx.total);
   return 0;

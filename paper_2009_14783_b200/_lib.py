@@ -88,6 +88,10 @@ class BatchDesc(C.Structure):
                 ("mask_orig", C.c_void_p), ("label", C.c_void_p)]
 
 
+class LoadedDesc(C.Structure):
+    _fields_ = [("batch_index", C.c_uint64), ("dummy", C.c_int), ("batch", BatchDesc)]
+
+
 class CkptDesc(C.Structure):
     _fields_ = [("epoch", C.c_uint64), ("step", C.c_uint64), ("seed", C.c_uint64),
                 ("policy", C.c_int), ("world_size", C.c_uint64), ("update_freq", C.c_uint64),
@@ -131,6 +135,14 @@ _SIGS = {
     "hp_engine_broadcast_params": [P, I],
     "hp_engine_get_adam": [P, P, P, P],
     "hp_engine_set_adam": [P, P, P, U64],
+    "hp_shards_open": [C.c_char_p, P],
+    "hp_shards_info": [P, P, P],
+    "hp_shards_token_lengths": [P, P, U64],
+    "hp_shards_close": [P],
+    "hp_mlm_write_shards": [C.c_char_p, U64, U64, P, P, P, P, P, P, P],
+    "hp_loader_create": [P, P, P, U64, P, P, U64, U64, P],
+    "hp_loader_next": [P, P, P],
+    "hp_loader_destroy": [P],
     "hp_checkpoint_write": [C.c_char_p, P, P, P, P, P],
     "hp_checkpoint_read": [C.c_char_p, P, P, P, P, P, U64],
     "hp_engine_save_checkpoint": [P, C.c_char_p, P],

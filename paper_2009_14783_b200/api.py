@@ -402,6 +402,124 @@ class StepReport:
     updated: bool = True
 
 
+# ---------------------------------------------------------------- HSD1 shards
+def write_mlm_shards(directory: str, records: "Records", shards: int) -> None:
+    """generate_mlm_shards' files (datagen.cpp:71-127) for these records:
+    ``shards`` contiguous chunks (earlier ones one longer), shard_%04d.hsd,
+    byte-identical to the reference writer for the same records."""
+    r = records
+    call("hp_mlm_write_shards", directory.encode(), len(r.label), shards, _p(r.tok_off), _p(r.tokens),
+         _p(r.segments), _p(r.mask_off), _p(r.mask_pos), _p(r.mask_orig), _p(r.label))
+
+
+class LoadedBatch:
+    """One scheduled batch from a ShardLoader (LoadedBatch, loader.hpp): its
+    arrays live in the loader until the next ``next()``; ``stage()`` it
+    right away, or ``to_csr()`` to keep a copy."""
+
+    def __init__(self, d: _lib.LoadedDesc):
+        self._d = d
+        self.batch_index = d.batch_index
+        self.dummy = bool(d.dummy)
+
+    def desc(self) -> _lib.BatchDesc:
+        return self._d.batch
+
+    @property
+    def n_inst(self) -> int:
+        return int(self._d.batch.n_inst)
+
+    def to_csr(self) -> BatchCSR:
+        b = self._d.batch
+        n = b.n_inst
+
+        def arr(ptr, count, dt):
+            if count == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dt))),
+                                         shape=(count,)).copy()
+        tok_off = arr(b.tok_off, n + 1, np.uint64)
+        mask_off = arr(b.mask_off, n + 1, np.uint64)
+        t, m = int(tok_off[-1]), int(mask_off[-1])
+        return BatchCSR(tok_off, arr(b.tokens, t, np.int64), arr(b.segments, t, np.int64), mask_off,
+                        arr(b.mask_pos, m, np.int64), arr(b.mask_orig, m, np.int64),
+                        arr(b.label, n, np.int64))
+
+    def host_bytes(self) -> int:
+        return self.to_csr().host_bytes()
+
+
+class ShardLoader:
+    """BatchLoader (loader.cpp:80-139): serves one rank's schedule in order;
+    a producer thread keeps ``prefetch_depth`` batches decoded ahead (0:
+    decode on demand).  Iterating yields LoadedBatch."""
+
+    def __init__(self, data: "ShardDataset", plan: BatchPlan, schedule, prefetch_depth: int = 2):
+        order = np.ascontiguousarray(np.concatenate(plan.batches) if plan.batches else np.zeros(0),
+                                     np.uint64)
+        sizes = np.ascontiguousarray([len(b) for b in plan.batches], np.uint64)
+        sb = np.ascontiguousarray([rb.batch_index for rb in schedule], np.uint64)
+        sd = np.ascontiguousarray([1 if rb.dummy else 0 for rb in schedule], np.uint8)
+        self._data = data  # keeps the mapping alive
+        self._h = C.c_void_p()
+        call("hp_loader_create", data._h, _p(order), _p(sizes), len(sizes), _p(sb), _p(sd), len(sb),
+             prefetch_depth, C.byref(self._h))
+
+    def next(self) -> Optional[LoadedBatch]:
+        d, has = _lib.LoadedDesc(), C.c_int()
+        call("hp_loader_next", self._h, C.byref(d), C.byref(has))
+        return LoadedBatch(d) if has.value else None
+
+    def __iter__(self):
+        while True:
+            b = self.next()
+            if b is None:
+                return
+            yield b
+
+    def close(self):
+        if self._h:
+            call("hp_loader_destroy", self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ShardDataset:
+    """list_shards + build_index (dataset.cpp:10-50): every *.hsd file of a
+    directory, sorted, memory-mapped as one global record space."""
+
+    def __init__(self, directory: str):
+        self._h = C.c_void_p()
+        call("hp_shards_open", directory.encode(), C.byref(self._h))
+        t, k = C.c_uint64(), C.c_uint64()
+        call("hp_shards_info", self._h, C.byref(t), C.byref(k))
+        self.total, self.nshards = t.value, k.value
+
+    def token_lengths(self) -> np.ndarray:
+        out = np.empty(self.total, np.uint32)
+        call("hp_shards_token_lengths", self._h, _p(out), self.total)
+        return out
+
+    def loader(self, plan: BatchPlan, schedule, prefetch_depth: int = 2) -> ShardLoader:
+        return ShardLoader(self, plan, schedule, prefetch_depth)
+
+    def close(self):
+        if self._h:
+            call("hp_shards_close", self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 @dataclass
 class CheckpointMeta:
     """TrainState fields an HCK1 file carries besides the tensors
@@ -610,8 +728,16 @@ class StepEngine:
 
     # -- rounds
     def stage(self, batch) -> None:
+        """Validate the rank batch and queue its H2D copy (from the engine's
+        pinned staging block).  Accepts a BatchCSR, a LoadedBatch straight
+        from a ShardLoader, or a list of instances."""
+        if isinstance(batch, LoadedBatch):
+            d = batch.desc()
+            call("hp_engine_stage_batch", self._h, C.byref(d))
+            self.last_h2d_bytes = 0
+            return
         csr = batch if isinstance(batch, BatchCSR) else pack_batch(batch)
-        self._staged = csr  # keep host arrays alive for the async copy
+        self._staged = csr
         d = csr.desc()
         call("hp_engine_stage_batch", self._h, C.byref(d))
         self.last_h2d_bytes = csr.host_bytes()

@@ -6,7 +6,10 @@
 #include <cstring>
 #include <string>
 
+#include <memory>
+
 #include "checkpoint.h"
+#include "shards.h"
 #include "engine.h"
 #include "hetpar_b200.h"
 #include "hostdata.h"
@@ -23,6 +26,13 @@ using hp::fail;
 
 struct hp_engine {
   hp::Engine* e = nullptr;
+};
+struct hp_shards {
+  std::shared_ptr<const hp::ShardSet> set;
+};
+struct hp_loader {
+  std::unique_ptr<hp::ShardLoader> loader;
+  hp::ShardLoader::Loaded cur;
 };
 
 static void need(const void* p, const char* what) {
@@ -448,6 +458,95 @@ hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf1
     if (dO) hp::attention_bwd(b, H, dk, qkv, o, dO, lse, dqkv, t, 0);
   }
   HP_CUDA(cudaDeviceSynchronize());
+  HP_API_END
+}
+
+hp_status hp_shards_open(const char* dir, hp_shards** out) {
+  HP_API_BEGIN
+  need(dir, "dir");
+  need(out, "out");
+  auto h = std::make_unique<hp_shards>();
+  h->set = std::make_shared<const hp::ShardSet>(dir);
+  *out = h.release();
+  HP_API_END
+}
+
+hp_status hp_shards_info(hp_shards* s, uint64_t* total, uint64_t* nshards) {
+  HP_API_BEGIN
+  need(s, "shards");
+  if (total) *total = s->set->total();
+  if (nshards) *nshards = s->set->nshards();
+  HP_API_END
+}
+
+hp_status hp_shards_token_lengths(hp_shards* s, uint32_t* out, uint64_t n) {
+  HP_API_BEGIN
+  need(s, "shards");
+  need(out, "out");
+  const auto& l = s->set->token_lengths();
+  if (n != l.size()) fail(HP_ESHAPE, "token length table has " + std::to_string(l.size()) + " entries");
+  std::memcpy(out, l.data(), 4 * n);
+  HP_API_END
+}
+
+hp_status hp_shards_close(hp_shards* s) {
+  HP_API_BEGIN
+  delete s;
+  HP_API_END
+}
+
+hp_status hp_mlm_write_shards(const char* dir, uint64_t n, uint64_t shards, const uint64_t* tok_off,
+                              const int64_t* tokens, const int64_t* segments,
+                              const uint64_t* mask_off, const int64_t* mask_pos,
+                              const int64_t* mask_orig, const int64_t* label) {
+  HP_API_BEGIN
+  need(dir, "dir");
+  need(tok_off, "tok_off");
+  need(mask_off, "mask_off");
+  hp::write_mlm_shards(dir, n, shards, tok_off, tokens, segments, mask_off, mask_pos, mask_orig, label);
+  HP_API_END
+}
+
+hp_status hp_loader_create(hp_shards* s, const uint64_t* batch_order, const uint64_t* batch_sizes,
+                           uint64_t nbatches, const uint64_t* sched_batch,
+                           const uint8_t* sched_dummy, uint64_t nsched, uint64_t prefetch_depth,
+                           hp_loader** out) {
+  HP_API_BEGIN
+  need(s, "shards");
+  need(out, "out");
+  std::vector<std::vector<uint64_t>> plan(nbatches);
+  uint64_t at = 0;
+  for (uint64_t b = 0; b < nbatches; ++b) {
+    plan[b].assign(batch_order + at, batch_order + at + batch_sizes[b]);
+    at += batch_sizes[b];
+  }
+  auto h = std::make_unique<hp_loader>();
+  h->loader = std::make_unique<hp::ShardLoader>(
+      s->set, std::move(plan), std::vector<uint64_t>(sched_batch, sched_batch + nsched),
+      std::vector<uint8_t>(sched_dummy, sched_dummy + nsched), prefetch_depth);
+  *out = h.release();
+  HP_API_END
+}
+
+hp_status hp_loader_next(hp_loader* l, hp_loaded_batch* out, int* has) {
+  HP_API_BEGIN
+  need(l, "loader");
+  need(out, "out");
+  need(has, "has");
+  *has = l->loader->next(l->cur) ? 1 : 0;
+  if (*has) {
+    const auto& c = l->cur.csr;
+    out->batch_index = l->cur.batch_index;
+    out->dummy = l->cur.dummy ? 1 : 0;
+    out->batch = hp_batch{c.label.size(), c.tok_off.data(), c.tokens.data(), c.segments.data(),
+                          c.mask_off.data(), c.mask_pos.data(), c.mask_orig.data(), c.label.data()};
+  }
+  HP_API_END
+}
+
+hp_status hp_loader_destroy(hp_loader* l) {
+  HP_API_BEGIN
+  delete l;
   HP_API_END
 }
 

@@ -319,3 +319,25 @@ def test_save_load_resume_is_bit_exact(compute):
         rep = b2.round(b, lr=1e-3)
     assert rep.step == 4
     assert b2.digest() == a.digest()
+
+
+def test_c1_trained_from_shards_matches_reference(tmp_path):
+    # the HSD1 read path end to end: C1 records -> shard files -> one
+    # prefetching loader per rank -> pinned staging -> HBM; W = 2 replayed on
+    # one GPU as K = 2 (rank 0's batch, then rank 1's), against the
+    # reference's W = 2 trajectory
+    from paper_2009_14783_b200 import api
+    rec = hp.generate_mlm_records(hp.MlmGenConfig(**C1_GEN))
+    api.write_mlm_shards(str(tmp_path), rec, 4)
+    ds = api.ShardDataset(str(tmp_path))
+    plan = hp.build_epoch_batches(ds.token_lengths(), 8, 0, 21, 0)
+    loaders = [ds.loader(plan, hp.partition_for_rank(plan, 2, r), 2) for r in range(2)]
+    t = golden("c1_ref_train.npz")
+    eng = c1_engine(update_freq=2)
+    losses = []
+    for step in range(10):
+        assert eng.round(loaders[0].next(), lr=1e-3) is None
+        rep = eng.round(loaders[1].next(), lr=1e-3)
+        losses.append(rep.loss)
+    assert np.max(np.abs(np.array(losses) - t["losses_f64"]) / np.abs(t["losses_f64"])) <= 1e-4
+    assert rel_norm(eng.get_params(), t["params_f64_as_f32"]) <= 1e-4

@@ -62,11 +62,29 @@ def hck1_golden():
                   f, indent=1)
 
 
+def hsd1_golden():
+    """The reference's own HSD1 files for the ragged generator config: the
+    repo's shard reader must decode them record for record and its writer
+    must reproduce them byte for byte (tests/test_shards.py)."""
+    import shutil
+    out = os.path.join(GOLD, "hsd1")
+    os.makedirs(out, exist_ok=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        g = os.path.join(tmp, "g")
+        run("gen", out=g, n=97, vocab=64, min_words=3, max_words=8, data_seed=11, shards=3, keep_shards=1)
+        for f in sorted(os.listdir(os.path.join(g, "kept_shards"))):
+            shutil.copy(os.path.join(g, "kept_shards", f), os.path.join(out, f))
+
+
 def main():
     import sys
     if "--only-hck1" in sys.argv:
         hck1_golden()
         return
+    if "--only-hsd1" in sys.argv:
+        hsd1_golden()
+        return
+    hsd1_golden()
     os.makedirs(GOLD, exist_ok=True)
     hck1_golden()
     with tempfile.TemporaryDirectory() as tmp:
