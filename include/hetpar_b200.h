@@ -136,6 +136,24 @@ hp_status hp_comm_unique_id(uint8_t id[128]);
 hp_status hp_comm_create(int world, int rank, int device, const uint8_t id[128],
                          hp_comm** out);
 hp_status hp_comm_destroy(hp_comm* c);
+/* Form the world without a Python control plane: rank 0 listens on
+ * host:port and serves its ncclUniqueId to the other ranks (the rendezvous
+ * role of comm_tcp.cpp:154-237); retries / waits up to timeout_ms. */
+hp_status hp_comm_create_tcp(const char* host, uint16_t port, int world, int rank, int device,
+                             int timeout_ms, hp_comm** out);
+/* ProcessGroup (comm.hpp:16-49) over the communicator -- the NcclProcessGroup
+ * control plane; host-staged, blocking:
+ *   broadcast: every rank gets the root's bytes (*out_len = their length;
+ *     HP_ECONFIG when cap is smaller);
+ *   all_reduce_sum: the rank-ordered left fold 0..world-1, identical bytes on
+ *     every rank; differing lengths are HP_ECOMM;
+ *   gather_scalars: the master (rank 0) receives [v_0..v_{w-1}] in out;
+ *   barrier: returns once every rank entered. */
+hp_status hp_pg_broadcast(hp_comm* c, const void* payload, uint64_t len, uint64_t root, void* out,
+                          uint64_t cap, uint64_t* out_len);
+hp_status hp_pg_all_reduce_sum(hp_comm* c, const double* v, uint64_t n, double* out);
+hp_status hp_pg_gather_scalars(hp_comm* c, double v, double* out);
+hp_status hp_pg_barrier(hp_comm* c);
 
 /* ------------------------------------------------------------------------
  * Step engine: StepEngine<T>::round (include/hetpar/engine.hpp:125-165).

@@ -135,6 +135,11 @@ _SIGS = {
     "hp_engine_broadcast_params": [P, I],
     "hp_engine_get_adam": [P, P, P, P],
     "hp_engine_set_adam": [P, P, P, U64],
+    "hp_comm_create_tcp": [C.c_char_p, C.c_uint16, I, I, I, I, P],
+    "hp_pg_broadcast": [P, P, U64, U64, P, U64, P],
+    "hp_pg_all_reduce_sum": [P, P, U64, P],
+    "hp_pg_gather_scalars": [P, C.c_double, P],
+    "hp_pg_barrier": [P],
     "hp_shards_open": [C.c_char_p, P],
     "hp_shards_info": [P, P, P],
     "hp_shards_token_lengths": [P, P, U64],

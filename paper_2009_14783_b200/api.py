@@ -620,9 +620,46 @@ class Communicator:
         call("hp_comm_create", world, rank, device, uid, C.byref(self._h))
         self.world, self.rank, self.device = world, rank, device
 
+    @classmethod
+    def tcp(cls, host: str, port: int, world: int, rank: int, device: int,
+            timeout_ms: int = 30000) -> "Communicator":
+        """Form the world with the engine's own TCP rendezvous (rank 0 serves
+        the ncclUniqueId on host:port) -- no torch.distributed involved."""
+        self = cls.__new__(cls)
+        self._h = C.c_void_p()
+        call("hp_comm_create_tcp", host.encode(), port, world, rank, device, timeout_ms,
+             C.byref(self._h))
+        self.world, self.rank, self.device = world, rank, device
+        return self
+
     @property
     def handle(self):
         return self._h
+
+    # ---- ProcessGroup (comm.hpp:16-49): the NcclProcessGroup control plane
+    def broadcast(self, payload: bytes, root: int = 0, max_len: int = 1 << 20) -> bytes:
+        """Every rank returns the root's exact bytes (non-root inputs ignored)."""
+        buf = (C.c_uint8 * max(max_len, 1))()
+        n = C.c_uint64()
+        src = (C.c_uint8 * max(len(payload), 1)).from_buffer_copy(payload or b"\0")
+        call("hp_pg_broadcast", self._h, src, len(payload), root, buf, max_len, C.byref(n))
+        return bytes(buf[:n.value])
+
+    def all_reduce_sum(self, values) -> list:
+        """Rank-ordered left fold (0 -> world-1), identical bytes on every rank."""
+        v = np.ascontiguousarray(values, np.float64)
+        out = np.empty_like(v)
+        call("hp_pg_all_reduce_sum", self._h, _p(v), len(v), _p(out))
+        return out.tolist()
+
+    def gather_scalars(self, value: float) -> list:
+        """Master receives [v_0 .. v_{w-1}] in rank order; other ranks get []."""
+        out = np.empty(self.world, np.float64)
+        call("hp_pg_gather_scalars", self._h, float(value), _p(out))
+        return out.tolist() if self.rank == 0 else []
+
+    def barrier(self) -> None:
+        call("hp_pg_barrier", self._h)
 
     def close(self):
         if self._h:

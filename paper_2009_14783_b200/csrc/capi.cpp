@@ -207,6 +207,8 @@ hp_status hp_comm_destroy(hp_comm* c) {
   HP_API_BEGIN
   if (c) {
     if (c->nccl) ncclCommDestroy(c->nccl);
+    if (c->pg_buf) cudaFree(c->pg_buf);
+    if (c->pg_stream) cudaStreamDestroy(c->pg_stream);
     delete c;
   }
   HP_API_END

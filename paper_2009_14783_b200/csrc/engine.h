@@ -18,6 +18,10 @@
 struct hp_comm {
   ncclComm_t nccl = nullptr;
   int world = 1, rank = 0, device = 0;
+  // control-plane collectives (pgroup.cpp): their stream and device scratch
+  cudaStream_t pg_stream = nullptr;
+  void* pg_buf = nullptr;
+  size_t pg_cap = 0;
 };
 
 namespace hp {

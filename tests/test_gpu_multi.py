@@ -73,3 +73,67 @@ def test_c1_w2_nccl_matches_reference(tmp_path):
     p = np.load(tmp_path / "params.npy")
     assert rel_norm(p, t["params_f64_as_f32"]) <= 1e-4
     assert r0["dummy_weight"] == 8.0             # only rank 0's 8 sentences count
+
+
+PG_WORKER = r'''
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.environ["HP_ROOT"]); sys.path.insert(0, os.path.join(os.environ["HP_ROOT"], "tests"))
+import paper_2009_14783_b200 as hp
+from paper_2009_14783_b200 import _lib
+from helpers import C1_GEN, C1_SPEC
+rank, world = int(os.environ["HP_RANK"]), 2
+comm = hp.Communicator.tcp("127.0.0.1", int(os.environ["HP_PORT"]), world, rank, rank)
+out = {}
+# broadcast: the root's exact bytes, whatever the others pass
+out["bcast"] = comm.broadcast(b"root payload \x00\x01\xff" if rank == 1 else b"ignored", root=1).hex()
+# all_reduce_sum: the rank-ordered fold (order matters for these values)
+vals = [[1e16, 1.0, 0.1], [-1e16, 1.0, 0.2]][rank]
+out["ar"] = comm.all_reduce_sum(vals)
+out["gather"] = comm.gather_scalars(10.0 + rank)
+comm.barrier()
+try:
+    comm.all_reduce_sum([1.0] * (2 + rank))
+    out["mismatch"] = "accepted"
+except _lib.CommError as e:
+    out["mismatch"] = str(e)
+# the engine on the TCP-formed communicator: three C1 rounds at W = 2
+eng = hp.StepEngine(hp.ModelSpec(**C1_SPEC), hp.OptimConfig("adam", 0.9, 0.98, 1e-9),
+                    hp.ExecConfig(compute="f32", device=rank, max_tokens=1024, max_batch=16, max_masks=256),
+                    comm=comm, seed=21 if rank == 0 else None)
+eng.broadcast_params(0)
+rec = hp.generate_mlm_records(hp.MlmGenConfig(**C1_GEN))
+plan = hp.build_epoch_batches(rec.token_lengths(), 8, 0, 21, 0)
+sched = hp.partition_for_rank(plan, world, rank)
+out["losses"] = [eng.round(rec.batch(plan.batches[sched[s].batch_index]), sched[s].dummy, 1e-3).loss
+                 for s in range(3)]
+out["digest"] = eng.digest()
+with open(os.environ["HP_OUT"] + f"/pg{rank}.json", "w") as f:
+    json.dump(out, f)
+eng.close(); comm.close()
+'''
+
+
+def test_process_group_over_tcp_rendezvous(tmp_path):
+    # NcclProcessGroup (comm.hpp:16-49) on a world formed by the engine's own
+    # TCP rendezvous -- no torch.distributed in the processes
+    script = tmp_path / "pg.py"
+    script.write_text(PG_WORKER)
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, HP_ROOT=ROOT, HP_OUT=str(tmp_path), HP_RANK=str(r), HP_PORT="29533")
+        procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT, text=True))
+    for p in procs:
+        out, _ = p.communicate(timeout=600)
+        assert p.returncode == 0, out[-3000:]
+    r0 = json.loads((tmp_path / "pg0.json").read_text())
+    r1 = json.loads((tmp_path / "pg1.json").read_text())
+    assert bytes.fromhex(r0["bcast"]) == b"root payload \x00\x01\xff" == bytes.fromhex(r1["bcast"])
+    fold = [(1e16 + -1e16), (1.0 + 1.0), (0.1 + 0.2)]
+    assert r0["ar"] == fold and r1["ar"] == fold
+    assert r0["gather"] == [10.0, 11.0] and r1["gather"] == []
+    assert "length mismatch" in r0["mismatch"] and "length mismatch" in r1["mismatch"]
+    t = golden("c1_ref_train.npz")
+    assert np.max(np.abs(np.array(r0["losses"]) - t["losses_f64"][:3]) / np.abs(t["losses_f64"][:3])) <= 1e-4
+    assert r0["losses"] == r1["losses"] and r0["digest"] == r1["digest"]
