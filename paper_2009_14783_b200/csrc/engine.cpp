@@ -113,6 +113,24 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   HP_CUDA(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming));
   ev_bucket_.resize(buckets_.size());
   for (auto& e : ev_bucket_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  {
+    const char* e = std::getenv("HP_WGRAD_STREAM");
+    wg_on_ = bert_ && !(e && std::string(e) == "0");
+  }
+  if (bert_) {  // events exist whenever the call sites index them (stream or not)
+    if (wg_on_) HP_CUDA(cudaStreamCreateWithPriority(&s_wg_, cudaStreamNonBlocking, prio_lo));
+    auto mk = [](std::vector<cudaEvent_t>& v, size_t n) {
+      v.resize(n);
+      for (auto& e : v) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    };
+    mk(ev_fork_, 4 * static_cast<size_t>(L_) + 1);
+    mk(ev_w2_, L_);
+    mk(ev_w1_, L_);
+    mk(ev_wo_, L_);
+    mk(ev_wq_, L_);
+    mk(ev_wgb_, buckets_.size());
+    HP_CUDA(cudaEventCreateWithFlags(&ev_wg_join_, cudaEventDisableTiming));
+  }
 
   params_ = static_cast<float*>(dalloc(n_ * 4));
   grads_ = static_cast<float*>(dalloc(n_ * 4));
@@ -309,6 +327,10 @@ Engine::~Engine() {
   if (h_params_) cudaFreeHost(h_params_);
   for (auto& e : ev_bucket_) cudaEventDestroy(e);
   for (auto& e : final_evs_) cudaEventDestroy(e);
+  for (auto* v : {&ev_fork_, &ev_w2_, &ev_w1_, &ev_wo_, &ev_wq_, &ev_wgb_})
+    for (auto& e : *v) cudaEventDestroy(e);
+  if (ev_wg_join_) cudaEventDestroy(ev_wg_join_);
+  if (s_wg_) cudaStreamDestroy(s_wg_);
   for (auto& e : marks_)
     if (e) cudaEventDestroy(e);
   if (ev_fwd_) cudaEventDestroy(ev_fwd_);
@@ -617,6 +639,27 @@ void Engine::gemm_t(const GemmArgs& g) {
             (g.ct == DType::f32 ? 4.0 : 2.0) * g.M * g.N);
 }
 
+void Engine::wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done) {
+  if (!wg_on_) {
+    gemm_t(g);
+    return;
+  }
+  HP_CUDA(cudaEventRecord(fork, s_main_));
+  HP_CUDA(cudaStreamWaitEvent(s_wg_, fork, 0));
+  wg_forked_ = true;
+  tstart(TM_GEMM, s_wg_);
+  gemm(g, s_wg_);
+  tstop(TM_GEMM, 2.0 * g.M * g.N * g.K,
+        (double)asz_ * ((double)g.M * g.K + (double)g.K * g.N) +
+            (g.ct == DType::f32 ? 4.0 : 2.0) * g.M * g.N,
+        s_wg_);
+  HP_CUDA(cudaEventRecord(done, s_wg_));
+}
+
+void Engine::wait_wg(cudaEvent_t e) {
+  if (wg_on_) HP_CUDA(cudaStreamWaitEvent(s_main_, e, 0));
+}
+
 // ------------------------------------------------------------------ forward
 void Engine::forward(bool need_grad) {
   const DevBatch& b = batch_;
@@ -732,6 +775,10 @@ void Engine::issue_bucket(size_t k) {
   const Bucket& bk = buckets_[k];
   HP_CUDA(cudaEventRecord(ev_bucket_[k], s_main_));
   HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_bucket_[k], 0));
+  if (wg_forked_) {  // and every weight gradient issued so far this round
+    HP_CUDA(cudaEventRecord(ev_wgb_[k], s_wg_));
+    HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_wgb_[k], 0));
+  }
   if (comm_)
     HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, ncclSum,
                           comm_->nccl, s_comm_));
@@ -795,6 +842,8 @@ void Engine::backward() {
     if (bert_) {
       const int ibo = iwo + 1, ig1 = iwo + 2, iw1 = iwo + 4, ib1 = iwo + 5, iw2 = iwo + 6,
                 ib2 = iwo + 7, ig2 = iwo + 8;
+      // dB_ is about to be overwritten: layer l+1's d(wo) must have read it
+      if (l + 1 < L_) wait_wg(ev_wo_[l + 1]);
       tstart(TM_NORM);
       // LN2' also yields d(ffn.b2) = colsum(dP2) (P2 = G W2 + b2 + X1)
       {
@@ -809,20 +858,21 @@ void Engine::backward() {
       w2.a = Operand{y.g, F_, 1, 0, 0};
       w2.b = Operand{dB_, d_, 0, 0, 0};
       w2.c = gp(iw2); w2.ldc = d_; w2.ct = DType::f32;
-      gemm_t(w2);
+      wgrad_t(w2, wg_on_ ? ev_fork_[4 * l] : nullptr, wg_on_ ? ev_w2_[l] : nullptr);
       GemmArgs du;  // dU = (dP2 W2^T) * gelu'(U)
       du.M = T; du.N = F_; du.K = d_; du.ab = at_;
       du.a = Operand{dB_, d_, 0, 0, 0};
       du.b = Operand{w(iw2), wld(iw2), 1, 0, 0};
       du.c = dU_; du.ldc = F_; du.ct = at_;
       du.act = ACT_DGELU; du.aux = y.u;
+      if (l + 1 < L_) wait_wg(ev_w1_[l + 1]);  // dU_ is reused: layer l+1's d(w1) read it
       gemm_t(du);
       GemmArgs w1;  // d(ffn.w1) = X1^T dU
       w1.M = d_; w1.N = F_; w1.K = T; w1.ab = at_;
       w1.a = Operand{y.x1, d_, 1, 0, 0};
       w1.b = Operand{dU_, F_, 0, 0, 0};
       w1.c = gp(iw1); w1.ldc = F_; w1.ct = DType::f32;
-      gemm_t(w1);
+      wgrad_t(w1, wg_on_ ? ev_fork_[4 * l + 1] : nullptr, wg_on_ ? ev_w1_[l] : nullptr);
       tstart(TM_NORM);
       {
         DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, F_));
@@ -837,6 +887,7 @@ void Engine::backward() {
       dx1.c = dC_; dx1.ldc = d_; dx1.ct = at_;
       dx1.resid = dB_; dx1.ld_resid = d_;
       gemm_t(dx1);
+      wait_wg(ev_w2_[l]);  // dB_ (dP2) is overwritten next: d(w2) must have read it
       tstart(TM_NORM);
       // LN1' also yields d(bo) = colsum(dP1)
       {
@@ -855,13 +906,17 @@ void Engine::backward() {
     wo.a = Operand{y.o, d_, 1, 0, 0};
     wo.b = Operand{dP1, d_, 0, 0, 0};
     wo.c = gp(iwo); wo.ldc = d_; wo.ct = DType::f32;
-    gemm_t(wo);
+    if (bert_)
+      wgrad_t(wo, wg_on_ ? ev_fork_[4 * l + 2] : nullptr, wg_on_ ? ev_wo_[l] : nullptr);
+    else
+      gemm_t(wo);
     GemmArgs dO;  // dO = dP1 Wo^T
     dO.M = T; dO.N = d_; dO.K = d_; dO.ab = at_;
     dO.a = Operand{dP1, d_, 0, 0, 0};
     dO.b = Operand{w(iwo), wld(iwo), 1, 0, 0};
     dO.c = dC_; dO.ldc = d_; dO.ct = at_;
     gemm_t(dO);
+    if (bert_ && l + 1 < L_) wait_wg(ev_wq_[l + 1]);  // dqkv_ reused: layer l+1's d(wqkv) read it
     tstart(TM_ATTN);
     if (attn_tc_)
       attention_bwd_tc(b, H_, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
@@ -879,7 +934,10 @@ void Engine::backward() {
     wq.c = gp(iq); wq.ldc = dk_; wq.c_group = dk_;
     wq.c_gstride = (int64_t)(table_[iq + 1].offset - table_[iq].offset);
     wq.ct = DType::f32;
-    gemm_t(wq);
+    if (bert_)
+      wgrad_t(wq, wg_on_ ? ev_fork_[4 * l + 3] : nullptr, wg_on_ ? ev_wq_[l] : nullptr);
+    else
+      gemm_t(wq);
     GemmArgs dx;  // dX = dQKV Wqkv^T (+ dP1 through the residual)
     dx.M = T; dx.N = d_; dx.K = 3 * d_; dx.ab = at_;
     dx.a = Operand{dqkv_, 3 * d_, 0, 0, 0};
@@ -897,6 +955,7 @@ void Engine::backward() {
   const void* dx0 = dB_;
   if (bert_) {
     const int g = pidx("emb_ln.g");
+    wait_wg(ev_wo_[0]);  // dB_ is overwritten: layer 0's d(wo) must have read it
     tstart(TM_NORM);
     {
       DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, d_));
@@ -912,6 +971,10 @@ void Engine::backward() {
   embed_bwd(b, d_, dx0, at_, gp(0), gp(1), gp(2), scratch_, s_main_);
   tstop(TM_EMBED, 0, (double)T * d_ * (asz_ + 8));
   grads_ready(0);
+  if (wg_forked_) {  // the wgrad stream joins the compute stream (graph capture needs it)
+    HP_CUDA(cudaEventRecord(ev_wg_join_, s_wg_));
+    HP_CUDA(cudaStreamWaitEvent(s_main_, ev_wg_join_, 0));
+  }
 }
 
 // ------------------------------------------------------------------ round
@@ -1013,6 +1076,7 @@ void Engine::issue_final(DeferredFinal& f) {
 
 void Engine::round_body(int dummy) {
   final_n_ = 0;
+  wg_forked_ = false;
   HP_CUDA(cudaMemsetAsync(flags_, 0, 8, s_main_));
   // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
   forward(!dummy);

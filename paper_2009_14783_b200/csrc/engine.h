@@ -71,6 +71,10 @@ class Engine {
   float* pp(int idx) const { return params_ + table_[idx].offset; }
   int pidx(const std::string& name) const;
   void gemm_t(const GemmArgs& g);
+  // a weight-gradient GEMM on the wgrad stream (see backward): forks from the
+  // compute stream, records `done` when finished
+  void wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done);
+  void wait_wg(cudaEvent_t e);  // compute stream waits for a pending wgrad
   void tstart(int cls, cudaStream_t st = nullptr);
   void tstop(int cls, double flops, double bytes, cudaStream_t st = nullptr);
   void forward(bool need_grad_state);
@@ -139,6 +143,15 @@ class Engine {
   float* h_params_ = nullptr;
 
   cudaStream_t s_main_ = nullptr, s_comm_ = nullptr;
+  // weight-gradient GEMMs run beside the data-gradient chain (bert_encoder):
+  // they fill the SMs the N = d GEMMs leave idle and the GEMM tails
+  cudaStream_t s_wg_ = nullptr;
+  bool wg_on_ = false;
+  bool wg_forked_ = false;  // the wgrad stream took work this round (capture-safe waits)
+  std::vector<cudaEvent_t> ev_fork_;                      // [4 L + 1] fork points
+  std::vector<cudaEvent_t> ev_w2_, ev_w1_, ev_wo_, ev_wq_;  // [L] wgrad done
+  std::vector<cudaEvent_t> ev_wgb_;                        // [buckets] wgrads so far
+  cudaEvent_t ev_wg_join_ = nullptr;
   cudaEvent_t ev_fwd_ = nullptr, ev_comm_done_ = nullptr, ev_done_ = nullptr;
   std::vector<cudaEvent_t> ev_bucket_;
   size_t next_bucket_ = 0;
