@@ -130,6 +130,8 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     mk(ev_wq_, L_);
     mk(ev_wgb_, buckets_.size());
     HP_CUDA(cudaEventCreateWithFlags(&ev_wg_join_, cudaEventDisableTiming));
+    HP_CUDA(cudaEventCreateWithFlags(&ev_emb_zero_, cudaEventDisableTiming));
+    HP_CUDA(cudaEventCreateWithFlags(&ev_head_fork_, cudaEventDisableTiming));
   }
 
   params_ = static_cast<float*>(dalloc(n_ * 4));
@@ -280,6 +282,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
                                    colsum_scratch_floats((int)Mm, Vp_),
                                    colsum_scratch_floats((int)T, d_)});
   scratch_ = static_cast<float*>(dalloc(scratch * 4));
+  if (wg_on_) scratch_wg_ = static_cast<float*>(dalloc(colsum_scratch_floats((int)T, F_) * 4));
   // [round loss, round weight, local loss, local weight, K-total loss, K-total weight]
   d_lw_ = static_cast<double*>(dalloc(6 * 8));
   HP_CUDA(cudaMemset(d_lw_, 0, 6 * 8));
@@ -330,6 +333,8 @@ Engine::~Engine() {
   for (auto* v : {&ev_fork_, &ev_w2_, &ev_w1_, &ev_wo_, &ev_wq_, &ev_wgb_})
     for (auto& e : *v) cudaEventDestroy(e);
   if (ev_wg_join_) cudaEventDestroy(ev_wg_join_);
+  if (ev_emb_zero_) cudaEventDestroy(ev_emb_zero_);
+  if (ev_head_fork_) cudaEventDestroy(ev_head_fork_);
   if (s_wg_) cudaStreamDestroy(s_wg_);
   for (auto& e : marks_)
     if (e) cudaEventDestroy(e);
@@ -802,6 +807,15 @@ void Engine::issue_bucket(size_t k) {
 void Engine::backward() {
   const DevBatch& b = batch_;
   const int T = b.T;
+  if (wg_on_) {
+    // the word-embedding gradient (94 MB at C2) is zeroed beside the head /
+    // top layers instead of at the end of backward
+    HP_CUDA(cudaEventRecord(ev_fork_[4 * L_], s_main_));
+    HP_CUDA(cudaStreamWaitEvent(s_wg_, ev_fork_[4 * L_], 0));
+    wg_forked_ = true;
+    HP_CUDA(cudaMemsetAsync(gp(0), 0, sizeof(float) * table_[0].size(), s_wg_));
+    HP_CUDA(cudaEventRecord(ev_emb_zero_, s_wg_));
+  }
   const int iw = pidx("mlm.w");
   // MLM head: d(mlm.w) = Hm^T dZ, d(mlm.b) = colsum dZ, dHm = dZ W^T
   if (b.M > 0) {
@@ -810,7 +824,11 @@ void Engine::backward() {
     gw.a = Operand{hm_, d_, 1, 0, 0};
     gw.b = Operand{dz_, Vp_, 0, 0, 0};
     gw.c = gp(iw); gw.ldc = V_; gw.ct = DType::f32;
-    gemm_t(gw);
+    // beside the head's data gradient and layer L-1's backward (wgrad stream)
+    if (wg_on_)
+      wgrad_t(gw, ev_head_fork_, ev_wg_join_);
+    else
+      gemm_t(gw);
     tstart(TM_HEAD);
     {
       const uint64_t Mm = (std::max<uint64_t>(x_.max_masks, 1) + mpad_ - 1) / mpad_ * mpad_;
@@ -875,9 +893,20 @@ void Engine::backward() {
       wgrad_t(w1, wg_on_ ? ev_fork_[4 * l + 1] : nullptr, wg_on_ ? ev_w1_[l] : nullptr);
       tstart(TM_NORM);
       {
-        DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, F_));
-        col_sum(T, F_, dU_, F_, at_, gp(ib1), scratch_, s_main_, &f);
-        issue_final(f);
+        if (wg_on_) {
+          // d(ffn.b1) = colsum(dU) beside the chain (its own scratch), before
+          // the event that lets the next layer reuse dU_
+          tstop(TM_NORM, 0, 0);
+          tstart(TM_NORM, s_wg_);
+          col_sum(T, F_, dU_, F_, at_, gp(ib1), scratch_wg_, s_wg_);
+          tstop(TM_NORM, 0, 0, s_wg_);
+          HP_CUDA(cudaEventRecord(ev_w1_[l], s_wg_));
+          tstart(TM_NORM);
+        } else {
+          DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, F_));
+          col_sum(T, F_, dU_, F_, at_, gp(ib1), scratch_, s_main_, &f);
+          issue_final(f);
+        }
       }
       tstop(TM_NORM, 0, 0);
       GemmArgs dx1;  // dX1 = dU W1^T + dP2
@@ -967,7 +996,10 @@ void Engine::backward() {
     dx0 = dB_;
   }
   tstart(TM_EMBED);
-  HP_CUDA(cudaMemsetAsync(gp(0), 0, sizeof(float) * table_[0].size(), s_main_));
+  if (wg_forked_)
+    HP_CUDA(cudaStreamWaitEvent(s_main_, ev_emb_zero_, 0));  // zeroed on the wgrad stream
+  else
+    HP_CUDA(cudaMemsetAsync(gp(0), 0, sizeof(float) * table_[0].size(), s_main_));
   embed_bwd(b, d_, dx0, at_, gp(0), gp(1), gp(2), scratch_, s_main_);
   tstop(TM_EMBED, 0, (double)T * d_ * (asz_ + 8));
   grads_ready(0);

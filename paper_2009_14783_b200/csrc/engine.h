@@ -152,6 +152,8 @@ class Engine {
   std::vector<cudaEvent_t> ev_w2_, ev_w1_, ev_wo_, ev_wq_;  // [L] wgrad done
   std::vector<cudaEvent_t> ev_wgb_;                        // [buckets] wgrads so far
   cudaEvent_t ev_wg_join_ = nullptr;
+  cudaEvent_t ev_emb_zero_ = nullptr, ev_head_fork_ = nullptr;
+  float* scratch_wg_ = nullptr;  // column-sum scratch of the wgrad stream
   cudaEvent_t ev_fwd_ = nullptr, ev_comm_done_ = nullptr, ev_done_ = nullptr;
   std::vector<cudaEvent_t> ev_bucket_;
   size_t next_bucket_ = 0;
