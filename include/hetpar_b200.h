@@ -154,6 +154,17 @@ hp_status hp_pg_broadcast(hp_comm* c, const void* payload, uint64_t len, uint64_
 hp_status hp_pg_all_reduce_sum(hp_comm* c, const double* v, uint64_t n, double* out);
 hp_status hp_pg_gather_scalars(hp_comm* c, double v, double* out);
 hp_status hp_pg_barrier(hp_comm* c);
+/* Gradient-allreduce measurement (BASELINE metric "allreduce bus GB/s", the
+ * C5 sweep): `bytes` of fp32 on this rank's device, cut into contiguous
+ * buckets of at most bucket_mb MiB (the engine's layout), each bucket one
+ * in-place ncclAllReduce(ncclSum) on one stream -- the engine's call
+ * (engine.cpp issue_bucket; the reference's all_reduce_sum,
+ * engine.hpp:145).  warmup untimed iterations, then iters timed with CUDA
+ * events on that stream; *ms = mean milliseconds per iteration (every
+ * bucket of the buffer).  Collective: every rank calls it with the same
+ * arguments. */
+hp_status hp_comm_allreduce_bench(hp_comm* c, uint64_t bytes, double bucket_mb, int iters,
+                                  int warmup, double* ms);
 
 /* ------------------------------------------------------------------------
  * Step engine: StepEngine<T>::round (include/hetpar/engine.hpp:125-165).
@@ -323,6 +334,11 @@ hp_status hp_engine_synchronize(hp_engine* e);
 /* bytes one hp_engine_stage_batch copies host->device, and one round copies
  * device->host (the [loss, weight] readback + status flags). */
 hp_status hp_engine_io_bytes(hp_engine* e, uint64_t* h2d, uint64_t* d2h);
+/* Measurement only (bench.py's overlap figure): on = 0 skips the gradient
+ * bucket allreduces of later rounds (the [loss, weight] allreduce stays), so
+ * t_step(on) - t_step(off) is the gradient communication left exposed behind
+ * backward.  Ranks then diverge; default on. */
+hp_status hp_engine_set_grad_comm(hp_engine* e, int on);
 
 /* ------------------------------------------------------------------------
  * Test hooks (used by tests/ only): run one GEMM of the engine's dispatch on

@@ -11,6 +11,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhetpar_b200.so")
+if os.environ.get("HP_LIB_VARIANT"):  # A/B builds (tools/build_native.py HP_VARIANT)
+    LIB_PATH = os.path.join(_HERE, f"libhetpar_b200_{os.environ['HP_LIB_VARIANT']}.so")
 
 HP_OK, HP_ESHAPE, HP_ECONFIG, HP_EINDEX, HP_EIO, HP_ECOMM, HP_ENUMERIC, HP_ECUDA = range(8)
 HP_ARCH_MASKED_TOKEN_MODEL = 3
@@ -140,6 +142,7 @@ _SIGS = {
     "hp_pg_all_reduce_sum": [P, P, U64, P],
     "hp_pg_gather_scalars": [P, C.c_double, P],
     "hp_pg_barrier": [P],
+    "hp_comm_allreduce_bench": [P, U64, D, I, I, P],
     "hp_shards_open": [C.c_char_p, P],
     "hp_shards_info": [P, P, P],
     "hp_shards_token_lengths": [P, P, U64],
@@ -168,6 +171,7 @@ _SIGS = {
     "hp_engine_elapsed": [P, I, I, P],
     "hp_engine_synchronize": [P],
     "hp_engine_io_bytes": [P, P, P],
+    "hp_engine_set_grad_comm": [P, I],
     "hp_debug_gemm": [I, I, I, I, P, I64, I, P, I64, I, I64, I64, P, I64, I, I64, I64, P, I, P, P,
                       I64, I, I, I],
     "hp_debug_sync": [],

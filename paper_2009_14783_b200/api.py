@@ -661,6 +661,19 @@ class Communicator:
     def barrier(self) -> None:
         call("hp_pg_barrier", self._h)
 
+    def allreduce_bench(self, nbytes: int, bucket_mb: float = 25.0, iters: int = 10,
+                        warmup: int = 3) -> dict:
+        """Time the engine's bucketed gradient allreduce (fp32, ncclSum, buckets
+        of <= bucket_mb MiB) over nbytes; collective.  busbw = S/t * 2(W-1)/W."""
+        ms = C.c_double()
+        call("hp_comm_allreduce_bench", self._h, int(nbytes), float(bucket_mb), int(iters),
+             int(warmup), C.byref(ms))
+        t = ms.value / 1e3
+        w = self.world
+        algbw = nbytes / t / 1e9
+        return {"bytes": int(nbytes), "bucket_mb": float(bucket_mb), "ms": ms.value,
+                "algbw_gbps": algbw, "busbw_gbps": algbw * 2 * (w - 1) / w}
+
     def close(self):
         if self._h:
             call("hp_comm_destroy", self._h)
@@ -746,6 +759,11 @@ class StepEngine:
 
     def set_capture(self, on: bool):
         call("hp_engine_set_capture", self._h, int(on))
+
+    def set_grad_comm(self, on: bool):
+        """Measurement only: off skips the gradient-bucket allreduces (ranks
+        diverge); bench.py uses it for the exposed-communication figure."""
+        call("hp_engine_set_grad_comm", self._h, int(on))
 
     def local_grads(self) -> np.ndarray:
         out = np.empty(self.n, np.float32)

@@ -108,11 +108,19 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   HP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   HP_CUDA(cudaStreamCreateWithPriority(&s_main_, cudaStreamNonBlocking, prio_hi));
   HP_CUDA(cudaStreamCreateWithPriority(&s_comm_, cudaStreamNonBlocking, prio_lo));
+  if (comm_) {
+    // per-bucket updates on their own stream, so bucket k+1's allreduce
+    // starts as soon as bucket k's finishes instead of behind k's update
+    HP_CUDA(cudaStreamCreateWithPriority(&s_upd_, cudaStreamNonBlocking, prio_lo));
+    HP_CUDA(cudaEventCreateWithFlags(&ev_upd_done_, cudaEventDisableTiming));
+  }
   HP_CUDA(cudaEventCreateWithFlags(&ev_fwd_, cudaEventDisableTiming));
   HP_CUDA(cudaEventCreateWithFlags(&ev_comm_done_, cudaEventDisableTiming));
   HP_CUDA(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming));
   ev_bucket_.resize(buckets_.size());
   for (auto& e : ev_bucket_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ev_reduced_.resize(buckets_.size());
+  for (auto& e : ev_reduced_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   {
     const char* e = std::getenv("HP_WGRAD_STREAM");
     wg_on_ = bert_ && !(e && std::string(e) == "0");
@@ -312,6 +320,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
 Engine::~Engine() {
   if (s_main_) cudaStreamSynchronize(s_main_);
   if (s_comm_) cudaStreamSynchronize(s_comm_);
+  if (s_upd_) cudaStreamSynchronize(s_upd_);
   for (auto& kv : graphs_)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (have_premul_ && comm_) ncclRedOpDestroy(premul_, comm_->nccl);
@@ -329,6 +338,7 @@ Engine::~Engine() {
   if (h_flags_) cudaFreeHost(h_flags_);
   if (h_params_) cudaFreeHost(h_params_);
   for (auto& e : ev_bucket_) cudaEventDestroy(e);
+  if (ev_ser_) cudaEventDestroy(ev_ser_);
   for (auto& e : final_evs_) cudaEventDestroy(e);
   for (auto* v : {&ev_fork_, &ev_w2_, &ev_w1_, &ev_wo_, &ev_wq_, &ev_wgb_})
     for (auto& e : *v) cudaEventDestroy(e);
@@ -343,6 +353,9 @@ Engine::~Engine() {
   if (ev_done_) cudaEventDestroy(ev_done_);
   if (s_main_) cudaStreamDestroy(s_main_);
   if (s_comm_) cudaStreamDestroy(s_comm_);
+  if (s_upd_) cudaStreamDestroy(s_upd_);
+  if (ev_upd_done_) cudaEventDestroy(ev_upd_done_);
+  for (auto& e : ev_reduced_) cudaEventDestroy(e);
 }
 
 // ------------------------------------------------------------------ state I/O
@@ -595,6 +608,7 @@ double Engine::elapsed(int a, int b) {
 void Engine::synchronize() {
   HP_CUDA(cudaStreamSynchronize(s_main_));
   HP_CUDA(cudaStreamSynchronize(s_comm_));
+  if (s_upd_) HP_CUDA(cudaStreamSynchronize(s_upd_));
 }
 
 void Engine::tstart(int cls, cudaStream_t st) {
@@ -659,6 +673,16 @@ void Engine::wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done) {
             (g.ct == DType::f32 ? 4.0 : 2.0) * g.M * g.N,
         s_wg_);
   HP_CUDA(cudaEventRecord(done, s_wg_));
+  serialize_if_timed(s_wg_);
+}
+
+// Timer passes serialise the side streams into the compute stream, so each
+// kernel's event span is its own duration, not a share of concurrent work.
+void Engine::serialize_if_timed(cudaStream_t st) {
+  if (!timers_on_) return;
+  if (!ev_ser_) HP_CUDA(cudaEventCreateWithFlags(&ev_ser_, cudaEventDisableTiming));
+  HP_CUDA(cudaEventRecord(ev_ser_, st));
+  HP_CUDA(cudaStreamWaitEvent(s_main_, ev_ser_, 0));
 }
 
 void Engine::wait_wg(cudaEvent_t e) {
@@ -784,7 +808,7 @@ void Engine::issue_bucket(size_t k) {
     HP_CUDA(cudaEventRecord(ev_wgb_[k], s_wg_));
     HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_wgb_[k], 0));
   }
-  if (comm_)
+  if (comm_ && grad_comm_)
     HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, ncclSum,
                           comm_->nccl, s_comm_));
   if (phase_ == 1) {
@@ -794,14 +818,22 @@ void Engine::issue_bucket(size_t k) {
   }
   // the bucket's update runs behind the rest of backward (engine.hpp:147-153:
   // every rank applies the identical update to the identical reduced sum)
+  cudaStream_t su = s_comm_;
+  if (s_upd_) {
+    HP_CUDA(cudaEventRecord(ev_reduced_[k], s_comm_));
+    HP_CUDA(cudaStreamWaitEvent(s_upd_, ev_reduced_[k], 0));
+    su = s_upd_;
+    upd_forked_ = true;
+  }
   AdamArgs a = adam_args_;
   a.g2 = phase_ == 2 ? acc_grads_ : nullptr;
   a.items = adam_items_ + 5 * static_cast<size_t>(bucket_items_[k].first);
   a.nitems = bucket_items_[k].second;
-  tstart(TM_ADAM, s_comm_);
-  adam_update(a, s_comm_);
+  tstart(TM_ADAM, su);
+  adam_update(a, su);
   tstop(TM_ADAM, 0, 28.0 * (double)(bk.hi - bk.lo) + (bf16_ ? 2.0 * (double)(bk.hi - bk.lo) : 0.0),
-        s_comm_);
+        su);
+  serialize_if_timed(su);
 }
 
 void Engine::backward() {
@@ -1044,7 +1076,8 @@ void Engine::round_async(int dummy, double lr) {
   HP_CUDA(cudaMemcpyAsync(d_hyper_, hyper, sizeof(hyper), cudaMemcpyHostToDevice, s_main_));
 
   if (graphs_on_ && !timers_on_ && !capture_) {
-    GraphEntry& e = graphs_[std::make_tuple(batch_.T, batch_.B, batch_.M, (dummy ? 1 : 0) | (phase_ << 1))];
+    GraphEntry& e = graphs_[std::make_tuple(batch_.T, batch_.B, batch_.M,
+                                           (dummy ? 1 : 0) | (phase_ << 1) | (grad_comm_ ? 0 : 8))];
     if (e.exec) {
       HP_CUDA(cudaGraphLaunch(e.exec, s_main_));
       count_launch(static_cast<int>(e.launches));
@@ -1103,12 +1136,14 @@ void Engine::issue_final(DeferredFinal& f) {
   HP_CUDA(cudaEventRecord(final_evs_[final_n_], s_main_));
   HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[final_n_], 0));
   launch_final(f, s_comm_);
+  serialize_if_timed(s_comm_);
   ++final_n_;
 }
 
 void Engine::round_body(int dummy) {
   final_n_ = 0;
   wg_forked_ = false;
+  upd_forked_ = false;
   HP_CUDA(cudaMemsetAsync(flags_, 0, 8, s_main_));
   // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
   forward(!dummy);
@@ -1157,6 +1192,10 @@ void Engine::round_body(int dummy) {
   // the round ends when the last bucket's update has landed
   HP_CUDA(cudaEventRecord(ev_comm_done_, s_comm_));
   HP_CUDA(cudaStreamWaitEvent(s_main_, ev_comm_done_, 0));
+  if (upd_forked_) {
+    HP_CUDA(cudaEventRecord(ev_upd_done_, s_upd_));
+    HP_CUDA(cudaStreamWaitEvent(s_main_, ev_upd_done_, 0));
+  }
   HP_CUDA(cudaMemcpyAsync(h_lw_, d_lw_, 6 * 8, cudaMemcpyDeviceToHost, s_main_));
   HP_CUDA(cudaMemcpyAsync(h_flags_, flags_, 2 * 4, cudaMemcpyDeviceToHost, s_main_));
 }

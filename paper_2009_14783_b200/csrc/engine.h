@@ -44,6 +44,7 @@ class Engine {
   void save_checkpoint(const std::string& path, const hp_ckpt_desc& c);
   void load_checkpoint(const std::string& path, hp_ckpt_desc* out);
   void set_capture(bool on) { capture_ = on; }
+  void set_grad_comm(bool on) { grad_comm_ = on; }
   void get_local_grads(float* flat, uint64_t n);
   void stage_batch(const hp_batch& b);
   void round_async(int dummy, double lr);
@@ -74,7 +75,8 @@ class Engine {
   // a weight-gradient GEMM on the wgrad stream (see backward): forks from the
   // compute stream, records `done` when finished
   void wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done);
-  void wait_wg(cudaEvent_t e);  // compute stream waits for a pending wgrad
+  void wait_wg(cudaEvent_t e);
+  void serialize_if_timed(cudaStream_t st);  // compute stream waits for a pending wgrad
   void tstart(int cls, cudaStream_t st = nullptr);
   void tstop(int cls, double flops, double bytes, cudaStream_t st = nullptr);
   void forward(bool need_grad_state);
@@ -143,6 +145,10 @@ class Engine {
   float* h_params_ = nullptr;
 
   cudaStream_t s_main_ = nullptr, s_comm_ = nullptr;
+  cudaStream_t s_upd_ = nullptr;   // N > 1: per-bucket updates beside the allreduces
+  cudaEvent_t ev_upd_done_ = nullptr;
+  std::vector<cudaEvent_t> ev_reduced_;
+  bool upd_forked_ = false;
   // weight-gradient GEMMs run beside the data-gradient chain (bert_encoder):
   // they fill the SMs the N = d GEMMs leave idle and the GEMM tails
   cudaStream_t s_wg_ = nullptr;
@@ -161,6 +167,7 @@ class Engine {
   bool have_premul_ = false;
 
   bool capture_ = false;
+  bool grad_comm_ = true;  // measurement toggle (hp_engine_set_grad_comm)
   float* local_grads_ = nullptr;
   uint64_t step_ = 0, adam_t_ = 0;
   bool in_flight_ = false;
@@ -173,6 +180,7 @@ class Engine {
   bool last_final_ = true;
 
   bool timers_on_ = false;
+  cudaEvent_t ev_ser_ = nullptr;
   struct TimerAcc {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
     size_t used = 0;

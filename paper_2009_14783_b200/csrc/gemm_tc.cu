@@ -32,6 +32,7 @@
 
 #include "hp_common.h"
 #include "kernels.h"
+#include "launch.cuh"
 #include "tc_common.cuh"
 
 namespace hp {
@@ -654,6 +655,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before use
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  // the prologue above overlapped the previous kernel's tail (launch.cuh)
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0) trace_at(p, 1);
 
   // Work units: static striding, unit u = blockIdx / CG + i * (gridDim / CG).
@@ -1005,23 +1009,7 @@ static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Pa
     attr = true;
   }
   const int grid = CG * std::min(p.units, num_sms() / CG);
-  if constexpr (CG == 1) {
-    tc::gemm_tc_kernel<BN, 1, EK><<<grid, tc::kThreads, smem, s>>>(ma, mb, p);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(tc::kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    HP_CUDA(cudaLaunchKernelEx(&cfg, tc::gemm_tc_kernel<BN, 2, EK>, ma, mb, p));
-  }
+  launch_pdl(PDL_GEMM, tc::gemm_tc_kernel<BN, CG, EK>, dim3(grid), dim3(tc::kThreads), smem, s, CG, ma, mb, p);
   HP_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -18,6 +18,7 @@
 
 #include "hp_common.h"
 #include "kernels.h"
+#include "launch.cuh"
 #include "tc_common.cuh"
 
 namespace hp {
@@ -26,6 +27,17 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 }
 uint64_t kernel_launch_count() { return g_launches.load(); }
+bool pdl_on(int cls) {
+  static const int mask = [] {
+    const char* e = std::getenv("HP_PDL");
+    if (!e || std::string(e) == "0") return 0;  // default off: measured no gain
+    if (std::string(e) == "1") return 7;
+    const std::string v(e);
+    return (v.find("gemm") != std::string::npos ? 1 : 0) |
+           (v.find("attn") != std::string::npos ? 2 : 0) | (v.find("ln") != std::string::npos ? 4 : 0);
+  }();
+  return (mask >> cls) & 1;
+}
 void count_launch(int n) { g_launches += n; }
 
 #define LAUNCH_CHECK() HP_CUDA(cudaGetLastError())
@@ -624,6 +636,8 @@ __global__ void __launch_bounds__(256) ln_fwd_bulk(int T, const bf16* __restrict
                                                    const float* __restrict__ bta, bf16* __restrict__ y,
                                                    float* __restrict__ mean, float* __restrict__ rstd) {
   constexpr int d = 256 * NV;
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t lsm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(lsm);
   bf16* xs = reinterpret_cast<bf16*>(lsm + 128);
@@ -688,6 +702,8 @@ __global__ void __launch_bounds__(256, 1) ln_bwd_bulk(int T, const bf16* __restr
                                                       bf16* __restrict__ dx, float* __restrict__ part) {
   constexpr int d = 256 * NV;
   constexpr int RPW = kLnBwdRows / 8;
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t lsm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(lsm);
   bf16* xs = reinterpret_cast<bf16*>(lsm + 128);
@@ -791,10 +807,10 @@ void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
     const int gb = (T + rows_cta - 1) / rows_cta;
     const size_t sm = 128 + (size_t)rows_cta * d * 2;
     switch (d / 256) {
-      case 1: ln_fwd_bulk<1><<<gb, 256, sm, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      case 2: ln_fwd_bulk<2><<<gb, 256, sm, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      case 3: ln_fwd_bulk<3><<<gb, 256, sm, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      default: ln_fwd_bulk<4><<<gb, 256, sm, s>>>(T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 1: launch_pdl(PDL_LN, ln_fwd_bulk<1>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 2: launch_pdl(PDL_LN, ln_fwd_bulk<2>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 3: launch_pdl(PDL_LN, ln_fwd_bulk<3>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      default: launch_pdl(PDL_LN, ln_fwd_bulk<4>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
     }
   } else {
     DISPATCH1(xt, X, DISPATCH1(yt, Y,
@@ -823,8 +839,8 @@ void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
       HP_CUDA(cudaFuncSetAttribute(ln_bwd_bulk<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
       attr_##NV = sm;                                                                           \
     }                                                                                           \
-    ln_bwd_bulk<NV><<<chunks, 256, sm, s>>>(T, (const bf16*)dy, (const bf16*)x, mean, rstd, g,  \
-                                           (bf16*)dx, part);                                    \
+    launch_pdl(PDL_LN, ln_bwd_bulk<NV>, dim3(chunks), dim3(256), sm, s, 1, T, (const bf16*)dy,      \
+               (const bf16*)x, mean, rstd, g, (bf16*)dx, part);                                 \
   } break;
       LNB(1) LNB(2) LNB(3) default: LNB(4)
 #undef LNB

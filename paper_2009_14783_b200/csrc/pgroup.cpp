@@ -19,6 +19,7 @@
 #include <sys/socket.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -223,6 +224,58 @@ hp_status hp_pg_gather_scalars(hp_comm* c, double v, double* out) {
     if (!out) hp::fail(HP_ECONFIG, "hp_pg_gather_scalars: the master needs an output buffer");
     std::memcpy(out, all.data(), sizeof(double) * all.size());
   }
+  HP_API_END
+}
+
+hp_status hp_comm_allreduce_bench(hp_comm* c, uint64_t bytes, double bucket_mb, int iters,
+                                  int warmup, double* ms) {
+  HP_API_BEGIN
+  if (!c || !ms) hp::fail(HP_ECONFIG, "hp_comm_allreduce_bench: null argument");
+  if (bytes < 4 || iters < 1 || warmup < 0 || !(bucket_mb > 0))
+    hp::fail(HP_ECONFIG, "hp_comm_allreduce_bench: bad sizes");
+  HP_CUDA(cudaSetDevice(c->device));
+  const size_t n = bytes / 4;
+  const size_t cap = std::max<size_t>(1, static_cast<size_t>(bucket_mb * 1048576.0) / 4);
+  float* buf = nullptr;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  HP_CUDA(cudaMalloc(&buf, n * 4));
+  try {
+    HP_CUDA(cudaMemsetAsync(buf, 0, n * 4));
+    HP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    HP_CUDA(cudaEventCreate(&e0));
+    HP_CUDA(cudaEventCreate(&e1));
+    HP_CUDA(cudaDeviceSynchronize());
+    // buckets walk the buffer from its end (the engine's order: bucket 0
+    // holds the last parameters, the first gradients backward produces)
+    auto one = [&]() {
+      for (size_t hi = n; hi > 0;) {
+        const size_t lo = hi > cap ? hi - cap : 0;
+        hp::check_nccl(ncclAllReduce(buf + lo, buf + lo, hi - lo, ncclFloat, ncclSum, c->nccl, s),
+                       "ncclAllReduce");
+        hi = lo;
+      }
+    };
+    for (int i = 0; i < warmup; ++i) one();
+    HP_CUDA(cudaStreamSynchronize(s));
+    HP_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < iters; ++i) one();
+    HP_CUDA(cudaEventRecord(e1, s));
+    HP_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    HP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = static_cast<double>(t) / iters;
+  } catch (...) {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+    cudaFree(buf);
+    throw;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(s);
+  cudaFree(buf);
   HP_API_END
 }
 

@@ -46,6 +46,9 @@ p = eng.get_params()
 rb0 = plan.batches[0]
 rep = eng.round(rec.batch(rb0), rank == 1, 1e-3)
 out = {"losses": losses, "digest": digest, "dummy_loss": rep.loss, "dummy_weight": rep.weight}
+# the bucketed-allreduce measurement (bench.py / tools/allreduce_sweep.py): 4 MiB in 1 MiB buckets
+ar = comm.allreduce_bench(1 << 22, 1.0, iters=2, warmup=1)
+out["ar_ok"] = ar["ms"] > 0 and ar["busbw_gbps"] > 0
 if rank == 0:
     np.save(os.environ["HP_OUT"] + "/params.npy", p)
 with open(os.environ["HP_OUT"] + f"/rank{rank}.json", "w") as f:
@@ -73,6 +76,7 @@ def test_c1_w2_nccl_matches_reference(tmp_path):
     p = np.load(tmp_path / "params.npy")
     assert rel_norm(p, t["params_f64_as_f32"]) <= 1e-4
     assert r0["dummy_weight"] == 8.0             # only rank 0's 8 sentences count
+    assert r0["ar_ok"] and r1["ar_ok"]
 
 
 PG_WORKER = r'''

@@ -34,12 +34,17 @@ def build(verbose: bool = False) -> str:
     # HP_GEMM_PROFILE=1: compile the GEMM's timeline trace / debug hooks in
     # (tools/gemm_trace.py); separate object dir so builds never mix
     profile = os.environ.get("HP_GEMM_PROFILE") == "1"
-    obj_dir = OBJ + ("_profile" if profile else "")
+    # HP_VARIANT=name HP_VARIANT_DEFS="A B": an A/B build with -DA -DB into
+    # libhetpar_b200_<name>.so (loaded when HP_LIB_VARIANT=name)
+    variant = os.environ.get("HP_VARIANT", "")
+    vdefs = ["-D" + d for d in os.environ.get("HP_VARIANT_DEFS", "").split()]
+    obj_dir = OBJ + ("_profile" if profile else "") + ("_" + variant if variant else "")
+    out = OUT[:-3] + "_" + variant + ".so" if variant else OUT
     os.makedirs(obj_dir, exist_ok=True)
     nd = nccl_dir()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include")]
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-                    "--expt-relaxed-constexpr"] + inc + (["-DHP_GEMM_PROFILE"] if profile else [])
+                    "--expt-relaxed-constexpr"] + inc + (["-DHP_GEMM_PROFILE"] if profile else []) + vdefs
     srcs = sorted(glob.glob(os.path.join(SRC, "*.cu")) + glob.glob(os.path.join(SRC, "*.cpp")))
     hdrs = (glob.glob(os.path.join(SRC, "*.h")) + glob.glob(os.path.join(SRC, "*.cuh")) +
             glob.glob(os.path.join(ROOT, "include", "*.h")))
@@ -59,8 +64,8 @@ def build(verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
         objs = list(ex.map(compile_one, srcs))
-    if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", OUT] + objs + [
+    if not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs + [
             "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
             "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
         if verbose:
@@ -68,7 +73,7 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
