@@ -464,9 +464,482 @@ __global__ void __launch_bounds__(kThreadsB, 2)
   }
 }
 
+
+// ==================================================================== long
+// Sequences of 128 < n <= 512 (BERT-large C4: seq 512), dk = 64.  Blocks of
+// 128 rows: query block i, key block j (nb = ceil(n / 128) <= 4).  Exact
+// softmax, no online rescaling: S for a query block against every key block
+// fits TMEM (128 lanes x 128 nb fp32 columns).  Three kernels, no atomics
+// (deterministic like the rest of the step):
+//   fwd   grid (b, h, i): S_j = Q_i K_j^T for all j (TMEM [128 j, +128)), a
+//         max pass and an exp pass over TMEM; P_j (bf16, double-buffered smem)
+//         feeds O += P_j V_j into TMEM [0, 64) (S_0's columns, consumed).
+//   bwd_kv grid (b, h, j): K_j, V_j resident; for each query block i (Q_i,
+//         dO_i double-buffered): S = Q_i K_j^T, dP = dO_i V_j^T, then
+//         P = exp(S / sqrt(dk) - lse), dS = P (dP - D) / sqrt(dk) written as
+//         [q][key] bf16 tiles; dV += P^T dO_i, dK += dS^T Q_i in TMEM.
+//   bwd_q grid (b, h, i): Q_i, dO_i resident; for each key block j (K_j, V_j
+//         double-buffered): S, dP, dS as above; dQ += dS K_j in TMEM.
+// D = rowsum(dO * O) is recomputed per row from global memory.
+constexpr int kMaxKB = 4;
+
+__device__ __forceinline__ uint32_t long_cols(int nb) {
+  return nb <= 1 ? 128u : (nb == 2 ? 256u : 512u);
+}
+
+struct LongFwdSmem {
+  uint8_t q[kTile];
+  uint8_t k[kMaxKB][kTile];
+  uint8_t v[kMaxKB][kTile];
+  uint8_t p[2][2 * kTile];  // P_j: [128 q][128 keys] as two [128][64] sub-tiles
+  uint64_t full, s_done, o_done, p_ready[2], pv_done[2];
+  uint32_t tmem;
+};
+struct LongKvSmem {
+  uint8_t k[kTile], v[kTile];
+  uint8_t q[2][kTile], g[2][kTile];  // Q_i, dO_i ring
+  uint8_t p[2 * kTile], ds[2 * kTile];
+  uint64_t kv_full, full[2], freeb[2], s_done, pds_ready, pds_free;
+  uint32_t tmem;
+};
+struct LongQSmem {
+  uint8_t q[kTile], g[kTile];
+  uint8_t k[2][kTile], v[2][kTile];  // K_j, V_j ring
+  uint8_t ds[2 * kTile];
+  uint64_t qg_full, full[2], freeb[2], s_done, ds_ready, ds_free;
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(slot)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_free(uint32_t tmem, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+}
+
+// D_r = rowsum(dO * O) of one query row (64 columns)
+__device__ __forceinline__ float row_dot_do(const bf16* o, const bf16* dO) {
+  const uint4* po = reinterpret_cast<const uint4*>(o);
+  const uint4* pg = reinterpret_cast<const uint4*>(dO);
+  float d4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint4 a = po[q], g = pg[q];
+    const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 af = __bfloat1622float2(ah[e]), gf = __bfloat1622float2(gh[e]);
+      d4[e] = fmaf(af.x, gf.x, d4[e]);
+      d4[e] = fmaf(af.y, gf.y, d4[e]);
+    }
+  }
+  return (d4[0] + d4[1]) + (d4[2] + d4[3]);
+}
+
+__global__ void __launch_bounds__(kThreadsF, 1)
+    attn_fwd_long(const __grid_constant__ CUtensorMap map_qkv, const int* __restrict__ cu, int H,
+                  bf16* __restrict__ o, float* __restrict__ lse, int T_total) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  LongFwdSmem& sm = *reinterpret_cast<LongFwdSmem*>(align1024(raw));
+  const int b = blockIdx.x, h = blockIdx.y, qb = blockIdx.z;
+  const int row0 = cu[b], n = cu[b + 1] - row0;
+  if (128 * qb >= n) return;
+  const int nb = (n + 127) / 128;
+  const uint32_t cols = long_cols(nb);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = H * DK;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.full, 1);
+    mbar_init(&sm.s_done, 1);
+    mbar_init(&sm.o_done, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.p_ready[s], 32 * kSoftWarpsF);
+      mbar_init(&sm.pv_done[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(&sm.tmem, cols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_expect_tx(&sm.full, (1 + 2 * nb) * kTile);
+      tma_2d(&map_qkv, &sm.full, sm.q, h * DK, row0 + 128 * qb);
+      for (int j = 0; j < nb; ++j) {
+        tma_2d(&map_qkv, &sm.full, sm.k[j], d + h * DK, row0 + 128 * j);
+        tma_2d(&map_qkv, &sm.full, sm.v[j], 2 * d + h * DK, row0 + 128 * j);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    mbar_wait(&sm.full, 0);
+    tmem_fence_after();
+    if (elect_one()) {
+      const uint32_t id = idesc(128, 0, 0);
+      const uint64_t aq = kmaj(smem_u32(sm.q));
+      for (int j = 0; j < nb; ++j) {
+        const uint64_t bk = kmaj(smem_u32(sm.k[j]));
+#pragma unroll
+        for (int kk = 0; kk < DK / 16; ++kk)
+          umma_bf16(tmem + 128 * j, aq + 2 * kk, bk + 2 * kk, id, kk > 0);
+      }
+      umma_commit(&sm.s_done);
+    }
+    __syncwarp();
+    for (int j = 0; j < nb; ++j) {
+      mbar_wait(&sm.p_ready[j & 1], (j >> 1) & 1);
+      tmem_fence_after();
+      if (elect_one()) {
+        const uint32_t id = idesc(64, 0, 1);
+        const uint32_t pb = smem_u32(sm.p[j & 1]);
+        const uint64_t bv = mnmaj(smem_u32(sm.v[j]));
+#pragma unroll
+        for (int kk = 0; kk < NQ / 16; ++kk)
+          umma_bf16(tmem, kmaj2(pb, kk, kTile), bv + kk * (2048 >> 4), id, (j > 0 || kk > 0) ? 1 : 0);
+        umma_commit(&sm.pv_done[j & 1]);
+        if (j == nb - 1) umma_commit(&sm.o_done);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r = 32 * quarter + lane;  // query row within the block
+    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
+    const float scale = rsqrtf(static_cast<float>(DK));
+    const float sl2 = scale * 1.4426950408889634f;
+    mbar_wait(&sm.s_done, 0);
+    tmem_fence_after();
+    float m4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int j = 0; j < nb; ++j) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        TMEM_LD32(trow + 128 * j + 32 * c, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int kbase = 128 * j + 32 * c;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (kbase + i < n) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(v[i]));
+      }
+    }
+    const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    const float mo = -mx * sl2;
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < nb; ++j) {
+      // buffer j & 1 is free once O += P_{j-2} V_{j-2} has read it
+      if (j >= 2) mbar_wait(&sm.pv_done[j & 1], ((j - 2) >> 1) & 1);
+      const uint32_t pb = smem_u32(sm.p[j & 1]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        TMEM_LD32(trow + 128 * j + 32 * c, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int kbase = 128 * j + 32 * c;
+        float p[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          p[i] = (kbase + i < n) ? ex2(fmaf(__uint_as_float(v[i]), sl2, mo)) : 0.f;
+          s4[i & 3] += p[i];
+        }
+        put_row32(pb, r, c, p);
+      }
+      fence_async_smem();
+      tmem_fence_before();
+      mbar_arrive(&sm.p_ready[j & 1]);
+    }
+    const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    mbar_wait(&sm.o_done, 0);
+    tmem_fence_after();
+    const int q = 128 * qb + r;
+    const bool ok = q < n;
+    bf16* orow = o + (int64_t)(row0 + q) * d + h * DK;
+    tmem_row32_to_global(trow, 1.f / sum, orow, ok);
+    tmem_row32_to_global(trow + 32, 1.f / sum, orow + 32, ok);
+    if (ok) lse[(int64_t)h * T_total + row0 + q] = mx * scale + logf(sum);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tmem_fence_after();
+    tmem_free(tmem, cols);
+  }
+}
+
+// softmax-side step shared by the two backward kernels: this thread's row r
+// of S (TMEM [0,128)) and dP ([128,256)), its 64 columns `half` -> P, dS
+// (bf16, [q][key] tiles); keys k0 + column, query valid = rok
+__device__ __forceinline__ void long_bwd_rows(uint32_t trow, int half, int r, int k0, int n, bool rok,
+                                              float sl2, float lo, float Dr, float scale,
+                                              uint32_t p_base, uint32_t ds_base) {
+#pragma unroll 1
+  for (int c2 = 0; c2 < 2; ++c2) {
+    const int c = 2 * half + c2;
+    uint32_t sv[32], dv[32];
+    TMEM_LD32(trow + 32 * c, sv);
+    TMEM_LD32(trow + 128 + 32 * c, dv);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float p[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const bool ok = rok && (k0 + 32 * c + i < n);
+      p[i] = ok ? ex2(fmaf(__uint_as_float(sv[i]), sl2, lo)) : 0.f;
+    }
+    if (p_base) put_row32(p_base, r, c, p);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) p[i] = p[i] * (__uint_as_float(dv[i]) - Dr) * scale;
+    put_row32(ds_base, r, c, p);
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsB, 1)
+    attn_bwd_kv_long(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                     const int* __restrict__ cu, int H, const bf16* __restrict__ o,
+                     const bf16* __restrict__ dO, const float* __restrict__ lse,
+                     bf16* __restrict__ dqkv, int T_total) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  LongKvSmem& sm = *reinterpret_cast<LongKvSmem*>(align1024(raw));
+  const int b = blockIdx.x, h = blockIdx.y, kb = blockIdx.z;
+  const int row0 = cu[b], n = cu[b + 1] - row0;
+  if (128 * kb >= n) return;
+  const int nb = (n + 127) / 128;
+  constexpr uint32_t cols = 512;  // S [0,128), dP [128,256), dV [256,320), dK [320,384)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = H * DK;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.freeb[s], 1);
+    }
+    mbar_init(&sm.s_done, 1);
+    mbar_init(&sm.pds_ready, 32 * kSoftWarpsB);
+    mbar_init(&sm.pds_free, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(&sm.tmem, cols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_expect_tx(&sm.kv_full, 2 * kTile);
+      tma_2d(&map_qkv, &sm.kv_full, sm.k, d + h * DK, row0 + 128 * kb);
+      tma_2d(&map_qkv, &sm.kv_full, sm.v, 2 * d + h * DK, row0 + 128 * kb);
+    }
+    __syncwarp();
+    for (int i = 0; i < nb; ++i) {
+      const int s = i & 1;
+      if (i >= 2) mbar_wait(&sm.freeb[s], ((i - 2) >> 1) & 1);
+      if (elect_one()) {
+        mbar_expect_tx(&sm.full[s], 2 * kTile);
+        tma_2d(&map_qkv, &sm.full[s], sm.q[s], h * DK, row0 + 128 * i);
+        tma_2d(&map_do, &sm.full[s], sm.g[s], h * DK, row0 + 128 * i);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    mbar_wait(&sm.kv_full, 0);
+    const uint32_t tk = smem_u32(sm.k), tv = smem_u32(sm.v);
+    const uint32_t tp = smem_u32(sm.p), tds = smem_u32(sm.ds);
+    for (int i = 0; i < nb; ++i) {
+      const int s = i & 1;
+      mbar_wait(&sm.full[s], (i >> 1) & 1);
+      tmem_fence_after();
+      const uint32_t tq = smem_u32(sm.q[s]), tdo = smem_u32(sm.g[s]);
+      if (elect_one()) {
+        const uint32_t id = idesc(128, 0, 0);
+#pragma unroll
+        for (int kk = 0; kk < DK / 16; ++kk) {
+          umma_bf16(tmem, kmaj(tq) + 2 * kk, kmaj(tk) + 2 * kk, id, kk > 0);         // S
+          umma_bf16(tmem + 128, kmaj(tdo) + 2 * kk, kmaj(tv) + 2 * kk, id, kk > 0);  // dP
+        }
+        umma_commit(&sm.s_done);
+      }
+      __syncwarp();
+      mbar_wait(&sm.pds_ready, i & 1);
+      tmem_fence_after();
+      if (elect_one()) {
+        const uint32_t id_t = idesc(64, 1, 1);
+#pragma unroll
+        for (int kk = 0; kk < NQ / 16; ++kk) {
+          const uint64_t step = kk * (2048 >> 4);  // 16 query rows
+          const uint32_t acc = (i > 0 || kk > 0) ? 1 : 0;
+          umma_bf16(tmem + 256, mnmaj2(tp, kTile) + step, mnmaj(tdo) + step, id_t, acc);   // dV += P^T dO
+          umma_bf16(tmem + 320, mnmaj2(tds, kTile) + step, mnmaj(tq) + step, id_t, acc);  // dK += dS^T Q
+        }
+        umma_commit(&sm.freeb[s]);
+        umma_commit(&sm.pds_free);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int r = 32 * quarter + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
+    const float scale = rsqrtf(static_cast<float>(DK));
+    const float l2e = 1.4426950408889634f;
+    for (int i = 0; i < nb; ++i) {
+      const int q = 128 * i + r;
+      const bool rok = q < n;
+      float Dr = 0.f, lr = 0.f;
+      if (rok) {
+        Dr = row_dot_do(o + (int64_t)(row0 + q) * d + h * DK, dO + (int64_t)(row0 + q) * d + h * DK);
+        lr = lse[(int64_t)h * T_total + row0 + q];
+      }
+      mbar_wait(&sm.s_done, i & 1);
+      if (i > 0) mbar_wait(&sm.pds_free, (i - 1) & 1);  // P / dS tiles read by block i-1's MMAs
+      tmem_fence_after();
+      long_bwd_rows(trow, half, r, 128 * kb, n, rok, scale * l2e, -lr * l2e, Dr, scale,
+                    smem_u32(sm.p), smem_u32(sm.ds));
+      fence_async_smem();
+      tmem_fence_before();
+      mbar_arrive(&sm.pds_ready);
+    }
+    mbar_wait(&sm.pds_free, (nb - 1) & 1);
+    tmem_fence_after();
+    const int key = 128 * kb + r;
+    const bool ok = key < n;
+    bf16* row = dqkv + (int64_t)(row0 + key) * 3 * d + h * DK + 32 * half;
+    tmem_row32_to_global(trow + 320 + 32 * half, 1.f, row + d, ok);      // dK
+    tmem_row32_to_global(trow + 256 + 32 * half, 1.f, row + 2 * d, ok);  // dV
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tmem_fence_after();
+    tmem_free(tmem, cols);
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsB, 1)
+    attn_bwd_q_long(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                    const int* __restrict__ cu, int H, const bf16* __restrict__ o,
+                    const bf16* __restrict__ dO, const float* __restrict__ lse,
+                    bf16* __restrict__ dqkv, int T_total) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  LongQSmem& sm = *reinterpret_cast<LongQSmem*>(align1024(raw));
+  const int b = blockIdx.x, h = blockIdx.y, qb = blockIdx.z;
+  const int row0 = cu[b], n = cu[b + 1] - row0;
+  if (128 * qb >= n) return;
+  const int nb = (n + 127) / 128;
+  constexpr uint32_t cols = 512;  // S [0,128), dP [128,256), dQ [256,320)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = H * DK;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.qg_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.freeb[s], 1);
+    }
+    mbar_init(&sm.s_done, 1);
+    mbar_init(&sm.ds_ready, 32 * kSoftWarpsB);
+    mbar_init(&sm.ds_free, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(&sm.tmem, cols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_expect_tx(&sm.qg_full, 2 * kTile);
+      tma_2d(&map_qkv, &sm.qg_full, sm.q, h * DK, row0 + 128 * qb);
+      tma_2d(&map_do, &sm.qg_full, sm.g, h * DK, row0 + 128 * qb);
+    }
+    __syncwarp();
+    for (int j = 0; j < nb; ++j) {
+      const int s = j & 1;
+      if (j >= 2) mbar_wait(&sm.freeb[s], ((j - 2) >> 1) & 1);
+      if (elect_one()) {
+        mbar_expect_tx(&sm.full[s], 2 * kTile);
+        tma_2d(&map_qkv, &sm.full[s], sm.k[s], d + h * DK, row0 + 128 * j);
+        tma_2d(&map_qkv, &sm.full[s], sm.v[s], 2 * d + h * DK, row0 + 128 * j);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    mbar_wait(&sm.qg_full, 0);
+    const uint32_t tq = smem_u32(sm.q), tdo = smem_u32(sm.g), tds = smem_u32(sm.ds);
+    for (int j = 0; j < nb; ++j) {
+      const int s = j & 1;
+      mbar_wait(&sm.full[s], (j >> 1) & 1);
+      tmem_fence_after();
+      const uint32_t tk = smem_u32(sm.k[s]), tv = smem_u32(sm.v[s]);
+      if (elect_one()) {
+        const uint32_t id = idesc(128, 0, 0);
+#pragma unroll
+        for (int kk = 0; kk < DK / 16; ++kk) {
+          umma_bf16(tmem, kmaj(tq) + 2 * kk, kmaj(tk) + 2 * kk, id, kk > 0);         // S
+          umma_bf16(tmem + 128, kmaj(tdo) + 2 * kk, kmaj(tv) + 2 * kk, id, kk > 0);  // dP
+        }
+        umma_commit(&sm.s_done);
+      }
+      __syncwarp();
+      mbar_wait(&sm.ds_ready, j & 1);
+      tmem_fence_after();
+      if (elect_one()) {
+        const uint32_t id_q = idesc(64, 0, 1);
+#pragma unroll
+        for (int kk = 0; kk < NQ / 16; ++kk)
+          umma_bf16(tmem + 256, kmaj2(tds, kk, kTile), mnmaj(tk) + kk * (2048 >> 4), id_q,
+                    (j > 0 || kk > 0) ? 1 : 0);  // dQ += dS K
+        umma_commit(&sm.freeb[s]);
+        umma_commit(&sm.ds_free);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int r = 32 * quarter + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
+    const float scale = rsqrtf(static_cast<float>(DK));
+    const float l2e = 1.4426950408889634f;
+    const int q = 128 * qb + r;
+    const bool rok = q < n;
+    float Dr = 0.f, lr = 0.f;
+    if (rok) {
+      Dr = row_dot_do(o + (int64_t)(row0 + q) * d + h * DK, dO + (int64_t)(row0 + q) * d + h * DK);
+      lr = lse[(int64_t)h * T_total + row0 + q];
+    }
+    for (int j = 0; j < nb; ++j) {
+      mbar_wait(&sm.s_done, j & 1);
+      if (j > 0) mbar_wait(&sm.ds_free, (j - 1) & 1);
+      tmem_fence_after();
+      long_bwd_rows(trow, half, r, 128 * j, n, rok, scale * l2e, -lr * l2e, Dr, scale, 0u,
+                    smem_u32(sm.ds));
+      fence_async_smem();
+      tmem_fence_before();
+      mbar_arrive(&sm.ds_ready);
+    }
+    mbar_wait(&sm.ds_free, (nb - 1) & 1);
+    tmem_fence_after();
+    bf16* row = dqkv + (int64_t)(row0 + q) * 3 * d + h * DK + 32 * half;
+    tmem_row32_to_global(trow + 256 + 32 * half, 1.f, row, rok);  // dQ
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tmem_fence_after();
+    tmem_free(tmem, cols);
+  }
+}
+
 }  // namespace attn_tc
 
 bool attention_tc_supported(int dk, int max_seq) { return dk == attn_tc::DK && max_seq <= attn_tc::NQ; }
+bool attention_long_supported(int dk, int max_seq) {
+  return dk == attn_tc::DK && max_seq <= attn_tc::NQ * attn_tc::kMaxKB;
+}
 
 static unsigned long long* g_attn_trace = nullptr;
 void attention_tc_set_trace(unsigned long long* buf) { g_attn_trace = buf; }
@@ -517,4 +990,51 @@ void attention_bwd_tc(const DevBatch& b, int H, const void* qkv, const void* o, 
   count_launch();
 }
 
+}  // namespace hp
+
+namespace hp {
+void attention_fwd_long(const DevBatch& b, int H, int max_seq, const void* qkv, void* o, float* lse,
+                        cudaStream_t s) {
+  if (b.B == 0) return;
+  const int d = H * attn_tc::DK;
+  const CUtensorMap mq = act_map(qkv, b.T, 3 * d);
+  const int sm = static_cast<int>(sizeof(attn_tc::LongFwdSmem)) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_fwd_long, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    attr = true;
+  }
+  const int nblk = (max_seq + attn_tc::NQ - 1) / attn_tc::NQ;
+  attn_tc::attn_fwd_long<<<dim3(b.B, H, nblk), attn_tc::kThreadsF, sm, s>>>(
+      mq, b.cu, H, static_cast<attn_tc::bf16*>(o), lse, b.T);
+  HP_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void attention_bwd_long(const DevBatch& b, int H, int max_seq, const void* qkv, const void* o,
+                        const void* dO, const float* lse, void* dqkv, cudaStream_t s) {
+  if (b.B == 0) return;
+  const int d = H * attn_tc::DK;
+  const CUtensorMap mq = act_map(qkv, b.T, 3 * d);
+  const CUtensorMap mg = act_map(dO, b.T, d);
+  const int smkv = static_cast<int>(sizeof(attn_tc::LongKvSmem)) + 1024;
+  const int smq = static_cast<int>(sizeof(attn_tc::LongQSmem)) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_kv_long, cudaFuncAttributeMaxDynamicSharedMemorySize, smkv));
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_q_long, cudaFuncAttributeMaxDynamicSharedMemorySize, smq));
+    attr = true;
+  }
+  const int nblk = (max_seq + attn_tc::NQ - 1) / attn_tc::NQ;
+  const auto* ob = static_cast<const attn_tc::bf16*>(o);
+  const auto* gb = static_cast<const attn_tc::bf16*>(dO);
+  auto* out = static_cast<attn_tc::bf16*>(dqkv);
+  attn_tc::attn_bwd_kv_long<<<dim3(b.B, H, nblk), attn_tc::kThreadsB, smkv, s>>>(mq, mg, b.cu, H, ob, gb,
+                                                                              lse, out, b.T);
+  HP_CUDA(cudaGetLastError());
+  attn_tc::attn_bwd_q_long<<<dim3(b.B, H, nblk), attn_tc::kThreadsB, smq, s>>>(mq, mg, b.cu, H, ob, gb,
+                                                                            lse, out, b.T);
+  HP_CUDA(cudaGetLastError());
+  count_launch(2);
+}
 }  // namespace hp

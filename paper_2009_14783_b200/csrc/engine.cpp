@@ -66,8 +66,10 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   if (x_.update_freq == 0) fail(HP_ECONFIG, "update_freq must be >= 1");
   if (x_.max_tokens == 0 || x_.max_batch == 0)
     fail(HP_ECONFIG, "exec capacities max_tokens/max_batch must be > 0");
-  if (m_.max_seq > static_cast<uint64_t>(kAttnMaxSeq))
-    fail(HP_ECONFIG, "max_seq > 128 is not supported by the attention kernel yet");
+  if (m_.max_seq > static_cast<uint64_t>(kAttnMaxSeq) &&
+      !(x_.compute == HP_COMPUTE_BF16 && m_.heads > 0 && m_.d_model / m_.heads == 64 &&
+        m_.max_seq <= 512))
+    fail(HP_ECONFIG, "max_seq > 128 needs the bf16 path with d_model / heads == 64 (max 512)");
   if (o_.kind != HP_OPT_ADAM && o_.kind != HP_OPT_SGD) fail(HP_ECONFIG, "unknown optimizer kind");
   if (x_.policy != HP_POLICY_SENTENCES && x_.policy != HP_POLICY_TOKENS)
     fail(HP_ECONFIG, "unknown weight policy");
@@ -218,6 +220,8 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     // the mma.sync kernels, for A/B comparisons)
     const char* a = std::getenv("HP_ATTN");
     attn_tc_ = bf16_ && attention_tc_supported(dk_, (int)m_.max_seq) && !(a && std::string(a) == "mma");
+    attn_long_ = bf16_ && !attention_tc_supported(dk_, (int)m_.max_seq) &&
+                 attention_long_supported(dk_, (int)m_.max_seq);
   }
   // staged batch block (fixed layout at capacity)
   const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch,
@@ -719,7 +723,9 @@ void Engine::forward(bool need_grad) {
     q.c = y.qkv; q.ldc = 3 * d_; q.ct = at_;
     gemm_t(q);
     tstart(TM_ATTN);
-    if (attn_tc_)
+    if (attn_long_)
+      attention_fwd_long(b, H_, (int)m_.max_seq, y.qkv, y.o, y.lse, s_main_);
+    else if (attn_tc_)
       attention_fwd_tc(b, H_, y.qkv, y.o, y.lse, s_main_);
     else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
       attention_fwd_mma(b, H_, y.qkv, y.o, y.lse, s_main_);
@@ -979,7 +985,9 @@ void Engine::backward() {
     gemm_t(dO);
     if (bert_ && l + 1 < L_) wait_wg(ev_wq_[l + 1]);  // dqkv_ reused: layer l+1's d(wqkv) read it
     tstart(TM_ATTN);
-    if (attn_tc_)
+    if (attn_long_)
+      attention_bwd_long(b, H_, (int)m_.max_seq, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
+    else if (attn_tc_)
       attention_bwd_tc(b, H_, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
     else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
       attention_bwd_mma(b, H_, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);

@@ -167,6 +167,7 @@ class Engine {
   bool have_premul_ = false;
 
   bool capture_ = false;
+  bool attn_long_ = false;  // 128 < max_seq <= 512: attention_*_long
   bool grad_comm_ = true;  // measurement toggle (hp_engine_set_grad_comm)
   float* local_grads_ = nullptr;
   uint64_t step_ = 0, adam_t_ = 0;

@@ -138,6 +138,13 @@ void attention_fwd_tc(const DevBatch& b, int H, const void* qkv, void* o, float*
                       cudaStream_t s);
 void attention_bwd_tc(const DevBatch& b, int H, const void* qkv, const void* o, const void* dO,
                       const float* lse, void* dqkv, cudaStream_t s);
+// tcgen05 attention for 128 < seq <= 512 (attn_tc.cu, C4): 128-row query /
+// key blocks; forward, then backward as a dK/dV kernel and a dQ kernel
+bool attention_long_supported(int dk, int max_seq);
+void attention_fwd_long(const DevBatch& b, int H, int max_seq, const void* qkv, void* o, float* lse,
+                        cudaStream_t s);
+void attention_bwd_long(const DevBatch& b, int H, int max_seq, const void* qkv, const void* o,
+                        const void* dO, const float* lse, void* dqkv, cudaStream_t s);
 
 // rows of src selected by idx -> dst (dst[r] = src[idx[r]]); idx < 0 marks a
 // padding row (zeros here, skipped by the scatters, no loss in ls_ce).

@@ -180,6 +180,66 @@ def test_bert_extension_bf16_tcgen05_path():
     assert losses[-1] < losses[0]
 
 
+def _long_spec(max_seq=512):
+    kw = dict(arch="bert_encoder", d_model=128, heads=2, vocab=203, max_seq=max_seq, layers=1,
+              d_ff=256, label_smooth_eps=0.1)
+    return hp.ModelSpec(**kw), mo.Spec(**kw)
+
+
+def _check_long(spec, ospec, batch, oinst):
+    eng = hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(compute="bf16", max_tokens=4096,
+                                                               max_batch=16, max_masks=1024), seed=9)
+    eng.set_capture(True)
+    rep = eng.round(batch, lr=0.0)
+    g = eng.local_grads()
+    l, w, og = mo.forward_backward(ospec, mo.init_parameters(ospec, 9), oinst)
+    assert abs(rep.local_loss_sum - l) <= 2e-2 * abs(l)
+    assert rel_norm(g, og) <= 5e-2
+    # every attention block on its own: a wrong dQ / dK / dV shows up here even
+    # when the embedding / head gradients dominate the flat norm
+    for p in hp.param_shapes(spec):
+        if p.name.startswith("layer0.w"):
+            sl = slice(p.offset, p.offset + p.size)
+            assert rel_norm(g[sl], og[sl]) <= 5e-2, p.name
+    eng.close()
+
+
+def test_bert_long_sequences_tcgen05():
+    """128 < seq <= 512 (C4's sequence length): the blocked tcgen05 attention
+    (forward, dK/dV and dQ kernels) against the f64 oracle, with instances of
+    every block count (<= 128, two, three and four 128-row blocks)."""
+    spec, ospec = _long_spec()
+    rec = hp.generate_mlm_records(hp.MlmGenConfig(n=24, vocab=203, min_sentence_words=20,
+                                                  max_sentence_words=255, seed=4,
+                                                  max_seq_tokens=512))
+    ids = [3, 12, 2, 9, 16, 21, 1, 5]  # lengths 99, 153, 274, 409, 484, 97, 446, 218
+    assert sorted(int(rec.token_lengths()[i]) for i in ids) == [97, 99, 153, 218, 274, 409, 446, 484]
+    _check_long(spec, ospec, rec.batch(ids), _oracle_from_records(rec, ids))
+
+
+def test_bert_long_sequences_block_edges():
+    """Lengths on the 128-row block edges, up to the 512 cap."""
+    spec, ospec = _long_spec()
+    rng = np.random.default_rng(11)
+    insts, oinst = [], []
+    for n in (512, 129, 128, 257, 384, 385, 1 + 2):
+        tok = rng.integers(4, 203, n)
+        tok[0] = 0
+        seg = (np.arange(n) >= n // 2).astype(np.int64)
+        mp = np.sort(rng.choice(np.arange(1, n), size=max(1, n // 7), replace=False))
+        mo_ = rng.integers(4, 203, len(mp))
+        insts.append(hp.Instance(tok, seg, mp, mo_, int(n % 2)))
+        oinst.append(mo.Instance(tok, seg, mp, mo_, int(n % 2)))
+    _check_long(spec, ospec, hp.pack_batch(insts), oinst)
+
+
+def test_long_sequences_need_the_bf16_path():
+    spec, _ = _long_spec()
+    with pytest.raises(hp.ConfigError):
+        hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(compute="f32", max_tokens=1024,
+                                                              max_batch=4, max_masks=64), seed=1)
+
+
 def _graph_run(monkeypatch, graphs, make_engine, batches, lrs):
     monkeypatch.setenv("HP_GRAPHS", "1" if graphs else "0")
     eng = make_engine()
