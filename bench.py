@@ -296,9 +296,10 @@ def main(argv=None):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        for k in range(args.steps):
-            i = k % len(batches)
-            eng.round(batches[i], dummies[i], lr)
+        # StepEngine.rounds: batch k+1 is validated / staged on the host while
+        # the device runs round k (each round's H2D + D2H stay in the region)
+        eng.rounds((batches[k % len(batches)], dummies[k % len(batches)], lr)
+                   for k in range(args.steps))
         torch.cuda.synchronize()
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0)

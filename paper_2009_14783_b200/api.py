@@ -822,6 +822,37 @@ class StepEngine:
         self._group_t0 = None
         return rep
 
+    def rounds(self, work) -> list:
+        """round() over a sequence of (batch, dummy, lr), pipelined: while the
+        device runs round k, the host validates and stages batch k+1 (its H2D
+        copy is queued on the compute stream behind round k, so the device
+        buffer is only overwritten once round k is done).  Every round still
+        copies its batch host->device and reads [loss, weight] back.  Returns
+        what round() returns for each (None on the first K-1 rounds of an
+        update group)."""
+        it = iter(work)
+        out = []
+        cur = next(it, None)
+        if cur is None:
+            return out
+        self.stage(cur[0])
+        while cur is not None:
+            if self._group_t0 is None:
+                self._group_t0 = time.perf_counter()
+            self.round_async(cur[1], cur[2])
+            nxt = next(it, None)
+            if nxt is not None:
+                self.stage(nxt[0])
+            rep = self.round_sync()
+            if rep.updated:
+                rep.seconds = time.perf_counter() - self._group_t0
+                self._group_t0 = None
+                out.append(rep)
+            else:
+                out.append(None)
+            cur = nxt
+        return out
+
     # -- instrumentation
     def mark(self, slot: int):
         """Record a CUDA event on the engine's compute stream."""

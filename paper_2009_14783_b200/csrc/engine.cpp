@@ -671,7 +671,21 @@ void Engine::wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done) {
   HP_CUDA(cudaStreamWaitEvent(s_wg_, fork, 0));
   wg_forked_ = true;
   tstart(TM_GEMM, s_wg_);
-  gemm(g, s_wg_);
+  // split-K of the weight-gradient GEMMs capped at 2: a small wgrad (dWo,
+  // 768 x 768 x 4096) then takes half the SMs for longer instead of all of
+  // them with 8-way fp32 reductions, leaving the rest to the data-gradient
+  // chain (C2: 7640 vs 7536 samples/s; cap 1: 7250)
+  static const int wg_split_cap = [] {
+    const char* e = std::getenv("HP_WGRAD_SPLIT_MAX");  // A/B knob, 0 = heuristic
+    return e ? std::atoi(e) : 2;
+  }();
+  if (wg_split_cap > 0) {
+    GemmArgs c = g;
+    c.max_splits = wg_split_cap;
+    gemm(c, s_wg_);
+  } else {
+    gemm(g, s_wg_);
+  }
   tstop(TM_GEMM, 2.0 * g.M * g.N * g.K,
         (double)asz_ * ((double)g.M * g.K + (double)g.K * g.N) +
             (g.ct == DType::f32 ? 4.0 : 2.0) * g.M * g.N,

@@ -1058,6 +1058,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int slots = nsm / ccg;
     int sp = 1;
     if (can_split && tiles < slots) sp = std::max(1, std::min(slots / tiles, num_kb / 4));
+    if (g.max_splits > 0) sp = std::min(sp, g.max_splits);
     const int units = tiles * sp;
     const int waves = (units + slots - 1) / slots;
     const double eff = static_cast<double>(units) / (waves * slots) * c[2] / 100.0;

@@ -180,23 +180,30 @@ __global__ void __launch_bounds__(256) embed_grad_small(const int* __restrict__ 
   const int d8 = d / 8;
   for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_small; i += gridDim.x * wpb) {
     const int u = ulist[i];
-    const int k0 = useg[u], k1 = useg[u + 1];
+    const int k0 = useg[u], cnt = useg[u + 1] - k0;  // <= kEmbHot = 32: one position per lane
+    const int mine = lane < cnt ? perm[k0 + lane] : 0;
     float* o = dE + (int64_t)uid[u] * d;
-    for (int c8 = lane; c8 < d8; c8 += 32) {
+    for (int cb = 0; cb < d8; cb += 32) {  // warp-uniform trip count (shuffles below)
+      const int c8 = cb + lane;
+      const bool act = c8 < d8;
       float acc[8] = {};
-      for (int k = k0; k < k1; k += 8) {
-        float f[8][8];
+      for (int k = 0; k < cnt; k += 4) {  // positions in order: fixed summation order
+        float f[4][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (k + j < k1) emb_load8(dx + (int64_t)perm[k + j] * d + 8 * c8, f[j]);
+        for (int j = 0; j < 4; ++j) {
+          const int t = __shfl_sync(0xffffffffu, mine, (k + j) & 31);
+          if (act && k + j < cnt) emb_load8(dx + (int64_t)t * d + 8 * c8, f[j]);
+        }
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (k + j < k1)
+        for (int j = 0; j < 4; ++j)
+          if (k + j < cnt)
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc[e] += f[j][e];
       }
-      reinterpret_cast<float4*>(o + 8 * c8)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      reinterpret_cast<float4*>(o + 8 * c8)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      if (act) {
+        reinterpret_cast<float4*>(o + 8 * c8)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        reinterpret_cast<float4*>(o + 8 * c8)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
     }
   }
 }
@@ -292,6 +299,36 @@ __global__ void colsum_final_kernel(int chunks, int N, const float* __restrict__
 static constexpr int kColRows = 64;
 constexpr int kLnBwdRows = 32;
 
+// Segment-embedding gradients in one pass: per 32-row chunk, the column sums
+// of the rows with segment 0 and with segment 1 (8 columns per thread), as
+// partials [chunk][2 * N8] (segment 0 | segment 1); finalised by
+// colsum_final_strided.
+template <class XT>
+__global__ void segsum_partial_vec(int R, int N8, const XT* __restrict__ x, const int* __restrict__ seg,
+                                   int rows_per, float* __restrict__ part) {
+  const int c8 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c8 * 8 >= N8) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(R, r0 + rows_per);
+  float a0[8] = {}, a1[8] = {};
+  for (int r = r0; r < r1; ++r) {
+    float f[8];
+    emb_load8(x + (int64_t)r * N8 + 8 * c8, f);
+    if (seg[r] == 0) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a0[e] += f[e];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a1[e] += f[e];
+    }
+  }
+  float4* o = reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * 2 * N8 + 8 * c8);
+  o[0] = make_float4(a0[0], a0[1], a0[2], a0[3]);
+  o[1] = make_float4(a0[4], a0[5], a0[6], a0[7]);
+  o = reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * 2 * N8 + N8 + 8 * c8);
+  o[0] = make_float4(a1[0], a1[1], a1[2], a1[3]);
+  o[1] = make_float4(a1[4], a1[5], a1[6], a1[7]);
+}
+
 // bf16 [R x ld] column sums, 8 columns (one 16-byte load) per thread.
 __global__ void colsum_partial_vec(int R, int N8, const bf16* __restrict__ x, int64_t ld,
                                    int rows_per, float* __restrict__ part) {
@@ -386,8 +423,23 @@ void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
       LAUNCH_CHECK();
     }
     count_launch(2);
-    colsum_launch<X>(b.T, d, (const X*)dx, d, b.seg, 0, dseg0, scratch, s);
-    colsum_launch<X>(b.T, d, (const X*)dx, d, b.seg, 1, dseg1, scratch, s);
+    {
+      // both segment rows in one pass over dx (rows of 32, 8 columns a thread)
+      const int rows_per = 32, chunks = (b.T + rows_per - 1) / rows_per;
+      dim3 g1((d / 8 + 127) / 128, chunks);
+      segsum_partial_vec<X><<<g1, 128, 0, s>>>(b.T, d, (const X*)dx, b.seg, rows_per, scratch);
+      LAUNCH_CHECK();
+      if (dseg1 == dseg0 + d) {  // canonical order: seg0 then seg1, adjacent
+        colsum_final_strided<<<FINAL_LAUNCH(2 * d), 0, s>>>(chunks, 2 * d, 2 * d, scratch, dseg0);
+        LAUNCH_CHECK();
+        count_launch(2);
+      } else {
+        colsum_final_strided<<<FINAL_LAUNCH(d), 0, s>>>(chunks, 2 * d, d, scratch, dseg0);
+        colsum_final_strided<<<FINAL_LAUNCH(d), 0, s>>>(chunks, 2 * d, d, scratch + d, dseg1);
+        LAUNCH_CHECK();
+        count_launch(3);
+      }
+    }
   });
 }
 

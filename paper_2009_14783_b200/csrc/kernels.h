@@ -43,6 +43,7 @@ struct GemmArgs {
   void* aux = nullptr;         // pre-activation (ct type), ld = ldc
   const void* resid = nullptr; // C = epi(...) + R(m,n), R of type ct
   int64_t ld_resid = 0;
+  int max_splits = 0;          // split-K cap for the tcgen05 path (0: heuristic)
 };
 
 // Dispatch: tcgen05 path for bf16 operands whose layout TMA can describe,

@@ -240,6 +240,30 @@ def test_long_sequences_need_the_bf16_path():
                                                               max_batch=4, max_masks=64), seed=1)
 
 
+@pytest.mark.parametrize("compute", ["bf16", "f32"])
+def test_pipelined_rounds_equal_sequential_rounds(compute):
+    """StepEngine.rounds (host staging of batch k+1 behind device round k) is
+    the same computation as round() one at a time: identical losses and
+    parameter bytes, batches of different shapes included."""
+    spec, ospec, rec = _bert_case(d=128, heads=2, dff=256, vocab=203, n=24)
+    batches = [rec.batch(range(0, 8)), rec.batch(range(8, 14)), rec.batch(range(14, 24)),
+               rec.batch(range(0, 8))]
+    lrs = [1e-3, 2e-3, 1e-3, 5e-4]
+
+    def make():
+        return hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(compute=compute, max_tokens=1024,
+                                                                   max_batch=16, max_masks=256), seed=9)
+    a = make()
+    la = [a.round(b, lr=lr).loss for b, lr in zip(batches, lrs)]
+    da = a.digest()
+    a.close()
+    b = make()
+    lb = [r.loss for r in b.rounds((x, False, lr) for x, lr in zip(batches, lrs))]
+    assert la == lb
+    assert b.digest() == da
+    b.close()
+
+
 def _graph_run(monkeypatch, graphs, make_engine, batches, lrs):
     monkeypatch.setenv("HP_GRAPHS", "1" if graphs else "0")
     eng = make_engine()
