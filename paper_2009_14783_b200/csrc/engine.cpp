@@ -325,8 +325,14 @@ Engine::~Engine() {
   if (s_main_) cudaStreamSynchronize(s_main_);
   if (s_comm_) cudaStreamSynchronize(s_comm_);
   if (s_upd_) cudaStreamSynchronize(s_upd_);
-  for (auto& kv : graphs_)
+  for (auto& kv : graphs_) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& gt : kv.second.timers)
+      for (auto& pr : gt.ev) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+      }
+  }
   if (have_premul_ && comm_) ncclRedOpDestroy(premul_, comm_->nccl);
   for (auto& t : tm_)
     for (auto& pr : t.ev) {
@@ -588,6 +594,7 @@ void Engine::stage_batch(const hp_batch& b) {
 
 // ------------------------------------------------------------------ timers
 void Engine::timers(bool on) {
+  if (timed_pending_) collect_timed();
   timers_on_ = on;
   for (auto& t : tm_) {
     t.used = 0;
@@ -624,22 +631,45 @@ void Engine::tstart(int cls, cudaStream_t st) {
     HP_CUDA(cudaEventCreate(&b));
     t.ev.emplace_back(a, b);
   }
-  HP_CUDA(cudaEventRecord(t.ev[t.used].first, st ? st : s_main_));
+  HP_CUDA(cudaEventRecordWithFlags(t.ev[t.used].first, st ? st : s_main_,
+                                  capturing_ ? cudaEventRecordExternal : cudaEventRecordDefault));
 }
 void Engine::tstop(int cls, double flops, double bytes, cudaStream_t st) {
   if (!timers_on_) return;
   TimerAcc& t = tm_[cls];
-  HP_CUDA(cudaEventRecord(t.ev[t.used].second, st ? st : s_main_));
+  HP_CUDA(cudaEventRecordWithFlags(t.ev[t.used].second, st ? st : s_main_,
+                                  capturing_ ? cudaEventRecordExternal : cudaEventRecordDefault));
   ++t.used;
   t.flops += flops;
   t.bytes += bytes;
   ++t.launches;
 }
+// Event spans of a timed graph replay (graph nodes: no host launch gaps in
+// the spans) -> the class accumulators.
+void Engine::collect_timed() {
+  GraphEntry* e = timed_pending_;
+  timed_pending_ = nullptr;
+  HP_CUDA(cudaEventSynchronize(ev_done_));
+  for (int c = 0; c < TM_COUNT; ++c) {
+    TimerAcc& t = tm_[c];
+    const GraphTimers& gt = e->timers[c];
+    for (const auto& pr : gt.ev) {
+      float ms = 0;
+      HP_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      t.ms += ms;
+    }
+    t.flops += gt.flops;
+    t.bytes += gt.bytes;
+    t.launches += gt.launches;
+  }
+}
+
 void Engine::timer_read(int which, std::string* name, double* ms, uint64_t* launches,
                         double* bytes, double* flops) {
   static const char* names[TM_COUNT] = {"gemm", "attention", "layernorm", "heads", "adam", "embedding"};
   if (which < 0 || which >= TM_COUNT) fail(HP_EINDEX, "timer index out of range");
   HP_CUDA(cudaStreamSynchronize(s_main_));
+  if (timed_pending_) collect_timed();
   TimerAcc& t = tm_[which];
   for (size_t i = 0; i < t.used; ++i) {
     float e = 0;
@@ -694,6 +724,9 @@ void Engine::wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done) {
   serialize_if_timed(s_wg_);
 }
 
+// (timer events are recorded with cudaEventRecordExternal: under stream
+// capture they become event-record nodes whose timestamps can be read after
+// each replay, instead of capture-internal dependencies)
 // Timer passes serialise the side streams into the compute stream, so each
 // kernel's event span is its own duration, not a share of concurrent work.
 void Engine::serialize_if_timed(cudaStream_t st) {
@@ -1097,32 +1130,67 @@ void Engine::round_async(int dummy, double lr) {
   const float hyper[4] = {a.lr, a.c1, a.c2, 0.f};
   HP_CUDA(cudaMemcpyAsync(d_hyper_, hyper, sizeof(hyper), cudaMemcpyHostToDevice, s_main_));
 
-  if (graphs_on_ && !timers_on_ && !capture_) {
+  // a timed graph's events are re-recorded by every replay: read the previous
+  // replay's before launching the next
+  if (timed_pending_) collect_timed();
+  if (graphs_on_ && !capture_) {
     GraphEntry& e = graphs_[std::make_tuple(batch_.T, batch_.B, batch_.M,
-                                           (dummy ? 1 : 0) | (phase_ << 1) | (grad_comm_ ? 0 : 8))];
+                                           (dummy ? 1 : 0) | (phase_ << 1) | (grad_comm_ ? 0 : 8) |
+                                               (timers_on_ ? 16 : 0))];
     if (e.exec) {
       HP_CUDA(cudaGraphLaunch(e.exec, s_main_));
       count_launch(static_cast<int>(e.launches));
+      if (timers_on_) timed_pending_ = &e;
     } else if (e.seen++ == 0) {
       round_body(dummy);
     } else {
       const uint64_t k0 = kernel_launch_count();
+      // timer pass: the event pairs recorded during capture become graph
+      // nodes; they leave the eager pool and belong to the graph from here on
+      std::array<size_t, TM_COUNT> u0{};
+      std::array<double, TM_COUNT> f0{}, b0{};
+      std::array<uint64_t, TM_COUNT> l0{};
+      for (int c = 0; c < TM_COUNT; ++c) {
+        u0[c] = tm_[c].used;
+        f0[c] = tm_[c].flops;
+        b0[c] = tm_[c].bytes;
+        l0[c] = tm_[c].launches;
+      }
       HP_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeThreadLocal));
+      capturing_ = true;
       try {
         round_body(dummy);
       } catch (...) {
+        capturing_ = false;
         cudaGraph_t g = nullptr;
         cudaStreamEndCapture(s_main_, &g);
         if (g) cudaGraphDestroy(g);
         throw;
       }
       cudaGraph_t g = nullptr;
+      capturing_ = false;
       HP_CUDA(cudaStreamEndCapture(s_main_, &g));
       e.launches = kernel_launch_count() - k0;
       const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
       cudaGraphDestroy(g);
       if (ie != cudaSuccess) fail(HP_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+      if (timers_on_) {
+        for (int c = 0; c < TM_COUNT; ++c) {
+          TimerAcc& t = tm_[c];
+          GraphTimers& gt = e.timers[c];
+          gt.ev.assign(t.ev.begin() + u0[c], t.ev.begin() + t.used);
+          t.ev.erase(t.ev.begin() + u0[c], t.ev.begin() + t.used);
+          t.used = u0[c];
+          gt.flops = t.flops - f0[c];
+          gt.bytes = t.bytes - b0[c];
+          gt.launches = t.launches - l0[c];
+          t.flops = f0[c];  // counted when the replay's events are read
+          t.bytes = b0[c];
+          t.launches = l0[c];
+        }
+      }
       HP_CUDA(cudaGraphLaunch(e.exec, s_main_));
+      if (timers_on_) timed_pending_ = &e;
     }
   } else {
     round_body(dummy);

@@ -195,11 +195,22 @@ class Engine {
   // CUDA graphs of round_body, keyed by batch shape (T, B, padded M, dummy):
   // first sighting runs eagerly, the second is captured, later ones replay
   // (one graph launch instead of ~300 kernel launches per round).
+  // timer event pairs baked into a captured (timed) graph, per class, and the
+  // work they stand for; accumulated after every replay
+  struct GraphTimers {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    double flops = 0, bytes = 0;
+    uint64_t launches = 0;
+  };
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     uint64_t launches = 0;  // kernels inside, for kernel_launch_count()
     int seen = 0;
+    std::array<GraphTimers, TM_COUNT> timers;  // timed graphs only
   };
+  GraphEntry* timed_pending_ = nullptr;
+  bool capturing_ = false;  // inside cudaStreamBeginCapture .. EndCapture  // a timed replay whose events are unread
+  void collect_timed();
   std::map<std::tuple<int, int, int, int>, GraphEntry> graphs_;
   bool graphs_on_ = true;
   bool attn_tc_ = false;      // tcgen05 attention kernels (attn_tc.cu)

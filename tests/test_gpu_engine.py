@@ -264,6 +264,29 @@ def test_pipelined_rounds_equal_sequential_rounds(compute):
     b.close()
 
 
+def test_timer_pass_is_the_same_computation():
+    """The timer pass (event pairs captured into the round's graph) runs the
+    same kernels: identical losses and parameters to an untimed run, and every
+    class reports time for the launches it counted."""
+    spec, ospec, rec = _bert_case(d=128, heads=2, dff=256, vocab=203, n=16)
+    b = rec.batch(range(12))
+
+    def run(timed):
+        eng = hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(compute="bf16", max_tokens=512,
+                                                                   max_batch=16, max_masks=128), seed=9)
+        eng.timers(timed)
+        losses = [eng.round(b, lr=1e-3).loss for _ in range(5)]
+        t = [eng.timer(i) for i in range(6)]
+        d = eng.digest()
+        eng.close()
+        return losses, d, t
+    la, da, _ = run(False)
+    lb, db, t = run(True)
+    assert la == lb and da == db
+    g = t[0]
+    assert g["name"] == "gemm" and g["launches"] > 0 and g["ms"] > 0 and g["flops"] > 0
+
+
 def _graph_run(monkeypatch, graphs, make_engine, batches, lrs):
     monkeypatch.setenv("HP_GRAPHS", "1" if graphs else "0")
     eng = make_engine()
