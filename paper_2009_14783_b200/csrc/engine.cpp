@@ -121,6 +121,22 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   HP_CUDA(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming));
   ev_bucket_.resize(buckets_.size());
   for (auto& e : ev_bucket_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  {
+    // row-sparse word-embedding exchange: worth it when every rank's rows
+    // (max_tokens x (d + 4) floats, allgathered) are fewer bytes than the
+    // dense ring allreduce moves (2 (W-1)/W V d)
+    const char* e = std::getenv("HP_SPARSE_EMB");
+    const Bucket& last = buckets_.back();
+    const uint64_t W = comm_ ? static_cast<uint64_t>(comm_->world) : 1;
+    sparse_emb_ = W > 1 && !(e && std::string(e) == "0") && last.first_param == 0 &&
+                  last.last_param == 0 && d_ % 8 == 0 &&
+                  x_.max_tokens * (d_ + 4) * W < 2 * (W - 1) * m_.vocab * d_;
+    if (sparse_emb_) {
+      emb_cap_ = static_cast<int>(x_.max_tokens);
+      emb_rows_ = static_cast<float*>(dalloc((size_t)emb_cap_ * (d_ + 4) * 4));
+      emb_gath_ = static_cast<float*>(dalloc((size_t)W * emb_cap_ * (d_ + 4) * 4));
+    }
+  }
   ev_reduced_.resize(buckets_.size());
   for (auto& e : ev_reduced_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   {
@@ -861,9 +877,21 @@ void Engine::issue_bucket(size_t k) {
     HP_CUDA(cudaEventRecord(ev_wgb_[k], s_wg_));
     HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_wgb_[k], 0));
   }
-  if (comm_ && grad_comm_)
+  if (k + 1 == buckets_.size() && emb_sparse_round_) {
+    // word-embedding gradient: every rank's (id, row) slots, then dE[id] +=
+    // row rank by rank -- the same sum on every rank, in a fixed order
+    const size_t slot_floats = (size_t)emb_cap_ * (d_ + 4);
+    if (grad_comm_) {
+      HP_NCCL(ncclAllGather(emb_rows_, emb_gath_, slot_floats, ncclFloat, comm_->nccl, s_comm_));
+      for (int r = 0; r < comm_->world; ++r)
+        embed_rows_scatter(emb_gath_ + r * slot_floats, emb_cap_, d_, gp(0), s_comm_);
+    } else {
+      embed_rows_scatter(emb_rows_, emb_cap_, d_, gp(0), s_comm_);  // measurement pass
+    }
+  } else if (comm_ && grad_comm_) {
     HP_NCCL(ncclAllReduce(grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, ncclFloat, ncclSum,
                           comm_->nccl, s_comm_));
+  }
   if (phase_ == 1) {
     // a non-final round of K: the reduced bucket joins the accumulator
     accumulate_grad(acc_grads_ + bk.lo, grads_ + bk.lo, bk.hi - bk.lo, s_comm_);
@@ -1087,7 +1115,14 @@ void Engine::backward() {
     HP_CUDA(cudaStreamWaitEvent(s_main_, ev_emb_zero_, 0));  // zeroed on the wgrad stream
   else
     HP_CUDA(cudaMemsetAsync(gp(0), 0, sizeof(float) * table_[0].size(), s_main_));
-  embed_bwd(b, d_, dx0, at_, gp(0), gp(1), gp(2), scratch_, s_main_);
+  if (sparse_emb_ && !capture_) {
+    // the rows go to the exchange buffer; the zeroed dense gradient receives
+    // every rank's rows in issue_bucket
+    embed_bwd_rows(b, d_, dx0, at_, emb_rows_, emb_cap_, gp(1), gp(2), scratch_, s_main_);
+    emb_sparse_round_ = true;
+  } else {
+    embed_bwd(b, d_, dx0, at_, gp(0), gp(1), gp(2), scratch_, s_main_);
+  }
   tstop(TM_EMBED, 0, (double)T * d_ * (asz_ + 8));
   grads_ready(0);
   if (wg_forked_) {  // the wgrad stream joins the compute stream (graph capture needs it)
@@ -1234,6 +1269,7 @@ void Engine::round_body(int dummy) {
   final_n_ = 0;
   wg_forked_ = false;
   upd_forked_ = false;
+  emb_sparse_round_ = false;
   HP_CUDA(cudaMemsetAsync(flags_, 0, 8, s_main_));
   // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
   forward(!dummy);
@@ -1268,6 +1304,11 @@ void Engine::round_body(int dummy) {
   if (dummy) {
     // zero loss, weight and gradient (engine.hpp:141-142)
     HP_CUDA(cudaMemsetAsync(grads_, 0, n_ * 4, s_main_));
+    if (sparse_emb_ && !capture_) {
+      // every rank issues the same collectives: an empty row set (all ids -1)
+      HP_CUDA(cudaMemsetAsync(emb_rows_, 0xFF, (size_t)emb_cap_ * (d_ + 4) * 4, s_main_));
+      emb_sparse_round_ = true;
+    }
     grads_ready(0);
   } else {
     backward();

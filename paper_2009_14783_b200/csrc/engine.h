@@ -167,6 +167,13 @@ class Engine {
   bool have_premul_ = false;
 
   bool capture_ = false;
+  // N > 1, word embedding alone in the last bucket: its gradient leaves the
+  // rank row-sparse (distinct ids of the batch) -- allgather + rank-ordered
+  // scatter instead of a dense allreduce (see backward / issue_bucket)
+  bool sparse_emb_ = false, emb_sparse_round_ = false;
+  int emb_cap_ = 0;
+  float* emb_rows_ = nullptr;  // [cap][d + 4]
+  float* emb_gath_ = nullptr;  // [world][cap][d + 4]
   bool attn_long_ = false;  // 128 < max_seq <= 512: attention_*_long
   bool grad_comm_ = true;  // measurement toggle (hp_engine_set_grad_comm)
   float* local_grads_ = nullptr;

@@ -1026,6 +1026,7 @@ static void launch_ek(int cg, int bn, const CUtensorMap& ma, const CUtensorMap& 
                       const tc::Params& p, cudaStream_t s) {
   if (cg == 2) {
     if (bn == 256) launch_tc<256, 2, EK>(ma, mb, p, s);
+    else if (bn == 192) launch_tc<192, 2, EK>(ma, mb, p, s);
     else launch_tc<128, 2, EK>(ma, mb, p, s);
   } else {
     if (bn == 256) launch_tc<256, 1, EK>(ma, mb, p, s);
@@ -1047,12 +1048,17 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   // fewest bytes per FLOP, one CTA with a 128-wide tile the most.
   int bn = 256, cg = 2, splits = 1;
   double best = -1;
-  const int cands[5][3] = {{2, 256, 118}, {2, 128, 100}, {1, 256, 100}, {1, 192, 97}, {1, 128, 90}};
+  // (weights ~ FLOP per staged byte: 128 / 112 / 87 / 87 / 77 / 65)
+  const int cands[6][3] = {{2, 256, 118}, {2, 192, 112}, {2, 128, 100}, {1, 256, 100},
+                           {1, 192, 97},  {1, 128, 90}};
   for (const auto& c : cands) {
     const int ccg = c[0], cbn = c[1];
     if (g_force_cg && ccg != g_force_cg) continue;
     if (g_force_bn && cbn != g_force_bn) continue;
     if (g.b.group && !g.b.trans && (cbn / ccg) % 64) continue;
+    // a 96-column half of B per CTA: only as a K-major operand (rows of the
+    // box); an MN-major B tile is whole 64-column swizzle atoms
+    if (!g.b.trans && (cbn / ccg) % 64) continue;
     const int mt = (g.M + tc::BM * ccg - 1) / (tc::BM * ccg);
     const int tiles = mt * ((g.N + cbn - 1) / cbn);
     const int slots = nsm / ccg;

@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(256) embed_grad_small(const int* __restrict__ 
                                                         const int* __restrict__ useg,
                                                         const int* __restrict__ perm, int d,
                                                         const XT* __restrict__ dx,
-                                                        float* __restrict__ dE) {
+                                                        float* __restrict__ dE, int64_t ostride,
+                                                        int by_slot) {
   const int n_small = counts[0];
   const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
   const int d8 = d / 8;
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(256) embed_grad_small(const int* __restrict__ 
     const int u = ulist[i];
     const int k0 = useg[u], cnt = useg[u + 1] - k0;  // <= kEmbHot = 32: one position per lane
     const int mine = lane < cnt ? perm[k0 + lane] : 0;
-    float* o = dE + (int64_t)uid[u] * d;
+    float* o = dE + (int64_t)(by_slot ? u : uid[u]) * ostride;
     for (int cb = 0; cb < d8; cb += 32) {  // warp-uniform trip count (shuffles below)
       const int c8 = cb + lane;
       const bool act = c8 < d8;
@@ -215,7 +216,8 @@ __global__ void __launch_bounds__(1024) embed_grad_hot(const int* __restrict__ c
                                                        const int* __restrict__ useg,
                                                        const int* __restrict__ perm, int d,
                                                        const XT* __restrict__ dx,
-                                                       float* __restrict__ dE) {
+                                                       float* __restrict__ dE, int64_t ostride,
+                                                       int by_slot) {
   extern __shared__ float part[];  // [32 warps][d]
   const int n_small = counts[0], n_hot = counts[1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(1024) embed_grad_hot(const int* __restrict__ c
       for (int e = 0; e < 8; ++e) part[w * d + 8 * c8 + e] = acc[e];
     }
     __syncthreads();
-    float* o = dE + (int64_t)uid[u] * d;
+    float* o = dE + (int64_t)(by_slot ? u : uid[u]) * ostride;
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
       float acc = 0.f;
       for (int j = 0; j < 32; ++j) acc += part[j * d + c];
@@ -403,13 +405,61 @@ static void colsum_launch(int R, int N, const XT* x, int64_t ld, const int* sel,
   count_launch(2);
 }
 
+static void embed_bwd_impl(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
+                           int64_t ostride, int by_slot, float* dseg0, float* dseg1,
+                           float* scratch, cudaStream_t s);
+// slot ids of the row-sparse embedding gradient (embed_bwd_rows)
+__global__ void emb_slot_ids_kernel(const int* __restrict__ counts, const int* __restrict__ uid,
+                                    float* __restrict__ rows, int cap, int64_t stride) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= cap) return;
+  const int U = counts[0] + counts[1];
+  rows[(int64_t)u * stride] = __int_as_float(u < U ? uid[u] : -1);
+}
+__global__ void emb_scatter_kernel(const float* __restrict__ rows, int cap, int d,
+                                   float* __restrict__ dE) {
+  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (u >= cap) return;
+  const float* r = rows + (int64_t)u * (d + 4);
+  const int id = __float_as_int(r[0]);
+  if (id < 0) return;
+  float* o = dE + (int64_t)id * d;
+  for (int c = 4 * lane; c < d; c += 128) {
+    const float4 v = *reinterpret_cast<const float4*>(r + 4 + c);
+    float4 w = *reinterpret_cast<float4*>(o + c);
+    w.x += v.x; w.y += v.y; w.z += v.z; w.w += v.w;
+    *reinterpret_cast<float4*>(o + c) = w;
+  }
+}
+void embed_rows_scatter(const float* rows, int cap, int d, float* dE, cudaStream_t s) {
+  if (cap == 0) return;
+  if (d % 4) fail(HP_ECONFIG, "embedding rows: d_model must be a multiple of 4");
+  emb_scatter_kernel<<<(cap + 7) / 8, 256, 0, s>>>(rows, cap, d, dE);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+void embed_bwd_rows(const DevBatch& b, int d, const void* dx, DType xt, float* rows, int cap,
+                    float* dseg0, float* dseg1, float* scratch, cudaStream_t s) {
+  emb_slot_ids_kernel<<<(cap + 255) / 256, 256, 0, s>>>(b.ucount, b.uid, rows, cap, d + 4);
+  LAUNCH_CHECK();
+  count_launch();
+  embed_bwd_impl(b, d, dx, xt, rows + 4, d + 4, 1, dseg0, dseg1, scratch, s);
+}
+
 void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
                float* dseg0, float* dseg1, float* scratch, cudaStream_t s) {
+  embed_bwd_impl(b, d, dx, xt, dE, d, 0, dseg0, dseg1, scratch, s);
+}
+
+static void embed_bwd_impl(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
+                           int64_t ostride, int by_slot, float* dseg0, float* dseg1,
+                           float* scratch, cudaStream_t s) {
   if (b.T == 0) return;
   DISPATCH1(xt, X, {
     if (d % 8) fail(HP_ECONFIG, "embedding gradient: d_model must be a multiple of 8");
     embed_grad_small<X><<<148 * 4, 256, 0, s>>>(b.ucount, b.ulist, b.uid, b.useg, b.perm, d,
-                                                (const X*)dx, dE);
+                                                (const X*)dx, dE, ostride, by_slot);
     LAUNCH_CHECK();
     {
       const int sm = 32 * d * (int)sizeof(float);
@@ -419,7 +469,7 @@ void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
         set_for = sm;
       }
       embed_grad_hot<X><<<64, 1024, sm, s>>>(b.ucount, b.ulist, b.uid, b.useg, b.perm, d,
-                                             (const X*)dx, dE);
+                                             (const X*)dx, dE, ostride, by_slot);
       LAUNCH_CHECK();
     }
     count_launch(2);

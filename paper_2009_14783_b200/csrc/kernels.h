@@ -84,6 +84,15 @@ struct DevBatch {
 void embed_fwd(const DevBatch& b, int d, const void* E, const void* seg0,
                const void* seg1, DType wt, const float* pe, void* x, DType xt,
                cudaStream_t s);
+// Row-sparse form of the word-embedding gradient for the N > 1 exchange:
+// slot u of `rows` (stride d + 4 floats) = [distinct token id u as int bits,
+// 3 pad, its d gradient values]; slots [U, cap) carry id -1.  Segment
+// gradients as embed_bwd.
+void embed_bwd_rows(const DevBatch& b, int d, const void* dx, DType xt, float* rows, int cap,
+                    float* dseg0, float* dseg1, float* scratch, cudaStream_t s);
+// dE[id] += row for every slot of one rank's gathered row set (ids are
+// distinct within a set; call once per rank, in rank order)
+void embed_rows_scatter(const float* rows, int cap, int d, float* dE, cudaStream_t s);
 // dE[id] = sum of dx over the tokens with that id (dE zeroed by the caller;
 // deterministic, position order), dseg{0,1} = column sums over the segment's tokens.
 void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,

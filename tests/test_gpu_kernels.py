@@ -277,3 +277,16 @@ def test_tc_gemm_pair_and_single_edge_cases(cg, epi_kind):
     _check(res, torch.bfloat16, 256)
     res = run_gemm(256, 384, 512, torch.bfloat16, 1, 0, path=2, bn=code, c_dtype=torch.float32, c_group=64)
     _check(res, torch.bfloat16, 512)
+
+
+def test_tc_gemm_pair_192_kmajor_b(epi_kind):
+    """CTA pair with a 256 x 192 tile (96 B rows per CTA): the data-gradient
+    GEMMs with N = 768 and a K-major weight operand (dO, dX1, grouped dX)."""
+    for (M, N, K, resid) in [(4096, 768, 768, 0), (1000, 768, 3072, 1), (600, 384, 200, 0),
+                             (130, 192, 104, 1)]:
+        res = run_gemm(M, N, K, torch.bfloat16, 0, 1, path=2, bn=2192, resid=bool(resid))
+        _check(res, torch.bfloat16, K)
+    res = run_gemm(512, 768, 2304, torch.bfloat16, 0, 1, path=2, bn=2192, group=64, resid=True)
+    _check(res, torch.bfloat16, 2304)
+    res = run_gemm(512, 768, 768, torch.bfloat16, 0, 1, path=2, bn=2192, c_dtype=torch.float32)
+    _check(res, torch.bfloat16, 768)

@@ -141,3 +141,66 @@ def test_process_group_over_tcp_rendezvous(tmp_path):
     t = golden("c1_ref_train.npz")
     assert np.max(np.abs(np.array(r0["losses"]) - t["losses_f64"][:3]) / np.abs(t["losses_f64"][:3])) <= 1e-4
     assert r0["losses"] == r1["losses"] and r0["digest"] == r1["digest"]
+
+
+SPARSE_WORKER = r'''
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.environ["HP_ROOT"]); sys.path.insert(0, os.path.join(os.environ["HP_ROOT"], "tests"))
+import torch, torch.distributed as dist
+import paper_2009_14783_b200 as hp
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+torch.cuda.set_device(rank)
+comm = hp.Communicator(world, rank, rank)
+spec = hp.ModelSpec(arch="bert_encoder", d_model=128, heads=2, vocab=4000, max_seq=64, layers=1,
+                    d_ff=256, label_smooth_eps=0.1)
+rec = hp.generate_mlm_records(hp.MlmGenConfig(n=64, vocab=4000, min_sentence_words=10,
+                                              max_sentence_words=30, seed=3, max_seq_tokens=64))
+plan = hp.build_epoch_batches(rec.token_lengths(), 8, 0, 21, 0)
+sched = hp.partition_for_rank(plan, world, rank)
+out = {}
+for mode in ("1", "0"):
+    os.environ["HP_SPARSE_EMB"] = mode
+    eng = hp.StepEngine(spec, hp.OptimConfig("adam", 0.9, 0.98, 1e-9),
+                        hp.ExecConfig(compute="f32", device=rank, max_tokens=512, max_batch=8,
+                                      max_masks=128, bucket_mb=0.5),
+                        comm=comm, seed=21 if rank == 0 else None)
+    eng.broadcast_params(0)
+    losses = []
+    for s in range(4):
+        rb = sched[s]
+        losses.append(eng.round(rec.batch(plan.batches[rb.batch_index]), rb.dummy, 1e-3).loss)
+    # a round where rank 1 is a dummy (empty row set on that rank)
+    losses.append(eng.round(rec.batch(plan.batches[0]), rank == 1, 1e-3).loss)
+    out[mode] = {"losses": losses, "digest": eng.digest()}
+    if rank == 0:
+        np.save(os.environ["HP_OUT"] + f"/p{mode}.npy", eng.get_params())
+    eng.close()
+with open(os.environ["HP_OUT"] + f"/sp{rank}.json", "w") as f:
+    json.dump(out, f)
+comm.close()
+dist.destroy_process_group()
+'''
+
+
+def test_row_sparse_embedding_exchange_matches_dense(tmp_path):
+    """N > 1 with the word embedding alone in the last bucket: the row-sparse
+    exchange (allgather of (id, row) slots, rank-ordered scatter) trains like
+    the dense allreduce (fp32 summation order aside), identical on every rank,
+    dummy rounds included."""
+    script = tmp_path / "sparse_worker.py"
+    script.write_text(SPARSE_WORKER)
+    env = dict(os.environ, HP_ROOT=ROOT, HP_OUT=str(tmp_path))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29519", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    r0 = json.loads((tmp_path / "sp0.json").read_text())
+    r1 = json.loads((tmp_path / "sp1.json").read_text())
+    for mode in ("1", "0"):
+        assert r0[mode]["losses"] == r1[mode]["losses"]
+        assert r0[mode]["digest"] == r1[mode]["digest"]
+    a, b = np.array(r0["1"]["losses"]), np.array(r0["0"]["losses"])
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5
+    assert rel_norm(np.load(tmp_path / "p1.npy"), np.load(tmp_path / "p0.npy")) <= 1e-5
