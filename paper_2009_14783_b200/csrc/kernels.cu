@@ -1521,101 +1521,109 @@ __global__ void __launch_bounds__(256, 6) adam_kernel(const AdamArgs a0) {
     a.c1 = a.hyper[1];
     a.c2 = a.hyper[2];
   }
-  const uint64_t* it = a.items + 5 * blockIdx.x;
-  const uint64_t lo = it[0], n = it[1], slo = it[2], cols = it[3], pcols = it[4];
   const bool scale = a.inv_w64 != nullptr;
   const double sc = scale ? *a.inv_w64 : 1.0;
   bf16* sh = (bf16*)a.shadow;
-  const bool contig = cols == pcols;
-  auto sidx = [&](uint64_t local) {
-    return contig ? slo + local : slo + (local / cols) * pcols + local % cols;
-  };
   int bad = 0;
-  if ((lo & 3) == 0 && (!sh || !contig || (slo & 3) == 0)) {
-    const uint64_t n4 = n & ~uint64_t(3);
-    for (uint64_t i = 4 * threadIdx.x; i < n4; i += 4 * blockDim.x) {
-      float4 p = *reinterpret_cast<const float4*>(a.p + lo + i);
-      float4 m = *reinterpret_cast<const float4*>(a.m + lo + i);
-      float4 v = *reinterpret_cast<const float4*>(a.v + lo + i);
-      float4 g = *reinterpret_cast<const float4*>(a.g + lo + i);
-      float* pp = &p.x; float* mm = &m.x; float* vv = &v.x; const float* gg = &g.x;
-      // g /= total weight in f64, then cast to T (engine.hpp:151, optim.hpp:135)
-      float gs[4];
-      if constexpr (ACC) {  // K > 1: earlier rounds' sums, consumed (zeroed) here
-        const float4 q = *reinterpret_cast<const float4*>(a.g2 + lo + i);
-        *reinterpret_cast<float4*>(a.g2 + lo + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float* qq = &q.x;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double gd = (double)gg[e] + (double)qq[e];
-          gs[e] = scale ? (float)(gd * sc) : (float)gd;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) gs[e] = scale ? (float)((double)gg[e] * sc) : gg[e];
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float ge = gs[e];
-        if (!isfinite(ge)) { bad = 1; continue; }
-        adam_one(a, pp[e], mm[e], vv[e], ge);
-      }
-      *reinterpret_cast<float4*>(a.p + lo + i) = p;
-      *reinterpret_cast<float4*>(a.m + lo + i) = m;
-      *reinterpret_cast<float4*>(a.v + lo + i) = v;
-      if (sh) {
-        if (contig) {
-          __nv_bfloat162 h0 = __floats2bfloat162_rn(p.x, p.y), h1 = __floats2bfloat162_rn(p.z, p.w);
-          uint2 u;
-          u.x = *reinterpret_cast<uint32_t*>(&h0);
-          u.y = *reinterpret_cast<uint32_t*>(&h1);
-          *reinterpret_cast<uint2*>(sh + slo + i) = u;
+  // grid-stride over the work items (the grid may be capped: HP_ADAM_GRID)
+  for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+    const uint64_t* it = a.items + 5 * (uint64_t)item;
+    const uint64_t lo = it[0], n = it[1], slo = it[2], cols = it[3], pcols = it[4];
+    const bool contig = cols == pcols;
+    auto sidx = [&](uint64_t local) {
+      return contig ? slo + local : slo + (local / cols) * pcols + local % cols;
+    };
+    if ((lo & 3) == 0 && (!sh || !contig || (slo & 3) == 0)) {
+      const uint64_t n4 = n & ~uint64_t(3);
+      for (uint64_t i = 4 * threadIdx.x; i < n4; i += 4 * blockDim.x) {
+        float4 p = *reinterpret_cast<const float4*>(a.p + lo + i);
+        float4 m = *reinterpret_cast<const float4*>(a.m + lo + i);
+        float4 v = *reinterpret_cast<const float4*>(a.v + lo + i);
+        float4 g = *reinterpret_cast<const float4*>(a.g + lo + i);
+        float* pp = &p.x; float* mm = &m.x; float* vv = &v.x; const float* gg = &g.x;
+        // g /= total weight in f64, then cast to T (engine.hpp:151, optim.hpp:135)
+        float gs[4];
+        if constexpr (ACC) {  // K > 1: earlier rounds' sums, consumed (zeroed) here
+          const float4 q = *reinterpret_cast<const float4*>(a.g2 + lo + i);
+          *reinterpret_cast<float4*>(a.g2 + lo + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+          const float* qq = &q.x;
+  #pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const double gd = (double)gg[e] + (double)qq[e];
+            gs[e] = scale ? (float)(gd * sc) : (float)gd;
+          }
         } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sh[sidx(i + e)] = __float2bfloat16_rn(pp[e]);
+  #pragma unroll
+          for (int e = 0; e < 4; ++e) gs[e] = scale ? (float)((double)gg[e] * sc) : gg[e];
+        }
+  #pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float ge = gs[e];
+          if (!isfinite(ge)) { bad = 1; continue; }
+          adam_one(a, pp[e], mm[e], vv[e], ge);
+        }
+        *reinterpret_cast<float4*>(a.p + lo + i) = p;
+        *reinterpret_cast<float4*>(a.m + lo + i) = m;
+        *reinterpret_cast<float4*>(a.v + lo + i) = v;
+        if (sh) {
+          if (contig) {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(p.x, p.y), h1 = __floats2bfloat162_rn(p.z, p.w);
+            uint2 u;
+            u.x = *reinterpret_cast<uint32_t*>(&h0);
+            u.y = *reinterpret_cast<uint32_t*>(&h1);
+            *reinterpret_cast<uint2*>(sh + slo + i) = u;
+          } else {
+  #pragma unroll
+            for (int e = 0; e < 4; ++e) sh[sidx(i + e)] = __float2bfloat16_rn(pp[e]);
+          }
         }
       }
-    }
-    for (uint64_t i = n4 + threadIdx.x; i < n; i += blockDim.x) {
-      float ge;
-      if constexpr (ACC) {
-        const double gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
-        a.g2[lo + i] = 0.f;
-        ge = scale ? (float)(gd * sc) : (float)gd;
-      } else {
-        ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+      for (uint64_t i = n4 + threadIdx.x; i < n; i += blockDim.x) {
+        float ge;
+        if constexpr (ACC) {
+          const double gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
+          a.g2[lo + i] = 0.f;
+          ge = scale ? (float)(gd * sc) : (float)gd;
+        } else {
+          ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+        }
+        if (!isfinite(ge)) { bad = 1; continue; }
+        float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
+        adam_one(a, p, m, v, ge);
+        a.p[lo + i] = p; a.m[lo + i] = m; a.v[lo + i] = v;
+        if (sh) sh[sidx(i)] = __float2bfloat16_rn(p);
       }
-      if (!isfinite(ge)) { bad = 1; continue; }
-      float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
-      adam_one(a, p, m, v, ge);
-      a.p[lo + i] = p; a.m[lo + i] = m; a.v[lo + i] = v;
-      if (sh) sh[sidx(i)] = __float2bfloat16_rn(p);
-    }
-  } else {
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      float ge;
-      if constexpr (ACC) {
-        const double gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
-        a.g2[lo + i] = 0.f;
-        ge = scale ? (float)(gd * sc) : (float)gd;
-      } else {
-        ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+    } else {
+      for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        float ge;
+        if constexpr (ACC) {
+          const double gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
+          a.g2[lo + i] = 0.f;
+          ge = scale ? (float)(gd * sc) : (float)gd;
+        } else {
+          ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+        }
+        if (!isfinite(ge)) { bad = 1; continue; }
+        float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
+        adam_one(a, p, m, v, ge);
+        a.p[lo + i] = p; a.m[lo + i] = m; a.v[lo + i] = v;
+        if (sh) sh[sidx(i)] = __float2bfloat16_rn(p);
       }
-      if (!isfinite(ge)) { bad = 1; continue; }
-      float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
-      adam_one(a, p, m, v, ge);
-      a.p[lo + i] = p; a.m[lo + i] = m; a.v[lo + i] = v;
-      if (sh) sh[sidx(i)] = __float2bfloat16_rn(p);
     }
   }
   if (bad) *a.bad = 1;
 }
 void adam_update(const AdamArgs& a, cudaStream_t s) {
   if (a.nitems == 0) return;
+  static const int cap = [] {
+    const char* e = std::getenv("HP_ADAM_GRID");  // A/B knob: cap on CTAs (0: one per item)
+    return e ? std::atoi(e) : 0;
+  }();
+  const int grid = cap > 0 ? std::min(a.nitems, cap) : a.nitems;
   if (a.g2)
-    adam_kernel<true><<<a.nitems, 256, 0, s>>>(a);
+    adam_kernel<true><<<grid, 256, 0, s>>>(a);
   else
-    adam_kernel<false><<<a.nitems, 256, 0, s>>>(a);
+    adam_kernel<false><<<grid, 256, 0, s>>>(a);
   LAUNCH_CHECK();
   count_launch();
 }

@@ -136,6 +136,21 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// 16 bytes into another cluster CTA's smem; the bytes complete on that CTA's
+// mbarrier (its owner sets expect_tx)
+__device__ __forceinline__ void st_async_v4(uint32_t cluster_addr, uint4 v, uint32_t cluster_bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+          cluster_addr),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(cluster_bar)
+      : "memory");
+}
+// arrive on another cluster CTA's mbarrier, releasing this thread's prior
+// shared-memory reads / writes at cluster scope
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 // TMA load into this CTA's smem, completing bytes on the (leader's) barrier
 __device__ __forceinline__ void tma_2d_cg2(const CUtensorMap* map, uint32_t bar_cluster, void* dst,
                                            int c0, int c1) {

@@ -3,6 +3,7 @@ major-ness, grouped per-head operands, tails, fused epilogues) and the SIMT
 fp32 GEMM against a torch fp32 reference; Adam bit-exact against the C
 oracle's restatement of kern::scalar::adam_update<float>."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -290,3 +291,33 @@ def test_tc_gemm_pair_192_kmajor_b(epi_kind):
     _check(res, torch.bfloat16, 2304)
     res = run_gemm(512, 768, 768, torch.bfloat16, 0, 1, path=2, bn=2192, c_dtype=torch.float32)
     _check(res, torch.bfloat16, 768)
+
+
+def test_tc_gemm_cluster_split_k_weight_gradients(tmp_path):
+    """(run in a child process with HP_GEMM_CSPLIT=1, the deterministic mode)"""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0] = [%r, %r]; import test_gpu_kernels as t; "
+            "t._cluster_split_cases()") % (os.path.dirname(os.path.abspath(__file__)),
+                                           os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, HP_GEMM_CSPLIT="1"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def _cluster_split_cases():
+    """Split-K fp32 GEMMs (the weight gradients: A^T dY over the tokens) run
+    as two K halves per tile reduced inside a CTA cluster: exact vs torch at
+    the C2 shapes, with grouped (per-head) output, tails and an odd number of
+    K blocks -- and bit-identical from run to run (no atomics)."""
+    # (N % 32 != 0 takes the generic epilogue: split-K with fp32 atomics, so
+    # only its values are checked)
+    cases = [(768, 3072, 4096, 0, 1), (3072, 768, 4096, 0, 1), (768, 768, 4096, 0, 1),
+             (768, 2304, 4096, 64, 1), (200, 160, 1000, 0, 1), (200, 136, 1000, 0, 0),
+             (384, 512, 192, 0, 1)]
+    for (M, N, K, cgrp, det) in cases:
+        a = run_gemm(M, N, K, torch.bfloat16, 1, 0, path=2, c_dtype=torch.float32, c_group=cgrp, seed=5)
+        _check(a, torch.bfloat16, K)
+        if det:
+            b = run_gemm(M, N, K, torch.bfloat16, 1, 0, path=2, c_dtype=torch.float32, c_group=cgrp, seed=5)
+            assert torch.equal(a["out"], b["out"]), (M, N, K)
