@@ -306,6 +306,20 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   dC_ = dalloc(T * wmax * asz_);
   dU_ = bert_ ? dalloc(T * F_ * asz_) : nullptr;
   dqkv_ = dalloc(T * 3 * d_ * asz_);
+  if (bert_) {
+    // per-layer-parity gradient buffers (layer l uses slot l & 1): a buffer a
+    // weight-gradient GEMM reads is rewritten two layers later, so the
+    // data-gradient chain does not wait on the weight-gradient stream
+    // (HP_LAYER_SLOTS=1: one slot, reuse distance one layer -- A/B)
+    const char* e = std::getenv("HP_LAYER_SLOTS");
+    rd_ = (e && std::string(e) == "1") ? 1 : 2;
+    pbuf_[0] = dB_;
+    for (int i = 1; i < 4; ++i) pbuf_[i] = dalloc(T * d_ * asz_);
+    ubuf_[0] = dU_;
+    ubuf_[1] = dalloc(T * F_ * asz_);
+    qbuf_[0] = dqkv_;
+    qbuf_[1] = dalloc(T * 3 * d_ * asz_);
+  }
   const size_t scratch = std::max({colsum_scratch_floats((int)T, (int)wmax),
                                    colsum_scratch_floats((int)Mm, Vp_),
                                    colsum_scratch_floats((int)T, d_)});
@@ -973,13 +987,16 @@ void Engine::backward() {
     if (bert_) {
       const int ibo = iwo + 1, ig1 = iwo + 2, iw1 = iwo + 4, ib1 = iwo + 5, iw2 = iwo + 6,
                 ib2 = iwo + 7, ig2 = iwo + 8;
-      // dB_ is about to be overwritten: layer l+1's d(wo) must have read it
-      if (l + 1 < L_) wait_wg(ev_wo_[l + 1]);
+      void* const dP2 = pbuf_[slot(l)];
+      void* const dP1b = pbuf_[2 + slot(l)];
+      void* const dU = ubuf_[slot(l)];
+      // dP2's slot was last read by layer l+2's d(ffn.w2)
+      if (l + rd_ < L_) wait_wg(ev_w2_[l + rd_]);
       tstart(TM_NORM);
       // LN2' also yields d(ffn.b2) = colsum(dP2) (P2 = G W2 + b2 + X1)
       {
         DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, d_));
-        layernorm_bwd(T, d_, dA_, at_, y.p2, at_, y.mean2, y.rstd2, pp(ig2), dB_, at_, gp(ig2),
+        layernorm_bwd(T, d_, dA_, at_, y.p2, at_, y.mean2, y.rstd2, pp(ig2), dP2, at_, gp(ig2),
                       gp(ig2 + 1), gp(ib2), scratch_, s_main_, &f);
         issue_final(f);
       }
@@ -987,21 +1004,21 @@ void Engine::backward() {
       GemmArgs w2;  // d(ffn.w2) = G^T dP2
       w2.M = F_; w2.N = d_; w2.K = T; w2.ab = at_;
       w2.a = Operand{y.g, F_, 1, 0, 0};
-      w2.b = Operand{dB_, d_, 0, 0, 0};
+      w2.b = Operand{dP2, d_, 0, 0, 0};
       w2.c = gp(iw2); w2.ldc = d_; w2.ct = DType::f32;
       wgrad_t(w2, wg_on_ ? ev_fork_[4 * l] : nullptr, wg_on_ ? ev_w2_[l] : nullptr);
       GemmArgs du;  // dU = (dP2 W2^T) * gelu'(U)
       du.M = T; du.N = F_; du.K = d_; du.ab = at_;
-      du.a = Operand{dB_, d_, 0, 0, 0};
+      du.a = Operand{dP2, d_, 0, 0, 0};
       du.b = Operand{w(iw2), wld(iw2), 1, 0, 0};
-      du.c = dU_; du.ldc = F_; du.ct = at_;
+      du.c = dU; du.ldc = F_; du.ct = at_;
       du.act = ACT_DGELU; du.aux = y.u;
-      if (l + 1 < L_) wait_wg(ev_w1_[l + 1]);  // dU_ is reused: layer l+1's d(w1) read it
+      if (l + rd_ < L_) wait_wg(ev_w1_[l + rd_]);  // dU's slot: layer l+2's d(w1) / d(b1) read it
       gemm_t(du);
       GemmArgs w1;  // d(ffn.w1) = X1^T dU
       w1.M = d_; w1.N = F_; w1.K = T; w1.ab = at_;
       w1.a = Operand{y.x1, d_, 1, 0, 0};
-      w1.b = Operand{dU_, F_, 0, 0, 0};
+      w1.b = Operand{dU, F_, 0, 0, 0};
       w1.c = gp(iw1); w1.ldc = F_; w1.ct = DType::f32;
       wgrad_t(w1, wg_on_ ? ev_fork_[4 * l + 1] : nullptr, wg_on_ ? ev_w1_[l] : nullptr);
       tstart(TM_NORM);
@@ -1011,35 +1028,35 @@ void Engine::backward() {
           // the event that lets the next layer reuse dU_
           tstop(TM_NORM, 0, 0);
           tstart(TM_NORM, s_wg_);
-          col_sum(T, F_, dU_, F_, at_, gp(ib1), scratch_wg_, s_wg_);
+          col_sum(T, F_, dU, F_, at_, gp(ib1), scratch_wg_, s_wg_);
           tstop(TM_NORM, 0, 0, s_wg_);
           HP_CUDA(cudaEventRecord(ev_w1_[l], s_wg_));
           tstart(TM_NORM);
         } else {
           DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, F_));
-          col_sum(T, F_, dU_, F_, at_, gp(ib1), scratch_, s_main_, &f);
+          col_sum(T, F_, dU, F_, at_, gp(ib1), scratch_, s_main_, &f);
           issue_final(f);
         }
       }
       tstop(TM_NORM, 0, 0);
       GemmArgs dx1;  // dX1 = dU W1^T + dP2
       dx1.M = T; dx1.N = d_; dx1.K = F_; dx1.ab = at_;
-      dx1.a = Operand{dU_, F_, 0, 0, 0};
+      dx1.a = Operand{dU, F_, 0, 0, 0};
       dx1.b = Operand{w(iw1), wld(iw1), 1, 0, 0};
       dx1.c = dC_; dx1.ldc = d_; dx1.ct = at_;
-      dx1.resid = dB_; dx1.ld_resid = d_;
+      dx1.resid = dP2; dx1.ld_resid = d_;
       gemm_t(dx1);
-      wait_wg(ev_w2_[l]);  // dB_ (dP2) is overwritten next: d(w2) must have read it
+      if (l + rd_ < L_) wait_wg(ev_wo_[l + rd_]);  // dP1's slot: layer l+2's d(wo) read it
       tstart(TM_NORM);
       // LN1' also yields d(bo) = colsum(dP1)
       {
         DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, d_));
-        layernorm_bwd(T, d_, dC_, at_, y.p1, at_, y.mean1, y.rstd1, pp(ig1), dB_, at_, gp(ig1),
+        layernorm_bwd(T, d_, dC_, at_, y.p1, at_, y.mean1, y.rstd1, pp(ig1), dP1b, at_, gp(ig1),
                       gp(ig1 + 1), gp(ibo), scratch_, s_main_, &f);
         issue_final(f);
       }
       tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
-      dP1 = dB_;
+      dP1 = dP1b;
     } else {
       dP1 = dA_;
     }
@@ -1058,23 +1075,24 @@ void Engine::backward() {
     dO.b = Operand{w(iwo), wld(iwo), 1, 0, 0};
     dO.c = dC_; dO.ldc = d_; dO.ct = at_;
     gemm_t(dO);
-    if (bert_ && l + 1 < L_) wait_wg(ev_wq_[l + 1]);  // dqkv_ reused: layer l+1's d(wqkv) read it
+    void* const dqkv = bert_ ? qbuf_[slot(l)] : dqkv_;
+    if (bert_ && l + rd_ < L_) wait_wg(ev_wq_[l + rd_]);  // the slot: layer l+2's d(wqkv) read it
     tstart(TM_ATTN);
     if (attn_long_)
-      attention_bwd_long(b, H_, (int)m_.max_seq, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
+      attention_bwd_long(b, H_, (int)m_.max_seq, y.qkv, y.o, dC_, y.lse, dqkv, s_main_);
     else if (attn_tc_)
-      attention_bwd_tc(b, H_, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
+      attention_bwd_tc(b, H_, y.qkv, y.o, dC_, y.lse, dqkv, s_main_);
     else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
-      attention_bwd_mma(b, H_, y.qkv, y.o, dC_, y.lse, dqkv_, s_main_);
+      attention_bwd_mma(b, H_, y.qkv, y.o, dC_, y.lse, dqkv, s_main_);
     else
-      attention_bwd(b, H_, dk_, y.qkv, y.o, dC_, y.lse, dqkv_, at_, s_main_);
+      attention_bwd(b, H_, dk_, y.qkv, y.o, dC_, y.lse, dqkv, at_, s_main_);
     tstop(TM_ATTN, 8.0 * H_ * dk_ * (double)T * (double)m_.max_seq, 0);
     const int64_t gstride_w = bf16_ ? (int64_t)(shadow_off_[iq + 1] - shadow_off_[iq])
                                     : (int64_t)(table_[iq + 1].offset - table_[iq].offset);
     GemmArgs wq;  // d(wq.*, wk.*, wv.*) = X^T dQKV, scattered into the 3h blocks
     wq.M = d_; wq.N = 3 * d_; wq.K = T; wq.ab = at_;
     wq.a = Operand{y.x, d_, 1, 0, 0};
-    wq.b = Operand{dqkv_, 3 * d_, 0, 0, 0};
+    wq.b = Operand{dqkv, 3 * d_, 0, 0, 0};
     wq.c = gp(iq); wq.ldc = dk_; wq.c_group = dk_;
     wq.c_gstride = (int64_t)(table_[iq + 1].offset - table_[iq].offset);
     wq.ct = DType::f32;
@@ -1084,7 +1102,7 @@ void Engine::backward() {
       gemm_t(wq);
     GemmArgs dx;  // dX = dQKV Wqkv^T (+ dP1 through the residual)
     dx.M = T; dx.N = d_; dx.K = 3 * d_; dx.ab = at_;
-    dx.a = Operand{dqkv_, 3 * d_, 0, 0, 0};
+    dx.a = Operand{dqkv, 3 * d_, 0, 0, 0};
     dx.b = Operand{w(iq), wld(iq), 1, dk_, gstride_w};
     dx.c = bert_ ? dA_ : dB_; dx.ldc = d_; dx.ct = at_;
     if (bert_) {
@@ -1099,16 +1117,18 @@ void Engine::backward() {
   const void* dx0 = dB_;
   if (bert_) {
     const int g = pidx("emb_ln.g");
-    wait_wg(ev_wo_[0]);  // dB_ is overwritten: layer 0's d(wo) must have read it
+    // into layer 1's dP1 slot (layer 0 uses slots 0 and 2): read by d(wo) of layer 1
+    void* const dE0 = pbuf_[2 + slot(rd_ - 1)];
+    if (rd_ - 1 < L_) wait_wg(ev_wo_[rd_ - 1]);
     tstart(TM_NORM);
     {
       DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, d_));
-      layernorm_bwd(T, d_, dA_, at_, p0_, at_, mean0_, rstd0_, pp(g), dB_, at_, gp(g), gp(g + 1),
+      layernorm_bwd(T, d_, dA_, at_, p0_, at_, mean0_, rstd0_, pp(g), dE0, at_, gp(g), gp(g + 1),
                     nullptr, scratch_, s_main_, &f);
       issue_final(f);
     }
     tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
-    dx0 = dB_;
+    dx0 = dE0;
   }
   tstart(TM_EMBED);
   if (wg_forked_)

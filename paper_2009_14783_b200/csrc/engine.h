@@ -135,6 +135,13 @@ class Engine {
   void *hm_ = nullptr, *dz_ = nullptr, *dhm_ = nullptr;
   float *z_ = nullptr, *row_loss_ = nullptr;
   void *dA_ = nullptr, *dB_ = nullptr, *dC_ = nullptr, *dqkv_ = nullptr, *dU_ = nullptr;
+  // bert: layer-parity slots -- pbuf_ {dP2 even, dP2 odd, dP1 even, dP1 odd}
+  // (pbuf_[0] = dB_), ubuf_ dU (ubuf_[0] = dU_), qbuf_ dQKV (qbuf_[0] = dqkv_)
+  void* pbuf_[4] = {};
+  int rd_ = 2;  // slots per buffer = reuse distance in layers
+  int slot(int l) const { return rd_ == 2 ? (l & 1) : 0; }
+  void* ubuf_[2] = {};
+  void* qbuf_[2] = {};
   float* scratch_ = nullptr;
   double* d_lw_ = nullptr;  // [loss, weight] (global after the allreduce)
   float* inv_w_ = nullptr;
