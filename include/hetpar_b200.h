@@ -355,6 +355,9 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
                         const float* bias, int act, void* aux, const void* resid,
                         int64_t ld_resid, int accumulate, int path, int bn);
 hp_status hp_debug_sync(void);
+/* stream for hp_debug_gemm (NULL: the legacy default stream) -- lets a
+ * microbenchmark capture its launches into a CUDA graph */
+hp_status hp_debug_set_stream(void* stream);
 /* Profiling hook: when buf (device, >= 1024 u64) is non-null, CTA 0 of every
  * following tcgen05 GEMM writes a clock64 timeline into it; null disables. */
 hp_status hp_debug_gemm_trace(unsigned long long* buf);

@@ -175,6 +175,7 @@ _SIGS = {
     "hp_debug_gemm": [I, I, I, I, P, I64, I, P, I64, I, I64, I64, P, I64, I, I64, I64, P, I, P, P,
                       I64, I, I, I],
     "hp_debug_sync": [],
+    "hp_debug_set_stream": [P],
     "hp_debug_gemm_trace": [P],
     "hp_debug_gemm_generic": [I],
     "hp_debug_attention": [I, P, I, I, I, I, P, P, P, P, P, I],

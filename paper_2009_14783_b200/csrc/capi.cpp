@@ -386,6 +386,15 @@ hp_status hp_engine_io_bytes(hp_engine* e, uint64_t* h2d, uint64_t* d2h) {
   HP_API_END
 }
 
+namespace {
+cudaStream_t g_debug_stream = nullptr;  // hp_debug_gemm's stream (0: legacy default)
+}
+hp_status hp_debug_set_stream(void* stream) {
+  HP_API_BEGIN
+  g_debug_stream = static_cast<cudaStream_t>(stream);
+  HP_API_END
+}
+
 hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t lda, int a_trans,
                         const void* B, int64_t ldb, int b_trans, int64_t b_group, int64_t b_gstride,
                         void* C, int64_t ldc, int c_bf16, int64_t c_group, int64_t c_gstride,
@@ -402,19 +411,19 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
   g.bias = bias; g.act = act; g.aux = aux; g.resid = resid; g.ld_resid = ld_resid;
   g.accumulate = accumulate;
   if (path == 1) {
-    hp::gemm_simt(g, 0);
+    hp::gemm_simt(g, g_debug_stream);
   } else if (path == 2) {
     hp::gemm_tc_set_bn(bn % 1000);
     hp::gemm_tc_set_cg((bn / 1000) % 10);
     hp::gemm_tc_set_splits((bn / 10000) % 10);
     hp::gemm_tc_set_debug(bn / 100000);
-    hp::gemm_tc(g, 0);
+    hp::gemm_tc(g, g_debug_stream);
     hp::gemm_tc_set_debug(0);
     hp::gemm_tc_set_bn(0);
     hp::gemm_tc_set_cg(0);
     hp::gemm_tc_set_splits(0);
   } else {
-    hp::gemm(g, 0);
+    hp::gemm(g, g_debug_stream);
   }
   HP_API_END
 }

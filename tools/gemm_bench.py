@@ -52,6 +52,9 @@ PER_STEP.update({"qkv_fwd": 12, "wo_fwd": 12, "ffn1_fwd_gelu": 12, "ffn2_fwd": 1
             "mlm_logits": 1, "dmlm_w": 1, "dhm": 1})
 
 
+GRAPH = True
+
+
 def p(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
@@ -89,12 +92,28 @@ def run(shape, iters, bn):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # keep the GPU busy while the host enqueues, so the timed launches run
     # back to back (device time, not host launch overhead)
-    torch.cuda._sleep(100_000_000)
-    e0.record()
-    for _ in range(iters):
-        _lib.call("hp_debug_gemm", *args)
-    e1.record()
-    torch.cuda.synchronize()
+    if GRAPH:
+        # the launches as CUDA graph nodes (the engine's mode): stream launches
+        # complete on a ~2 us grid on this platform (profiles/r01_launch_granularity.txt)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            _lib.call("hp_debug_set_stream", C.c_void_p(torch.cuda.current_stream().cuda_stream))
+            for _ in range(iters):
+                _lib.call("hp_debug_gemm", *args)
+            _lib.call("hp_debug_set_stream", None)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+    else:
+        torch.cuda._sleep(100_000_000)
+        e0.record()
+        for _ in range(iters):
+            _lib.call("hp_debug_gemm", *args)
+        e1.record()
+        torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / iters
     # cuBLAS on the same math (plain matmul, no epilogue) for context
     a2 = A.t() if at else A
@@ -104,11 +123,22 @@ def run(shape, iters, bn):
     for _ in range(3):
         torch.matmul(x, y)
     torch.cuda.synchronize()
-    torch.cuda._sleep(100_000_000)
-    e0.record()
-    for _ in range(iters):
-        torch.matmul(x, y)
-    e1.record()
+    if GRAPH:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(iters):
+                torch.matmul(x, y)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+    else:
+        torch.cuda._sleep(100_000_000)
+        e0.record()
+        for _ in range(iters):
+            torch.matmul(x, y)
+        e1.record()
     torch.cuda.synchronize()
     us_cb = e0.elapsed_time(e1) * 1e3 / iters
     fl = 2.0 * M * N * K
@@ -122,7 +152,11 @@ def main():
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--json", default=None)
     ap.add_argument("--only", default=None, help="comma-separated shape names")
+    ap.add_argument("--stream", action="store_true",
+                    help="time stream launches instead of CUDA-graph replays")
     a = ap.parse_args()
+    global GRAPH
+    GRAPH = not a.stream
     shapes = [s for s in SHAPES + VARIANTS if (not a.only and s in SHAPES) or
               (a.only and (s[0] in a.only.split(",") or (a.only == "variants" and s in VARIANTS)))]
     res = [run(s, a.iters, a.bn) for s in shapes]
