@@ -604,11 +604,19 @@ struct Tile {
 //   ships its accumulator chunk by chunk into the first CTA's smem (st.async
 //   completing on the receiver's mbarrier), the first adds it to its own and
 //   stores -- no zero-fill of C, no global atomics, a fixed summation order.
-template <int BN, int CG, int EK, bool CS = false>
+// MC (multicast, CG = 1, BN = 256): a 2 x 2 cluster computes a 256 x 512
+//   super-tile; CTA (i, j) owns rows m0 + 128 i, columns (2 nt + j) 256. The
+//   A tile is shared along the cluster row and the B tile along the column:
+//   each CTA loads half of each and multicasts it to its peer, so L2 serves
+//   24 KB per CTA per k-block instead of 48 (the CTA pair's 256 x 256 tile
+//   needs 32). A stage is released once this CTA and both peers writing into
+//   it have consumed it (empty count 3, commits multicast to those CTAs).
+template <int BN, int CG, int EK, bool CS = false, bool MC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const Params p) {
   static_assert(!CS || (CG == 1 && EK == EK_F32), "cluster split-K: one CTA per tile, fp32 C");
+  static_assert(!MC || (CG == 1 && BN == 256 && !CS), "multicast: single-CTA 128 x 256 tiles");
   using TL = Tile<BN, CG, CS>;
   constexpr int BNL = TL::BNL;
   constexpr int STAGES = TL::kStages;
@@ -630,15 +638,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     trace_at(p, 0);
     trace_cta(p, 0);
   }
-  constexpr int kClu = (CG == 2 || CS) ? 2 : 1;  // CTAs per cluster
-  const uint32_t rank = kClu == 2 ? cluster_rank() : 0;
+  constexpr int kClu = MC ? 4 : ((CG == 2 || CS) ? 2 : 1);  // CTAs per cluster
+  const uint32_t rank = kClu > 1 ? cluster_rank() : 0;
   const uint32_t row_rank = CG == 2 ? rank : 0;  // which 128 rows of the tile this CTA owns
+  const int mc_i = MC ? static_cast<int>(rank >> 1) : 0, mc_j = MC ? static_cast<int>(rank & 1) : 0;
+  // MC: this CTA's tile within the cluster's super-tile
+  auto mc_tile = [&](int& m0, int& nt) {
+    if constexpr (MC) {
+      m0 += mc_i * BM;
+      nt = 2 * nt + mc_j;
+    }
+  };
   const int unit0 = blockIdx.x / kClu, unit_step = gridDim.x / kClu;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 3 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
@@ -670,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if constexpr (kClu == 2) cluster_sync_all();  // peer barriers initialised before use
+  if constexpr (kClu > 1) cluster_sync_all();  // peer barriers initialised before use
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
   // the prologue above overlapped the previous kernel's tail (launch.cuh)
@@ -700,7 +716,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int u = take_unit(ui);
       if (u < 0) break;
       int m0, nt, kb0, kb1;
-      decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
+      decode_unit(p, u, BM * CG * (MC ? 2 : 1), m0, nt, kb0, kb1);
+      mc_tile(m0, nt);
       const int am0 = m0 + static_cast<int>(row_rank) * BM;       // this CTA's A rows
       const int bn0 = nt * BN + static_cast<int>(row_rank) * BNL;  // this CTA's B columns
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -714,6 +731,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
           if (debug_bit(p, 1)) {  // profiling mode: no loads, MMA on stale smem
             if (CG == 1 || rank == 0) mbar_arrive(&full[s]);
+          } else if constexpr (MC) {
+            uint64_t* bar = &full[s];
+            mbar_expect_tx(bar, kStageBytes);  // own halves + the peers' halves
+            const uint16_t amask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 1)));
+            const uint16_t bmask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2)));
+            // A rows [64 j, +64) of the tile shared with the row peer (half-height maps)
+            if (!p.a_mn) tma_2d_mc(&map_a, bar, sa + mc_j * 8192, k0, am0 + mc_j * 64, amask);
+            else tma_3d_mc(&map_a, bar, sa + mc_j * 8192, 0, k0, am0 / 64 + mc_j, amask);
+            // B columns [128 i, +128) of the tile shared with the column peer
+            if (!p.b_mn) tma_2d_mc(&map_b, bar, sb + mc_i * 16384, k0, bn0 + mc_i * 128, bmask);
+            else tma_3d_mc(&map_b, bar, sb + mc_i * 16384, 0, k0, (bn0 + mc_i * 128) / 64, bmask);
           } else if constexpr (CG == 1) {
             uint64_t* bar = &full[s];
             mbar_expect_tx(bar, kStageBytes);
@@ -781,7 +809,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int u = take_unit(lt);
         if (u < 0) break;
         int m0, nt, kb0, kb1;
-        decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
+        decode_unit(p, u, BM * CG * (MC ? 2 : 1), m0, nt, kb0, kb1);
+        mc_tile(m0, nt);
         const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
         mbar_wait(&tmem_empty[as], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -804,7 +833,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                   umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
               }
             }
-            if constexpr (CG == 2) umma_commit_cg2(&empty[s]); else umma_commit(&empty[s]);
+            if constexpr (CG == 2) umma_commit_cg2(&empty[s]);
+            else if constexpr (MC)  // this CTA and the two peers that write into its stages
+              umma_commit_mc(&empty[s], static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 1)) |
+                                                              (1u << (rank ^ 2))));
+            else umma_commit(&empty[s]);
           }
           __syncwarp();
           if (lane == 0) trace_at(p, kTrC + it, kTrE);
@@ -847,7 +880,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int u = take_unit(lt);
       if (u < 0) break;
       int m0, nt, kb0, kb1;
-      decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
+      decode_unit(p, u, BM * CG * (MC ? 2 : 1), m0, nt, kb0, kb1);
+      mc_tile(m0, nt);
       const int n0 = nt * BN;
       const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
       const int row0 = m0 + static_cast<int>(row_rank) * BM + quarter * 32;
@@ -940,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   // both CTAs done before the pair frees TMEM / before a CS sender exits
   // while its receiver still signals it
-  if constexpr (kClu == 2) cluster_sync_all();
+  if constexpr (kClu > 1) cluster_sync_all();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if constexpr (CG == 2)
@@ -1054,22 +1088,45 @@ static int epilogue_vec_ok(const GemmArgs& g) {
   return 0;
 }
 
-template <int BN, int CG, int EK, bool CS = false>
+template <int BN, int CG, int EK, bool CS = false, bool MC = false>
 static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Params& p,
                       cudaStream_t s) {
   // stages + barriers (1 KB) + epilogue staging tiles + alignment slack
   constexpr size_t smem = tc::Tile<BN, CG, CS>::kSmem;
   static bool attr = false;
   if (!attr) {
-    HP_CUDA(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, CG, EK, CS>,
+    HP_CUDA(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, CG, EK, CS, MC>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  // CS: units = tiles x 2 halves, one cluster of two CTAs per tile at a time
-  const int clu = CS ? 2 : CG;
-  const int grid = CS ? 2 * std::min(p.units / 2, num_sms() / 2) : CG * std::min(p.units, num_sms() / CG);
-  launch_pdl(PDL_GEMM, tc::gemm_tc_kernel<BN, CG, EK, CS>, dim3(grid), dim3(tc::kThreads), smem, s, clu,
-             ma, mb, p);
+  // CS: units = tiles x 2 halves, one cluster of two CTAs per tile at a time;
+  // MC: units = super-tiles (x splits), one 2 x 2 cluster per unit
+  const int clu = MC ? 4 : (CS ? 2 : CG);
+  int mc_clusters = num_sms() / 4;
+  if constexpr (MC) {
+    // 4-CTA clusters must fit whole GPCs: ask how many can be resident at once
+    static int active = 0;
+    if (!active) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(4 * mc_clusters);
+      cfg.blockDim = dim3(tc::kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 4;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      HP_CUDA(cudaOccupancyMaxActiveClusters(&active, tc::gemm_tc_kernel<BN, CG, EK, CS, MC>, &cfg));
+      if (active < 1) active = 1;
+    }
+    mc_clusters = std::min(mc_clusters, active);
+  }
+  const int grid = MC ? 4 * std::min(p.units, mc_clusters)
+                      : (CS ? 2 * std::min(p.units / 2, num_sms() / 2) : CG * std::min(p.units, num_sms() / CG));
+  launch_pdl(PDL_GEMM, tc::gemm_tc_kernel<BN, CG, EK, CS, MC>, dim3(grid), dim3(tc::kThreads), smem, s,
+             clu, ma, mb, p);
   HP_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -1083,8 +1140,12 @@ void gemm_tc_set_generic(int on) { g_generic_only = on; }
 
 template <int EK>
 static void launch_ek(int cg, int bn, const CUtensorMap& ma, const CUtensorMap& mb,
-                      const tc::Params& p, cudaStream_t s, bool cs = false) {
+                      const tc::Params& p, cudaStream_t s, bool cs = false, bool mc = false) {
   if constexpr (EK == tc::EK_F32) {
+    if (mc) {
+      launch_tc<256, 1, EK, false, true>(ma, mb, p, s);
+      return;
+    }
     if (cs) {
       if (bn == 256) launch_tc<256, 1, EK, true>(ma, mb, p, s);
       else if (bn == 192) launch_tc<192, 1, EK, true>(ma, mb, p, s);
@@ -1181,7 +1242,30 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
       splits = 2;
     }
   }
-  const int m_tiles = (g.M + tc::BM * cg - 1) / (tc::BM * cg);
+  // Multicast mode (HP_GEMM_MC=1) for the fp32 split-K GEMMs: 2 x 2 clusters
+  // of 128 x 256 tiles sharing A along rows and B along columns (gemm_tc_kernel MC)
+  bool mc = false;
+  {
+    static const int mc_env = [] {
+      const char* e = std::getenv("HP_GEMM_MC");
+      return e ? std::atoi(e) : 0;
+    }();
+    const bool f32_plain = epilogue_vec_ok(g) == 1 && g.N % 32 == 0 && !g_generic_only &&
+                           g.ct == DType::f32 && g.act == ACT_NONE && !g.resid;
+    const bool a_ok = !g.a.trans || 64LL * ((g.M + 63) / 64) <= g.a.ld;
+    const bool b_ok = g.b.trans || 64LL * ((g.N + 63) / 64) <= g.b.ld;
+    if (mc_env && !cs && can_split && f32_plain && !g.b.group && a_ok && b_ok && !g_force_splits &&
+        !g_force_cg && !g_force_bn) {
+      mc = true;
+      cg = 1;
+      bn = 256;
+      const int st = ((g.M + 255) / 256) * ((g.N + 511) / 512);
+      const int slots = nsm / 4;
+      splits = std::max(1, std::min(std::max(1, slots / st), num_kb / 4));
+      if (g.max_splits > 0) splits = std::min(splits, g.max_splits);
+    }
+  }
+  const int m_tiles = mc ? (g.M + 255) / 256 : (g.M + tc::BM * cg - 1) / (tc::BM * cg);
   const int kb_per_split = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per_split - 1) / kb_per_split;  // no empty splits
   const int bnl = bn / cg;  // B columns per CTA
@@ -1202,11 +1286,11 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
       rank = 3;
       dims[0] = 64; dims[1] = g.K; dims[2] = a_blocks;
       str[0] = g.a.ld; str[1] = 64;
-      box[0] = 64; box[1] = 64; box[2] = tc::BM / 64;
+      box[0] = 64; box[1] = 64; box[2] = mc ? 1 : tc::BM / 64;  // MC: half a tile per load
     } else if (g.a.trans) {
       dims[0] = g.M; dims[1] = g.K; str[0] = g.a.ld; box[0] = 64; box[1] = 64;
     } else {          // memory [M rows][K cols]
-      dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = tc::BM;
+      dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = mc ? 64 : tc::BM;
     }
     ma = make_map(g.a.p, rank, dims, str, box);
   }
@@ -1216,7 +1300,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     int rank = 2;
     if (!g.b.trans) {  // MN-major: memory [K rows][N cols] (or grouped blocks)
       rank = 3;
-      box[0] = 64; box[1] = 64; box[2] = (uint32_t)(bnl / 64);
+      box[0] = 64; box[1] = 64; box[2] = (uint32_t)((mc ? bnl / 2 : bnl) / 64);
       if (g.b.group) {
         dims[0] = 64; dims[1] = g.K; dims[2] = g.N / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
@@ -1234,7 +1318,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         str[0] = g.b.ld; str[1] = g.b.gstride;
         box[0] = 64; box[1] = (uint32_t)bnl; box[2] = 1;
       } else {
-        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64; box[1] = (uint32_t)bnl;
+        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64; box[1] = (uint32_t)(mc ? bnl / 2 : bnl);
       }
     }
     mb = make_map(g.b.p, rank, dims, str, box);
@@ -1247,7 +1331,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.a_atoms = a_atoms ? 1 : 0;
   p.b_atoms = b_atoms ? 1 : 0;
   p.m_tiles = m_tiles;
-  p.n_tiles = (g.N + bn - 1) / bn;
+  p.n_tiles = mc ? (g.N + 511) / 512 : (g.N + bn - 1) / bn;
   p.splits = splits;
   p.kb_per_split = kb_per_split;
   p.units = m_tiles * p.n_tiles * splits;
@@ -1283,7 +1367,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     case tc::EK_BF16: launch_ek<tc::EK_BF16>(cg, bn, ma, mb, p, s); break;
     case tc::EK_GELU: launch_ek<tc::EK_GELU>(cg, bn, ma, mb, p, s); break;
     case tc::EK_DGELU: launch_ek<tc::EK_DGELU>(cg, bn, ma, mb, p, s); break;
-    case tc::EK_F32: launch_ek<tc::EK_F32>(cg, bn, ma, mb, p, s, cs); break;
+    case tc::EK_F32: launch_ek<tc::EK_F32>(cg, bn, ma, mb, p, s, cs, mc); break;
     default: launch_ek<tc::EK_GENERIC>(cg, bn, ma, mb, p, s); break;
   }
 }

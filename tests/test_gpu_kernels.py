@@ -321,3 +321,26 @@ def _cluster_split_cases():
         if det:
             b = run_gemm(M, N, K, torch.bfloat16, 1, 0, path=2, c_dtype=torch.float32, c_group=cgrp, seed=5)
             assert torch.equal(a["out"], b["out"]), (M, N, K)
+
+
+def test_tc_gemm_multicast_weight_gradients():
+    """HP_GEMM_MC=1 (child process): fp32 split-K GEMMs on 2 x 2 clusters
+    with A / B multicast -- the C2 weight-gradient shapes, K-major operands,
+    tails and super-tile edges against torch."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0] = [%r, %r]; import test_gpu_kernels as t; "
+            "t._multicast_cases()") % (os.path.dirname(os.path.abspath(__file__)),
+                                       os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, HP_GEMM_MC="1"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def _multicast_cases():
+    for (M, N, K, at, bt, cgrp) in [(768, 3072, 4096, 1, 0, 0), (3072, 768, 4096, 1, 0, 0),
+                                    (768, 768, 4096, 1, 0, 0), (768, 2304, 4096, 1, 0, 64),
+                                    (512, 1024, 512, 0, 1, 0), (300, 700, 1000, 1, 0, 0),
+                                    (256, 512, 256, 0, 0, 0)]:
+        res = run_gemm(M, N, K, torch.bfloat16, at, bt, path=0, c_dtype=torch.float32, c_group=cgrp, seed=7)
+        _check(res, torch.bfloat16, K)
