@@ -316,6 +316,14 @@ hp_status hp_engine_round_sync(hp_engine* e, hp_round_out* out);
 hp_status hp_engine_round(hp_engine* e, int dummy, double lr, hp_round_out* out);
 /* params_digest (model.hpp:211-217): FNV-1a over the f32 parameter bytes. */
 hp_status hp_engine_params_digest(hp_engine* e, uint64_t* digest);
+/* check_digest_on_cadence (engine.hpp:170-184), run by hp_engine_round_sync
+ * after an update whose step is a multiple of `every` (every update when
+ * debug != 0; every = 0 disables; default 100, the reference's
+ * EngineConfig::check_interval): rank 0's parameter digest is broadcast,
+ * mismatches are summed over the ranks, and any mismatch is HP_ENUMERIC
+ * ("k ranks diverged from master parameters at step P") on every rank.
+ * Collective when the engine has a communicator of world > 1. */
+hp_status hp_engine_set_digest_check(hp_engine* e, uint64_t every, int debug);
 /* Number of this library's kernels launched since creation (for bench). */
 hp_status hp_engine_kernel_launches(hp_engine* e, uint64_t* n);
 /* CUDA-event time (ms) of the dominant kernel class over the last sync

@@ -172,6 +172,7 @@ _SIGS = {
     "hp_engine_synchronize": [P],
     "hp_engine_io_bytes": [P, P, P],
     "hp_engine_set_grad_comm": [P, I],
+    "hp_engine_set_digest_check": [P, U64, I],
     "hp_debug_gemm": [I, I, I, I, P, I64, I, P, I64, I, I64, I64, P, I64, I, I64, I64, P, I, P, P,
                       I64, I, I, I],
     "hp_debug_sync": [],

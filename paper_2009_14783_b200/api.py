@@ -760,6 +760,12 @@ class StepEngine:
     def set_capture(self, on: bool):
         call("hp_engine_set_capture", self._h, int(on))
 
+    def set_digest_check(self, every: int = 100, debug: bool = False):
+        """check_digest_on_cadence (engine.hpp:170-184): after every `every`-th
+        update (each update with debug) the ranks compare parameter digests
+        with rank 0's; a divergence raises NumericError on every rank."""
+        call("hp_engine_set_digest_check", self._h, int(every), int(debug))
+
     def set_grad_comm(self, on: bool):
         """Measurement only: off skips the gradient-bucket allreduces (ranks
         diverge); bench.py uses it for the exposed-communication figure."""

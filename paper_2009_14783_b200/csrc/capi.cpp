@@ -283,6 +283,12 @@ hp_status hp_engine_set_capture(hp_engine* e, int on) {
   E.set_capture(on != 0);
   HP_API_END
 }
+hp_status hp_engine_set_digest_check(hp_engine* e, uint64_t every, int debug) {
+  HP_API_BEGIN
+  ENG(e);
+  E.set_digest_check(every, debug != 0);
+  HP_API_END
+}
 hp_status hp_engine_set_grad_comm(hp_engine* e, int on) {
   HP_API_BEGIN
   ENG(e);

@@ -1351,6 +1351,32 @@ void Engine::round_body(int dummy) {
   HP_CUDA(cudaMemcpyAsync(h_flags_, flags_, 2 * 4, cudaMemcpyDeviceToHost, s_main_));
 }
 
+// The reference's cross-rank parameter check (engine.hpp:170-184): rank 0's
+// digest is broadcast, every rank compares it with its own, the mismatch
+// count is summed over the ranks, and a non-zero count is a numeric error on
+// every rank.  The digest here is FNV-1a over the FNV-1a values of 64 KB
+// blocks of the parameter bytes, computed on the device in parallel (the exact
+// byte-serial params_digest stays available as digest()).
+void Engine::check_digest_on_cadence() {
+  if (!comm_ || comm_->world < 2 || !grad_comm_) return;
+  const uint64_t every = check_debug_ ? 1 : check_every_;
+  if (every == 0 || step_ % every != 0) return;
+  const uint64_t bytes = n_ * 4;
+  if (!d_dig_) d_dig_ = static_cast<uint64_t*>(dalloc(8 * (4 + fnv1a_chunked_scratch(bytes))));
+  fnv1a_chunked(params_, bytes, d_dig_ + 4, d_dig_, s_main_);
+  HP_CUDA(cudaMemcpyAsync(d_dig_ + 1, d_dig_, 8, cudaMemcpyDeviceToDevice, s_main_));
+  HP_NCCL(ncclBroadcast(d_dig_ + 1, d_dig_ + 1, 1, ncclUint64, 0, comm_->nccl, s_main_));
+  double* bad = reinterpret_cast<double*>(d_dig_ + 2);
+  digest_mismatch(d_dig_, bad, s_main_);
+  HP_NCCL(ncclAllReduce(bad, bad, 1, ncclDouble, ncclSum, comm_->nccl, s_main_));
+  double h = 0;
+  HP_CUDA(cudaMemcpyAsync(&h, bad, 8, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  if (h != 0.0)
+    fail(HP_ENUMERIC, std::to_string(static_cast<int>(h)) +
+                          " ranks diverged from master parameters at step " + std::to_string(step_));
+}
+
 void Engine::round_sync(hp_round_out* out) {
   if (!in_flight_) fail(HP_ECONFIG, "round_sync without a round in flight");
   HP_CUDA(cudaEventSynchronize(ev_done_));
@@ -1371,6 +1397,7 @@ void Engine::round_sync(hp_round_out* out) {
     fail(HP_ENUMERIC, "total batch weight is zero: every rank was dummy");
   }
   if (h_flags_[1]) fail(HP_ENUMERIC, "non-finite gradient at step " + std::to_string(step_));
+  if (last_final_) check_digest_on_cadence();
   if (out) {
     // K > 1: the report covers the K rounds (loss_sum / weight of the flush)
     const bool totals = last_final_ && x_.update_freq > 1;

@@ -45,6 +45,10 @@ class Engine {
   void load_checkpoint(const std::string& path, hp_ckpt_desc* out);
   void set_capture(bool on) { capture_ = on; }
   void set_grad_comm(bool on) { grad_comm_ = on; }
+  void set_digest_check(uint64_t every, bool debug) {
+    check_every_ = every;
+    check_debug_ = debug;
+  }
   void get_local_grads(float* flat, uint64_t n);
   void stage_batch(const hp_batch& b);
   void round_async(int dummy, double lr);
@@ -183,6 +187,12 @@ class Engine {
   float* emb_gath_ = nullptr;  // [world][cap][d + 4]
   bool attn_long_ = false;  // 128 < max_seq <= 512: attention_*_long
   bool grad_comm_ = true;  // measurement toggle (hp_engine_set_grad_comm)
+  // check_digest_on_cadence (engine.hpp:170-184): every check_every_ updates
+  // (every update when check_debug_), N > 1
+  uint64_t check_every_ = 100;
+  bool check_debug_ = false;
+  uint64_t* d_dig_ = nullptr;  // [4 + chunks]: mine, master, bad (double)
+  void check_digest_on_cadence();
   float* local_grads_ = nullptr;
   uint64_t step_ = 0, adam_t_ = 0;
   bool in_flight_ = false;

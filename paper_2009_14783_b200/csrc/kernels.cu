@@ -1670,6 +1670,51 @@ __global__ void fnv_kernel(const uint8_t* p, uint64_t n, uint64_t* out) {
   }
   *out = h;
 }
+// FNV-1a of each `chunk`-byte block (one thread per block, bytes in order)
+__global__ void fnv_chunks_kernel(const uint8_t* __restrict__ p, uint64_t n, uint64_t chunk,
+                                  uint64_t nchunks, uint64_t* __restrict__ out) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  const uint8_t* q = p + c * chunk;
+  const uint64_t m = min(chunk, n - c * chunk);
+  uint64_t h = 0xcbf29ce484222325ull;
+  uint64_t i = 0;
+  for (; i + 16 <= m; i += 16) {
+    const uint4 v = *reinterpret_cast<const uint4*>(q + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        h ^= (w[k] >> (8 * b)) & 0xffu;
+        h *= 0x100000001b3ull;
+      }
+  }
+  for (; i < m; ++i) {
+    h ^= q[i];
+    h *= 0x100000001b3ull;
+  }
+  out[c] = h;
+}
+__global__ void digest_mismatch_kernel(const uint64_t* d, double* bad) {
+  *bad = d[0] == d[1] ? 0.0 : 1.0;
+}
+void fnv1a_chunked(const void* p, uint64_t n, uint64_t* scratch, uint64_t* out, cudaStream_t s) {
+  constexpr uint64_t kChunk = 65536;
+  const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+  fnv_chunks_kernel<<<(unsigned)((nchunks + 127) / 128), 128, 0, s>>>(
+      static_cast<const uint8_t*>(p), n, kChunk, nchunks, scratch);
+  LAUNCH_CHECK();
+  count_launch();
+  fnv1a(reinterpret_cast<const uint8_t*>(scratch), nchunks * 8, out, s);
+}
+size_t fnv1a_chunked_scratch(uint64_t n) { return (n + 65535) / 65536; }
+void digest_mismatch(const uint64_t* d, double* bad, cudaStream_t s) {
+  digest_mismatch_kernel<<<1, 1, 0, s>>>(d, bad);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
 void fnv1a(const uint8_t* p, uint64_t n, uint64_t* out, cudaStream_t s) {
   fnv_kernel<<<1, 1, 0, s>>>(p, n, out);
   LAUNCH_CHECK();

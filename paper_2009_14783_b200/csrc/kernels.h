@@ -222,6 +222,12 @@ void refresh_shadow(const float* p, void* shadow, const uint64_t* seg_table,
 void fill_f32(float* p, uint64_t n, float v, cudaStream_t s);
 // FNV-1a over bytes (params_digest) -- single-thread kernel, off the hot path.
 void fnv1a(const uint8_t* p, uint64_t n, uint64_t* out, cudaStream_t s);
+// parallel digest for the cross-rank cadence check: FNV-1a over the FNV-1a
+// values of 64 KB blocks (scratch: fnv1a_chunked_scratch(n) u64); *bad =
+// (d[0] != d[1]) as a double
+void fnv1a_chunked(const void* p, uint64_t n, uint64_t* scratch, uint64_t* out, cudaStream_t s);
+size_t fnv1a_chunked_scratch(uint64_t n);
+void digest_mismatch(const uint64_t* d, double* bad, cudaStream_t s);
 
 uint64_t kernel_launch_count();
 void count_launch(int n = 1);

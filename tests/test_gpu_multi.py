@@ -204,3 +204,60 @@ def test_row_sparse_embedding_exchange_matches_dense(tmp_path):
     a, b = np.array(r0["1"]["losses"]), np.array(r0["0"]["losses"])
     assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5
     assert rel_norm(np.load(tmp_path / "p1.npy"), np.load(tmp_path / "p0.npy")) <= 1e-5
+
+
+DIGEST_WORKER = r'''
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.environ["HP_ROOT"]); sys.path.insert(0, os.path.join(os.environ["HP_ROOT"], "tests"))
+import torch, torch.distributed as dist
+import paper_2009_14783_b200 as hp
+from helpers import C1_GEN, C1_SPEC
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+torch.cuda.set_device(rank)
+comm = hp.Communicator(world, rank, rank)
+eng = hp.StepEngine(hp.ModelSpec(**C1_SPEC), hp.OptimConfig("adam", 0.9, 0.98, 1e-9),
+                    hp.ExecConfig(compute="f32", device=rank, max_tokens=1024, max_batch=16, max_masks=256),
+                    comm=comm, seed=21 if rank == 0 else None)
+eng.broadcast_params(0)
+eng.set_digest_check(1, debug=True)   # every update
+rec = hp.generate_mlm_records(hp.MlmGenConfig(**C1_GEN))
+plan = hp.build_epoch_batches(rec.token_lengths(), 8, 0, 21, 0)
+sched = hp.partition_for_rank(plan, world, rank)
+out = {"clean": []}
+for s in range(3):
+    out["clean"].append(eng.round(rec.batch(plan.batches[sched[s].batch_index]), sched[s].dummy, 1e-3).loss)
+# rank 1 drifts (parameters not broadcast): the next update's check fails on every rank
+if rank == 1:
+    p = eng.get_params().astype(np.float64)
+    p[7] += 1e-3
+    eng.set_params(p)
+try:
+    eng.round(rec.batch(plan.batches[sched[3].batch_index]), sched[3].dummy, 1e-3)
+    out["drift"] = "accepted"
+except hp.NumericError as e:
+    out["drift"] = str(e)
+with open(os.environ["HP_OUT"] + f"/dg{rank}.json", "w") as f:
+    json.dump(out, f)
+eng.close(); comm.close()
+dist.destroy_process_group()
+'''
+
+
+def test_digest_cadence_check_detects_divergence(tmp_path):
+    """check_digest_on_cadence (engine.hpp:170-184) inside round(): clean
+    rounds pass; a rank whose parameters drifted makes every rank raise the
+    reference's numeric error."""
+    script = tmp_path / "digest_worker.py"
+    script.write_text(DIGEST_WORKER)
+    env = dict(os.environ, HP_ROOT=ROOT, HP_OUT=str(tmp_path))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29523", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    r0 = json.loads((tmp_path / "dg0.json").read_text())
+    r1 = json.loads((tmp_path / "dg1.json").read_text())
+    assert r0["clean"] == r1["clean"] and len(r0["clean"]) == 3
+    for r in (r0, r1):
+        assert "1 ranks diverged from master parameters at step 4" in r["drift"], r["drift"]
