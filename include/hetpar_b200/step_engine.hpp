@@ -156,11 +156,14 @@ class Communicator {
 // identical optimizer update; returns the update's StepReport.
 class DeviceStepEngine {
  public:
+  // check_interval / debug: the reference StepEngine's digest cadence
+  // (engine.hpp:117-123, 170-184)
   DeviceStepEngine(const ModelSpec& spec, const hp_optim_desc& opt, const hp_exec_desc& exec,
-                   Communicator* comm = nullptr)
+                   Communicator* comm = nullptr, uint64_t check_interval = 100, bool debug = false)
       : n_(flat_size(spec)) {
     const hp_model_desc d = spec.desc();
     check(hp_engine_create(&d, &opt, &exec, comm ? comm->handle() : nullptr, &h_));
+    check(hp_engine_set_digest_check(h_, check_interval, debug ? 1 : 0));
   }
   ~DeviceStepEngine() { if (h_) hp_engine_destroy(h_); }
   DeviceStepEngine(const DeviceStepEngine&) = delete;
