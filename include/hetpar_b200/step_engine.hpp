@@ -76,6 +76,7 @@ using Batch = std::vector<Instance>;
 struct StepReport {
   uint64_t step = 0;
   double loss = 0.0, weight = 0.0, seconds = 0.0;
+  std::vector<double> rank_seconds;  // master only (gather_scalars), engine.hpp:158-162
 };
 
 inline uint64_t flat_size(const ModelSpec& s) {
@@ -139,9 +140,12 @@ class Communicator {
     check(hp_comm_unique_id(id.data()));
     return id;
   }
-  Communicator(int world, int rank, int device, const std::vector<uint8_t>& id) {
+  Communicator(int world, int rank, int device, const std::vector<uint8_t>& id)
+      : world_(world), rank_(rank) {
     check(hp_comm_create(world, rank, device, id.data(), &h_));
   }
+  int world() const { return world_; }
+  int rank() const { return rank_; }
   ~Communicator() { if (h_) hp_comm_destroy(h_); }
   Communicator(const Communicator&) = delete;
   Communicator& operator=(const Communicator&) = delete;
@@ -149,6 +153,7 @@ class Communicator {
 
  private:
   hp_comm* h_ = nullptr;
+  int world_ = 1, rank_ = 0;
 };
 
 // StepEngine<T> on the device: round(batch, dummy) = forward -> [loss, weight]
@@ -160,7 +165,7 @@ class DeviceStepEngine {
   // (engine.hpp:117-123, 170-184)
   DeviceStepEngine(const ModelSpec& spec, const hp_optim_desc& opt, const hp_exec_desc& exec,
                    Communicator* comm = nullptr, uint64_t check_interval = 100, bool debug = false)
-      : n_(flat_size(spec)) {
+      : n_(flat_size(spec)), comm_(comm) {
     const hp_model_desc d = spec.desc();
     check(hp_engine_create(&d, &opt, &exec, comm ? comm->handle() : nullptr, &h_));
     check(hp_engine_set_digest_check(h_, check_interval, debug ? 1 : 0));
@@ -183,7 +188,9 @@ class DeviceStepEngine {
   }
 
   std::optional<StepReport> round(const Batch& batch, bool dummy, double lr) {
-    const auto t0 = std::chrono::steady_clock::now();
+    // seconds run from the update group's first round (engine.hpp:126)
+    if (!in_group_) group_start_ = std::chrono::steady_clock::now();
+    in_group_ = true;
     std::vector<uint64_t> tok_off{0}, mask_off{0};
     std::vector<int64_t> tokens, segments, mpos, morig, label;
     for (const auto& in : batch) {
@@ -205,17 +212,28 @@ class DeviceStepEngine {
     hp_round_out o{};
     check(hp_engine_round(h_, dummy ? 1 : 0, lr, &o));
     if (!o.updated) return std::nullopt;
+    in_group_ = false;
     StepReport r;
     r.step = o.step;
     r.loss = o.loss;
     r.weight = o.weight;
-    r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - group_start_).count();
+    if (comm_) {  // the per-rank seconds reach the master (group_.gather_scalars)
+      std::vector<double> all(static_cast<size_t>(comm_->world()));
+      check(hp_pg_gather_scalars(comm_->handle(), r.seconds, all.data()));
+      if (comm_->rank() == 0) r.rank_seconds = std::move(all);
+    } else {
+      r.rank_seconds = {r.seconds};
+    }
     return r;
   }
 
  private:
   hp_engine* h_ = nullptr;
   uint64_t n_;
+  Communicator* comm_ = nullptr;
+  bool in_group_ = false;
+  std::chrono::steady_clock::time_point group_start_{};
 };
 
 }  // namespace hetpar::b200

@@ -826,7 +826,16 @@ class StepEngine:
             return None
         rep.seconds = time.perf_counter() - self._group_t0
         self._group_t0 = None
+        self._gather_seconds(rep)
         return rep
+
+    def _gather_seconds(self, rep: StepReport) -> None:
+        # rank_seconds: every rank's seconds on the master (group_.gather_scalars,
+        # engine.hpp:158-162); a collective on the communicator
+        if self.comm is not None and self.comm.world > 1:
+            rep.rank_seconds = self.comm.gather_scalars(rep.seconds)
+        else:
+            rep.rank_seconds = [rep.seconds]
 
     def rounds(self, work) -> list:
         """round() over a sequence of (batch, dummy, lr), pipelined: while the
@@ -853,6 +862,7 @@ class StepEngine:
             if rep.updated:
                 rep.seconds = time.perf_counter() - self._group_t0
                 self._group_t0 = None
+                self._gather_seconds(rep)
                 out.append(rep)
             else:
                 out.append(None)

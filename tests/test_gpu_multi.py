@@ -40,12 +40,14 @@ for step in range(10):
     rb = sched[step]
     rep = eng.round(rec.batch(plan.batches[rb.batch_index]), rb.dummy, 1e-3)
     losses.append(rep.loss)
+rank_seconds = rep.rank_seconds  # gathered on the master only (engine.hpp:158-162)
 digest = eng.digest()
 p = eng.get_params()
 # a round where rank 1 is a dummy: must equal rank 0 training alone (W=1 math)
 rb0 = plan.batches[0]
 rep = eng.round(rec.batch(rb0), rank == 1, 1e-3)
-out = {"losses": losses, "digest": digest, "dummy_loss": rep.loss, "dummy_weight": rep.weight}
+out = {"losses": losses, "digest": digest, "dummy_loss": rep.loss, "dummy_weight": rep.weight,
+       "rank_seconds": rank_seconds}
 # the bucketed-allreduce measurement (bench.py / tools/allreduce_sweep.py): 4 MiB in 1 MiB buckets
 ar = comm.allreduce_bench(1 << 22, 1.0, iters=2, warmup=1)
 out["ar_ok"] = ar["ms"] > 0 and ar["busbw_gbps"] > 0
@@ -77,6 +79,8 @@ def test_c1_w2_nccl_matches_reference(tmp_path):
     assert rel_norm(p, t["params_f64_as_f32"]) <= 1e-4
     assert r0["dummy_weight"] == 8.0             # only rank 0's 8 sentences count
     assert r0["ar_ok"] and r1["ar_ok"]
+    assert len(r0["rank_seconds"]) == 2 and all(t > 0 for t in r0["rank_seconds"])
+    assert r1["rank_seconds"] == []
 
 
 PG_WORKER = r'''
