@@ -8,3 +8,8 @@ from .api import *  # noqa: F401,F403
 from .api import __all__ as _api_all
 
 __all__ = list(_api_all)
+from .trainer import (EngineConfig, RunReport, checkpoint_final_path,  # noqa: F401
+                      checkpoint_step_path, train_run)
+
+__all__ += ["EngineConfig", "RunReport", "train_run", "checkpoint_step_path",
+            "checkpoint_final_path"]

@@ -448,3 +448,47 @@ def test_c1_trained_from_shards_matches_reference(tmp_path):
         losses.append(rep.loss)
     assert np.max(np.abs(np.array(losses) - t["losses_f64"]) / np.abs(t["losses_f64"])) <= 1e-4
     assert rel_norm(eng.get_params(), t["params_f64_as_f32"]) <= 1e-4
+
+
+def _c1_run_config(tmp_path, **kw):
+    from paper_2009_14783_b200 import api
+    d = tmp_path / "shards"
+    if not d.exists():
+        api.write_mlm_shards(str(d), hp.generate_mlm_records(hp.MlmGenConfig(**C1_GEN)), 4)
+    base = dict(spec=hp.ModelSpec(**C1_SPEC), opt_kind="adam", beta1=0.9, beta2=0.98, eps=1e-9,
+                sched=hp.SchedulerConfig("fixed", 1e-3), seed=21, data_dir=str(d), max_sentences=8,
+                update_freq=2, max_steps=10)
+    base.update(kw)
+    return hp.EngineConfig(**base)
+
+
+def test_train_run_matches_reference_trajectory(tmp_path):
+    """train_run (engine.hpp:197-330) end to end on one GPU -- shards, epoch
+    plans, the rank's loader, scheduled lr, the update protocol -- at W = 1,
+    K = 2, which is the reference's W = 2 run (W x K equivalence)."""
+    rep = hp.train_run(_c1_run_config(tmp_path), exec_cfg=hp.ExecConfig(compute="f32"))
+    t = golden("c1_ref_train.npz")
+    losses = np.array([s.loss for s in rep.steps])
+    assert rep.steps_run == 10 and rep.final_step == 10 and rep.world == 1
+    assert [s.step for s in rep.steps] == list(range(1, 11))
+    assert np.max(np.abs(losses - t["losses_f64"]) / np.abs(t["losses_f64"])) <= 1e-4
+    assert rep.final_loss == rep.steps[-1].loss
+
+
+def test_train_run_checkpoint_resume_is_exact(tmp_path):
+    """Checkpoints every 4 updates and at the end; resuming from step 4
+    (resume fast-forward, engine.hpp:211-245) reaches the same final state
+    bit for bit."""
+    from paper_2009_14783_b200 import api
+    ck_a, ck_b = tmp_path / "a", tmp_path / "b"
+    ra = hp.train_run(_c1_run_config(tmp_path, checkpoint_dir=str(ck_a), checkpoint_interval=4),
+                      exec_cfg=hp.ExecConfig(compute="f32"))
+    assert (ck_a / "checkpoint_000004.hck").exists() and (ck_a / "checkpoint_000008.hck").exists()
+    rb = hp.train_run(_c1_run_config(tmp_path, checkpoint_dir=str(ck_b),
+                                     resume_path=str(ck_a / "checkpoint_000004.hck")),
+                      exec_cfg=hp.ExecConfig(compute="f32"))
+    assert [s.step for s in rb.steps] == list(range(5, 11))
+    assert [s.loss for s in rb.steps] == [s.loss for s in ra.steps[4:]]
+    _, _, pa, ma, va = api.read_checkpoint(str(ck_a / "checkpoint_final.hck"))
+    _, _, pb, mb, vb = api.read_checkpoint(str(ck_b / "checkpoint_final.hck"))
+    assert np.array_equal(pa, pb) and np.array_equal(ma, mb) and np.array_equal(va, vb)

@@ -11,7 +11,7 @@ import sys
 import numpy as np
 import pytest
 
-from helpers import ROOT, golden, rel_norm
+from helpers import C1_GEN, ROOT, golden, rel_norm
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
@@ -265,3 +265,51 @@ def test_digest_cadence_check_detects_divergence(tmp_path):
     assert r0["clean"] == r1["clean"] and len(r0["clean"]) == 3
     for r in (r0, r1):
         assert "1 ranks diverged from master parameters at step 4" in r["drift"], r["drift"]
+
+
+TRAIN_WORKER = r'''
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.environ["HP_ROOT"]); sys.path.insert(0, os.path.join(os.environ["HP_ROOT"], "tests"))
+import torch, torch.distributed as dist
+import paper_2009_14783_b200 as hp
+from helpers import C1_GEN, C1_SPEC
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+torch.cuda.set_device(rank)
+comm = hp.Communicator(world, rank, rank)
+cfg = hp.EngineConfig(spec=hp.ModelSpec(**C1_SPEC), opt_kind="adam", sched=hp.SchedulerConfig("fixed", 1e-3),
+                      seed=21, data_dir=os.environ["HP_SHARDS"], max_sentences=8, update_freq=1,
+                      max_steps=10, checkpoint_dir=os.environ["HP_OUT"] + "/ck", debug_checks=True)
+rep = hp.train_run(cfg, comm=comm, exec_cfg=hp.ExecConfig(compute="f32", device=rank))
+with open(os.environ["HP_OUT"] + f"/tr{rank}.json", "w") as f:
+    json.dump({"losses": [s.loss for s in rep.steps], "final_step": rep.final_step,
+               "rank_seconds": [len(s.rank_seconds) for s in rep.steps]}, f)
+comm.close()
+dist.destroy_process_group()
+'''
+
+
+def test_train_run_w2_nccl_matches_reference(tmp_path):
+    """The reference's train_run at W = 2 over NCCL (digest checked every
+    update): the reference trajectory on both ranks, the final checkpoint
+    written by rank 0 holding the reference's parameters."""
+    from paper_2009_14783_b200 import api
+    shards = tmp_path / "shards"
+    api.write_mlm_shards(str(shards), api.generate_mlm_records(api.MlmGenConfig(**C1_GEN)), 4)
+    script = tmp_path / "train_worker.py"
+    script.write_text(TRAIN_WORKER)
+    env = dict(os.environ, HP_ROOT=ROOT, HP_OUT=str(tmp_path), HP_SHARDS=str(shards))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29525", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    t = golden("c1_ref_train.npz")
+    r0 = json.loads((tmp_path / "tr0.json").read_text())
+    r1 = json.loads((tmp_path / "tr1.json").read_text())
+    assert r0["losses"] == r1["losses"] and r0["final_step"] == 10
+    assert np.max(np.abs(np.array(r0["losses"]) - t["losses_f64"]) / np.abs(t["losses_f64"])) <= 1e-4
+    assert r0["rank_seconds"] == [2] * 10 and r1["rank_seconds"] == [0] * 10
+    _, meta, p, _, _ = api.read_checkpoint(str(tmp_path / "ck" / "checkpoint_final.hck"))
+    assert meta.step == 10 and meta.world_size == 2
+    assert rel_norm(p, t["params_f64_as_f32"]) <= 1e-4
