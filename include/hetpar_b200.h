@@ -348,6 +348,40 @@ hp_status hp_engine_io_bytes(hp_engine* e, uint64_t* h2d, uint64_t* d2h);
  * backward.  Ranks then diverge; default on. */
 hp_status hp_engine_set_grad_comm(hp_engine* e, int on);
 
+
+/* ------------------------------------------------------------------------
+ * Operator table: hetpar::kern (include/hetpar/kernels.hpp:44-68,
+ * src/kernels_scalar.cpp) on DEVICE pointers, ordered on `stream` (NULL: the
+ * legacy default stream); a reduction writes its scalar to device memory.
+ * Bit-identical to the reference's kernels: explicitly rounded operations
+ * (no FMA), IEEE sqrt / divide, and the reference's lane contract for
+ * reductions (L = 8 lanes for f32, 4 for f64 over the leading multiple-of-L
+ * prefix, lanes folded left to right, then the tail in order) -- sequential
+ * per lane by definition, so reductions run L threads wide.
+ * ---------------------------------------------------------------------- */
+hp_status hp_kern_dot_f32(const float* a, const float* b, uint64_t n, float* out, void* stream);
+hp_status hp_kern_sum_f32(const float* a, uint64_t n, float* out, void* stream);
+hp_status hp_kern_maxv_f32(const float* a, uint64_t n, float* out, void* stream);
+hp_status hp_kern_add_f32(const float* a, const float* b, float* out, uint64_t n, void* stream);
+hp_status hp_kern_scale_f32(const float* a, float s, float* out, uint64_t n, void* stream);
+hp_status hp_kern_axpy_f32(float alpha, const float* x, float* y, uint64_t n, void* stream);
+hp_status hp_kern_relu_f32(const float* a, float* out, uint64_t n, void* stream);
+hp_status hp_kern_relu_bwd_f32(const float* a, const float* g, float* da, uint64_t n, void* stream);
+hp_status hp_kern_sgd_update_f32(float* p, const float* g, uint64_t n, float lr, void* stream);
+hp_status hp_kern_adam_update_f32(float* p, float* m, float* v, const float* g, uint64_t n, float lr, float b1,
+                                  float b2, float eps, float c1, float c2, void* stream);
+hp_status hp_kern_dot_f64(const double* a, const double* b, uint64_t n, double* out, void* stream);
+hp_status hp_kern_sum_f64(const double* a, uint64_t n, double* out, void* stream);
+hp_status hp_kern_maxv_f64(const double* a, uint64_t n, double* out, void* stream);
+hp_status hp_kern_add_f64(const double* a, const double* b, double* out, uint64_t n, void* stream);
+hp_status hp_kern_scale_f64(const double* a, double s, double* out, uint64_t n, void* stream);
+hp_status hp_kern_axpy_f64(double alpha, const double* x, double* y, uint64_t n, void* stream);
+hp_status hp_kern_relu_f64(const double* a, double* out, uint64_t n, void* stream);
+hp_status hp_kern_relu_bwd_f64(const double* a, const double* g, double* da, uint64_t n, void* stream);
+hp_status hp_kern_sgd_update_f64(double* p, const double* g, uint64_t n, double lr, void* stream);
+hp_status hp_kern_adam_update_f64(double* p, double* m, double* v, const double* g, uint64_t n, double lr, double b1,
+                                  double b2, double eps, double c1, double c2, void* stream);
+
 /* ------------------------------------------------------------------------
  * Test hooks (used by tests/ only): run one GEMM of the engine's dispatch on
  * caller-owned device buffers.  path: 0 auto, 1 SIMT fp32, 2 tcgen05.

@@ -173,6 +173,26 @@ _SIGS = {
     "hp_engine_io_bytes": [P, P, P],
     "hp_engine_set_grad_comm": [P, I],
     "hp_engine_set_digest_check": [P, U64, I],
+    "hp_kern_dot_f32": [P, P, U64, P, P],
+    "hp_kern_sum_f32": [P, U64, P, P],
+    "hp_kern_maxv_f32": [P, U64, P, P],
+    "hp_kern_add_f32": [P, P, P, U64, P],
+    "hp_kern_scale_f32": [P, C.c_float, P, U64, P],
+    "hp_kern_axpy_f32": [C.c_float, P, P, U64, P],
+    "hp_kern_relu_f32": [P, P, U64, P],
+    "hp_kern_relu_bwd_f32": [P, P, P, U64, P],
+    "hp_kern_sgd_update_f32": [P, P, U64, C.c_float, P],
+    "hp_kern_adam_update_f32": [P, P, P, P, U64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, P],
+    "hp_kern_dot_f64": [P, P, U64, P, P],
+    "hp_kern_sum_f64": [P, U64, P, P],
+    "hp_kern_maxv_f64": [P, U64, P, P],
+    "hp_kern_add_f64": [P, P, P, U64, P],
+    "hp_kern_scale_f64": [P, D, P, U64, P],
+    "hp_kern_axpy_f64": [D, P, P, U64, P],
+    "hp_kern_relu_f64": [P, P, U64, P],
+    "hp_kern_relu_bwd_f64": [P, P, P, U64, P],
+    "hp_kern_sgd_update_f64": [P, P, U64, D, P],
+    "hp_kern_adam_update_f64": [P, P, P, P, U64, D, D, D, D, D, D, P],
     "hp_debug_gemm": [I, I, I, I, P, I64, I, P, I64, I, I64, I64, P, I64, I, I64, I64, P, I, P, P,
                       I64, I, I, I],
     "hp_debug_sync": [],

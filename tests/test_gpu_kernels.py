@@ -344,3 +344,108 @@ def _multicast_cases():
                                     (256, 512, 256, 0, 0, 0)]:
         res = run_gemm(M, N, K, torch.bfloat16, at, bt, path=0, c_dtype=torch.float32, c_group=cgrp, seed=7)
         _check(res, torch.bfloat16, K)
+
+
+def _kern_ref(name, dt, a, b, y, s, extra=None):
+    """numpy restatement of hetpar::kern::scalar (kernels_scalar.cpp:12-83):
+    IEEE-rounded elementwise ops, the L-lane reduction order."""
+    T = dt.type
+    L = 8 if dt == np.float32 else 4
+    n = len(a)
+    n0 = n - n % L
+    if name in ("dot", "sum", "maxv"):
+        acc = np.full(L, -np.inf if name == "maxv" else 0, dt)
+        for i in range(0, n0, L):
+            if name == "dot":
+                acc = acc + a[i:i + L] * b[i:i + L]
+            elif name == "sum":
+                acc = acc + a[i:i + L]
+            else:
+                acc = np.where(a[i:i + L] > acc, a[i:i + L], acc)
+        r = acc[0]
+        for k in range(1, L):
+            r = (acc[k] if acc[k] > r else r) if name == "maxv" else T(r + acc[k])
+        for i in range(n0, n):
+            if name == "dot":
+                r = T(r + T(a[i] * b[i]))
+            elif name == "sum":
+                r = T(r + a[i])
+            else:
+                r = a[i] if a[i] > r else r
+        return np.array([r], dt)
+    if name == "add":
+        return a + b
+    if name == "scale":
+        return a * T(s)
+    if name == "axpy":
+        return y + T(s) * a
+    if name == "relu":
+        return np.where(a > 0, a, T(0))
+    if name == "relu_bwd":
+        return y + np.where(a > 0, b, T(0))
+    if name == "sgd_update":
+        return y - T(s) * a
+    raise ValueError(name)
+
+
+@pytest.mark.parametrize("sfx", ["f32", "f64"])
+def test_operator_table_bit_exact_vs_reference_kernels(sfx):
+    """hp_kern_* (the reference's operator table on device pointers) equal
+    the reference's scalar kernels bit for bit, tails included."""
+    L = _lib()
+    dt = np.dtype(np.float32 if sfx == "f32" else np.float64)
+    tdt = torch.float32 if sfx == "f32" else torch.float64
+    rng = np.random.default_rng(3)
+    n = 1003
+    a = rng.standard_normal(n).astype(dt)
+    b = rng.standard_normal(n).astype(dt)
+    y = rng.standard_normal(n).astype(dt)
+    cs = C.c_float if sfx == "f32" else C.c_double
+    keep = []  # device copies stay alive until the kernels that read them have run
+
+    def dev(x):
+        t = torch.from_numpy(x.copy()).to("cuda")
+        keep.append(t)
+        return t
+    for name in ("dot", "sum", "maxv"):
+        out = torch.zeros(1, dtype=tdt, device="cuda")
+        args = (_ptr(dev(a)), _ptr(dev(b))) if name == "dot" else (_ptr(dev(a)),)
+        L.call(f"hp_kern_{name}_{sfx}", *args, n, _ptr(out), None)
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == _kern_ref(name, dt, a, b, y, 0).tobytes(), name
+    s = dt.type(0.37)
+    cases = {"add": lambda o: (_ptr(dev(a)), _ptr(dev(b)), _ptr(o), n),
+             "scale": lambda o: (_ptr(dev(a)), cs(s), _ptr(o), n),
+             "relu": lambda o: (_ptr(dev(a)), _ptr(o), n)}
+    for name, argf in cases.items():
+        o = torch.zeros(n, dtype=tdt, device="cuda")
+        L.call(f"hp_kern_{name}_{sfx}", *argf(o), None)
+        torch.cuda.synchronize()
+        assert o.cpu().numpy().tobytes() == _kern_ref(name, dt, a, b, y, s).tobytes(), name
+    yy = dev(y)
+    L.call(f"hp_kern_axpy_{sfx}", cs(s), _ptr(dev(a)), _ptr(yy), n, None)
+    torch.cuda.synchronize()
+    assert yy.cpu().numpy().tobytes() == _kern_ref("axpy", dt, a, b, y, s).tobytes()
+    yy = dev(y)
+    L.call(f"hp_kern_relu_bwd_{sfx}", _ptr(dev(a)), _ptr(dev(b)), _ptr(yy), n, None)
+    torch.cuda.synchronize()
+    assert yy.cpu().numpy().tobytes() == _kern_ref("relu_bwd", dt, a, b, y, 0).tobytes()
+    yy = dev(y)
+    L.call(f"hp_kern_sgd_update_{sfx}", _ptr(yy), _ptr(dev(a)), n, cs(s), None)
+    torch.cuda.synchronize()
+    assert yy.cpu().numpy().tobytes() == _kern_ref("sgd_update", dt, a, b, y, s).tobytes()
+    # adam_update (kernels_scalar.cpp:74-83)
+    T = dt.type
+    p, m, v, g = (rng.standard_normal(n).astype(dt) for _ in range(4))
+    v = np.abs(v)
+    lr, b1, b2, eps, c1, c2 = (T(x) for x in (1e-3, 0.9, 0.98, 1e-9, 1 / (1 - 0.9 ** 3), 1 / (1 - 0.98 ** 3)))
+    dp, dm, dv = dev(p), dev(m), dev(v)
+    L.call(f"hp_kern_adam_update_{sfx}", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(dev(g)), n,
+           *(cs(x) for x in (lr, b1, b2, eps, c1, c2)), None)
+    torch.cuda.synchronize()
+    m2 = b1 * m + (T(1) - b1) * g
+    v2 = b2 * v + (T(1) - b2) * (g * g)
+    p2 = p - lr * ((m2 * c1) / (np.sqrt(v2 * c2) + eps))
+    assert dm.cpu().numpy().tobytes() == m2.tobytes()
+    assert dv.cpu().numpy().tobytes() == v2.tobytes()
+    assert dp.cpu().numpy().tobytes() == p2.tobytes()
