@@ -311,6 +311,10 @@ hp_status hp_engine_stage_batch(hp_engine* e, const hp_batch* b);
  * /sum(weight) and the optimizer update.  lr = scheduled_lr(P+1).  _async
  * enqueues only; _sync waits and fills out (and raises numeric errors the way
  * engine.hpp:134-138 does). hp_engine_round = async + sync. */
+/* model_forward (model.hpp:260-390) on the staged batch alone: its summed
+ * loss (ForwardResult::loss_sum) and weight; no backward, no collective, no
+ * update (evaluation). */
+hp_status hp_engine_forward(hp_engine* e, double* loss_sum, double* weight);
 hp_status hp_engine_round_async(hp_engine* e, int dummy, double lr);
 hp_status hp_engine_round_sync(hp_engine* e, hp_round_out* out);
 hp_status hp_engine_round(hp_engine* e, int dummy, double lr, hp_round_out* out);

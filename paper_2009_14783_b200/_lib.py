@@ -173,6 +173,7 @@ _SIGS = {
     "hp_engine_io_bytes": [P, P, P],
     "hp_engine_set_grad_comm": [P, I],
     "hp_engine_set_digest_check": [P, U64, I],
+    "hp_engine_forward": [P, P, P],
     "hp_kern_dot_f32": [P, P, U64, P, P],
     "hp_kern_sum_f32": [P, U64, P, P],
     "hp_kern_maxv_f32": [P, U64, P, P],

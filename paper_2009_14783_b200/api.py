@@ -760,6 +760,14 @@ class StepEngine:
     def set_capture(self, on: bool):
         call("hp_engine_set_capture", self._h, int(on))
 
+    def forward(self, batch) -> tuple:
+        """model_forward (model.hpp:260-390) alone: (loss_sum, weight) of the
+        batch under the current parameters; no backward, collective or update."""
+        self.stage(batch)
+        ls, w = C.c_double(), C.c_double()
+        call("hp_engine_forward", self._h, C.byref(ls), C.byref(w))
+        return ls.value, w.value
+
     def set_digest_check(self, every: int = 100, debug: bool = False):
         """check_digest_on_cadence (engine.hpp:170-184): after every `every`-th
         update (each update with debug) the ranks compare parameter digests

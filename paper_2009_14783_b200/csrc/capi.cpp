@@ -283,6 +283,13 @@ hp_status hp_engine_set_capture(hp_engine* e, int on) {
   E.set_capture(on != 0);
   HP_API_END
 }
+hp_status hp_engine_forward(hp_engine* e, double* loss_sum, double* weight) {
+  HP_API_BEGIN
+  ENG(e);
+  if (!loss_sum || !weight) hp::fail(HP_ECONFIG, "hp_engine_forward: null output");
+  E.forward_only(loss_sum, weight);
+  HP_API_END
+}
 hp_status hp_engine_set_digest_check(hp_engine* e, uint64_t every, int debug) {
   HP_API_BEGIN
   ENG(e);

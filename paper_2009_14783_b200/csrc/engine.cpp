@@ -326,7 +326,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   scratch_ = static_cast<float*>(dalloc(scratch * 4));
   if (wg_on_) scratch_wg_ = static_cast<float*>(dalloc(colsum_scratch_floats((int)T, F_) * 4));
   // [round loss, round weight, local loss, local weight, K-total loss, K-total weight]
-  d_lw_ = static_cast<double*>(dalloc(6 * 8));
+  d_lw_ = static_cast<double*>(dalloc(8 * 8));  // [0,6): round scalars, [6]: forward_only
   HP_CUDA(cudaMemset(d_lw_, 0, 6 * 8));
   if (x_.update_freq > 1) {
     acc_grads_ = static_cast<float*>(dalloc(n_ * 4));
@@ -1375,6 +1375,22 @@ void Engine::check_digest_on_cadence() {
   if (h != 0.0)
     fail(HP_ENUMERIC, std::to_string(static_cast<int>(h)) +
                           " ranks diverged from master parameters at step " + std::to_string(step_));
+}
+
+// model_forward (model.hpp:260-390) alone on the staged batch: the summed
+// loss and the batch weight, no backward, no collective, no update.
+void Engine::forward_only(double* loss_sum, double* weight) {
+  if (!staged_) fail(HP_ECONFIG, "forward: no batch staged");
+  if (in_flight_) fail(HP_ECONFIG, "forward: a round is in flight");
+  HP_CUDA(cudaSetDevice(x_.device));
+  forward(false);
+  loss_reduce(row_loss_, batch_.M, row_loss_ + batch_.M, m_.with_nsp ? batch_.B : 0, d_lw_ + 6,
+              s_main_);
+  double h[2] = {0, 0};
+  HP_CUDA(cudaMemcpyAsync(h, d_lw_ + 6, 8, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaStreamSynchronize(s_main_));
+  *loss_sum = h[0];
+  *weight = local_weight_;
 }
 
 void Engine::round_sync(hp_round_out* out) {

@@ -53,6 +53,7 @@ class Engine {
   void stage_batch(const hp_batch& b);
   void round_async(int dummy, double lr);
   void round_sync(hp_round_out* out);
+  void forward_only(double* loss_sum, double* weight);
   uint64_t digest();
   uint64_t step() const { return step_; }
   void timers(bool on);

@@ -492,3 +492,24 @@ def test_train_run_checkpoint_resume_is_exact(tmp_path):
     _, _, pa, ma, va = api.read_checkpoint(str(ck_a / "checkpoint_final.hck"))
     _, _, pb, mb, vb = api.read_checkpoint(str(ck_b / "checkpoint_final.hck"))
     assert np.array_equal(pa, pb) and np.array_equal(ma, mb) and np.array_equal(va, vb)
+
+
+@pytest.mark.parametrize("compute", ["f32", "bf16"])
+def test_forward_only_matches_oracle_and_round(compute):
+    """StepEngine.forward = model_forward: the batch's summed loss and weight
+    without an update (parameters unchanged), equal to the oracle's and to
+    the local loss a round reports."""
+    spec, ospec, rec = _bert_case(d=128, heads=2, dff=256, vocab=203, n=16)
+    eng = hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(compute=compute, max_tokens=512,
+                                                               max_batch=16, max_masks=128), seed=9)
+    ids = np.arange(12)
+    d0 = eng.digest()
+    ls, w = eng.forward(rec.batch(ids))
+    assert eng.digest() == d0 and eng.step == 0
+    l, ow, _ = mo.forward_backward(ospec, mo.init_parameters(ospec, 9), _oracle_from_records(rec, ids),
+                                   need_grad=False)
+    tol = 1e-4 if compute == "f32" else 2e-2
+    assert abs(ls - l) <= tol * abs(l) and w == ow
+    rep = eng.round(rec.batch(ids), lr=1e-3)
+    assert rep.local_loss_sum == pytest.approx(ls, rel=1e-6)
+    eng.close()
