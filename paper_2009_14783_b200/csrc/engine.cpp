@@ -161,7 +161,21 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   }
 
   params_ = static_cast<float*>(dalloc(n_ * 4));
-  grads_ = static_cast<float*>(dalloc(n_ * 4));
+  {
+    // HP_NCCL_REG=1: the gradient buffer from ncclMemAlloc, registered with the
+    // communicator (zero-copy user-buffer collectives) -- A/B
+    const char* e = std::getenv("HP_NCCL_REG");
+    nccl_reg_ = comm_ && comm_->world > 1 && e && std::string(e) == "1";
+  }
+  if (nccl_reg_) {
+    void* g = nullptr;
+    HP_NCCL(ncclMemAlloc(&g, n_ * 4));
+    HP_CUDA(cudaMemset(g, 0, n_ * 4));
+    HP_NCCL(ncclCommRegister(comm_->nccl, g, n_ * 4, &grads_reg_));
+    grads_ = static_cast<float*>(g);
+  } else {
+    grads_ = static_cast<float*>(dalloc(n_ * 4));
+  }
   adam_m_ = static_cast<float*>(dalloc(n_ * 4));
   adam_v_ = static_cast<float*>(dalloc(n_ * 4));
   HP_CUDA(cudaMemset(params_, 0, n_ * 4));
@@ -370,6 +384,10 @@ Engine::~Engine() {
       cudaEventDestroy(pr.second);
     }
   for (void* p : allocs_) cudaFree(p);
+  if (nccl_reg_ && comm_) {
+    if (grads_reg_) ncclCommDeregister(comm_->nccl, grads_reg_);
+    ncclMemFree(grads_);
+  }
   for (int i = 0; i < kStageBufs; ++i) {
     if (h_stage_[i]) cudaFreeHost(h_stage_[i]);
     if (ev_stage_[i]) cudaEventDestroy(ev_stage_[i]);

@@ -188,6 +188,8 @@ class Engine {
   float* emb_gath_ = nullptr;  // [world][cap][d + 4]
   bool attn_long_ = false;  // 128 < max_seq <= 512: attention_*_long
   bool grad_comm_ = true;  // measurement toggle (hp_engine_set_grad_comm)
+  bool nccl_reg_ = false;      // grads_ from ncclMemAlloc + ncclCommRegister
+  void* grads_reg_ = nullptr;
   // check_digest_on_cadence (engine.hpp:170-184): every check_every_ updates
   // (every update when check_debug_), N > 1
   uint64_t check_every_ = 100;
