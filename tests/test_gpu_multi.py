@@ -313,3 +313,59 @@ def test_train_run_w2_nccl_matches_reference(tmp_path):
     _, meta, p, _, _ = api.read_checkpoint(str(tmp_path / "ck" / "checkpoint_final.hck"))
     assert meta.step == 10 and meta.world_size == 2
     assert rel_norm(p, t["params_f64_as_f32"]) <= 1e-4
+
+
+BF16_WORKER = r'''
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.environ["HP_ROOT"]); sys.path.insert(0, os.path.join(os.environ["HP_ROOT"], "tests"))
+import torch, torch.distributed as dist
+import paper_2009_14783_b200 as hp
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+torch.cuda.set_device(rank)
+comm = hp.Communicator(world, rank, rank)
+# the benchmark's execution path at small scale: bf16 tcgen05 GEMMs and
+# attention, weight-gradient stream, update stream, row-sparse embedding
+# exchange (embedding alone in the last bucket), K = 2 accumulation
+spec = hp.ModelSpec(arch="bert_encoder", d_model=128, heads=2, vocab=4000, max_seq=64, layers=2,
+                    d_ff=256, label_smooth_eps=0.1)
+rec = hp.generate_mlm_records(hp.MlmGenConfig(n=128, vocab=4000, min_sentence_words=10,
+                                              max_sentence_words=30, seed=3, max_seq_tokens=64))
+plan = hp.build_epoch_batches(rec.token_lengths(), 8, 0, 21, 0)
+sched = hp.partition_for_rank(plan, world, rank)
+eng = hp.StepEngine(spec, hp.OptimConfig("adam", 0.9, 0.98, 1e-9),
+                    hp.ExecConfig(compute="bf16", device=rank, max_tokens=512, max_batch=8,
+                                  max_masks=128, bucket_mb=0.5, update_freq=2),
+                    comm=comm, seed=21 if rank == 0 else None)
+eng.broadcast_params(0)
+eng.set_digest_check(1, debug=True)
+losses = []
+for s in range(8):
+    rep = eng.round(rec.batch(plan.batches[sched[s].batch_index]), sched[s].dummy, 1e-3)
+    if rep is not None:
+        losses.append(rep.loss)
+out = {"losses": losses, "digest": eng.digest()}
+with open(os.environ["HP_OUT"] + f"/bf{rank}.json", "w") as f:
+    json.dump(out, f)
+eng.close(); comm.close()
+dist.destroy_process_group()
+'''
+
+
+def test_bf16_benchmark_path_w2_ranks_identical(tmp_path):
+    """The benchmark's bf16 path at W = 2 with K = 2 (every stream, bucket and
+    exchange of the C2 step at small scale): identical reports and parameters
+    on both ranks, the digest checked on every update, a falling loss."""
+    script = tmp_path / "bf16_worker.py"
+    script.write_text(BF16_WORKER)
+    env = dict(os.environ, HP_ROOT=ROOT, HP_OUT=str(tmp_path))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29527", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    r0 = json.loads((tmp_path / "bf0.json").read_text())
+    r1 = json.loads((tmp_path / "bf1.json").read_text())
+    assert len(r0["losses"]) == 4
+    assert r0["losses"] == r1["losses"] and r0["digest"] == r1["digest"]
+    assert all(np.isfinite(r0["losses"]))
