@@ -299,7 +299,10 @@ __global__ void colsum_final_kernel(int chunks, int N, const float* __restrict__
 }
 
 static constexpr int kColRows = 64;
-constexpr int kLnBwdRows = 32;
+#ifndef HP_LN_BWD_ROWS
+#define HP_LN_BWD_ROWS 32
+#endif
+constexpr int kLnBwdRows = HP_LN_BWD_ROWS;  // rows per LayerNorm-backward CTA (multiple of 8)
 
 // Segment-embedding gradients in one pass: per 32-row chunk, the column sums
 // of the rows with segment 0 and with segment 1 (8 columns per thread), as
@@ -500,8 +503,10 @@ void col_sum(int R, int N, const void* x, int64_t ld, DType t, float* out,
 }
 
 size_t colsum_part_floats(int R, int N) {
-  const size_t chunks = (size_t)((R + 31) / 32);
-  return chunks * std::max<size_t>(3 * (size_t)N, (size_t)((N + 7) & ~7)) + 64;
+  // LayerNorm-backward partials ([R / kLnBwdRows][3N]) or column-sum partials ([R / 32][N8])
+  const size_t ln = (size_t)((R + kLnBwdRows - 1) / kLnBwdRows) * 3 * (size_t)N;
+  const size_t cs = (size_t)((R + 31) / 32) * (size_t)((N + 7) & ~7);
+  return std::max(ln, cs) + 64;
 }
 
 size_t colsum_scratch_floats(int R, int N) {
@@ -731,7 +736,10 @@ __device__ __forceinline__ void warp_bar_init(uint64_t* bar, int lane) {
   __syncwarp();
 }
 
-constexpr int kLnFwdRpw = 2;  // rows per warp (16 per CTA)
+#ifndef HP_LN_FWD_RPW
+#define HP_LN_FWD_RPW 2
+#endif
+constexpr int kLnFwdRpw = HP_LN_FWD_RPW;  // rows per warp (8 warps per CTA)
 template <int NV>
 __global__ void __launch_bounds__(256) ln_fwd_bulk(int T, const bf16* __restrict__ x,
                                                    const float* __restrict__ g,
