@@ -65,6 +65,7 @@ struct Params {
   const void* resid;
   int64_t ld_resid;
   int vec;  // C / aux / resid rows are 16-byte aligned
+  int split_boxes;  // operand tiles loaded as 64-row / one-atom TMA boxes
   int debug;  // profiling only: 0 normal, 1 skip TMA loads, 2 skip MMAs, 3 skip epilogue
   unsigned long long* trace;  // profiling only: CTA 0 clock64 timeline (see kTr*)
 };
@@ -742,6 +743,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             // B columns [128 i, +128) of the tile shared with the column peer
             if (!p.b_mn) tma_2d_mc(&map_b, bar, sb + mc_i * 16384, k0, bn0 + mc_i * 128, bmask);
             else tma_3d_mc(&map_b, bar, sb + mc_i * 16384, 0, k0, (bn0 + mc_i * 128) / 64, bmask);
+          } else if (p.split_boxes) {
+            // every operand tile as 64-row / one-atom boxes (8 KB per TMA
+            // instruction; HP_GEMM_SPLITBOX=1 -- A/B)
+            uint64_t* bar = &full[s];
+            uint32_t cbar = 0;
+            if constexpr (CG == 2) {
+              if (rank == 0) mbar_expect_tx(&full[s], 2 * kStageBytes);
+              cbar = mapa_shared(smem_u32(&full[s]), 0);
+            } else {
+              mbar_expect_tx(bar, kStageBytes);
+            }
+            auto ld2 = [&](const CUtensorMap* m, uint8_t* dst, int c0, int c1) {
+              if constexpr (CG == 2) tma_2d_cg2(m, cbar, dst, c0, c1); else tma_2d(m, bar, dst, c0, c1);
+            };
+            auto ld3 = [&](const CUtensorMap* m, uint8_t* dst, int c0, int c1, int c2) {
+              if constexpr (CG == 2) tma_3d_cg2(m, cbar, dst, c0, c1, c2); else tma_3d(m, bar, dst, c0, c1, c2);
+            };
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (!p.a_mn) ld2(&map_a, sa + h * 8192, k0, am0 + 64 * h);
+              else if (p.a_atoms) ld3(&map_a, sa + h * 8192, 0, k0, am0 / 64 + h);
+              else ld2(&map_a, sa + h * 8192, am0 + 64 * h, k0);
+            }
+#pragma unroll
+            for (int j = 0; j < BNL / 64; ++j) {
+              if (!p.b_mn) {
+                if (p.b_grouped) ld3(&map_b, sb + j * 8192, 0, bn0 + 64 * j, kb);
+                else ld2(&map_b, sb + j * 8192, k0, bn0 + 64 * j);
+              } else if (p.b_atoms) {
+                ld3(&map_b, sb + j * 8192, 0, k0, bn0 / 64 + j);
+              } else {
+                ld2(&map_b, sb + j * 8192, bn0 + 64 * j, k0);
+              }
+            }
           } else if constexpr (CG == 1) {
             uint64_t* bar = &full[s];
             mbar_expect_tx(bar, kStageBytes);
@@ -1269,6 +1304,11 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   const int kb_per_split = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per_split - 1) / kb_per_split;  // no empty splits
   const int bnl = bn / cg;  // B columns per CTA
+  static const bool sbox_env = [] {
+    const char* e = std::getenv("HP_GEMM_SPLITBOX");
+    return e && std::string(e) == "1";
+  }();
+  const bool sbox = sbox_env && !mc;
 
   // MN-major operands: "atom" maps view the row-major [K][MN] matrix as
   // (64 cols, K rows, MN/64 col-blocks) so one box brings every 8 KB swizzle
@@ -1286,11 +1326,11 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
       rank = 3;
       dims[0] = 64; dims[1] = g.K; dims[2] = a_blocks;
       str[0] = g.a.ld; str[1] = 64;
-      box[0] = 64; box[1] = 64; box[2] = mc ? 1 : tc::BM / 64;  // MC: half a tile per load
+      box[0] = 64; box[1] = 64; box[2] = (mc || sbox) ? 1 : tc::BM / 64;  // MC: half a tile per load
     } else if (g.a.trans) {
       dims[0] = g.M; dims[1] = g.K; str[0] = g.a.ld; box[0] = 64; box[1] = 64;
     } else {          // memory [M rows][K cols]
-      dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = mc ? 64 : tc::BM;
+      dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = (mc || sbox) ? 64 : tc::BM;
     }
     ma = make_map(g.a.p, rank, dims, str, box);
   }
@@ -1300,7 +1340,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     int rank = 2;
     if (!g.b.trans) {  // MN-major: memory [K rows][N cols] (or grouped blocks)
       rank = 3;
-      box[0] = 64; box[1] = 64; box[2] = (uint32_t)((mc ? bnl / 2 : bnl) / 64);
+      box[0] = 64; box[1] = 64; box[2] = sbox ? 1u : (uint32_t)((mc ? bnl / 2 : bnl) / 64);
       if (g.b.group) {
         dims[0] = 64; dims[1] = g.K; dims[2] = g.N / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
@@ -1316,9 +1356,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         rank = 3;
         dims[0] = 64; dims[1] = g.N; dims[2] = g.K / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
-        box[0] = 64; box[1] = (uint32_t)bnl; box[2] = 1;
+        box[0] = 64; box[1] = (uint32_t)(sbox ? 64 : bnl); box[2] = 1;
       } else {
-        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64; box[1] = (uint32_t)(mc ? bnl / 2 : bnl);
+        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64;
+        box[1] = (uint32_t)(sbox ? 64 : (mc ? bnl / 2 : bnl));
       }
     }
     mb = make_map(g.b.p, rank, dims, str, box);
@@ -1340,6 +1381,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias; p.act = g.act;
   p.aux = g.aux; p.resid = g.resid; p.ld_resid = g.ld_resid;
   p.vec = epilogue_vec_ok(g);
+  p.split_boxes = sbox ? 1 : 0;
   p.debug = g_debug_mode;
   p.trace = g_trace;
 
