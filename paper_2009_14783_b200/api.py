@@ -870,11 +870,24 @@ class StepEngine:
             if rep.updated:
                 rep.seconds = time.perf_counter() - self._group_t0
                 self._group_t0 = None
-                self._gather_seconds(rep)
                 out.append(rep)
             else:
                 out.append(None)
             cur = nxt
+        # rank_seconds for every update of the call in ONE collective after the
+        # last round (a per-update host-staged gather would stall the pipeline):
+        # each rank's seconds at its own offset, summed with zeros elsewhere
+        reps = [r for r in out if r is not None]
+        if self.comm is not None and self.comm.world > 1:
+            w, k = self.comm.world, len(reps)
+            v = np.zeros(w * k)
+            v[self.comm.rank * k:(self.comm.rank + 1) * k] = [r.seconds for r in reps]
+            allv = self.comm.all_reduce_sum(v) if k else []
+            for i, r in enumerate(reps):
+                r.rank_seconds = [allv[q * k + i] for q in range(w)] if self.comm.rank == 0 else []
+        else:
+            for r in reps:
+                r.rank_seconds = [r.seconds]
         return out
 
     # -- instrumentation

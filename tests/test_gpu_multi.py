@@ -341,11 +341,16 @@ eng = hp.StepEngine(spec, hp.OptimConfig("adam", 0.9, 0.98, 1e-9),
 eng.broadcast_params(0)
 eng.set_digest_check(1, debug=True)
 losses = []
-for s in range(8):
+for s in range(4):
     rep = eng.round(rec.batch(plan.batches[sched[s].batch_index]), sched[s].dummy, 1e-3)
     if rep is not None:
         losses.append(rep.loss)
-out = {"losses": losses, "digest": eng.digest()}
+# the pipelined API for the rest: rank_seconds gathered once for the call
+reps = eng.rounds((rec.batch(plan.batches[sched[s].batch_index]), sched[s].dummy, 1e-3)
+                  for s in range(4, 8))
+losses += [r.loss for r in reps if r is not None]
+out = {"losses": losses, "digest": eng.digest(),
+       "rank_seconds": [len(r.rank_seconds) for r in reps if r is not None]}
 with open(os.environ["HP_OUT"] + f"/bf{rank}.json", "w") as f:
     json.dump(out, f)
 eng.close(); comm.close()
@@ -368,4 +373,5 @@ def test_bf16_benchmark_path_w2_ranks_identical(tmp_path):
     r1 = json.loads((tmp_path / "bf1.json").read_text())
     assert len(r0["losses"]) == 4
     assert r0["losses"] == r1["losses"] and r0["digest"] == r1["digest"]
+    assert r0["rank_seconds"] == [2, 2] and r1["rank_seconds"] == [0, 0]
     assert all(np.isfinite(r0["losses"]))
