@@ -492,7 +492,7 @@ struct LongFwdSmem {
   uint8_t k[kMaxKB][kTile];
   uint8_t v[kMaxKB][kTile];
   uint8_t p[2][2 * kTile];  // P_j: [128 q][128 keys] as two [128][64] sub-tiles
-  uint64_t full, s_done, o_done, p_ready[2], pv_done[2];
+  uint64_t full, vfull, s_done, o_done, p_ready[2], pv_done[2];
   uint32_t tmem;
 };
 struct LongKvSmem {
@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   const int d = H * DK;
   if (threadIdx.x == 0) {
     mbar_init(&sm.full, 1);
+    mbar_init(&sm.vfull, 1);
     mbar_init(&sm.s_done, 1);
     mbar_init(&sm.o_done, 1);
     for (int s = 0; s < 2; ++s) {
@@ -569,12 +570,12 @@ __global__ void __launch_bounds__(kThreadsF, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      mbar_expect_tx(&sm.full, (1 + 2 * nb) * kTile);
+      // Q and K first (S needs only them); V lands while the softmax runs
+      mbar_expect_tx(&sm.full, (1 + nb) * kTile);
       tma_2d(&map_qkv, &sm.full, sm.q, h * DK, row0 + 128 * qb);
-      for (int j = 0; j < nb; ++j) {
-        tma_2d(&map_qkv, &sm.full, sm.k[j], d + h * DK, row0 + 128 * j);
-        tma_2d(&map_qkv, &sm.full, sm.v[j], 2 * d + h * DK, row0 + 128 * j);
-      }
+      for (int j = 0; j < nb; ++j) tma_2d(&map_qkv, &sm.full, sm.k[j], d + h * DK, row0 + 128 * j);
+      mbar_expect_tx(&sm.vfull, nb * kTile);
+      for (int j = 0; j < nb; ++j) tma_2d(&map_qkv, &sm.vfull, sm.v[j], 2 * d + h * DK, row0 + 128 * j);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -592,6 +593,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
       umma_commit(&sm.s_done);
     }
     __syncwarp();
+    mbar_wait(&sm.vfull, 0);
     for (int j = 0; j < nb; ++j) {
       mbar_wait(&sm.p_ready[j & 1], (j >> 1) & 1);
       tmem_fence_after();
