@@ -66,6 +66,7 @@ struct Params {
   int64_t ld_resid;
   int vec;  // C / aux / resid rows are 16-byte aligned
   int split_boxes;  // operand tiles loaded as 64-row / one-atom TMA boxes
+  int kb2;          // two k-blocks per stage, one 3-D TMA box per operand (A K-major)
   int debug;  // profiling only: 0 normal, 1 skip TMA loads, 2 skip MMAs, 3 skip epilogue
   unsigned long long* trace;  // profiling only: CTA 0 clock64 timeline (see kTr*)
 };
@@ -721,17 +722,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       mc_tile(m0, nt);
       const int am0 = m0 + static_cast<int>(row_rank) * BM;       // this CTA's A rows
       const int bn0 = nt * BN + static_cast<int>(row_rank) * BNL;  // this CTA's B columns
-      for (int kb = kb0; kb < kb1; ++kb, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
+      // kb2: a ring slot is two stages, [A kb | A kb+1][B kb | B kb+1]
+      const int kstep = p.kb2 ? 2 : 1;
+      const int nslots = p.kb2 ? STAGES / 2 : STAGES;
+      const uint32_t slot_bytes = p.kb2 ? 2 * kStageBytes : kStageBytes;
+      for (int kb = kb0; kb < kb1; kb += kstep, ++it) {
+        const int s = it % nslots;
+        const uint32_t ph = (it / nslots) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         if (lane == 0) trace_at(p, kTrP + it, kTrF);
-        uint8_t* sa = smem + s * kStageBytes;
-        uint8_t* sb = sa + kATileBytes;
+        uint8_t* sa = smem + s * slot_bytes;
+        uint8_t* sb = sa + (p.kb2 ? 2 : 1) * kATileBytes;
         const int k0 = kb * BK;
         if (elect_one()) {
           if (debug_bit(p, 1)) {  // profiling mode: no loads, MMA on stale smem
             if (CG == 1 || rank == 0) mbar_arrive(&full[s]);
+          } else if (!MC && p.kb2) {
+            // A: 3-D view (64, M, K / 64), box (64, BM, 2); B K-major likewise
+            // (box rows BNL), B MN-major atoms: box (64, 128 K rows, BNL / 64)
+            if constexpr (CG == 2) {
+              if (rank == 0) mbar_expect_tx(&full[s], 2 * slot_bytes);
+              const uint32_t cb = mapa_shared(smem_u32(&full[s]), 0);
+              tma_3d_cg2(&map_a, cb, sa, 0, am0, kb);
+              if (!p.b_mn) tma_3d_cg2(&map_b, cb, sb, 0, bn0, kb);
+              else tma_3d_cg2(&map_b, cb, sb, 0, k0, bn0 / 64);
+            } else {
+              mbar_expect_tx(&full[s], slot_bytes);
+              tma_3d(&map_a, &full[s], sa, 0, am0, kb);
+              if (!p.b_mn) tma_3d(&map_b, &full[s], sb, 0, bn0, kb);
+              else tma_3d(&map_b, &full[s], sb, 0, k0, bn0 / 64);
+            }
           } else if constexpr (MC) {
             uint64_t* bar = &full[s];
             mbar_expect_tx(bar, kStageBytes);  // own halves + the peers' halves
@@ -839,6 +859,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t db0 = umma_desc(s0 + kATileBytes, p.b_mn ? 8192 : 16, 1024);
       const uint64_t dak = p.a_mn ? (2048 >> 4) : (32 >> 4);
       const uint64_t dbk = p.b_mn ? (2048 >> 4) : (32 >> 4);
+      // kb2 slots: B after both A tiles; an MN-major B atom spans 128 K rows
+      const uint64_t db2 = umma_desc(s0 + 2 * kATileBytes, p.b_mn ? 16384 : 16, 1024);
+      const int kstep = p.kb2 ? 2 : 1;
+      const int nslots = p.kb2 ? STAGES / 2 : STAGES;
+      const uint32_t slot_bytes = p.kb2 ? 2 * kStageBytes : kStageBytes;
       uint32_t it = 0, lt = 0;
       for (;; ++lt) {
         const int u = take_unit(lt);
@@ -850,22 +875,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tmem_empty[as], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dacc = tmem_base + as * kAccStride;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
+        for (int kb = kb0; kb < kb1; kb += kstep, ++it) {
+          const int s = it % nslots;
+          const uint32_t ph = (it / nslots) & 1;
           mbar_wait(&full[s], ph);
           if (lane == 0) trace_at(p, kTrF + it, kTrC);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t soff = static_cast<uint64_t>(s) * (kStageBytes >> 4);
+          const uint64_t soff = static_cast<uint64_t>(s) * (slot_bytes >> 4);
           if (elect_one()) {
             if (!debug_bit(p, 2)) {
+              if (p.kb2) {
+                const int nq = (kb + 1 < kb1 ? 2 : 1) * (BK / 16);
+                for (int q = 0; q < nq; ++q) {
+                  const uint64_t ad = da0 + soff + (((q >> 2) * kATileBytes + (q & 3) * 32) >> 4);
+                  const uint64_t bd = db2 + soff + (p.b_mn ? q * (2048 >> 4)
+                                                           : (((q >> 2) * TL::kBTileBytes + (q & 3) * 32) >> 4));
+                  if constexpr (CG == 2)
+                    umma_bf16_cg2(dacc, ad, bd, idesc, (kb > kb0 || q > 0) ? 1u : 0u);
+                  else
+                    umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || q > 0) ? 1u : 0u);
+                }
+              } else {
 #pragma unroll
-              for (int k = 0; k < BK / 16; ++k) {
-                const uint64_t ad = da0 + soff + k * dak, bd = db0 + soff + k * dbk;
-                if constexpr (CG == 2)
-                  umma_bf16_cg2(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-                else
-                  umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                for (int k = 0; k < BK / 16; ++k) {
+                  const uint64_t ad = da0 + soff + k * dak, bd = db0 + soff + k * dbk;
+                  if constexpr (CG == 2)
+                    umma_bf16_cg2(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                  else
+                    umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                }
               }
             }
             if constexpr (CG == 2) umma_commit_cg2(&empty[s]);
@@ -1309,6 +1347,13 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     return e && std::string(e) == "1";
   }();
   const bool sbox = sbox_env && !mc;
+  static const bool kb2_env = [] {
+    const char* e = std::getenv("HP_GEMM_KB2");
+    return e && std::string(e) == "1";
+  }();
+  const bool b_atoms_pre = !g.b.trans && (g.b.group || 64LL * ((g.N + 63) / 64) <= g.b.ld);
+  const bool kb2 = kb2_env && !mc && !sbox && !g.a.trans && g.K % 64 == 0 && num_kb >= 2 &&
+                   (g.b.trans || b_atoms_pre) && tc::Tile<256, 1>::kStages >= 4;
 
   // MN-major operands: "atom" maps view the row-major [K][MN] matrix as
   // (64 cols, K rows, MN/64 col-blocks) so one box brings every 8 KB swizzle
@@ -1329,6 +1374,11 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
       box[0] = 64; box[1] = 64; box[2] = (mc || sbox) ? 1 : tc::BM / 64;  // MC: half a tile per load
     } else if (g.a.trans) {
       dims[0] = g.M; dims[1] = g.K; str[0] = g.a.ld; box[0] = 64; box[1] = 64;
+    } else if (kb2) {  // memory [M rows][K cols] as (64, M, K / 64): two k-blocks per box
+      rank = 3;
+      dims[0] = 64; dims[1] = g.M; dims[2] = g.K / 64;
+      str[0] = g.a.ld; str[1] = 64;
+      box[0] = 64; box[1] = tc::BM; box[2] = 2;
     } else {          // memory [M rows][K cols]
       dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = (mc || sbox) ? 64 : tc::BM;
     }
@@ -1340,7 +1390,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     int rank = 2;
     if (!g.b.trans) {  // MN-major: memory [K rows][N cols] (or grouped blocks)
       rank = 3;
-      box[0] = 64; box[1] = 64; box[2] = sbox ? 1u : (uint32_t)((mc ? bnl / 2 : bnl) / 64);
+      box[0] = 64; box[1] = kb2 ? 128 : 64; box[2] = sbox ? 1u : (uint32_t)((mc ? bnl / 2 : bnl) / 64);
       if (g.b.group) {
         dims[0] = 64; dims[1] = g.K; dims[2] = g.N / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
@@ -1356,7 +1406,12 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         rank = 3;
         dims[0] = 64; dims[1] = g.N; dims[2] = g.K / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
-        box[0] = 64; box[1] = (uint32_t)(sbox ? 64 : bnl); box[2] = 1;
+        box[0] = 64; box[1] = (uint32_t)(sbox ? 64 : bnl); box[2] = kb2 ? 2 : 1;
+      } else if (kb2) {  // (64, N, K / 64), two k-blocks per box
+        rank = 3;
+        dims[0] = 64; dims[1] = g.N; dims[2] = g.K / 64;
+        str[0] = g.b.ld; str[1] = 64;
+        box[0] = 64; box[1] = (uint32_t)bnl; box[2] = 2;
       } else {
         dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64;
         box[1] = (uint32_t)(sbox ? 64 : (mc ? bnl / 2 : bnl));
@@ -1382,6 +1437,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.aux = g.aux; p.resid = g.resid; p.ld_resid = g.ld_resid;
   p.vec = epilogue_vec_ok(g);
   p.split_boxes = sbox ? 1 : 0;
+  p.kb2 = kb2 ? 1 : 0;
   p.debug = g_debug_mode;
   p.trace = g_trace;
 
