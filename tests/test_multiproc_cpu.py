@@ -67,3 +67,16 @@ def test_two_rank_schedules_and_id_broadcast():
         assert real == list(range(nb))                       # exact partition of the batches
         assert res[1][key][1] == scheds                      # both ranks saw the same gather
     assert res[0]["uid"] == res[1]["uid"] == [1] * 128       # rank 0's id everywhere
+
+
+def test_tcp_rendezvous_missing_rank_times_out():
+    """A rank whose master never appears fails with the reference's comm
+    error after the timeout (test_comm.cpp:242-261 role) -- no hang."""
+    import time
+
+    import paper_2009_14783_b200 as hp
+    import pytest
+    t0 = time.time()
+    with pytest.raises(hp.CommError, match="tcp rendezvous"):
+        hp.Communicator.tcp("127.0.0.1", _free_port(), 2, 1, 0, timeout_ms=500)
+    assert time.time() - t0 < 10
