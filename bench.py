@@ -188,7 +188,10 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--bucket-mb", type=float, default=50.0)
+    # gradient bucket cap: 50 MB when buckets are allreduced (N > 1, measured
+    # against 25 / 100 MB); at N = 1 buckets only set the update granularity
+    # and 200 MB measured best (profiles/r01_ab_bucket_n1.txt)
+    ap.add_argument("--bucket-mb", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
@@ -201,6 +204,8 @@ def main(argv=None):
 
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)
+    if args.bucket_mb is None:
+        args.bucket_mb = 50.0 if world > 1 else 200.0
     if args.impl == "reference":
         return reference_arm(args, rank, world)
 
