@@ -16,6 +16,7 @@
 //     NCCL reduction (ncclRedOpCreatePreMulSum with a device scalar);
 //   * Adam (bit-exact f32 kern::adam_update) updates the fp32 master copy and
 //     refreshes the bf16 working copy the tcgen05 GEMMs read.
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (nsys / ncu range filters)
 #include "engine.h"
 
 #include <cstdlib>
@@ -30,6 +31,14 @@
 #include "hp_common.h"
 
 namespace hp {
+namespace {
+// host-side NVTX range for the phases of a round (eager and captured rounds
+// show the phases; a replayed round shows as one "hp.round" range)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 constexpr int kEmbHotTokens = 32;  // = kEmbHot in kernels.cu
 
@@ -536,6 +545,7 @@ uint64_t Engine::digest() {
 
 // ------------------------------------------------------------------ staging
 void Engine::stage_batch(const hp_batch& b) {
+  NvtxRange nv("hp.stage_batch");
   if (b.n_inst == 0)
     fail(HP_ECONFIG, "model_forward: empty batch (only the dummy path may skip data)");
   const uint64_t B = b.n_inst;
@@ -790,6 +800,7 @@ void Engine::wait_wg(cudaEvent_t e) {
 
 // ------------------------------------------------------------------ forward
 void Engine::forward(bool need_grad) {
+  NvtxRange nv("hp.forward");
   const DevBatch& b = batch_;
   const int T = b.T;
   const DType wt = bf16_ ? DType::bf16 : DType::f32;
@@ -950,6 +961,7 @@ void Engine::issue_bucket(size_t k) {
 }
 
 void Engine::backward() {
+  NvtxRange nv("hp.backward");
   const DevBatch& b = batch_;
   const int T = b.T;
   if (wg_on_) {
@@ -1171,6 +1183,7 @@ void Engine::backward() {
 
 // ------------------------------------------------------------------ round
 void Engine::round_async(int dummy, double lr) {
+  NvtxRange nv("hp.round");
   if (!staged_) fail(HP_ECONFIG, "round: no batch staged");
   HP_CUDA(cudaSetDevice(x_.device));
   // K micro rounds per update (Accumulator, optim.hpp:154-202): rounds 1..K-1
@@ -1376,6 +1389,7 @@ void Engine::round_body(int dummy) {
 // blocks of the parameter bytes, computed on the device in parallel (the exact
 // byte-serial params_digest stays available as digest()).
 void Engine::check_digest_on_cadence() {
+  NvtxRange nv("hp.digest_check");
   if (!comm_ || comm_->world < 2 || !grad_comm_) return;
   const uint64_t every = check_debug_ ? 1 : check_every_;
   if (every == 0 || step_ % every != 0) return;
