@@ -205,9 +205,9 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     constexpr uint64_t kChunk = 8192;
     std::vector<uint64_t> items;
     bucket_items_.clear();
-    for (const Bucket& bk : buckets_) {
+    auto build_items = [&](size_t first_param, size_t last_param) {
       std::vector<std::array<uint64_t, 5>> runs;
-      for (size_t i = bk.first_param; i <= bk.last_param; ++i) {
+      for (size_t i = first_param; i <= last_param; ++i) {
         const uint64_t lo = table_[i].offset, n = table_[i].size();
         const uint64_t slo = bf16_ ? shadow_off_[i] : lo;
         const uint64_t cols = table_[i].cols, pc = bf16_ ? shadow_ld_[i] : cols;
@@ -228,8 +228,20 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
           items.insert(items.end(), {r[0] + o, cnt, r[2] + srow, r[3], r[4]});
         }
       }
-      bucket_items_.push_back({first, static_cast<int>(items.size() / 5) - first});
-    }
+      return std::make_pair(first, static_cast<int>(items.size() / 5) - first);
+    };
+    for (const Bucket& bk : buckets_) bucket_items_.push_back(build_items(bk.first_param, bk.last_param));
+    // the last bucket without the word embedding (its rows go through
+    // adam_rows around the round's ids when the update is split, see round_body)
+    const Bucket& lb = buckets_.back();
+    // opt-in (HP_EMB_SPLIT=1): bit-identical, measured neutral on C2 at N = 1
+    // (profiles/r01_ab_emb_split.txt) -- the dense tail is not what bounds the step
+    const char* es = std::getenv("HP_EMB_SPLIT");
+    split_emb_ = es && std::string(es) == "1" && lb.first_param == 0 &&
+                 table_[0].rows == static_cast<uint64_t>(V_) && table_[0].cols == static_cast<uint64_t>(d_) &&
+                 d_ % 4 == 0 && table_[0].offset % 4 == 0;
+    if (split_emb_)
+      emb_rest_items_ = lb.last_param >= 1 ? build_items(1, lb.last_param) : std::make_pair(0, 0);
     nitems_ = static_cast<int>(items.size() / 5);
     adam_items_ = static_cast<uint64_t*>(dalloc(items.size() * 8));
     HP_CUDA(cudaMemcpy(adam_items_, items.data(), items.size() * 8, cudaMemcpyHostToDevice));
@@ -951,10 +963,15 @@ void Engine::issue_bucket(size_t k) {
   }
   AdamArgs a = adam_args_;
   a.g2 = phase_ == 2 ? acc_grads_ : nullptr;
-  a.items = adam_items_ + 5 * static_cast<size_t>(bucket_items_[k].first);
-  a.nitems = bucket_items_[k].second;
+  const bool split = emb_split_round_ && k + 1 == buckets_.size();
+  const auto& its = split ? emb_rest_items_ : bucket_items_[k];
+  a.items = adam_items_ + 5 * static_cast<size_t>(its.first);
+  a.nitems = its.second;
   tstart(TM_ADAM, su);
   adam_update(a, su);
+  if (split)  // the batch's rows of the word embedding, now that dE is final
+    adam_rows(a, 1, batch_.uid, batch_.ucount, V_, d_, table_[0].offset,
+              bf16_ ? shadow_off_[0] : table_[0].offset, bf16_ ? shadow_ld_[0] : table_[0].cols, su);
   tstop(TM_ADAM, 0, 28.0 * (double)(bk.hi - bk.lo) + (bf16_ ? 2.0 * (double)(bk.hi - bk.lo) : 0.0),
         su);
   serialize_if_timed(su);
@@ -1321,6 +1338,7 @@ void Engine::round_body(int dummy) {
   wg_forked_ = false;
   upd_forked_ = false;
   emb_sparse_round_ = false;
+  emb_split_round_ = false;
   HP_CUDA(cudaMemsetAsync(flags_, 0, 8, s_main_));
   // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
   forward(!dummy);
@@ -1350,6 +1368,25 @@ void Engine::round_body(int dummy) {
   // K > 1: running [loss, weight] totals; the K-th round's update divides by
   // the total weight (engine.hpp:147-151)
   if (phase_ != 0) accumulate_weight(d_lw_, d_acc_lw_, d_lw_ + 4, inv_w64_, phase_ == 2, sw);
+  // W = 1, K = 1: the word-embedding rows outside this batch's ids get their
+  // (zero-gradient) update now, behind backward, so the last bucket's update
+  // after backward touches only the batch's rows (bit-identical: adam_rows)
+  emb_split_round_ = split_emb_ && phase_ == 0 && !dummy && !capture_ &&
+                     (!comm_ || comm_->world == 1);
+  if (emb_split_round_) {
+    cudaStream_t su = sw;
+    if (s_upd_) {
+      HP_CUDA(cudaEventRecord(ev_reduced_[0], sw));
+      HP_CUDA(cudaStreamWaitEvent(s_upd_, ev_reduced_[0], 0));
+      su = s_upd_;
+      upd_forked_ = true;
+    }
+    tstart(TM_ADAM, su);
+    adam_rows(adam_args_, 0, batch_.uid, batch_.ucount, V_, d_, table_[0].offset,
+              bf16_ ? shadow_off_[0] : table_[0].offset, bf16_ ? shadow_ld_[0] : table_[0].cols, su);
+    tstop(TM_ADAM, 0, 24.0 * (double)table_[0].size() + (bf16_ ? 2.0 * (double)table_[0].size() : 0.0), su);
+    serialize_if_timed(su);
+  }
 
   next_bucket_ = 0;
   if (dummy) {

@@ -183,6 +183,9 @@ class Engine {
   // rank row-sparse (distinct ids of the batch) -- allgather + rank-ordered
   // scatter instead of a dense allreduce (see backward / issue_bucket)
   bool sparse_emb_ = false, emb_sparse_round_ = false;
+  // W = 1, K = 1 split of the word-embedding update (round_body, issue_bucket)
+  bool split_emb_ = false, emb_split_round_ = false;
+  std::pair<int, int> emb_rest_items_{0, 0};  // last bucket's items without param 0
   int emb_cap_ = 0;
   float* emb_rows_ = nullptr;  // [cap][d + 4]
   float* emb_gath_ = nullptr;  // [world][cap][d + 4]

@@ -1646,6 +1646,83 @@ void adam_update(const AdamArgs& a, cudaStream_t s) {
   count_launch();
 }
 
+// Word-embedding rows of a W = 1, K = 1 update, split around the round's
+// distinct token ids uid[0 .. U) (sorted, U = ucount[0] + ucount[1]): only
+// those rows receive a gradient (embed_bwd), every other row's is exactly 0.
+// mode 0 updates the rows NOT in uid with g = 0 -- no gradient read, so it
+// runs while backward is still producing dE; mode 1 updates the uid rows once
+// dE is final. Per element the arithmetic is adam_kernel's (g * (1 / Σw) in
+// f64, then adam_one), so the split update is bit-identical to the dense one.
+// One warp per row, float4 I/O (d % 4 == 0, lo % 4 == 0).
+__global__ void __launch_bounds__(256) adam_rows_kernel(const AdamArgs a0, int mode,
+                                                        const int* __restrict__ uid,
+                                                        const int* __restrict__ ucount, int V,
+                                                        int d, uint64_t lo, uint64_t slo,
+                                                        uint64_t pcols) {
+  if (a0.flags && *a0.flags) return;
+  AdamArgs a = a0;
+  if (a.hyper) {
+    a.lr = a.hyper[0];
+    a.c1 = a.hyper[1];
+    a.c2 = a.hyper[2];
+  }
+  const bool scale = a.inv_w64 != nullptr;
+  const double sc = scale ? *a.inv_w64 : 1.0;
+  const float g0 = scale ? (float)(0.0 * sc) : 0.f;  // what adam_kernel makes of a zero
+  bf16* sh = (bf16*)a.shadow;
+  const int U = ucount[0] + ucount[1];
+  const int nrows = mode ? U : V;
+  const int lane = threadIdx.x & 31;
+  int bad = 0;
+  for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < nrows; i += gridDim.x * 8) {
+    int r = i;
+    if (mode) {
+      r = uid[i];
+    } else {  // skip the batch's ids (warp-uniform binary search)
+      int l = 0, h = U;
+      while (l < h) {
+        const int mid = (l + h) >> 1;
+        if (uid[mid] < r) l = mid + 1; else h = mid;
+      }
+      if (l < U && uid[l] == r) continue;
+    }
+    const uint64_t base = lo + (uint64_t)r * d;
+    for (int c = 4 * lane; c < d; c += 128) {
+      float4 p = adam_ld4(a.p + base + c);
+      float4 m = adam_ld4(a.m + base + c);
+      float4 v = adam_ld4(a.v + base + c);
+      float gs[4] = {g0, g0, g0, g0};
+      if (mode) {
+        const float4 g = adam_ld4(a.g + base + c);
+        const float* gg = &g.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) gs[e] = scale ? (float)((double)gg[e] * sc) : gg[e];
+      }
+      float* pp = &p.x; float* mm = &m.x; float* vv = &v.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (!isfinite(gs[e])) { bad = 1; continue; }
+        adam_one(a, pp[e], mm[e], vv[e], gs[e]);
+      }
+      adam_st4(a.p + base + c, p);
+      adam_st4(a.m + base + c, m);
+      adam_st4(a.v + base + c, v);
+      if (sh) {
+        const uint64_t so = slo + (uint64_t)r * pcols + c;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sh[so + e] = __float2bfloat16_rn(pp[e]);
+      }
+    }
+  }
+  if (bad) *a.bad = 1;
+}
+void adam_rows(const AdamArgs& a, int mode, const int* uid, const int* ucount, int V, int d,
+               uint64_t lo, uint64_t slo, uint64_t pcols, cudaStream_t s) {
+  adam_rows_kernel<<<148 * 6, 256, 0, s>>>(a, mode, uid, ucount, V, d, lo, slo, pcols);
+  LAUNCH_CHECK();
+  count_launch();
+}
+
 __global__ void shadow_kernel(const float* p, bf16* sh, const uint64_t* seg, int nseg, uint64_t n) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)

@@ -513,3 +513,48 @@ def test_forward_only_matches_oracle_and_round(compute):
     rep = eng.round(rec.batch(ids), lr=1e-3)
     assert rep.local_loss_sum == pytest.approx(ls, rel=1e-6)
     eng.close()
+
+
+def _split_run(monkeypatch, split, make_engine, batches, lrs):
+    monkeypatch.setenv("HP_EMB_SPLIT", "1" if split else "0")
+    eng = make_engine()
+    k0 = eng.kernel_launches()
+    losses = [eng.round(b, lr=lr).loss for b, lr in zip(batches, lrs)]
+    launches = eng.kernel_launches() - k0
+    m, v, t = eng.get_adam()
+    out = (np.array(losses), eng.digest(), eng.get_params(), m.copy(), v.copy(), t, launches)
+    eng.close()
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("arch,compute", [("bert_encoder", "bf16"), ("bert_encoder", "f32"),
+                                          ("masked_token_model", "f32")])
+def test_split_embedding_update_bit_identical(monkeypatch, arch, compute):
+    # W = 1, K = 1: the word-embedding rows outside the batch's ids are updated
+    # with a zero gradient while backward runs, the batch's rows after it
+    # (adam_rows); parameters, Adam state and losses must equal the dense
+    # update's bit for bit, eager and graph-replayed rounds alike.
+    if arch == "bert_encoder":
+        spec, _, rec = _bert_case(d=128, heads=2, dff=256, vocab=203, n=16)
+    else:
+        spec = hp.ModelSpec(arch="masked_token_model", d_model=128, heads=4, vocab=1000,
+                            max_seq=64, label_smooth_eps=0.1)
+        rec = hp.generate_mlm_records(hp.MlmGenConfig(n=16, vocab=1000, min_sentence_words=30,
+                                                      max_sentence_words=30, seed=7))
+
+    def make():
+        return hp.StepEngine(spec, hp.OptimConfig(), hp.ExecConfig(
+            compute=compute, max_tokens=1024, max_batch=16, max_masks=256), seed=9)
+
+    ids = [np.arange(12), np.arange(2, 14)]
+    batches = [rec.batch(ids[k % 2]) for k in range(6)]
+    lrs = [1e-3 * (1 + 0.5 * k) for k in range(6)]
+    a = _split_run(monkeypatch, True, make, batches, lrs)
+    b = _split_run(monkeypatch, False, make, batches, lrs)
+    assert np.array_equal(a[0], b[0])
+    assert a[1] == b[1]
+    for x, y in zip(a[2:5], b[2:5]):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    assert a[5] == b[5]
+    assert a[6] == b[6] + 2 * len(batches)  # the split ran: two adam_rows launches per round
