@@ -177,8 +177,31 @@ def reference_arm(args, rank, world):
                              "kind": kind, "sample": sample},
             "e2e": {"value": r["samples_per_s"], "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
+
+
+# The JSON line is the only thing on stdout: native libraries print to fd 1
+# (NCCL's "NCCL version ..." banner at communicator init on rank 0), so fd 1
+# is pointed at stderr for the whole run and the line goes to a saved copy.
+_JSON_FD = None
+
+
+def _stdout_to_stderr():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
 
 
 # ---------------------------------------------------------------- our arm
@@ -196,6 +219,7 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     args = ap.parse_args(argv)
+    _stdout_to_stderr()
     global BATCH, SEQ
     wspec, BATCH, SEQ, wmin, wmax, wdesc, wmodel = WORKLOADS[args.workload]
     if args.workload != "c2":
@@ -409,7 +433,7 @@ def main(argv=None):
                 "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
                 "roofline": roofline, "hbm_kernels": hbm_kernels, "allreduce": allreduce, "cpu_baseline": cpu, "breakdown_ms_per_step": breakdown,
                 "final_loss": rep.loss}
-        print(json.dumps(line), flush=True)
+        emit(line)
     eng.close()
     if comm:
         comm.close()
