@@ -240,8 +240,16 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     split_emb_ = es && std::string(es) == "1" && lb.first_param == 0 &&
                  table_[0].rows == static_cast<uint64_t>(V_) && table_[0].cols == static_cast<uint64_t>(d_) &&
                  d_ % 4 == 0 && table_[0].offset % 4 == 0;
-    if (split_emb_)
+    if (split_emb_) {
       emb_rest_items_ = lb.last_param >= 1 ? build_items(1, lb.last_param) : std::make_pair(0, 0);
+      // every rank's distinct-id list (W > 1: allgathered before backward) and
+      // the zero count a dummy round contributes
+      const int W = comm_ ? comm_->world : 1;
+      uid_all_ = static_cast<int*>(dalloc(sizeof(int) * x_.max_tokens * W));
+      ucnt_all_ = static_cast<int*>(dalloc(sizeof(int) * 2 * W));
+      ucount_zero_ = static_cast<int*>(dalloc(sizeof(int) * 2));
+      HP_CUDA(cudaMemset(ucount_zero_, 0, sizeof(int) * 2));
+    }
     nitems_ = static_cast<int>(items.size() / 5);
     adam_items_ = static_cast<uint64_t*>(dalloc(items.size() * 8));
     HP_CUDA(cudaMemcpy(adam_items_, items.data(), items.size() * 8, cudaMemcpyHostToDevice));
@@ -924,6 +932,12 @@ void Engine::grads_ready(int first_done) {
     issue_bucket(next_bucket_++);
 }
 
+void Engine::emb_rows_update(int mode, cudaStream_t su) {
+  adam_rows(adam_args_, mode, emb_lists_.uids, emb_lists_.cnts, emb_lists_.n,
+            static_cast<int>(x_.max_tokens), V_, d_, table_[0].offset,
+            bf16_ ? shadow_off_[0] : table_[0].offset, bf16_ ? shadow_ld_[0] : table_[0].cols, su);
+}
+
 void Engine::issue_bucket(size_t k) {
   const Bucket& bk = buckets_[k];
   HP_CUDA(cudaEventRecord(ev_bucket_[k], s_main_));
@@ -969,9 +983,7 @@ void Engine::issue_bucket(size_t k) {
   a.nitems = its.second;
   tstart(TM_ADAM, su);
   adam_update(a, su);
-  if (split)  // the batch's rows of the word embedding, now that dE is final
-    adam_rows(a, 1, batch_.uid, batch_.ucount, V_, d_, table_[0].offset,
-              bf16_ ? shadow_off_[0] : table_[0].offset, bf16_ ? shadow_ld_[0] : table_[0].cols, su);
+  if (split) emb_rows_update(1, su);  // the batch rows of the word embedding, dE final
   tstop(TM_ADAM, 0, 28.0 * (double)(bk.hi - bk.lo) + (bf16_ ? 2.0 * (double)(bk.hi - bk.lo) : 0.0),
         su);
   serialize_if_timed(su);
@@ -1368,12 +1380,20 @@ void Engine::round_body(int dummy) {
   // K > 1: running [loss, weight] totals; the K-th round's update divides by
   // the total weight (engine.hpp:147-151)
   if (phase_ != 0) accumulate_weight(d_lw_, d_acc_lw_, d_lw_ + 4, inv_w64_, phase_ == 2, sw);
-  // W = 1, K = 1: the word-embedding rows outside this batch's ids get their
+  // K = 1: the word-embedding rows outside every rank's batch ids get their
   // (zero-gradient) update now, behind backward, so the last bucket's update
-  // after backward touches only the batch's rows (bit-identical: adam_rows)
-  emb_split_round_ = split_emb_ && phase_ == 0 && !dummy && !capture_ &&
-                     (!comm_ || comm_->world == 1);
+  // after backward touches only the batch rows (bit-identical: adam_rows)
+  emb_split_round_ = split_emb_ && phase_ == 0 && !capture_;
   if (emb_split_round_) {
+    const int* cnt = dummy ? ucount_zero_ : batch_.ucount;
+    const int W = comm_ ? comm_->world : 1;
+    if (W > 1 && grad_comm_) {  // symmetric on every rank, dummies included
+      HP_NCCL(ncclAllGather(batch_.uid, uid_all_, x_.max_tokens, ncclInt, comm_->nccl, sw));
+      HP_NCCL(ncclAllGather(cnt, ucnt_all_, 2, ncclInt, comm_->nccl, sw));
+      emb_lists_ = {uid_all_, ucnt_all_, W};
+    } else {
+      emb_lists_ = {batch_.uid, cnt, 1};
+    }
     cudaStream_t su = sw;
     if (s_upd_) {
       HP_CUDA(cudaEventRecord(ev_reduced_[0], sw));
@@ -1382,8 +1402,7 @@ void Engine::round_body(int dummy) {
       upd_forked_ = true;
     }
     tstart(TM_ADAM, su);
-    adam_rows(adam_args_, 0, batch_.uid, batch_.ucount, V_, d_, table_[0].offset,
-              bf16_ ? shadow_off_[0] : table_[0].offset, bf16_ ? shadow_ld_[0] : table_[0].cols, su);
+    emb_rows_update(0, su);
     tstop(TM_ADAM, 0, 24.0 * (double)table_[0].size() + (bf16_ ? 2.0 * (double)table_[0].size() : 0.0), su);
     serialize_if_timed(su);
   }

@@ -183,9 +183,14 @@ class Engine {
   // rank row-sparse (distinct ids of the batch) -- allgather + rank-ordered
   // scatter instead of a dense allreduce (see backward / issue_bucket)
   bool sparse_emb_ = false, emb_sparse_round_ = false;
-  // W = 1, K = 1 split of the word-embedding update (round_body, issue_bucket)
+  // K = 1 split of the word-embedding update (round_body, issue_bucket)
   bool split_emb_ = false, emb_split_round_ = false;
   std::pair<int, int> emb_rest_items_{0, 0};  // last bucket's items without param 0
+  int* uid_all_ = nullptr;     // [W][max_tokens] every rank's sorted distinct ids
+  int* ucnt_all_ = nullptr;    // [W][2] their counts
+  int* ucount_zero_ = nullptr; // [2] a dummy round's (empty) count
+  struct { const int* uids; const int* cnts; int n; } emb_lists_{nullptr, nullptr, 0};
+  void emb_rows_update(int mode, cudaStream_t su);
   int emb_cap_ = 0;
   float* emb_rows_ = nullptr;  // [cap][d + 4]
   float* emb_gath_ = nullptr;  // [world][cap][d + 4]

@@ -1646,19 +1646,29 @@ void adam_update(const AdamArgs& a, cudaStream_t s) {
   count_launch();
 }
 
-// Word-embedding rows of a W = 1, K = 1 update, split around the round's
-// distinct token ids uid[0 .. U) (sorted, U = ucount[0] + ucount[1]): only
-// those rows receive a gradient (embed_bwd), every other row's is exactly 0.
-// mode 0 updates the rows NOT in uid with g = 0 -- no gradient read, so it
-// runs while backward is still producing dE; mode 1 updates the uid rows once
+// Word-embedding rows of a K = 1 update, split around the round's distinct
+// token ids: nl sorted id lists (one per rank, list l = uids[l * stride ..],
+// length ucnts[2 l] + ucnts[2 l + 1]); only rows in their union receive a
+// gradient (embed_bwd, then the exchange), every other row's is exactly 0.
+// mode 0 updates the rows in NO list with g = 0 -- no gradient read, so it
+// runs while backward is still producing dE; mode 1 updates the union's rows
+// (each once: a row is skipped in list l when an earlier list holds it) once
 // dE is final. Per element the arithmetic is adam_kernel's (g * (1 / Σw) in
 // f64, then adam_one), so the split update is bit-identical to the dense one.
 // One warp per row, float4 I/O (d % 4 == 0, lo % 4 == 0).
+__device__ __forceinline__ bool in_sorted(const int* __restrict__ u, int n, int r) {
+  int l = 0, h = n;
+  while (l < h) {
+    const int mid = (l + h) >> 1;
+    if (u[mid] < r) l = mid + 1; else h = mid;
+  }
+  return l < n && u[l] == r;
+}
 __global__ void __launch_bounds__(256) adam_rows_kernel(const AdamArgs a0, int mode,
-                                                        const int* __restrict__ uid,
-                                                        const int* __restrict__ ucount, int V,
-                                                        int d, uint64_t lo, uint64_t slo,
-                                                        uint64_t pcols) {
+                                                        const int* __restrict__ uids,
+                                                        const int* __restrict__ ucnts, int nl,
+                                                        int stride, int V, int d, uint64_t lo,
+                                                        uint64_t slo, uint64_t pcols) {
   if (a0.flags && *a0.flags) return;
   AdamArgs a = a0;
   if (a.hyper) {
@@ -1670,22 +1680,25 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(const AdamArgs a0, int m
   const double sc = scale ? *a.inv_w64 : 1.0;
   const float g0 = scale ? (float)(0.0 * sc) : 0.f;  // what adam_kernel makes of a zero
   bf16* sh = (bf16*)a.shadow;
-  const int U = ucount[0] + ucount[1];
-  const int nrows = mode ? U : V;
+  int total = 0;
+  for (int l = 0; l < nl; ++l) total += ucnts[2 * l] + ucnts[2 * l + 1];
+  const int nrows = mode ? total : V;
   const int lane = threadIdx.x & 31;
   int bad = 0;
   for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < nrows; i += gridDim.x * 8) {
     int r = i;
-    if (mode) {
-      r = uid[i];
-    } else {  // skip the batch's ids (warp-uniform binary search)
-      int l = 0, h = U;
-      while (l < h) {
-        const int mid = (l + h) >> 1;
-        if (uid[mid] < r) l = mid + 1; else h = mid;
-      }
-      if (l < U && uid[l] == r) continue;
+    bool skip = false;
+    if (mode) {  // i-th entry of the concatenated lists; first list holding it wins
+      int l = 0, j = i;
+      while (j >= ucnts[2 * l] + ucnts[2 * l + 1]) { j -= ucnts[2 * l] + ucnts[2 * l + 1]; ++l; }
+      r = uids[(int64_t)l * stride + j];
+      for (int k = 0; k < l && !skip; ++k)
+        skip = in_sorted(uids + (int64_t)k * stride, ucnts[2 * k] + ucnts[2 * k + 1], r);
+    } else {  // warp-uniform binary searches
+      for (int k = 0; k < nl && !skip; ++k)
+        skip = in_sorted(uids + (int64_t)k * stride, ucnts[2 * k] + ucnts[2 * k + 1], r);
     }
+    if (skip) continue;
     const uint64_t base = lo + (uint64_t)r * d;
     for (int c = 4 * lane; c < d; c += 128) {
       float4 p = adam_ld4(a.p + base + c);
@@ -1716,9 +1729,9 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(const AdamArgs a0, int m
   }
   if (bad) *a.bad = 1;
 }
-void adam_rows(const AdamArgs& a, int mode, const int* uid, const int* ucount, int V, int d,
-               uint64_t lo, uint64_t slo, uint64_t pcols, cudaStream_t s) {
-  adam_rows_kernel<<<148 * 6, 256, 0, s>>>(a, mode, uid, ucount, V, d, lo, slo, pcols);
+void adam_rows(const AdamArgs& a, int mode, const int* uids, const int* ucnts, int nl, int stride,
+               int V, int d, uint64_t lo, uint64_t slo, uint64_t pcols, cudaStream_t s) {
+  adam_rows_kernel<<<148 * 6, 256, 0, s>>>(a, mode, uids, ucnts, nl, stride, V, d, lo, slo, pcols);
   LAUNCH_CHECK();
   count_launch();
 }

@@ -212,10 +212,11 @@ struct AdamArgs {
 };
 void adam_update(const AdamArgs& a, cudaStream_t s);
 // word-embedding rows [V x d] at flat offset lo (shadow slo, row pitch pcols),
-// split around the sorted distinct ids uid[0 .. ucount[0] + ucount[1]):
-// mode 0 = the other rows with a zero gradient, mode 1 = the uid rows
-void adam_rows(const AdamArgs& a, int mode, const int* uid, const int* ucount, int V, int d,
-               uint64_t lo, uint64_t slo, uint64_t pcols, cudaStream_t s);
+// split around nl sorted distinct-id lists (uids + l * stride, length
+// ucnts[2 l] + ucnts[2 l + 1]): mode 0 = the rows in no list, zero gradient;
+// mode 1 = the union's rows, each once
+void adam_rows(const AdamArgs& a, int mode, const int* uids, const int* ucnts, int nl, int stride,
+               int V, int d, uint64_t lo, uint64_t slo, uint64_t pcols, cudaStream_t s);
 // K > 1 gradient accumulation (Accumulator, optim.hpp:154-202)
 void accumulate_weight(const double* lw, double* acc, double* out, double* inv_w64, int final_round,
                        cudaStream_t s);

@@ -164,8 +164,9 @@ rec = hp.generate_mlm_records(hp.MlmGenConfig(n=64, vocab=4000, min_sentence_wor
 plan = hp.build_epoch_batches(rec.token_lengths(), 8, 0, 21, 0)
 sched = hp.partition_for_rank(plan, world, rank)
 out = {}
-for mode in ("1", "0"):
-    os.environ["HP_SPARSE_EMB"] = mode
+for mode in ("1", "0", "1s", "0s"):  # s: split word-embedding update (HP_EMB_SPLIT=1)
+    os.environ["HP_SPARSE_EMB"] = mode[0]
+    os.environ["HP_EMB_SPLIT"] = "1" if mode.endswith("s") else "0"
     eng = hp.StepEngine(spec, hp.OptimConfig("adam", 0.9, 0.98, 1e-9),
                         hp.ExecConfig(compute="f32", device=rank, max_tokens=512, max_batch=8,
                                       max_masks=128, bucket_mb=0.5),
@@ -202,9 +203,15 @@ def test_row_sparse_embedding_exchange_matches_dense(tmp_path):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     r0 = json.loads((tmp_path / "sp0.json").read_text())
     r1 = json.loads((tmp_path / "sp1.json").read_text())
-    for mode in ("1", "0"):
+    for mode in ("1", "0", "1s", "0s"):
         assert r0[mode]["losses"] == r1[mode]["losses"]
         assert r0[mode]["digest"] == r1[mode]["digest"]
+    # the split update (rows outside every rank's ids during backward, the
+    # union's rows after the exchange) is bit-identical to the unsplit one
+    for mode in ("1", "0"):
+        assert r0[mode + "s"] == r0[mode]
+        assert np.array_equal(np.load(tmp_path / f"p{mode}s.npy").view(np.uint32),
+                              np.load(tmp_path / f"p{mode}.npy").view(np.uint32))
     a, b = np.array(r0["1"]["losses"]), np.array(r0["0"]["losses"])
     assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5
     assert rel_norm(np.load(tmp_path / "p1.npy"), np.load(tmp_path / "p0.npy")) <= 1e-5
