@@ -118,7 +118,11 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   int prio_lo = 0, prio_hi = 0;
   HP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   HP_CUDA(cudaStreamCreateWithPriority(&s_main_, cudaStreamNonBlocking, prio_hi));
-  HP_CUDA(cudaStreamCreateWithPriority(&s_comm_, cudaStreamNonBlocking, prio_lo));
+  // A/B switch HP_COMM_PRIO=hi (W > 1): the NCCL buckets' stream at the
+  // compute stream's priority (profiles/r01_ab_comm_prio.txt)
+  const char* cprio = std::getenv("HP_COMM_PRIO");
+  const bool comm_hi = comm_ && cprio && std::string(cprio) == "hi";
+  HP_CUDA(cudaStreamCreateWithPriority(&s_comm_, cudaStreamNonBlocking, comm_hi ? prio_hi : prio_lo));
   if (comm_) {
     // per-bucket updates on their own stream, so bucket k+1's allreduce
     // starts as soon as bucket k's finishes instead of behind k's update
