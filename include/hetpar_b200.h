@@ -285,12 +285,15 @@ hp_status hp_checkpoint_read(const char* path, hp_model_desc* m, hp_ckpt_desc* c
                              float* adam_m, float* adam_v, uint64_t n);
 /* save_checkpoint from device state (master rank): c supplies epoch, seed,
  * policy, world, update_freq and the scheduler; step, the optimizer and its
- * moments come from the engine.  Refused while an update group (K > 1) is
- * partially accumulated -- the format has no accumulator block. */
+ * moments come from the engine.  Inside a partially accumulated update group
+ * (K > 1) the file holds the last update's state and the pending rounds stay
+ * pending (the format has no accumulator block, as the reference's). */
 hp_status hp_engine_save_checkpoint(hp_engine* e, const char* path, const hp_ckpt_desc* c);
-/* load_checkpoint into device state: parameters, Adam moments and t, step;
- * the file's model must equal the engine's.  c (may be null) receives the
- * file's metadata. */
+/* load_checkpoint into device state: parameters, Adam moments and t, step,
+ * and the file's optimizer (kind, betas, eps) and weight policy, as the
+ * reference's TrainState (checkpoint.cpp:254, 282-289); the file's model must
+ * equal the engine's; a pending accumulation is dropped.  c (may be null)
+ * receives the file's metadata. */
 hp_status hp_engine_load_checkpoint(hp_engine* e, const char* path, hp_ckpt_desc* c);
 /* Epoch and rounds to skip after `step` updates of world x update_freq
  * lockstep rounds (engine.hpp:225-244). */
@@ -326,7 +329,7 @@ hp_status hp_engine_params_digest(hp_engine* e, uint64_t* digest);
  * EngineConfig::check_interval): rank 0's parameter digest is broadcast,
  * mismatches are summed over the ranks, and any mismatch is HP_ENUMERIC
  * ("k ranks diverged from master parameters at step P") on every rank.
- * Collective when the engine has a communicator of world > 1. */
+ * Collective whenever the engine has a communicator (world 1 included). */
 hp_status hp_engine_set_digest_check(hp_engine* e, uint64_t every, int debug);
 /* Number of this library's kernels launched since creation (for bench). */
 hp_status hp_engine_kernel_launches(hp_engine* e, uint64_t* n);
@@ -337,6 +340,9 @@ hp_status hp_engine_timer_read(hp_engine* e, int which, char* name, uint64_t cap
                                double* ms, uint64_t* launches, double* bytes,
                                double* flops);
 hp_status hp_engine_step_count(hp_engine* e, uint64_t* step);
+/* StepEngine::pending_rounds (engine.hpp:165): rounds accumulated since the
+ * last update (0 .. update_freq - 1). */
+hp_status hp_engine_pending_rounds(hp_engine* e, uint64_t* n);
 /* CUDA events on the engine's compute stream (the stream every kernel of the
  * step is launched on): mark(slot) records, elapsed(a, b) waits for b and
  * returns milliseconds between the two marks. slots 0..7. */
@@ -416,6 +422,14 @@ hp_status hp_debug_gemm_generic(int on);
 hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf16,
                              const void* qkv, void* o, float* lse, const void* dO,
                              void* dqkv, int path);
+/* LayerNorm of the engine (x [T x d] -> y, mean/rstd [T]) and, when dy is
+ * non-null, its backward: dx, dg = colsum(dy * xhat), db = colsum(dy) and
+ * (dbias non-null) colsum(dx).  bf16 = 1: bf16 x / y / dy / dx (d % 256 == 0,
+ * d <= 1024 takes the bulk-copy kernels the BERT step runs); deferred = 1
+ * runs the column-sum final as a separate launch, as the engine does. */
+hp_status hp_debug_layernorm(int T, int d, int bf16, const void* x, const float* g, const float* b,
+                             void* y, float* mean, float* rstd, const void* dy, void* dx, float* dg,
+                             float* db, float* dbias, int deferred);
 /* One Adam (sgd=0) or SGD (sgd=1) update of the device kernel on caller-owned
  * device fp32 buffers, no scaling: compare with kern::adam_update<float>. */
 hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n,

@@ -167,6 +167,7 @@ _SIGS = {
     "hp_engine_timers": [P, I],
     "hp_engine_timer_read": [P, I, C.c_char_p, U64, P, P, P, P],
     "hp_engine_step_count": [P, P],
+    "hp_engine_pending_rounds": [P, P],
     "hp_engine_mark": [P, I],
     "hp_engine_elapsed": [P, I, I, P],
     "hp_engine_synchronize": [P],
@@ -201,6 +202,7 @@ _SIGS = {
     "hp_debug_gemm_trace": [P],
     "hp_debug_gemm_generic": [I],
     "hp_debug_attention": [I, P, I, I, I, I, P, P, P, P, P, I],
+    "hp_debug_layernorm": [I, I, I, P, P, P, P, P, P, P, P, P, P, P, I],
     "hp_debug_adam": [P, P, P, P, U64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float,
                       C.c_float, I],
 }

@@ -747,10 +747,14 @@ class StepEngine:
         call("hp_engine_save_checkpoint", self._h, path.encode(), C.byref(cd))
 
     def load_checkpoint(self, path: str) -> CheckpointMeta:
-        """HCK1 into device state: parameters, Adam m / v / t, step."""
+        """HCK1 into device state: parameters, Adam m / v / t, step, and the
+        file's optimizer and weight policy (checkpoint.cpp:254, 282-289)."""
         cd = _lib.CkptDesc()
         call("hp_engine_load_checkpoint", self._h, path.encode(), C.byref(cd))
-        return CheckpointMeta.from_desc(cd)
+        meta = CheckpointMeta.from_desc(cd)
+        self.optim = OptimConfig(meta.optimizer, meta.beta1, meta.beta2, meta.eps)
+        self.exec.policy = meta.policy
+        return meta
 
     def step_count(self) -> int:
         s = C.c_uint64()
@@ -788,6 +792,13 @@ class StepEngine:
         d = C.c_uint64()
         call("hp_engine_params_digest", self._h, C.byref(d))
         return d.value
+
+    def pending_rounds(self) -> int:
+        """StepEngine::pending_rounds (engine.hpp:165): rounds accumulated
+        since the last update."""
+        n = C.c_uint64()
+        call("hp_engine_pending_rounds", self._h, C.byref(n))
+        return n.value
 
     @property
     def step(self) -> int:

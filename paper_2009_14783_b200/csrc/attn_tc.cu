@@ -168,8 +168,6 @@ __global__ void __launch_bounds__(kThreadsF, 4)
                 bf16* __restrict__ o, float* __restrict__ lse, int T_total,
                 unsigned long long* tr) {
   if (threadIdx.x == 0) atr(tr, 0);
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t raw[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(raw));
   const int b = blockIdx.x, h = blockIdx.y;
@@ -298,8 +296,6 @@ __global__ void __launch_bounds__(kThreadsB, 2)
                 const int* __restrict__ cu, int H, const bf16* __restrict__ o,
                 const bf16* __restrict__ dO, const float* __restrict__ lse, bf16* __restrict__ dqkv,
                 int T_total) {
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t raw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(align1024(raw));
   const int b = blockIdx.x, h = blockIdx.y;
@@ -966,7 +962,7 @@ void attention_fwd_tc(const DevBatch& b, int H, const void* qkv, void* o, float*
     HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr = true;
   }
-  launch_pdl(PDL_ATTN, attn_tc::attn_fwd_tc, dim3(b.B, H), dim3(attn_tc::kThreadsF), sm, s, 1, mq,
+  launch_ex(attn_tc::attn_fwd_tc, dim3(b.B, H), dim3(attn_tc::kThreadsF), sm, s, 1, mq,
              (const int*)b.cu, H, static_cast<attn_tc::bf16*>(o), lse, b.T, g_attn_trace);
   HP_CUDA(cudaGetLastError());
   count_launch();
@@ -984,7 +980,7 @@ void attention_bwd_tc(const DevBatch& b, int H, const void* qkv, const void* o, 
     HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr = true;
   }
-  launch_pdl(PDL_ATTN, attn_tc::attn_bwd_tc, dim3(b.B, H), dim3(attn_tc::kThreadsB), sm, s, 1, mq, mg,
+  launch_ex(attn_tc::attn_bwd_tc, dim3(b.B, H), dim3(attn_tc::kThreadsB), sm, s, 1, mq, mg,
              (const int*)b.cu, H, static_cast<const attn_tc::bf16*>(o),
              static_cast<const attn_tc::bf16*>(dO), (const float*)lse,
              static_cast<attn_tc::bf16*>(dqkv), b.T);

@@ -371,6 +371,14 @@ hp_status hp_engine_step_count(hp_engine* e, uint64_t* step) {
   HP_API_END
 }
 
+hp_status hp_engine_pending_rounds(hp_engine* e, uint64_t* n) {
+  HP_API_BEGIN
+  ENG(e);
+  need(n, "n");
+  *n = E.pending_rounds();
+  HP_API_END
+}
+
 hp_status hp_engine_mark(hp_engine* e, int slot) {
   HP_API_BEGIN
   ENG(e);
@@ -444,13 +452,14 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
 hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n, float lr,
                         float b1, float b2, float eps, float c1, float c2, int sgd) {
   HP_API_BEGIN
-  int* bad = nullptr;
-  HP_CUDA(cudaMalloc(&bad, 4));
-  HP_CUDA(cudaMemset(bad, 0, 4));
+  unsigned long long* err = nullptr;
+  HP_CUDA(cudaMalloc(&err, hp::kErrWords * 8));
+  const unsigned long long e0[hp::kErrWords] = {0ull, ~0ull, ~0ull, ~0ull};
+  HP_CUDA(cudaMemcpy(err, e0, sizeof(e0), cudaMemcpyHostToDevice));
   hp::AdamArgs a{};
   a.p = p; a.m = m; a.v = v; a.g = g; a.n = n;
   a.lr = lr; a.b1 = b1; a.b2 = b2; a.eps = eps; a.c1 = c1; a.c2 = c2;
-  a.bad = bad; a.sgd = sgd;
+  a.err = err; a.sgd = sgd;
   std::vector<uint64_t> items;
   for (uint64_t o = 0; o < n; o += 65536)
     items.insert(items.end(), {o, std::min<uint64_t>(65536, n - o), o, 1, 1});
@@ -461,8 +470,35 @@ hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n
   a.nitems = static_cast<int>(items.size() / 5);
   hp::adam_update(a, 0);
   HP_CUDA(cudaDeviceSynchronize());
-  HP_CUDA(cudaFree(bad));
+  unsigned long long h[hp::kErrWords];
+  HP_CUDA(cudaMemcpy(h, err, sizeof(h), cudaMemcpyDeviceToHost));
+  HP_CUDA(cudaFree(err));
   HP_CUDA(cudaFree(d_items));
+  // the other elements are updated; the lowest offending index is reported
+  if (h[2] != ~0ull) hp::fail(HP_ENUMERIC, "non-finite gradient at flat index " + std::to_string(h[2]));
+  HP_API_END
+}
+
+hp_status hp_debug_layernorm(int T, int d, int bf16, const void* x, const float* g, const float* b,
+                             void* y, float* mean, float* rstd, const void* dy, void* dx, float* dg,
+                             float* db, float* dbias, int deferred) {
+  HP_API_BEGIN
+  const hp::DType t = bf16 ? hp::DType::bf16 : hp::DType::f32;
+  hp::layernorm_fwd(T, d, x, t, g, b, y, t, mean, rstd, 0);
+  if (dy) {
+    const size_t fl = std::max(hp::colsum_scratch_floats(T, d), hp::colsum_part_floats(T, d));
+    float* scratch = nullptr;
+    HP_CUDA(cudaMalloc(&scratch, fl * 4));
+    hp::DeferredFinal f;
+    f.part = scratch;
+    // deferred: the engine's form (partials now, the final launched separately)
+    hp::layernorm_bwd(T, d, dy, t, x, t, mean, rstd, g, dx, t, dg, db, dbias, scratch, 0,
+                      deferred ? &f : nullptr);
+    if (deferred) hp::launch_final(f, 0);
+    HP_CUDA(cudaDeviceSynchronize());
+    HP_CUDA(cudaFree(scratch));
+  }
+  HP_CUDA(cudaDeviceSynchronize());
   HP_API_END
 }
 

@@ -11,11 +11,12 @@
 //     the loss kernel retires -- it does not block backward (gradients are
 //     unnormalized sums);
 //   * gradient buckets (contiguous ranges of the canonical flat order, walked
-//     from the end) are allreduced on the comm stream as soon as
-//     backward finishes their parameters, with 1/sum(weight) folded into the
-//     NCCL reduction (ncclRedOpCreatePreMulSum with a device scalar);
-//   * Adam (bit-exact f32 kern::adam_update) updates the fp32 master copy and
-//     refreshes the bf16 working copy the tcgen05 GEMMs read.
+//     from the end) are allreduced (plain ncclSum) on the comm
+//     stream as soon as backward finishes their parameters;
+//   * the update divides each reduced bucket by sum(weight) in f64 -- the
+//     reference's order, all_reduce_sum then g /= weight (engine.hpp:145-151)
+//     -- and runs Adam (bit-exact f32 kern::adam_update) on the fp32 master
+//     copy, refreshing the bf16 working copy the tcgen05 GEMMs read.
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (nsys / ncu range filters)
 #include "engine.h"
 
@@ -58,6 +59,12 @@ int Engine::pidx(const std::string& name) const {
   for (size_t i = 0; i < table_.size(); ++i)
     if (table_[i].name == name) return static_cast<int>(i);
   fail(HP_EINDEX, "no parameter named " + name);
+}
+
+std::string Engine::param_at(uint64_t flat_index) const {
+  for (const ParamEntry& p : table_)
+    if (flat_index >= p.offset && flat_index < p.offset + p.size()) return p.name;
+  return "#" + std::to_string(flat_index);
 }
 
 const void* Engine::w(int idx) const {
@@ -118,11 +125,9 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   int prio_lo = 0, prio_hi = 0;
   HP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   HP_CUDA(cudaStreamCreateWithPriority(&s_main_, cudaStreamNonBlocking, prio_hi));
-  // A/B switch HP_COMM_PRIO=hi (W > 1): the NCCL buckets' stream at the
-  // compute stream's priority (profiles/r01_ab_comm_prio.txt)
-  const char* cprio = std::getenv("HP_COMM_PRIO");
-  const bool comm_hi = comm_ && cprio && std::string(cprio) == "hi";
-  HP_CUDA(cudaStreamCreateWithPriority(&s_comm_, cudaStreamNonBlocking, comm_hi ? prio_hi : prio_lo));
+  // (the NCCL buckets' stream at the compute stream's priority measured
+  // neutral at N = 2 and 4, profiles/r01_ab_comm_prio.txt)
+  HP_CUDA(cudaStreamCreateWithPriority(&s_comm_, cudaStreamNonBlocking, prio_lo));
   if (comm_) {
     // per-bucket updates on their own stream, so bucket k+1's allreduce
     // starts as soon as bucket k's finishes instead of behind k's update
@@ -141,9 +146,12 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     const char* e = std::getenv("HP_SPARSE_EMB");
     const Bucket& last = buckets_.back();
     const uint64_t W = comm_ ? static_cast<uint64_t>(comm_->world) : 1;
-    sparse_emb_ = W > 1 && !(e && std::string(e) == "0") && last.first_param == 0 &&
-                  last.last_param == 0 && d_ % 8 == 0 &&
-                  x_.max_tokens * (d_ + 4) * W < 2 * (W - 1) * m_.vocab * d_;
+    // (HP_SPARSE_EMB=1 forces it whenever the engine has a communicator --
+    // world 1 included, so one GPU runs the exchange's collectives)
+    const bool forced = comm_ && e && std::string(e) == "1";
+    sparse_emb_ = (forced || (W > 1 && !(e && std::string(e) == "0") &&
+                              x_.max_tokens * (d_ + 4) * W < 2 * (W - 1) * m_.vocab * d_)) &&
+                  last.first_param == 0 && last.last_param == 0 && d_ % 8 == 0;
     if (sparse_emb_) {
       emb_cap_ = static_cast<int>(x_.max_tokens);
       emb_rows_ = static_cast<float*>(dalloc((size_t)emb_cap_ * (d_ + 4) * 4));
@@ -174,21 +182,9 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   }
 
   params_ = static_cast<float*>(dalloc(n_ * 4));
-  {
-    // HP_NCCL_REG=1: the gradient buffer from ncclMemAlloc, registered with the
-    // communicator (zero-copy user-buffer collectives) -- A/B
-    const char* e = std::getenv("HP_NCCL_REG");
-    nccl_reg_ = comm_ && comm_->world > 1 && e && std::string(e) == "1";
-  }
-  if (nccl_reg_) {
-    void* g = nullptr;
-    HP_NCCL(ncclMemAlloc(&g, n_ * 4));
-    HP_CUDA(cudaMemset(g, 0, n_ * 4));
-    HP_NCCL(ncclCommRegister(comm_->nccl, g, n_ * 4, &grads_reg_));
-    grads_ = static_cast<float*>(g);
-  } else {
-    grads_ = static_cast<float*>(dalloc(n_ * 4));
-  }
+  // (an ncclMemAlloc'd, communicator-registered gradient buffer measured no
+  // gain, profiles/r01_ab_nccl_register.txt)
+  grads_ = static_cast<float*>(dalloc(n_ * 4));
   adam_m_ = static_cast<float*>(dalloc(n_ * 4));
   adam_v_ = static_cast<float*>(dalloc(n_ * 4));
   HP_CUDA(cudaMemset(params_, 0, n_ * 4));
@@ -357,9 +353,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     // per-layer-parity gradient buffers (layer l uses slot l & 1): a buffer a
     // weight-gradient GEMM reads is rewritten two layers later, so the
     // data-gradient chain does not wait on the weight-gradient stream
-    // (HP_LAYER_SLOTS=1: one slot, reuse distance one layer -- A/B)
-    const char* e = std::getenv("HP_LAYER_SLOTS");
-    rd_ = (e && std::string(e) == "1") ? 1 : 2;
+    rd_ = 2;
     pbuf_[0] = dB_;
     for (int i = 1; i < 4; ++i) pbuf_[i] = dalloc(T * d_ * asz_);
     ubuf_[0] = dU_;
@@ -383,11 +377,10 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   }
   inv_w_ = static_cast<float*>(dalloc(4));
   inv_w64_ = static_cast<double*>(dalloc(8));
-  flags_ = static_cast<int*>(dalloc(2 * 4));
+  err_ = static_cast<unsigned long long*>(dalloc(kErrWords * 8));
   d_hyper_ = static_cast<float*>(dalloc(4 * 4));
   HP_CUDA(cudaMallocHost(&h_lw_, 6 * 8));
-  HP_CUDA(cudaMallocHost(&h_flags_, 2 * 4));
-  HP_CUDA(cudaMemset(flags_, 0, 8));
+  HP_CUDA(cudaMallocHost(&h_err_, kErrWords * 8));
 
   if (comm_) {
     // gradient buckets reduce with plain ncclSum (NVLS-eligible: the NVSwitch
@@ -410,23 +403,18 @@ Engine::~Engine() {
         cudaEventDestroy(pr.second);
       }
   }
-  if (have_premul_ && comm_) ncclRedOpDestroy(premul_, comm_->nccl);
   for (auto& t : tm_)
     for (auto& pr : t.ev) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
     }
   for (void* p : allocs_) cudaFree(p);
-  if (nccl_reg_ && comm_) {
-    if (grads_reg_) ncclCommDeregister(comm_->nccl, grads_reg_);
-    ncclMemFree(grads_);
-  }
   for (int i = 0; i < kStageBufs; ++i) {
     if (h_stage_[i]) cudaFreeHost(h_stage_[i]);
     if (ev_stage_[i]) cudaEventDestroy(ev_stage_[i]);
   }
   if (h_lw_) cudaFreeHost(h_lw_);
-  if (h_flags_) cudaFreeHost(h_flags_);
+  if (h_err_) cudaFreeHost(h_err_);
   if (h_params_) cudaFreeHost(h_params_);
   for (auto& e : ev_bucket_) cudaEventDestroy(e);
   if (ev_ser_) cudaEventDestroy(ev_ser_);
@@ -506,8 +494,9 @@ void Engine::set_adam(const float* m, const float* v, uint64_t t) {
 // device state; the byte format lives in checkpoint.cpp.
 void Engine::save_checkpoint(const std::string& path, const hp_ckpt_desc& c) {
   if (in_flight_) fail(HP_ECONFIG, "save_checkpoint while a round is in flight");
-  if (acc_count_ != 0)
-    fail(HP_ECONFIG, "save_checkpoint inside a partially accumulated update group (update_freq > 1)");
+  // inside a partially accumulated update group (K > 1) the file holds the
+  // state of the last update, as the reference's does (TrainState has no
+  // accumulator, checkpoint.cpp:165-212); the pending rounds stay pending
   std::vector<float> p(n_), m(n_), v(n_);
   synchronize();
   HP_CUDA(cudaMemcpy(p.data(), params_, n_ * 4, cudaMemcpyDeviceToHost));
@@ -536,12 +525,31 @@ void Engine::load_checkpoint(const std::string& path, hp_ckpt_desc* out) {
   for (size_t i = 0; i < ft.size(); ++i)
     if (ft[i].name != table_[i].name || ft[i].rows != table_[i].rows || ft[i].cols != table_[i].cols)
       fail(HP_ECONFIG, "resume model spec does not match the checkpoint");
-  if (d.opt_kind != o_.kind) fail(HP_ECONFIG, "checkpoint optimizer kind differs from the engine's");
+  // the optimizer and the weight policy come from the file, as
+  // load_checkpoint's TrainState does (checkpoint.cpp:254, 282-289)
+  if (d.opt_kind != HP_OPT_ADAM && d.opt_kind != HP_OPT_SGD)
+    fail(HP_EIO, "checkpoint has an unknown optimizer kind");
+  if (d.policy != HP_POLICY_SENTENCES && d.policy != HP_POLICY_TOKENS)
+    fail(HP_EIO, "checkpoint has an unknown weight policy");
   hck1_parse(read_file(path), nullptr, nullptr, p.data(), m.data(), v.data(), n_);
+  o_.kind = d.opt_kind;
+  o_.beta1 = d.beta1;
+  o_.beta2 = d.beta2;
+  o_.eps = d.eps;
+  x_.policy = d.policy;
   set_params(p.data(), n_, 0);
-  if (d.opt_kind == HP_OPT_ADAM) set_adam(m.data(), v.data(), d.opt_t);
+  if (d.opt_kind == HP_OPT_ADAM) {
+    set_adam(m.data(), v.data(), d.opt_t);
+  } else {
+    HP_CUDA(cudaMemset(adam_m_, 0, n_ * 4));
+    HP_CUDA(cudaMemset(adam_v_, 0, n_ * 4));
+    adam_t_ = 0;
+  }
   step_ = d.step;
+  // a loaded state starts a fresh update group
   acc_count_ = 0;
+  if (acc_grads_) HP_CUDA(cudaMemset(acc_grads_, 0, n_ * 4));
+  if (d_acc_lw_) HP_CUDA(cudaMemset(d_acc_lw_, 0, 2 * 8));
   if (out) *out = d;
 }
 
@@ -787,17 +795,9 @@ void Engine::wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done) {
   // 768 x 768 x 4096) then takes half the SMs for longer instead of all of
   // them with 8-way fp32 reductions, leaving the rest to the data-gradient
   // chain (C2: 7640 vs 7536 samples/s; cap 1: 7250)
-  static const int wg_split_cap = [] {
-    const char* e = std::getenv("HP_WGRAD_SPLIT_MAX");  // A/B knob, 0 = heuristic
-    return e ? std::atoi(e) : 2;
-  }();
-  if (wg_split_cap > 0) {
-    GemmArgs c = g;
-    c.max_splits = wg_split_cap;
-    gemm(c, s_wg_);
-  } else {
-    gemm(g, s_wg_);
-  }
+  GemmArgs c = g;
+  c.max_splits = 2;
+  gemm(c, s_wg_);
   tstop(TM_GEMM, 2.0 * g.M * g.N * g.K,
         (double)asz_ * ((double)g.M * g.K + (double)g.K * g.N) +
             (g.ct == DType::f32 ? 4.0 : 2.0) * g.M * g.N,
@@ -1240,13 +1240,23 @@ void Engine::round_async(int dummy, double lr) {
   a.c2 = static_cast<float>(c2);
   a.hyper = d_hyper_;  // the same three values, read on the device
   a.inv_w64 = inv_w64_;  // g = (float)((double)sum * (1 / total weight))
-  a.flags = flags_;
-  a.bad = flags_ + 1;
+  a.err = err_;
   a.sgd = o_.kind == HP_OPT_SGD;
   a.shadow = shadow_;
+  // the first round after a sync starts a fresh error state; later unsynced
+  // rounds keep it (sticky), so round_sync reports the first error
+  if (!in_flight_) {
+    const unsigned long long e0[kErrWords] = {0ull, ~0ull, ~0ull, ~0ull};
+    HP_CUDA(cudaMemcpyAsync(err_, e0, sizeof(e0), cudaMemcpyHostToDevice, s_main_));
+    pending_.clear();
+  }
+  const uint32_t seq = ++seq_;
+  pending_.push_back(Pending{seq, step_, adam_t_, acc_count_, final_round});
+  if (final_round) pending_.back().adam_t = adam_t_ - 1;  // t before this round's ++t
   // pageable source: staged by the driver at the call, so the host array can
   // be reused at once; ordered before the round on s_main_
-  const float hyper[4] = {a.lr, a.c1, a.c2, 0.f};
+  float hyper[4] = {a.lr, a.c1, a.c2, 0.f};
+  std::memcpy(&hyper[3], &seq, 4);
   HP_CUDA(cudaMemcpyAsync(d_hyper_, hyper, sizeof(hyper), cudaMemcpyHostToDevice, s_main_));
 
   // a timed graph's events are re-recorded by every replay: read the previous
@@ -1355,7 +1365,6 @@ void Engine::round_body(int dummy) {
   upd_forked_ = false;
   emb_sparse_round_ = false;
   emb_split_round_ = false;
-  HP_CUDA(cudaMemsetAsync(flags_, 0, 8, s_main_));
   // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
   forward(!dummy);
   loss_reduce(row_loss_, batch_.M, row_loss_ + batch_.M, m_.with_nsp ? batch_.B : 0, d_lw_,
@@ -1380,7 +1389,7 @@ void Engine::round_body(int dummy) {
     // the side stream joins here (updates depend on the weight finalised below)
     HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_fwd_, 0));
   }
-  finalize_weight(d_lw_, inv_w_, inv_w64_, flags_, sw);
+  finalize_weight(d_lw_, inv_w_, inv_w64_, err_, d_hyper_, sw);
   // K > 1: running [loss, weight] totals; the K-th round's update divides by
   // the total weight (engine.hpp:147-151)
   if (phase_ != 0) accumulate_weight(d_lw_, d_acc_lw_, d_lw_ + 4, inv_w64_, phase_ == 2, sw);
@@ -1439,7 +1448,7 @@ void Engine::round_body(int dummy) {
     HP_CUDA(cudaStreamWaitEvent(s_main_, ev_upd_done_, 0));
   }
   HP_CUDA(cudaMemcpyAsync(h_lw_, d_lw_, 6 * 8, cudaMemcpyDeviceToHost, s_main_));
-  HP_CUDA(cudaMemcpyAsync(h_flags_, flags_, 2 * 4, cudaMemcpyDeviceToHost, s_main_));
+  HP_CUDA(cudaMemcpyAsync(h_err_, err_, kErrWords * 8, cudaMemcpyDeviceToHost, s_main_));
 }
 
 // The reference's cross-rank parameter check (engine.hpp:170-184): rank 0's
@@ -1450,7 +1459,7 @@ void Engine::round_body(int dummy) {
 // byte-serial params_digest stays available as digest()).
 void Engine::check_digest_on_cadence() {
   NvtxRange nv("hp.digest_check");
-  if (!comm_ || comm_->world < 2 || !grad_comm_) return;
+  if (!comm_ || !grad_comm_) return;  // world 1 included: the same collectives
   const uint64_t every = check_debug_ ? 1 : check_every_;
   if (every == 0 || step_ % every != 0) return;
   const uint64_t bytes = n_ * 4;
@@ -1489,22 +1498,30 @@ void Engine::round_sync(hp_round_out* out) {
   if (!in_flight_) fail(HP_ECONFIG, "round_sync without a round in flight");
   HP_CUDA(cudaEventSynchronize(ev_done_));
   in_flight_ = false;
-  // per-round checks on the aggregated [loss, weight] (engine.hpp:134-137)
-  if (h_flags_[0] & 1) {
-    if (last_final_) {
-      --step_;
-      --adam_t_;
+  // per-round checks (engine.hpp:134-137 on the aggregated [loss, weight],
+  // optim.hpp:131-133 on the gradient), of the FIRST failing round since the
+  // last sync; the counters return to that round's entry state (the loss
+  // checks throw before the update; a bad gradient throws inside it, after
+  // Optimizer::step's ++t, before the engine's ++step)
+  const unsigned long long kNone = ~0ull;
+  const unsigned long long loss_seq = h_err_[0] ? h_err_[1] : kNone, grad_seq = h_err_[3];
+  if (loss_seq != kNone || grad_seq != kNone) {
+    const bool loss_first = loss_seq <= grad_seq;
+    const unsigned long long seq = loss_first ? loss_seq : grad_seq;
+    Pending p{};
+    for (const Pending& q : pending_)
+      if (q.seq == seq) p = q;
+    pending_.clear();
+    step_ = p.step;
+    adam_t_ = p.adam_t + (!loss_first && p.final_round ? 1 : 0);
+    acc_count_ = 0;  // the update group is abandoned (its accumulator is re-zeroed by the next flush)
+    if (loss_first) {
+      if (h_err_[0] & 1) fail(HP_ENUMERIC, "non-finite aggregated loss after step " + std::to_string(p.step));
+      fail(HP_ENUMERIC, "total batch weight is zero: every rank was dummy");
     }
-    fail(HP_ENUMERIC, "non-finite aggregated loss after step " + std::to_string(step_));
+    fail(HP_ENUMERIC, "non-finite gradient for parameter " + param_at(h_err_[2]));
   }
-  if (h_flags_[0] & 2) {
-    if (last_final_) {
-      --step_;
-      --adam_t_;
-    }
-    fail(HP_ENUMERIC, "total batch weight is zero: every rank was dummy");
-  }
-  if (h_flags_[1]) fail(HP_ENUMERIC, "non-finite gradient at step " + std::to_string(step_));
+  pending_.clear();
   if (last_final_) check_digest_on_cadence();
   if (out) {
     // K > 1: the report covers the K rounds (loss_sum / weight of the flush)

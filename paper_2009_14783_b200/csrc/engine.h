@@ -56,12 +56,13 @@ class Engine {
   void forward_only(double* loss_sum, double* weight);
   uint64_t digest();
   uint64_t step() const { return step_; }
+  uint64_t pending_rounds() const { return acc_count_; }
   void timers(bool on);
   void mark(int slot);
   double elapsed(int a, int b);
   void synchronize();
   uint64_t stage_bytes() const { return stage_bytes_; }
-  uint64_t readback_bytes() const { return 6 * 8 + 2 * 4; }
+  uint64_t readback_bytes() const { return 6 * 8 + kErrWords * 8; }
   void timer_read(int which, std::string* name, double* ms, uint64_t* launches, double* bytes,
                   double* flops);
 
@@ -151,9 +152,19 @@ class Engine {
   double* d_lw_ = nullptr;  // [loss, weight] (global after the allreduce)
   float* inv_w_ = nullptr;
   double* inv_w64_ = nullptr;
-  int* flags_ = nullptr;  // [0] loss/weight flags, [1] bad grad
+  unsigned long long* err_ = nullptr;    // numeric-error state (kernels.h kErrWords)
   double* h_lw_ = nullptr;
-  int* h_flags_ = nullptr;
+  unsigned long long* h_err_ = nullptr;
+  // rounds issued since the last sync: a pipelined error rolls the counters
+  // back to the failing round (its sequence number travels in hyper[3])
+  struct Pending {
+    uint32_t seq;
+    uint64_t step, adam_t, acc_count;
+    bool final_round;
+  };
+  std::vector<Pending> pending_;
+  uint32_t seq_ = 0;
+  std::string param_at(uint64_t flat_index) const;
   float* h_params_ = nullptr;
 
   cudaStream_t s_main_ = nullptr, s_comm_ = nullptr;
@@ -175,8 +186,6 @@ class Engine {
   cudaEvent_t ev_fwd_ = nullptr, ev_comm_done_ = nullptr, ev_done_ = nullptr;
   std::vector<cudaEvent_t> ev_bucket_;
   size_t next_bucket_ = 0;
-  ncclRedOp_t premul_ = ncclSum;
-  bool have_premul_ = false;
 
   bool capture_ = false;
   // N > 1, word embedding alone in the last bucket: its gradient leaves the
@@ -196,8 +205,6 @@ class Engine {
   float* emb_gath_ = nullptr;  // [world][cap][d + 4]
   bool attn_long_ = false;  // 128 < max_seq <= 512: attention_*_long
   bool grad_comm_ = true;  // measurement toggle (hp_engine_set_grad_comm)
-  bool nccl_reg_ = false;      // grads_ from ncclMemAlloc + ncclCommRegister
-  void* grads_reg_ = nullptr;
   // check_digest_on_cadence (engine.hpp:170-184): every check_every_ updates
   // (every update when check_debug_), N > 1
   uint64_t check_every_ = 100;

@@ -65,8 +65,6 @@ struct Params {
   const void* resid;
   int64_t ld_resid;
   int vec;  // C / aux / resid rows are 16-byte aligned
-  int split_boxes;  // operand tiles loaded as 64-row / one-atom TMA boxes
-  int kb2;          // two k-blocks per stage, one 3-D TMA box per operand (A K-major)
   int debug;  // profiling only: 0 normal, 1 skip TMA loads, 2 skip MMAs, 3 skip epilogue
   unsigned long long* trace;  // profiling only: CTA 0 clock64 timeline (see kTr*)
 };
@@ -487,7 +485,7 @@ enum EpiKind : int {
 // Full 32-column chunk [n, n+32) of the warp's 32 rows starting at row0.
 // Preconditions (checked by the caller): n + 32 <= N, p.vec == 1.  `pre`:
 // the prefetched aux (pre_kind 1, dGELU) or residual (pre_kind 2) chunk.
-template <int EK, bool NoSplit = false>
+template <int EK>
 __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, int lane, int row0,
                                                 int n, float* v, const uint4 (&pre)[4], int pre_kind) {
   constexpr bool kAnyF32 = EK == EK_GENERIC || EK == EK_F32;
@@ -502,7 +500,7 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, in
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
   }
-  if constexpr (kAnyF32 && !NoSplit) {
+  if constexpr (kAnyF32) {
     if (p.splits > 1) {
       staged_out(true, st, lane, v, static_cast<char*>(p.c) + co0 * 4, p.ldc * 4, rows_left, 1);
       return;
@@ -579,16 +577,14 @@ __device__ __forceinline__ void decode_unit(const Params& p, int u, int mt_rows,
 // tile, 6 for 128x128 or a CTA pair's 128x128 half of 256x256).
 constexpr int kSmemBudget = 232448;  // 227 KB opt-in per CTA
 constexpr int kEpiStageBytes = 2048;  // per epilogue warp
-constexpr int kXSlotBytes = 4096;      // split-K exchange: one 32 x 32 fp32 chunk per epilogue warp
-template <int BN, int CG, bool CS = false>
+template <int BN, int CG>
 struct Tile {
   static constexpr int BNL = BN / CG;  // B columns staged by this CTA
   static constexpr uint32_t kBTileBytes = BNL * BK * 2;
   static constexpr uint32_t kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kXBytes = CS ? kEpiWarps * kXSlotBytes : 0;
-  static constexpr int kFit = (kSmemBudget - 2048 - kEpiWarps * kEpiStageBytes - kXBytes) / kStageBytes;
+  static constexpr int kFit = (kSmemBudget - 2048 - kEpiWarps * kEpiStageBytes) / kStageBytes;
   static constexpr int kStages = kFit < 8 ? kFit : 8;
-  static constexpr size_t kSmem = kStages * kStageBytes + 1024 + kEpiWarps * kEpiStageBytes + kXBytes + 1024;
+  static constexpr size_t kSmem = kStages * kStageBytes + 1024 + kEpiWarps * kEpiStageBytes + 1024;
   static_assert(kStages >= 3, "pipeline too shallow");
   static_assert(kSmem <= kSmemBudget, "smem plan over budget");
 };
@@ -601,25 +597,11 @@ struct Tile {
 //   traffic per FLOP drops by a third.  Both CTAs' TMA complete on the
 //   leader's full barrier; commits multicast to both CTAs' empty / tmem_full
 //   barriers; both CTAs' epilogues release the leader's tmem_empty barrier.
-// CS (cluster split-K, CG = 1, fp32 output): the two CTAs of a cluster take
-//   the same 128 x BN tile over the two halves of K; the second CTA's epilogue
-//   ships its accumulator chunk by chunk into the first CTA's smem (st.async
-//   completing on the receiver's mbarrier), the first adds it to its own and
-//   stores -- no zero-fill of C, no global atomics, a fixed summation order.
-// MC (multicast, CG = 1, BN = 256): a 2 x 2 cluster computes a 256 x 512
-//   super-tile; CTA (i, j) owns rows m0 + 128 i, columns (2 nt + j) 256. The
-//   A tile is shared along the cluster row and the B tile along the column:
-//   each CTA loads half of each and multicasts it to its peer, so L2 serves
-//   24 KB per CTA per k-block instead of 48 (the CTA pair's 256 x 256 tile
-//   needs 32). A stage is released once this CTA and both peers writing into
-//   it have consumed it (empty count 3, commits multicast to those CTAs).
-template <int BN, int CG, int EK, bool CS = false, bool MC = false>
+template <int BN, int CG, int EK>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const Params p) {
-  static_assert(!CS || (CG == 1 && EK == EK_F32), "cluster split-K: one CTA per tile, fp32 C");
-  static_assert(!MC || (CG == 1 && BN == 256 && !CS), "multicast: single-CTA 128 x 256 tiles");
-  using TL = Tile<BN, CG, CS>;
+  using TL = Tile<BN, CG>;
   constexpr int BNL = TL::BNL;
   constexpr int STAGES = TL::kStages;
   constexpr uint32_t kStageBytes = TL::kStageBytes;
@@ -631,44 +613,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
-  uint64_t* xfull = tmem_empty + 2;      // [kEpiWarps] (CS, receiver)
-  uint64_t* xempty = xfull + kEpiWarps;  // [kEpiWarps] (CS, sender)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + kEpiWarps);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     trace_at(p, 0);
     trace_cta(p, 0);
   }
-  constexpr int kClu = MC ? 4 : ((CG == 2 || CS) ? 2 : 1);  // CTAs per cluster
+  constexpr int kClu = CG;  // CTAs per cluster
   const uint32_t rank = kClu > 1 ? cluster_rank() : 0;
   const uint32_t row_rank = CG == 2 ? rank : 0;  // which 128 rows of the tile this CTA owns
-  const int mc_i = MC ? static_cast<int>(rank >> 1) : 0, mc_j = MC ? static_cast<int>(rank & 1) : 0;
-  // MC: this CTA's tile within the cluster's super-tile
-  auto mc_tile = [&](int& m0, int& nt) {
-    if constexpr (MC) {
-      m0 += mc_i * BM;
-      nt = 2 * nt + mc_j;
-    }
-  };
   const int unit0 = blockIdx.x / kClu, unit_step = gridDim.x / kClu;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MC ? 3 : 1);
+      mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
       mbar_init(&tmem_empty[a], CG * kEpiWarps);
     }
-    if constexpr (CS) {
-      for (int w = 0; w < kEpiWarps; ++w) {
-        mbar_init(&xfull[w], 1);
-        mbar_init(&xempty[w], 1);
-      }
-    }
-
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -691,9 +656,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (kClu > 1) cluster_sync_all();  // peer barriers initialised before use
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
-  // the prologue above overlapped the previous kernel's tail (launch.cuh)
-  pdl_wait();
-  pdl_trigger();
   if (threadIdx.x == 0) trace_at(p, 1);
 
   // Work units: static striding, unit u = blockIdx / CG + i * (gridDim / CG).
@@ -703,9 +665,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   // and no gain at N=4 under concurrent NCCL rings.)
   auto take_unit = [&](uint32_t i) -> int {
     const int u = unit0 + static_cast<int>(i) * unit_step;
-    if constexpr (CS) {  // u = tile; this CTA's unit = its K half (split = rank)
-      return u < p.units / 2 ? 2 * u + static_cast<int>(rank) : -1;
-    }
     return u < p.units ? u : -1;
   };
 
@@ -718,85 +677,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int u = take_unit(ui);
       if (u < 0) break;
       int m0, nt, kb0, kb1;
-      decode_unit(p, u, BM * CG * (MC ? 2 : 1), m0, nt, kb0, kb1);
-      mc_tile(m0, nt);
+      decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
       const int am0 = m0 + static_cast<int>(row_rank) * BM;       // this CTA's A rows
       const int bn0 = nt * BN + static_cast<int>(row_rank) * BNL;  // this CTA's B columns
-      // kb2: a ring slot is two stages, [A kb | A kb+1][B kb | B kb+1]
-      const int kstep = p.kb2 ? 2 : 1;
-      const int nslots = p.kb2 ? STAGES / 2 : STAGES;
-      const uint32_t slot_bytes = p.kb2 ? 2 * kStageBytes : kStageBytes;
-      for (int kb = kb0; kb < kb1; kb += kstep, ++it) {
-        const int s = it % nslots;
-        const uint32_t ph = (it / nslots) & 1;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         if (lane == 0) trace_at(p, kTrP + it, kTrF);
-        uint8_t* sa = smem + s * slot_bytes;
-        uint8_t* sb = sa + (p.kb2 ? 2 : 1) * kATileBytes;
+        uint8_t* sa = smem + s * kStageBytes;
+        uint8_t* sb = sa + kATileBytes;
         const int k0 = kb * BK;
         if (elect_one()) {
           if (debug_bit(p, 1)) {  // profiling mode: no loads, MMA on stale smem
             if (CG == 1 || rank == 0) mbar_arrive(&full[s]);
-          } else if (!MC && p.kb2) {
-            // A: 3-D view (64, M, K / 64), box (64, BM, 2); B K-major likewise
-            // (box rows BNL), B MN-major atoms: box (64, 128 K rows, BNL / 64)
-            if constexpr (CG == 2) {
-              if (rank == 0) mbar_expect_tx(&full[s], 2 * slot_bytes);
-              const uint32_t cb = mapa_shared(smem_u32(&full[s]), 0);
-              tma_3d_cg2(&map_a, cb, sa, 0, am0, kb);
-              if (!p.b_mn) tma_3d_cg2(&map_b, cb, sb, 0, bn0, kb);
-              else tma_3d_cg2(&map_b, cb, sb, 0, k0, bn0 / 64);
-            } else {
-              mbar_expect_tx(&full[s], slot_bytes);
-              tma_3d(&map_a, &full[s], sa, 0, am0, kb);
-              if (!p.b_mn) tma_3d(&map_b, &full[s], sb, 0, bn0, kb);
-              else tma_3d(&map_b, &full[s], sb, 0, k0, bn0 / 64);
-            }
-          } else if constexpr (MC) {
-            uint64_t* bar = &full[s];
-            mbar_expect_tx(bar, kStageBytes);  // own halves + the peers' halves
-            const uint16_t amask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 1)));
-            const uint16_t bmask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2)));
-            // A rows [64 j, +64) of the tile shared with the row peer (half-height maps)
-            if (!p.a_mn) tma_2d_mc(&map_a, bar, sa + mc_j * 8192, k0, am0 + mc_j * 64, amask);
-            else tma_3d_mc(&map_a, bar, sa + mc_j * 8192, 0, k0, am0 / 64 + mc_j, amask);
-            // B columns [128 i, +128) of the tile shared with the column peer
-            if (!p.b_mn) tma_2d_mc(&map_b, bar, sb + mc_i * 16384, k0, bn0 + mc_i * 128, bmask);
-            else tma_3d_mc(&map_b, bar, sb + mc_i * 16384, 0, k0, (bn0 + mc_i * 128) / 64, bmask);
-          } else if (p.split_boxes) {
-            // every operand tile as 64-row / one-atom boxes (8 KB per TMA
-            // instruction; HP_GEMM_SPLITBOX=1 -- A/B)
-            uint64_t* bar = &full[s];
-            uint32_t cbar = 0;
-            if constexpr (CG == 2) {
-              if (rank == 0) mbar_expect_tx(&full[s], 2 * kStageBytes);
-              cbar = mapa_shared(smem_u32(&full[s]), 0);
-            } else {
-              mbar_expect_tx(bar, kStageBytes);
-            }
-            auto ld2 = [&](const CUtensorMap* m, uint8_t* dst, int c0, int c1) {
-              if constexpr (CG == 2) tma_2d_cg2(m, cbar, dst, c0, c1); else tma_2d(m, bar, dst, c0, c1);
-            };
-            auto ld3 = [&](const CUtensorMap* m, uint8_t* dst, int c0, int c1, int c2) {
-              if constexpr (CG == 2) tma_3d_cg2(m, cbar, dst, c0, c1, c2); else tma_3d(m, bar, dst, c0, c1, c2);
-            };
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (!p.a_mn) ld2(&map_a, sa + h * 8192, k0, am0 + 64 * h);
-              else if (p.a_atoms) ld3(&map_a, sa + h * 8192, 0, k0, am0 / 64 + h);
-              else ld2(&map_a, sa + h * 8192, am0 + 64 * h, k0);
-            }
-#pragma unroll
-            for (int j = 0; j < BNL / 64; ++j) {
-              if (!p.b_mn) {
-                if (p.b_grouped) ld3(&map_b, sb + j * 8192, 0, bn0 + 64 * j, kb);
-                else ld2(&map_b, sb + j * 8192, k0, bn0 + 64 * j);
-              } else if (p.b_atoms) {
-                ld3(&map_b, sb + j * 8192, 0, k0, bn0 / 64 + j);
-              } else {
-                ld2(&map_b, sb + j * 8192, bn0 + 64 * j, k0);
-              }
-            }
           } else if constexpr (CG == 1) {
             uint64_t* bar = &full[s];
             mbar_expect_tx(bar, kStageBytes);
@@ -859,57 +753,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t db0 = umma_desc(s0 + kATileBytes, p.b_mn ? 8192 : 16, 1024);
       const uint64_t dak = p.a_mn ? (2048 >> 4) : (32 >> 4);
       const uint64_t dbk = p.b_mn ? (2048 >> 4) : (32 >> 4);
-      // kb2 slots: B after both A tiles; an MN-major B atom spans 128 K rows
-      const uint64_t db2 = umma_desc(s0 + 2 * kATileBytes, p.b_mn ? 16384 : 16, 1024);
-      const int kstep = p.kb2 ? 2 : 1;
-      const int nslots = p.kb2 ? STAGES / 2 : STAGES;
-      const uint32_t slot_bytes = p.kb2 ? 2 * kStageBytes : kStageBytes;
       uint32_t it = 0, lt = 0;
       for (;; ++lt) {
         const int u = take_unit(lt);
         if (u < 0) break;
         int m0, nt, kb0, kb1;
-        decode_unit(p, u, BM * CG * (MC ? 2 : 1), m0, nt, kb0, kb1);
-        mc_tile(m0, nt);
+        decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
         const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
         mbar_wait(&tmem_empty[as], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dacc = tmem_base + as * kAccStride;
-        for (int kb = kb0; kb < kb1; kb += kstep, ++it) {
-          const int s = it % nslots;
-          const uint32_t ph = (it / nslots) & 1;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
           if (lane == 0) trace_at(p, kTrF + it, kTrC);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t soff = static_cast<uint64_t>(s) * (slot_bytes >> 4);
+          const uint64_t soff = static_cast<uint64_t>(s) * (kStageBytes >> 4);
           if (elect_one()) {
             if (!debug_bit(p, 2)) {
-              if (p.kb2) {
-                const int nq = (kb + 1 < kb1 ? 2 : 1) * (BK / 16);
-                for (int q = 0; q < nq; ++q) {
-                  const uint64_t ad = da0 + soff + (((q >> 2) * kATileBytes + (q & 3) * 32) >> 4);
-                  const uint64_t bd = db2 + soff + (p.b_mn ? q * (2048 >> 4)
-                                                           : (((q >> 2) * TL::kBTileBytes + (q & 3) * 32) >> 4));
-                  if constexpr (CG == 2)
-                    umma_bf16_cg2(dacc, ad, bd, idesc, (kb > kb0 || q > 0) ? 1u : 0u);
-                  else
-                    umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || q > 0) ? 1u : 0u);
-                }
-              } else {
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                  const uint64_t ad = da0 + soff + k * dak, bd = db0 + soff + k * dbk;
-                  if constexpr (CG == 2)
-                    umma_bf16_cg2(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-                  else
-                    umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-                }
+              for (int k = 0; k < BK / 16; ++k) {
+                const uint64_t ad = da0 + soff + k * dak, bd = db0 + soff + k * dbk;
+                if constexpr (CG == 2)
+                  umma_bf16_cg2(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                else
+                  umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
               }
             }
             if constexpr (CG == 2) umma_commit_cg2(&empty[s]);
-            else if constexpr (MC)  // this CTA and the two peers that write into its stages
-              umma_commit_mc(&empty[s], static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 1)) |
-                                                              (1u << (rank ^ 2))));
             else umma_commit(&empty[s]);
           }
           __syncwarp();
@@ -942,19 +814,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t lt = 0;
     const uint32_t empty_leader[2] = {CG == 2 ? mapa_shared(smem_u32(&tmem_empty[0]), 0) : 0u,
                                       CG == 2 ? mapa_shared(smem_u32(&tmem_empty[1]), 0) : 0u};
-    // CS exchange: this warp's slot in the receiver (rank 0) and the barriers
-    const uint32_t xslot = smem_u32(smem + STAGES * kStageBytes + 1024 + kEpiWarps * kEpiStageBytes +
-                                    ew * kXSlotBytes);
-    const uint32_t xslot_rx = CS ? mapa_shared(xslot, 0) : 0u;
-    const uint32_t xfull_rx = CS ? mapa_shared(smem_u32(&xfull[ew]), 0) : 0u;
-    const uint32_t xempty_tx = CS ? mapa_shared(smem_u32(&xempty[ew]), 1) : 0u;
-    uint32_t xq = 0;  // chunks exchanged by this warp so far
     for (;; ++lt) {
       const int u = take_unit(lt);
       if (u < 0) break;
       int m0, nt, kb0, kb1;
-      decode_unit(p, u, BM * CG * (MC ? 2 : 1), m0, nt, kb0, kb1);
-      mc_tile(m0, nt);
+      decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
       const int n0 = nt * BN;
       const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
       const int row0 = m0 + static_cast<int>(row_rank) * BM + quarter * 32;
@@ -981,36 +845,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tslot = kTrX + 3 * ((c - first) / kChunkStep);
         if (tr) trace_at(p, tslot, 1024);
         uint32_t r[32];
-        if constexpr (CS) {
-          if (rank == 0 && lane == 0) mbar_expect_tx(&xfull[ew], 32 * 128);
-        }
         TMEM_LD32(taddr + c, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (tr) trace_at(p, tslot + 1, 1024);
-        if constexpr (CS) {
-          // row `lane`, 16-byte piece j at lane * 128 + ((j ^ (lane & 7)) << 4)
-          if (rank == 1) {
-            if (xq > 0) mbar_wait(&xempty[ew], (xq - 1) & 1);  // receiver drained the slot
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              st_async_v4(xslot_rx + lane * 128 + ((j ^ (lane & 7)) << 4),
-                          make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]), xfull_rx);
-            ++xq;
-            continue;
-          }
-          mbar_wait(&xfull[ew], xq & 1);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint4 o = lds128(xslot + lane * 128 + ((j ^ (lane & 7)) << 4));
-            r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + __uint_as_float(o.x));
-            r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + __uint_as_float(o.y));
-            r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + __uint_as_float(o.z));
-            r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + __uint_as_float(o.w));
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(xempty_tx);
-          ++xq;
-        }
         const int n = n0 + c;
         if (n < p.N && rows_left > 0 && !debug_bit(p, 4)) {
           float v[32];
@@ -1020,7 +857,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (EK != EK_GENERIC || (n + 32 <= p.N && p.vec == 1)) {
             uint4 pre[4];
             if (pre_kind) pre_consume(st, lane, cur, pre);
-            epilogue_staged<EK, CS>(p, st, lane, row0, n, v, pre, pre_kind);
+            epilogue_staged<EK>(p, st, lane, row0, n, v, pre, pre_kind);
           } else if constexpr (EK == EK_GENERIC) {
             epilogue_cols<32>(p, row0 + lane, n, v);
           }
@@ -1045,8 +882,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     trace_at(p, 2);
     trace_cta(p, 1);
   }
-  // both CTAs done before the pair frees TMEM / before a CS sender exits
-  // while its receiver still signals it
+  // both CTAs done before the pair frees TMEM
   if constexpr (kClu > 1) cluster_sync_all();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1161,45 +997,20 @@ static int epilogue_vec_ok(const GemmArgs& g) {
   return 0;
 }
 
-template <int BN, int CG, int EK, bool CS = false, bool MC = false>
+template <int BN, int CG, int EK>
 static void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Params& p,
                       cudaStream_t s) {
   // stages + barriers (1 KB) + epilogue staging tiles + alignment slack
-  constexpr size_t smem = tc::Tile<BN, CG, CS>::kSmem;
+  constexpr size_t smem = tc::Tile<BN, CG>::kSmem;
   static bool attr = false;
   if (!attr) {
-    HP_CUDA(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, CG, EK, CS, MC>,
+    HP_CUDA(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, CG, EK>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  // CS: units = tiles x 2 halves, one cluster of two CTAs per tile at a time;
-  // MC: units = super-tiles (x splits), one 2 x 2 cluster per unit
-  const int clu = MC ? 4 : (CS ? 2 : CG);
-  int mc_clusters = num_sms() / 4;
-  if constexpr (MC) {
-    // 4-CTA clusters must fit whole GPCs: ask how many can be resident at once
-    static int active = 0;
-    if (!active) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(4 * mc_clusters);
-      cfg.blockDim = dim3(tc::kThreads);
-      cfg.dynamicSmemBytes = smem;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = 4;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      HP_CUDA(cudaOccupancyMaxActiveClusters(&active, tc::gemm_tc_kernel<BN, CG, EK, CS, MC>, &cfg));
-      if (active < 1) active = 1;
-    }
-    mc_clusters = std::min(mc_clusters, active);
-  }
-  const int grid = MC ? 4 * std::min(p.units, mc_clusters)
-                      : (CS ? 2 * std::min(p.units / 2, num_sms() / 2) : CG * std::min(p.units, num_sms() / CG));
-  launch_pdl(PDL_GEMM, tc::gemm_tc_kernel<BN, CG, EK, CS, MC>, dim3(grid), dim3(tc::kThreads), smem, s,
-             clu, ma, mb, p);
+  const int grid = CG * std::min(p.units, num_sms() / CG);
+  launch_ex(tc::gemm_tc_kernel<BN, CG, EK>, dim3(grid), dim3(tc::kThreads), smem, s,
+             CG, ma, mb, p);
   HP_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -1213,19 +1024,7 @@ void gemm_tc_set_generic(int on) { g_generic_only = on; }
 
 template <int EK>
 static void launch_ek(int cg, int bn, const CUtensorMap& ma, const CUtensorMap& mb,
-                      const tc::Params& p, cudaStream_t s, bool cs = false, bool mc = false) {
-  if constexpr (EK == tc::EK_F32) {
-    if (mc) {
-      launch_tc<256, 1, EK, false, true>(ma, mb, p, s);
-      return;
-    }
-    if (cs) {
-      if (bn == 256) launch_tc<256, 1, EK, true>(ma, mb, p, s);
-      else if (bn == 192) launch_tc<192, 1, EK, true>(ma, mb, p, s);
-      else launch_tc<128, 1, EK, true>(ma, mb, p, s);
-      return;
-    }
-  }
+                      const tc::Params& p, cudaStream_t s) {
   if (cg == 2) {
     if (bn == 256) launch_tc<256, 2, EK>(ma, mb, p, s);
     else if (bn == 192) launch_tc<192, 2, EK>(ma, mb, p, s);
@@ -1281,79 +1080,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   }
   if (g_force_splits && can_split) splits = g_force_splits;
   if (!can_split) splits = 1;
-  // Deterministic mode (HP_GEMM_CSPLIT=1): split-K with an fp32 C as two K
-  // halves per tile reduced inside a CTA cluster (CS, see gemm_tc_kernel)
-  // instead of zero-fill + fp32 atomics -- bit-reproducible weight gradients.
-  // One CTA per tile half (128 x BN, BN for the most CTAs up to the SM
-  // count). Off by default: the C2 step measured 6931 vs 7430 samples/s (a
-  // single CTA's 128 x 256 tile stages more bytes per FLOP than the CTA
-  // pair's 256 x 256 that the atomic split-K keeps).
-  bool cs = false;
-  {
-    static const int cs_env = [] {
-      const char* e = std::getenv("HP_GEMM_CSPLIT");
-      return e ? std::atoi(e) : 0;
-    }();
-    const int eligible_ek = epilogue_vec_ok(g) == 1 && g.N % 32 == 0 && !g_generic_only;
-    if (cs_env && can_split && splits >= 2 && num_kb >= 2 && eligible_ek && !g_force_splits &&
-        !g_force_cg && !g_force_bn) {
-      double bestc = -1;
-      int cbn_best = 256;
-      for (const int cbn : {256, 192, 128}) {
-        if (g.b.group && !g.b.trans && cbn % 64) continue;
-        const int tiles = ((g.M + tc::BM - 1) / tc::BM) * ((g.N + cbn - 1) / cbn);
-        const double w = cbn == 256 ? 1.0 : (cbn == 192 ? 0.97 : 0.9);
-        const double sc = std::min(2 * tiles, nsm) * w;
-        if (sc > bestc + 1e-9) {
-          bestc = sc;
-          cbn_best = cbn;
-        }
-      }
-      cs = true;
-      cg = 1;
-      bn = cbn_best;
-      splits = 2;
-    }
-  }
-  // Multicast mode (HP_GEMM_MC=1) for the fp32 split-K GEMMs: 2 x 2 clusters
-  // of 128 x 256 tiles sharing A along rows and B along columns (gemm_tc_kernel MC)
-  bool mc = false;
-  {
-    static const int mc_env = [] {
-      const char* e = std::getenv("HP_GEMM_MC");
-      return e ? std::atoi(e) : 0;
-    }();
-    const bool f32_plain = epilogue_vec_ok(g) == 1 && g.N % 32 == 0 && !g_generic_only &&
-                           g.ct == DType::f32 && g.act == ACT_NONE && !g.resid;
-    const bool a_ok = !g.a.trans || 64LL * ((g.M + 63) / 64) <= g.a.ld;
-    const bool b_ok = g.b.trans || 64LL * ((g.N + 63) / 64) <= g.b.ld;
-    if (mc_env && !cs && can_split && f32_plain && !g.b.group && a_ok && b_ok && !g_force_splits &&
-        !g_force_cg && !g_force_bn) {
-      mc = true;
-      cg = 1;
-      bn = 256;
-      const int st = ((g.M + 255) / 256) * ((g.N + 511) / 512);
-      const int slots = nsm / 4;
-      splits = std::max(1, std::min(std::max(1, slots / st), num_kb / 4));
-      if (g.max_splits > 0) splits = std::min(splits, g.max_splits);
-    }
-  }
-  const int m_tiles = mc ? (g.M + 255) / 256 : (g.M + tc::BM * cg - 1) / (tc::BM * cg);
+  const int m_tiles = (g.M + tc::BM * cg - 1) / (tc::BM * cg);
   const int kb_per_split = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per_split - 1) / kb_per_split;  // no empty splits
   const int bnl = bn / cg;  // B columns per CTA
-  static const bool sbox_env = [] {
-    const char* e = std::getenv("HP_GEMM_SPLITBOX");
-    return e && std::string(e) == "1";
-  }();
-  const bool sbox = sbox_env && !mc;
-  static const bool kb2_env = [] {
-    const char* e = std::getenv("HP_GEMM_KB2");
-    return e && std::string(e) == "1";
-  }();
-  const bool b_atoms_pre = !g.b.trans && (g.b.group || 64LL * ((g.N + 63) / 64) <= g.b.ld);
-  const bool kb2 = kb2_env && !mc && !sbox && !g.a.trans && g.K % 64 == 0 && num_kb >= 2 &&
-                   (g.b.trans || b_atoms_pre) && tc::Tile<256, 1>::kStages >= 4;
 
   // MN-major operands: "atom" maps view the row-major [K][MN] matrix as
   // (64 cols, K rows, MN/64 col-blocks) so one box brings every 8 KB swizzle
@@ -1371,16 +1101,11 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
       rank = 3;
       dims[0] = 64; dims[1] = g.K; dims[2] = a_blocks;
       str[0] = g.a.ld; str[1] = 64;
-      box[0] = 64; box[1] = 64; box[2] = (mc || sbox) ? 1 : tc::BM / 64;  // MC: half a tile per load
+      box[0] = 64; box[1] = 64; box[2] = tc::BM / 64;
     } else if (g.a.trans) {
       dims[0] = g.M; dims[1] = g.K; str[0] = g.a.ld; box[0] = 64; box[1] = 64;
-    } else if (kb2) {  // memory [M rows][K cols] as (64, M, K / 64): two k-blocks per box
-      rank = 3;
-      dims[0] = 64; dims[1] = g.M; dims[2] = g.K / 64;
-      str[0] = g.a.ld; str[1] = 64;
-      box[0] = 64; box[1] = tc::BM; box[2] = 2;
     } else {          // memory [M rows][K cols]
-      dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = (mc || sbox) ? 64 : tc::BM;
+      dims[0] = g.K; dims[1] = g.M; str[0] = g.a.ld; box[0] = 64; box[1] = tc::BM;
     }
     ma = make_map(g.a.p, rank, dims, str, box);
   }
@@ -1390,7 +1115,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     int rank = 2;
     if (!g.b.trans) {  // MN-major: memory [K rows][N cols] (or grouped blocks)
       rank = 3;
-      box[0] = 64; box[1] = kb2 ? 128 : 64; box[2] = sbox ? 1u : (uint32_t)((mc ? bnl / 2 : bnl) / 64);
+      box[0] = 64; box[1] = 64; box[2] = (uint32_t)(bnl / 64);
       if (g.b.group) {
         dims[0] = 64; dims[1] = g.K; dims[2] = g.N / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
@@ -1406,15 +1131,9 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         rank = 3;
         dims[0] = 64; dims[1] = g.N; dims[2] = g.K / 64;
         str[0] = g.b.ld; str[1] = g.b.gstride;
-        box[0] = 64; box[1] = (uint32_t)(sbox ? 64 : bnl); box[2] = kb2 ? 2 : 1;
-      } else if (kb2) {  // (64, N, K / 64), two k-blocks per box
-        rank = 3;
-        dims[0] = 64; dims[1] = g.N; dims[2] = g.K / 64;
-        str[0] = g.b.ld; str[1] = 64;
-        box[0] = 64; box[1] = (uint32_t)bnl; box[2] = 2;
+        box[0] = 64; box[1] = (uint32_t)bnl; box[2] = 1;
       } else {
-        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64;
-        box[1] = (uint32_t)(sbox ? 64 : (mc ? bnl / 2 : bnl));
+        dims[0] = g.K; dims[1] = g.N; str[0] = g.b.ld; box[0] = 64; box[1] = (uint32_t)bnl;
       }
     }
     mb = make_map(g.b.p, rank, dims, str, box);
@@ -1427,7 +1146,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.a_atoms = a_atoms ? 1 : 0;
   p.b_atoms = b_atoms ? 1 : 0;
   p.m_tiles = m_tiles;
-  p.n_tiles = mc ? (g.N + 511) / 512 : (g.N + bn - 1) / bn;
+  p.n_tiles = (g.N + bn - 1) / bn;
   p.splits = splits;
   p.kb_per_split = kb_per_split;
   p.units = m_tiles * p.n_tiles * splits;
@@ -1436,12 +1155,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias; p.act = g.act;
   p.aux = g.aux; p.resid = g.resid; p.ld_resid = g.ld_resid;
   p.vec = epilogue_vec_ok(g);
-  p.split_boxes = sbox ? 1 : 0;
-  p.kb2 = kb2 ? 1 : 0;
   p.debug = g_debug_mode;
   p.trace = g_trace;
 
-  if (splits > 1 && !cs) {
+  if (splits > 1) {
     // partial sums are reduced into C: clear the output region first
     if (g.c_group) {
       HP_CUDA(cudaMemsetAsync(g.c, 0, sizeof(float) * (size_t)(g.N / g.c_group) * g.c_gstride, s));
@@ -1465,7 +1182,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     case tc::EK_BF16: launch_ek<tc::EK_BF16>(cg, bn, ma, mb, p, s); break;
     case tc::EK_GELU: launch_ek<tc::EK_GELU>(cg, bn, ma, mb, p, s); break;
     case tc::EK_DGELU: launch_ek<tc::EK_DGELU>(cg, bn, ma, mb, p, s); break;
-    case tc::EK_F32: launch_ek<tc::EK_F32>(cg, bn, ma, mb, p, s, cs, mc); break;
+    case tc::EK_F32: launch_ek<tc::EK_F32>(cg, bn, ma, mb, p, s); break;
     default: launch_ek<tc::EK_GENERIC>(cg, bn, ma, mb, p, s); break;
   }
 }

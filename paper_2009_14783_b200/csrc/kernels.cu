@@ -299,10 +299,7 @@ __global__ void colsum_final_kernel(int chunks, int N, const float* __restrict__
 }
 
 static constexpr int kColRows = 64;
-#ifndef HP_LN_BWD_ROWS
-#define HP_LN_BWD_ROWS 32
-#endif
-constexpr int kLnBwdRows = HP_LN_BWD_ROWS;  // rows per LayerNorm-backward CTA (multiple of 8)
+constexpr int kLnBwdRows = 32;  // rows per LayerNorm-backward CTA (multiple of 8)
 
 // Segment-embedding gradients in one pass: per 32-row chunk, the column sums
 // of the rows with segment 0 and with segment 1 (8 columns per thread), as
@@ -746,8 +743,6 @@ __global__ void __launch_bounds__(256) ln_fwd_bulk(int T, const bf16* __restrict
                                                    const float* __restrict__ bta, bf16* __restrict__ y,
                                                    float* __restrict__ mean, float* __restrict__ rstd) {
   constexpr int d = 256 * NV;
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ __align__(128) uint8_t lsm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(lsm);
   bf16* xs = reinterpret_cast<bf16*>(lsm + 128);
@@ -812,8 +807,6 @@ __global__ void __launch_bounds__(256, 1) ln_bwd_bulk(int T, const bf16* __restr
                                                       bf16* __restrict__ dx, float* __restrict__ part) {
   constexpr int d = 256 * NV;
   constexpr int RPW = kLnBwdRows / 8;
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ __align__(128) uint8_t lsm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(lsm);
   bf16* xs = reinterpret_cast<bf16*>(lsm + 128);
@@ -917,10 +910,10 @@ void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
     const int gb = (T + rows_cta - 1) / rows_cta;
     const size_t sm = 128 + (size_t)rows_cta * d * 2;
     switch (d / 256) {
-      case 1: launch_pdl(PDL_LN, ln_fwd_bulk<1>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      case 2: launch_pdl(PDL_LN, ln_fwd_bulk<2>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      case 3: launch_pdl(PDL_LN, ln_fwd_bulk<3>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
-      default: launch_pdl(PDL_LN, ln_fwd_bulk<4>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 1: launch_ex(ln_fwd_bulk<1>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 2: launch_ex(ln_fwd_bulk<2>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      case 3: launch_ex(ln_fwd_bulk<3>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
+      default: launch_ex(ln_fwd_bulk<4>, dim3(gb), dim3(256), sm, s, 1, T, (const bf16*)x, g, bta, (bf16*)y, mean, rstd); break;
     }
   } else {
     DISPATCH1(xt, X, DISPATCH1(yt, Y,
@@ -949,7 +942,7 @@ void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
       HP_CUDA(cudaFuncSetAttribute(ln_bwd_bulk<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
       attr_##NV = sm;                                                                           \
     }                                                                                           \
-    launch_pdl(PDL_LN, ln_bwd_bulk<NV>, dim3(chunks), dim3(256), sm, s, 1, T, (const bf16*)dy,      \
+    launch_ex(ln_bwd_bulk<NV>, dim3(chunks), dim3(256), sm, s, 1, T, (const bf16*)dy,      \
                (const bf16*)x, mean, rstd, g, (bf16*)dx, part);                                 \
   } break;
       LNB(1) LNB(2) LNB(3) default: LNB(4)
@@ -1423,18 +1416,23 @@ void loss_reduce(const float* a, int na, const float* b, int nb, double* out,
   count_launch();
 }
 
-__global__ void finalize_weight_kernel(const double* lw, float* inv_w, double* inv_w64, int* flags) {
+__device__ __forceinline__ unsigned long long round_seq(const float* hyper) {
+  return hyper ? (unsigned long long)__float_as_uint(hyper[3]) : 0ull;
+}
+__global__ void finalize_weight_kernel(const double* lw, float* inv_w, double* inv_w64,
+                                       unsigned long long* err, const float* hyper) {
   const double l = lw[0], w = lw[1];
-  int f = 0;
+  unsigned long long f = 0;
   if (!isfinite(l)) f |= 1;
   if (!(w > 0.0)) f |= 2;
-  *flags = f;
+  if (f && err[0] == 0) err[1] = round_seq(hyper);  // the first failing round
+  err[0] |= f;
   *inv_w64 = w > 0.0 ? 1.0 / w : 0.0;
   *inv_w = (float)(*inv_w64);
 }
-void finalize_weight(const double* lw, float* inv_w, double* inv_w64, int* flags,
-                     cudaStream_t s) {
-  finalize_weight_kernel<<<1, 1, 0, s>>>(lw, inv_w, inv_w64, flags);
+void finalize_weight(const double* lw, float* inv_w, double* inv_w64, unsigned long long* err,
+                     const float* hyper, cudaStream_t s) {
+  finalize_weight_kernel<<<1, 1, 0, s>>>(lw, inv_w, inv_w64, err, hyper);
   LAUNCH_CHECK();
   count_launch();
 }
@@ -1528,9 +1526,26 @@ __device__ __forceinline__ void adam_one(const AdamArgs& a, float& p, float& m, 
 // One CTA per work item.  float4 I/O when the item is 16-byte aligned.
 // Memory-bound: 6 CTAs (48 warps) per SM keep enough loads in flight, so the
 // register budget is pinned (<= 42).
+// the update is skipped when this round's loss / weight check failed, or an
+// earlier unsynced round's did (pipelined rounds stop at the first error)
+__device__ __forceinline__ bool skip_update(const AdamArgs& a) {
+  if (!a.err) return false;
+  return a.err[0] != 0 || a.err[3] < round_seq(a.hyper);
+}
+// a non-finite f64 gradient element (optim.hpp:131-133): skipped, recorded
+__device__ __forceinline__ void note_bad(const AdamArgs& a, uint64_t idx, unsigned long long& bad) {
+  bad = min(bad, (unsigned long long)idx);
+}
+__device__ __forceinline__ void flush_bad(const AdamArgs& a, unsigned long long bad) {
+  if (bad != ~0ull && a.err) {
+    atomicMin(&a.err[2], bad);
+    atomicMin(&a.err[3], round_seq(a.hyper));
+  }
+}
+
 template <bool ACC>  // ACC: add (then zero) the K > 1 accumulator a.g2
 __global__ void __launch_bounds__(256, 6) adam_kernel(const AdamArgs a0) {
-  if (a0.flags && *a0.flags) return;  // numeric error: leave parameters untouched
+  if (skip_update(a0)) return;  // numeric error: leave parameters untouched
   AdamArgs a = a0;
   if (a.hyper) {  // per-step scalars from device memory (graph replays)
     a.lr = a.hyper[0];
@@ -1540,8 +1555,8 @@ __global__ void __launch_bounds__(256, 6) adam_kernel(const AdamArgs a0) {
   const bool scale = a.inv_w64 != nullptr;
   const double sc = scale ? *a.inv_w64 : 1.0;
   bf16* sh = (bf16*)a.shadow;
-  int bad = 0;
-  // grid-stride over the work items (the grid may be capped: HP_ADAM_GRID)
+  unsigned long long bad = ~0ull;
+  // grid-stride over the work items
   for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
     const uint64_t* it = a.items + 5 * (uint64_t)item;
     const uint64_t lo = it[0], n = it[1], slo = it[2], cols = it[3], pcols = it[4];
@@ -1561,25 +1576,30 @@ __global__ void __launch_bounds__(256, 6) adam_kernel(const AdamArgs a0) {
         float* pp = &p.x; float* mm = &m.x; float* vv = &v.x; const float* gg = &g.x;
         // g /= total weight in f64, then cast to T (engine.hpp:151, optim.hpp:135)
         float gs[4];
+        bool ok[4];
         if constexpr (ACC) {  // K > 1: earlier rounds' sums, consumed (zeroed) here
           const float4 q = *reinterpret_cast<const float4*>(a.g2 + lo + i);
           *reinterpret_cast<float4*>(a.g2 + lo + i) = make_float4(0.f, 0.f, 0.f, 0.f);
           const float* qq = &q.x;
   #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const double gd = (double)gg[e] + (double)qq[e];
-            gs[e] = scale ? (float)(gd * sc) : (float)gd;
+            const double gd = scale ? ((double)gg[e] + (double)qq[e]) * sc : (double)gg[e] + (double)qq[e];
+            gs[e] = (float)gd;
+            ok[e] = isfinite(gd);
+            if (!ok[e]) note_bad(a, lo + i + e, bad);
           }
         } else {
   #pragma unroll
-          for (int e = 0; e < 4; ++e) gs[e] = scale ? (float)((double)gg[e] * sc) : gg[e];
+          for (int e = 0; e < 4; ++e) {
+            const double gd = scale ? (double)gg[e] * sc : (double)gg[e];
+            gs[e] = (float)gd;
+            ok[e] = isfinite(gd);
+            if (!ok[e]) note_bad(a, lo + i + e, bad);
+          }
         }
   #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float ge = gs[e];
-          if (!isfinite(ge)) { bad = 1; continue; }
-          adam_one(a, pp[e], mm[e], vv[e], ge);
-        }
+        for (int e = 0; e < 4; ++e)
+          if (ok[e]) adam_one(a, pp[e], mm[e], vv[e], gs[e]);
         adam_st4(a.p + lo + i, p);
         adam_st4(a.m + lo + i, m);
         adam_st4(a.v + lo + i, v);
@@ -1597,15 +1617,16 @@ __global__ void __launch_bounds__(256, 6) adam_kernel(const AdamArgs a0) {
         }
       }
       for (uint64_t i = n4 + threadIdx.x; i < n; i += blockDim.x) {
-        float ge;
+        double gd;
         if constexpr (ACC) {
-          const double gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
+          gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
           a.g2[lo + i] = 0.f;
-          ge = scale ? (float)(gd * sc) : (float)gd;
         } else {
-          ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+          gd = (double)a.g[lo + i];
         }
-        if (!isfinite(ge)) { bad = 1; continue; }
+        if (scale) gd *= sc;
+        if (!isfinite(gd)) { note_bad(a, lo + i, bad); continue; }
+        const float ge = (float)gd;
         float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
         adam_one(a, p, m, v, ge);
         a.p[lo + i] = p; a.m[lo + i] = m; a.v[lo + i] = v;
@@ -1613,15 +1634,16 @@ __global__ void __launch_bounds__(256, 6) adam_kernel(const AdamArgs a0) {
       }
     } else {
       for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        float ge;
+        double gd;
         if constexpr (ACC) {
-          const double gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
+          gd = (double)a.g[lo + i] + (double)a.g2[lo + i];
           a.g2[lo + i] = 0.f;
-          ge = scale ? (float)(gd * sc) : (float)gd;
         } else {
-          ge = scale ? (float)((double)a.g[lo + i] * sc) : a.g[lo + i];
+          gd = (double)a.g[lo + i];
         }
-        if (!isfinite(ge)) { bad = 1; continue; }
+        if (scale) gd *= sc;
+        if (!isfinite(gd)) { note_bad(a, lo + i, bad); continue; }
+        const float ge = (float)gd;
         float p = a.p[lo + i], m = a.m[lo + i], v = a.v[lo + i];
         adam_one(a, p, m, v, ge);
         a.p[lo + i] = p; a.m[lo + i] = m; a.v[lo + i] = v;
@@ -1629,15 +1651,11 @@ __global__ void __launch_bounds__(256, 6) adam_kernel(const AdamArgs a0) {
       }
     }
   }
-  if (bad) *a.bad = 1;
+  flush_bad(a, bad);
 }
 void adam_update(const AdamArgs& a, cudaStream_t s) {
   if (a.nitems == 0) return;
-  static const int cap = [] {
-    const char* e = std::getenv("HP_ADAM_GRID");  // A/B knob: cap on CTAs (0: one per item)
-    return e ? std::atoi(e) : 0;
-  }();
-  const int grid = cap > 0 ? std::min(a.nitems, cap) : a.nitems;
+  const int grid = a.nitems;
   if (a.g2)
     adam_kernel<true><<<grid, 256, 0, s>>>(a);
   else
@@ -1669,7 +1687,7 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(const AdamArgs a0, int m
                                                         const int* __restrict__ ucnts, int nl,
                                                         int stride, int V, int d, uint64_t lo,
                                                         uint64_t slo, uint64_t pcols) {
-  if (a0.flags && *a0.flags) return;
+  if (skip_update(a0)) return;
   AdamArgs a = a0;
   if (a.hyper) {
     a.lr = a.hyper[0];
@@ -1684,7 +1702,7 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(const AdamArgs a0, int m
   for (int l = 0; l < nl; ++l) total += ucnts[2 * l] + ucnts[2 * l + 1];
   const int nrows = mode ? total : V;
   const int lane = threadIdx.x & 31;
-  int bad = 0;
+  unsigned long long bad = ~0ull;
   for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < nrows; i += gridDim.x * 8) {
     int r = i;
     bool skip = false;
@@ -1705,18 +1723,22 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(const AdamArgs a0, int m
       float4 m = adam_ld4(a.m + base + c);
       float4 v = adam_ld4(a.v + base + c);
       float gs[4] = {g0, g0, g0, g0};
+      bool ok[4] = {true, true, true, true};
       if (mode) {
         const float4 g = adam_ld4(a.g + base + c);
         const float* gg = &g.x;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) gs[e] = scale ? (float)((double)gg[e] * sc) : gg[e];
+        for (int e = 0; e < 4; ++e) {
+          const double gd = scale ? (double)gg[e] * sc : (double)gg[e];
+          gs[e] = (float)gd;
+          ok[e] = isfinite(gd);
+          if (!ok[e]) note_bad(a, base + c + e, bad);
+        }
       }
       float* pp = &p.x; float* mm = &m.x; float* vv = &v.x;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (!isfinite(gs[e])) { bad = 1; continue; }
-        adam_one(a, pp[e], mm[e], vv[e], gs[e]);
-      }
+      for (int e = 0; e < 4; ++e)
+        if (ok[e]) adam_one(a, pp[e], mm[e], vv[e], gs[e]);
       adam_st4(a.p + base + c, p);
       adam_st4(a.m + base + c, m);
       adam_st4(a.v + base + c, v);
@@ -1727,7 +1749,7 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(const AdamArgs a0, int m
       }
     }
   }
-  if (bad) *a.bad = 1;
+  flush_bad(a, bad);
 }
 void adam_rows(const AdamArgs& a, int mode, const int* uids, const int* ucnts, int nl, int stride,
                int V, int d, uint64_t lo, uint64_t slo, uint64_t pcols, cudaStream_t s) {

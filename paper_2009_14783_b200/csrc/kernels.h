@@ -187,10 +187,19 @@ void col_sum(int R, int N, const void* x, int64_t ld, DType t, float* out,
 void loss_reduce(const float* a, int na, const float* b, int nb, double* out,
                  cudaStream_t s);
 
-// lw = [loss, weight]: finalize after the allreduce; inv_w = 1/weight (f32),
-// flags |= 1 when loss is non-finite, |= 2 when weight <= 0.
-void finalize_weight(const double* lw, float* inv_w, double* inv_w64, int* flags,
-                     cudaStream_t s);
+// Numeric-error state of the rounds issued since the last sync (sticky, so a
+// pipelined round_async sequence reports its FIRST error):
+//   err[0]  loss/weight flags (|= 1 non-finite aggregated loss, |= 2 weight <= 0)
+//   err[1]  sequence number of the round that first set err[0]
+//   err[2]  lowest flat index of a non-finite gradient
+//   err[3]  lowest sequence number of a round with a non-finite gradient
+// Reset to {0, ~0, ~0, ~0} by the engine before the first round after a sync.
+// A round's sequence number travels in hyper[3] (uint32 bits).
+constexpr int kErrWords = 4;
+// lw = [loss, weight]: finalize after the allreduce; inv_w = 1/weight (f32)
+// and the loss/weight checks of engine.hpp:134-137 into err.
+void finalize_weight(const double* lw, float* inv_w, double* inv_w64, unsigned long long* err,
+                     const float* hyper, cudaStream_t s);
 
 // Adam (kernels_scalar.cpp:74-83) bit-exact in f32 on identical inputs:
 //   g = grad * scale (scale from *inv_w64 when non-null, else 1)
@@ -202,8 +211,10 @@ struct AdamArgs {
   const float* hyper;     // device [lr, c1, c2]; overrides the scalars when non-null
   float* g2;              // K > 1: earlier rounds' gradient sums, added then zeroed (or null)
   const double* inv_w64;  // may be null
-  const int* flags;       // skip everything when *flags != 0
-  int* bad;               // set to 1 on a non-finite gradient
+  // error state (see kErrWords; may be null): the update is skipped when this
+  // or an earlier unsynced round failed a check; a non-finite f64 gradient
+  // (optim.hpp:131-133) skips that element and records its flat index
+  unsigned long long* err;
   int sgd;
   void* shadow;
   // work items [nitems][5] = {flat_lo, count, shadow_lo, cols, pcols}; one

@@ -181,13 +181,19 @@ hp_status hp_pg_broadcast(hp_comm* c, const void* payload, uint64_t len, uint64_
   if (!c || !out_len) hp::fail(HP_ECONFIG, "hp_pg_broadcast: null argument");
   if (root >= static_cast<uint64_t>(c->world))
     hp::fail(HP_ECOMM, "broadcast root " + std::to_string(root) + " out of range");
-  // the root's length first (non-root inputs are ignored)
-  double mine = c->rank == static_cast<int>(root) ? static_cast<double>(len) : 0.0;
-  const std::vector<double> lens = hp::all_gather(c, &mine, 1);
-  const uint64_t n = static_cast<uint64_t>(lens[root]);
+  // the root's length and every rank's capacity first (non-root lengths are
+  // ignored): a capacity short of the root's length fails on EVERY rank,
+  // before any of them enters the broadcast
+  const double mine[2] = {c->rank == static_cast<int>(root) ? static_cast<double>(len) : 0.0,
+                          static_cast<double>(cap)};
+  const std::vector<double> lens = hp::all_gather(c, mine, 2);
+  const uint64_t n = static_cast<uint64_t>(lens[2 * root]);
   *out_len = n;
-  if (n > cap) hp::fail(HP_ECONFIG, "broadcast: output buffer holds " + std::to_string(cap) +
-                                        " bytes, the root sent " + std::to_string(n));
+  for (int r = 0; r < c->world; ++r)
+    if (static_cast<uint64_t>(lens[2 * r + 1]) < n)
+      hp::fail(HP_ECONFIG, "broadcast: rank " + std::to_string(r) + "'s output buffer holds " +
+                               std::to_string(static_cast<uint64_t>(lens[2 * r + 1])) +
+                               " bytes, the root sent " + std::to_string(n));
   const hp::PgScratch p = hp::scratch(c);
   void* d = hp::ensure(p, n ? n : 1);
   if (c->rank == static_cast<int>(root) && n)

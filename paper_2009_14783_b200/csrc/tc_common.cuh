@@ -32,9 +32,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 // Spin on test_wait (non-blocking) rather than try_wait (which may suspend the
 // thread for an implementation-defined time): the C2 step measured 7480 vs
-// 7428 samples/s over five interleaved pairs.  -DHP_MBAR_TRYWAIT restores it.
+// 7428 samples/s over five interleaved pairs.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifndef HP_MBAR_TRYWAIT
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -46,19 +45,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
-#else
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-#endif
 }
 // Wait for threads that have nothing else to do (the epilogue warps while a
 // tile's mainloop runs): the suspend-time hint parks the warp in the barrier

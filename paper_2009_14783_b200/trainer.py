@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import math
 import os
+import sys
 import time
 from dataclasses import dataclass, field
 from typing import List, Optional
@@ -116,7 +117,16 @@ def train_run(cfg: EngineConfig, comm: Optional[api.Communicator] = None,
     ex = api.ExecConfig(**{**ex.__dict__, "max_tokens": tok, "max_batch": inst,
                            "max_masks": masks, "policy": cfg.policy,
                            "update_freq": cfg.update_freq})
-    opt = api.OptimConfig(cfg.opt_kind, cfg.beta1, cfg.beta2, cfg.eps)
+    # a resumed run takes the optimizer, its hyper-parameters, the weight
+    # policy, the scheduler and the seed from the checkpoint (TrainState,
+    # checkpoint.cpp:254, 282-289), not from cfg
+    if state:
+        opt = api.OptimConfig(state.optimizer, state.beta1, state.beta2, state.eps)
+        policy = state.policy
+        ex.policy = policy
+    else:
+        opt = api.OptimConfig(cfg.opt_kind, cfg.beta1, cfg.beta2, cfg.eps)
+        policy = cfg.policy
     seed = state.seed if state else cfg.seed
     eng = api.StepEngine(spec, opt, ex, comm=comm, seed=seed)
     try:
@@ -137,7 +147,7 @@ def train_run(cfg: EngineConfig, comm: Optional[api.Communicator] = None,
                 comm.barrier()
             if rank == 0:
                 eng.save_checkpoint(path, api.CheckpointMeta(
-                    epoch=epoch, seed=seed, policy=cfg.policy, world_size=world,
+                    epoch=epoch, seed=seed, policy=policy, world_size=world,
                     update_freq=cfg.update_freq, scheduler=sched))
 
         report = RunReport(world=world)
@@ -168,6 +178,9 @@ def train_run(cfg: EngineConfig, comm: Optional[api.Communicator] = None,
                 loader.close()
             if not stopped:
                 epoch += 1
+        if eng.pending_rounds() != 0:
+            print(f"hetpar_b200: warning: discarding a partial accumulation of "
+                  f"{eng.pending_rounds()} rounds at run end", file=sys.stderr)
         if saving:
             save_now(checkpoint_final_path(cfg.checkpoint_dir))
         if comm is not None and world > 1:

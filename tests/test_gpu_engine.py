@@ -558,3 +558,57 @@ def test_split_embedding_update_bit_identical(monkeypatch, arch, compute):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
     assert a[5] == b[5]
     assert a[6] == b[6] + 2 * len(batches)  # the split ran: two adam_rows launches per round
+
+
+def test_pipelined_rounds_report_the_first_error_and_roll_back():
+    """round_async pipelining (bench.py's value pass) with a failing round in
+    the middle: round_sync raises the FIRST error (engine.hpp:134-137), the
+    rounds after it do not update, and step / Adam t return to the failing
+    round's entry state -- parameters equal one clean round, bit for bit."""
+    rec, plan = c1_batches()
+    b = rec.batch(plan.batches[0])
+    ref = c1_engine()
+    ref.round(b, lr=1e-3)
+    want = ref.get_params()
+    eng = c1_engine()
+    eng.stage(b)
+    eng.round_async(False, 1e-3)
+    eng.round_async(True, 1e-3)    # every rank dummy: total weight 0
+    eng.round_async(False, 1e-3)   # must not update after the error
+    with pytest.raises(hp.NumericError, match="every rank was dummy"):
+        eng.round_sync()
+    assert eng.step == 1
+    assert eng.get_adam()[2] == 1
+    assert np.array_equal(eng.get_params().view(np.uint32), want.view(np.uint32))
+    # the engine carries on from there
+    rep = eng.round(b, lr=1e-3)
+    ref.round(b, lr=1e-3)
+    assert rep.step == 2 and np.array_equal(eng.get_params(), ref.get_params())
+
+
+def test_train_run_partial_accumulation_at_run_end_still_checkpoints(tmp_path, capfd):
+    """an epochs-bounded run with update_freq = 2 and an odd number
+    of rounds ends inside an update group; like the reference's train_run
+    (engine.hpp:310-314) it warns, discards the pending round and still writes
+    checkpoint_final with the last update's state."""
+    from paper_2009_14783_b200 import api
+    cfg = _c1_run_config(tmp_path, max_sentences=7, max_steps=1000, max_epochs=1,
+                         checkpoint_dir=str(tmp_path / "ck"))
+    rep = hp.train_run(cfg, exec_cfg=hp.ExecConfig(compute="f32"))
+    assert rep.final_step == 11  # 23 rounds -> 11 updates + 1 pending
+    assert "discarding a partial accumulation of 1 rounds" in capfd.readouterr().err
+    _, meta, p, _, _ = api.read_checkpoint(str(tmp_path / "ck" / "checkpoint_final.hck"))
+    assert meta.step == 11 and meta.opt_t == 11
+
+
+def test_resume_takes_the_optimizer_from_the_checkpoint(tmp_path):
+    """resuming an Adam checkpoint with a config that says SGD and
+    other betas continues with the file's Adam (kind, betas, eps), as the
+    reference's load_checkpoint does (checkpoint.cpp:254, 282-289)."""
+    ck = tmp_path / "a"
+    ra = hp.train_run(_c1_run_config(tmp_path, checkpoint_dir=str(ck), checkpoint_interval=4),
+                      exec_cfg=hp.ExecConfig(compute="f32"))
+    rb = hp.train_run(_c1_run_config(tmp_path, opt_kind="sgd", beta1=0.5, beta2=0.5, eps=1e-3,
+                                     resume_path=str(ck / "checkpoint_000004.hck")),
+                      exec_cfg=hp.ExecConfig(compute="f32"))
+    assert [s.loss for s in rb.steps] == [s.loss for s in ra.steps[4:]]

@@ -264,3 +264,36 @@ def test_reference_binary_grads_live(tmp_path):
     _, _, grad = mo.forward_backward(s, mo.init_parameters(s, 21),
                                      oracle_instances(golden("c1_records.npz"), ids))
     assert rel_norm(grad, g0) < 1e-13
+
+
+def test_torch_restatement_matches_numpy_oracle():
+    """oracle/torch_model.py (the fp32 autograd checker of the benchmark-shape
+    GPU tests) against the numpy f64 oracle on CPU: loss, weight and the flat
+    gradient, ragged instances, 2 layers; and its fp32 Adam against the
+    oracle's f32 restatement of kern::adam_update<float>."""
+    torch = pytest.importorskip("torch")
+    import torch_model as tm
+    s = mo.Spec(arch="bert_encoder", d_model=32, heads=4, vocab=53, max_seq=24, layers=2,
+                d_ff=48, label_smooth_eps=0.1)
+    rng = np.random.default_rng(8)
+    p = mo.init_parameters(s, 5) + 0.02 * rng.standard_normal(mo.flat_size(s))
+    batch = []
+    for n, m in ((24, 4), (9, 2), (1, 0)):
+        tok = rng.integers(0, s.vocab, n)
+        seg = np.array([0] * (n // 2) + [1] * (n - n // 2))
+        pos = np.sort(rng.choice(np.arange(0, n), m, replace=False))
+        batch.append(mo.Instance(tok, seg, pos, rng.integers(0, s.vocab, m), int(rng.integers(0, 2))))
+    l, w, g = mo.forward_backward(s, p, batch)
+    tl, tw, tg = tm.forward_backward(s, p, batch, device="cpu")
+    assert tw == w
+    assert abs(tl - l) <= 1e-5 * abs(l)
+    assert rel_norm(tg.double().numpy(), g) <= 1e-5
+    # Adam: torch fp32 vs the oracle's f32 restatement (torch's CPU vector
+    # kernels round a handful of elements differently: norm-wise 1e-7)
+    st = mo.AdamState()
+    p32 = p.astype(np.float32)
+    want = mo.adam_step(p32, g / w, st, 1e-3, np.float32)
+    gt = torch.from_numpy((g / w).astype(np.float32))
+    z = torch.zeros_like(gt)
+    got, _, _ = tm.adam_update_f32(torch.from_numpy(p32), z, z.clone(), gt, 1, 1e-3)
+    assert rel_norm(got.numpy(), want) <= 1e-7
