@@ -153,7 +153,7 @@ def reference_arm(args, rank, world):
         return 0
     cores = os.cpu_count() or 1
     if os.path.exists(REF_BIN):
-        threads = max(1, min(cores, 32))
+        threads = ref_threads()
         r = run_ref_bench(threads, 1, max(1, args.steps), args.warmup)
         kind = "reference"
         sample = (f"reference StepEngine<float>::round (engine.hpp:125-165) on {threads} in-process "
@@ -204,6 +204,69 @@ def emit(line):
         os.write(_JSON_FD, data)
 
 
+def ref_threads() -> int:
+    """Rank threads of the reference arm (all host cores, at most 32)."""
+    return max(1, min(os.cpu_count() or 1, 32))
+
+
+def check_first_loss(eng, wspec, batch) -> dict:
+    """Round 1's local loss (the engine's forward on batch 0 under the initial
+    parameters) against the numpy f64 oracle's forward of the same batch from
+    its own init of seed 21.  Tolerance 1e-2 relative (bf16 GEMM operands)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import model_oracle as mo  # the checker
+    t0 = time.perf_counter()
+    ls, w = eng.forward(batch)
+    ospec = mo.Spec(**wspec)
+    p = mo.init_parameters(ospec, 21).astype(np.float32).astype(np.float64)
+    n = batch.n_inst
+    insts = []
+    for i in range(n):
+        a, b = int(batch.tok_off[i]), int(batch.tok_off[i + 1])
+        c, d = int(batch.mask_off[i]), int(batch.mask_off[i + 1])
+        insts.append(mo.Instance(batch.tokens[a:b], batch.segments[a:b], batch.mask_pos[c:d],
+                                 batch.mask_orig[c:d], int(batch.label[i])))
+    ol, ow, _ = mo.forward_backward(ospec, p, insts, need_grad=False)
+    rel = abs(ls - ol) / abs(ol)
+    out = {"engine_loss": ls / w, "oracle_loss": ol / ow, "rel": rel, "tol": 1e-2,
+           "ok": bool(rel <= 1e-2 and w == ow), "seconds": time.perf_counter() - t0,
+           "oracle": "oracle/model_oracle.py forward (numpy f64), batch 0, init seed 21"}
+    if not out["ok"]:
+        raise RuntimeError(f"bench loss check failed: {out}")
+    return out
+
+
+def same_config_runs(hp, batch, args) -> dict:
+    """The reference arm's own workload on the GPU: masked_token_model (the
+    reference architecture, model.hpp:334-393) at d=768 h=12 V=30522 seq 128,
+    per-step batch of BATCH sequences, on the fp32 path and on the bf16
+    tcgen05 path; resident batch, CUDA events on the engine stream."""
+    spec = hp.ModelSpec(arch="masked_token_model", d_model=768, heads=12, vocab=30522, max_seq=SEQ,
+                        label_smooth_eps=0.1)
+    out = {"workload": f"masked_token_model d=768 h=12 V=30522 seq {SEQ} (the reference arm's "
+                       f"1-block proxy), {BATCH} sequences per step, Adam", "sequences_per_step": BATCH}
+    for comp in ("f32", "bf16"):
+        ex = hp.ExecConfig(compute=comp, policy="sentences", device=0, bucket_mb=200.0,
+                           max_tokens=BATCH * SEQ, max_batch=BATCH, max_masks=BATCH * SEQ // 2)
+        e = hp.StepEngine(spec, hp.OptimConfig("adam", 0.9, 0.98, 1e-9), ex, seed=21)
+        e.stage(batch)
+        for _ in range(max(3, args.warmup)):
+            e.round_async(False, 1e-4)
+        e.round_sync()
+        steps = max(5, min(args.steps, 20))
+        e.mark(0)
+        for _ in range(steps):
+            e.round_async(False, 1e-4)
+        e.mark(1)
+        ms = e.elapsed_ms(0, 1)
+        e.round_sync()
+        out[comp] = {"value": BATCH * steps / (ms / 1e3), "unit": "samples/s", "steps": steps,
+                     "ms_per_step": ms / steps}
+        e.close()
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 def main(argv=None):
     ap = argparse.ArgumentParser()
@@ -218,12 +281,15 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-loss-check", action="store_true")
+    ap.add_argument("--no-same-config", action="store_true")
     args = ap.parse_args(argv)
     _stdout_to_stderr()
     global BATCH, SEQ
     wspec, BATCH, SEQ, wmin, wmax, wdesc, wmodel = WORKLOADS[args.workload]
     if args.workload != "c2":
         args.no_cpu_baseline = True  # the CPU baseline is quoted on the headline config
+        args.no_same_config = True
     args.warmup = max(args.warmup, 3)
 
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
@@ -275,6 +341,14 @@ def main(argv=None):
     batches = [rec.batch(plan.batches[rb.batch_index]) for rb in sched]
     dummies = [rb.dummy for rb in sched]
     lr = 1e-4
+
+    # ---- first step's loss against the oracle (outside every timed region):
+    # the engine's forward on batch 0 under the initial parameters is round
+    # 1's local loss; the numpy f64 oracle (oracle/model_oracle.py, the
+    # checker) recomputes it from its own init of the same seed
+    loss_check = None
+    if rank == 0 and not args.no_loss_check:
+        loss_check = check_first_loss(eng, wspec, batches[0])
 
     # ---- value: batch resident in HBM ----
     eng.stage(batches[0])
@@ -369,25 +443,42 @@ def main(argv=None):
                      "hidden_frac": max(0.0, 1.0 - exposed / ar["ms"]) if ar["ms"] > 0 else None,
                      "note": "busbw = S/t*2(W-1)/W, S = fp32 gradient bytes, buckets alone on "
                              "one stream; exposed = t_step - t_step(no gradient allreduce)"}
-    clocks.stop()
+    # ---- the reference's own proxy workload on the GPU (like-for-like anchor) ----
+    same = None
+    if rank == 0 and world == 1 and not args.no_same_config:
+        same = same_config_runs(hp, batches[0], args)
 
-    # ---- roofline of the dominant kernel class (tcgen05 GEMMs) ----
+    # ---- roofline of the dominant kernel class (tcgen05 GEMMs): one round's
+    # GEMMs replayed back to back from a CUDA graph -- their serialised time,
+    # the quantity a per-kernel profile (the committed ncu launch list) sums --
+    # against their algorithmic FLOPs; the attention class likewise ----
+    gr = eng.class_replay(0, iters=10)
+    ar_ = eng.class_replay(1, iters=10)
+    clocks.stop()
     peaks, peak_src = load_peaks()
-    g = timers[0]
-    tflops = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
+    tflops = gr["flops"] / (gr["ms"] / 1e3) / 1e12 if gr["ms"] > 0 else 0.0
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+    step_ms = ms_max / args.steps
     roofline = {"bound": "tensor", "kernel": "gemm_tc_kernel (all GEMMs of the step)",
                 "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
                 "frac": tflops / peak if peak else None, "traffic": traffic,
                 "peak_source": f"bf16_tflops_sustained of {peak_src}",
-                "gemm_ms_per_step": g["ms"] / args.steps,
-                "gemm_share_of_step": (g["ms"] / ms_timed) if ms_timed > 0 else None,
-                "gemm_launches_per_step": g["launches"] / args.steps}
+                "method": "one round's GEMMs replayed back to back (CUDA graph, one stream); "
+                          "achieved = their algorithmic FLOPs / that serialised time",
+                "gemm_flops_per_step": gr["flops"],
+                "gemm_ms_per_step": gr["ms"],
+                "gemm_share_of_step": gr["ms"] / step_ms if step_ms > 0 else None,
+                "gemm_launches_per_step": gr["launches"],
+                "attention": {"ms_per_step": ar_["ms"], "flops_per_step": ar_["flops"],
+                              "tflops": ar_["flops"] / (ar_["ms"] / 1e3) / 1e12 if ar_["ms"] > 0 else None,
+                              "frac": (ar_["flops"] / (ar_["ms"] / 1e3) / 1e12 / peak)
+                              if ar_["ms"] > 0 and peak else None,
+                              "launches_per_step": ar_["launches"]}}
     breakdown = {t["name"]: round(t["ms"] / args.steps, 4) for t in timers}
     # the memory-bound classes against the measured HBM copy bandwidth
     # (algorithmic bytes / their serialised event time)
@@ -405,12 +496,15 @@ def main(argv=None):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             if os.path.exists(REF_BIN):
-                r = run_ref_bench(1, 8, 1, 0)
-                cpu = {"value": r["samples_per_s"], "unit": "samples/s", "cores": 1,
+                threads = ref_threads()
+                r = run_ref_bench(threads, 1, 2, 1)
+                cpu = {"value": r["samples_per_s"], "unit": "samples/s", "cores": threads,
                        "kind": "reference",
-                       "sample": "8 sequences x 128 tokens, one StepEngine<float>::round of the "
-                                 "reference compiled from source (oracle/_ref), 1 rank thread; "
-                                 "1-block proxy of C2 (masked_token_model d=768 h=12 V=30522)"}
+                       "sample": f"{threads} in-process rank threads x 1 sequence of 128 tokens, "
+                                 "1 warm-up + 2 timed StepEngine<float>::round of the reference "
+                                 "compiled from source (oracle/_ref) -- the reference arm's own "
+                                 "configuration; 1-block proxy of C2 (masked_token_model d=768 "
+                                 "h=12 V=30522)"}
             else:
                 r = port_bench()
                 cpu = {"value": r["samples_per_s"], "unit": "samples/s", "cores": 1,
@@ -431,8 +525,18 @@ def main(argv=None):
                                  "Adam state, activations) exceeds the 126 MB L2",
                            "bucket_mb": args.bucket_mb},
                 "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
-                "roofline": roofline, "hbm_kernels": hbm_kernels, "allreduce": allreduce, "cpu_baseline": cpu, "breakdown_ms_per_step": breakdown,
-                "final_loss": rep.loss}
+                "roofline": roofline, "hbm_kernels": hbm_kernels, "allreduce": allreduce,
+                "cpu_baseline": cpu, "breakdown_ms_per_step": breakdown,
+                "breakdown_note": "per-class CUDA events of a timer pass with the side streams "
+                                  "serialised (sums above the overlapped step)",
+                "loss_check": loss_check, "final_loss": rep.loss}
+        if same is not None:
+            ref_v = cpu["value"] if cpu and cpu.get("value") else None
+            for k in ("f32", "bf16"):
+                if k in same and ref_v:
+                    same[k]["ratio_vs_reference_cpu"] = same[k]["value"] / ref_v
+            same["reference_cpu"] = {"value": ref_v, "cores": cpu.get("cores") if cpu else None}
+            line["same_config"] = same
         emit(line)
     eng.close()
     if comm:

@@ -339,6 +339,14 @@ hp_status hp_engine_timers(hp_engine* e, int enable);
 hp_status hp_engine_timer_read(hp_engine* e, int which, char* name, uint64_t cap,
                                double* ms, uint64_t* launches, double* bytes,
                                double* flops);
+/* Measurement: the kernels of one class (0 GEMM, 1 attention; the
+ * hp_engine_timer_read classes) of one round, recorded during one eager round
+ * (a real update on the staged batch, lr 0) and replayed back to back on one
+ * stream from a CUDA graph `iters` times: *ms = the class's serialised time
+ * per round (what a per-kernel profile sums), *flops its algorithmic FLOPs,
+ * *launches its kernels per round.  Overwrites the class's outputs. */
+hp_status hp_engine_class_replay(hp_engine* e, int which, int iters, double* ms, double* flops,
+                                 uint64_t* launches);
 hp_status hp_engine_step_count(hp_engine* e, uint64_t* step);
 /* StepEngine::pending_rounds (engine.hpp:165): rounds accumulated since the
  * last update (0 .. update_freq - 1). */

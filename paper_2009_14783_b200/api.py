@@ -932,6 +932,16 @@ class StepEngine:
         return {"name": name.value.decode(), "ms": ms.value, "launches": n.value,
                 "bytes": by.value, "flops": fl.value}
 
+    def class_replay(self, which: int, iters: int = 10) -> dict:
+        """Measurement: one round's kernels of class `which` (0 GEMM, 1
+        attention) replayed back to back from a CUDA graph -- the class's
+        serialised time per round, its FLOPs and launches (runs one eager
+        round first; overwrites the class's outputs)."""
+        ms, fl = C.c_double(), C.c_double()
+        n = C.c_uint64()
+        call("hp_engine_class_replay", self._h, which, iters, C.byref(ms), C.byref(fl), C.byref(n))
+        return {"ms": ms.value, "flops": fl.value, "launches": n.value}
+
     @staticmethod
     def kernel_launches() -> int:
         n = C.c_uint64()

@@ -364,6 +364,17 @@ hp_status hp_engine_timer_read(hp_engine* e, int which, char* name, uint64_t cap
   }
   HP_API_END
 }
+hp_status hp_engine_class_replay(hp_engine* e, int which, int iters, double* ms, double* flops,
+                                 uint64_t* launches) {
+  HP_API_BEGIN
+  ENG(e);
+  need(ms, "ms");
+  need(flops, "flops");
+  need(launches, "launches");
+  if (which < 0 || which >= hp::TM_COUNT) fail(HP_EINDEX, "timer class out of range");
+  E.class_replay(which, iters, ms, flops, launches);
+  HP_API_END
+}
 hp_status hp_engine_step_count(hp_engine* e, uint64_t* step) {
   HP_API_BEGIN
   ENG(e);

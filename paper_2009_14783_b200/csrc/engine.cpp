@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 
 #include "checkpoint.h"
 #include "hp_common.h"
@@ -774,7 +775,72 @@ void Engine::timer_read(int which, std::string* name, double* ms, uint64_t* laun
   *flops = t.flops;
 }
 
+void Engine::record(int cls, double flops, std::function<void(cudaStream_t)> fn) {
+  if (rec_on_) rec_.push_back(RecOp{cls, flops, std::move(fn)});
+}
+
+// One round's kernels of a class replayed back to back on one stream, from a
+// CUDA graph (no launch gaps): the class's serialised duration -- what a
+// per-kernel profile (ncu's launch list) sums -- and its algorithmic FLOPs.
+// Runs one eager round first to record the class's launches (the round is a
+// real update), then overwrites that class's outputs; measurement only.
+void Engine::class_replay(int cls, int iters, double* ms, double* flops, uint64_t* launches) {
+  if (in_flight_) fail(HP_ECONFIG, "class_replay while a round is in flight");
+  if (!staged_) fail(HP_ECONFIG, "class_replay: no batch staged");
+  rec_.clear();
+  rec_on_ = true;
+  const bool g = graphs_on_;
+  graphs_on_ = false;
+  try {
+    round_async(0, 0.0);
+    round_sync(nullptr);
+  } catch (...) {
+    rec_on_ = false;
+    graphs_on_ = g;
+    throw;
+  }
+  rec_on_ = false;
+  graphs_on_ = g;
+  double fl = 0;
+  uint64_t n = 0;
+  const uint64_t k0 = kernel_launch_count();
+  HP_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeThreadLocal));
+  for (const RecOp& r : rec_)
+    if (r.cls == cls) {
+      r.fn(s_main_);
+      fl += r.flops;
+      ++n;
+    }
+  cudaGraph_t graph = nullptr;
+  HP_CUDA(cudaStreamEndCapture(s_main_, &graph));
+  const uint64_t kernels = kernel_launch_count() - k0;
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) fail(HP_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+  cudaEvent_t a, b;
+  HP_CUDA(cudaEventCreate(&a));
+  HP_CUDA(cudaEventCreate(&b));
+  HP_CUDA(cudaGraphLaunch(exec, s_main_));  // warm-up
+  HP_CUDA(cudaEventRecord(a, s_main_));
+  for (int i = 0; i < iters; ++i) HP_CUDA(cudaGraphLaunch(exec, s_main_));
+  HP_CUDA(cudaEventRecord(b, s_main_));
+  HP_CUDA(cudaEventSynchronize(b));
+  float t = 0;
+  HP_CUDA(cudaEventElapsedTime(&t, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaGraphExecDestroy(exec);
+  count_launch(static_cast<int>(kernels) * (iters + 1));
+  rec_.clear();
+  *ms = t / std::max(iters, 1);
+  *flops = fl;
+  *launches = kernels;
+  (void)n;
+}
+
 void Engine::gemm_t(const GemmArgs& g) {
+  record(TM_GEMM, 2.0 * g.M * g.N * g.K, [g](cudaStream_t st) { gemm(g, st); });
   tstart(TM_GEMM);
   gemm(g, s_main_);
   tstop(TM_GEMM, 2.0 * g.M * g.N * g.K,
@@ -797,6 +863,7 @@ void Engine::wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done) {
   // chain (C2: 7640 vs 7536 samples/s; cap 1: 7250)
   GemmArgs c = g;
   c.max_splits = 2;
+  record(TM_GEMM, 2.0 * g.M * g.N * g.K, [c](cudaStream_t st) { gemm(c, st); });
   gemm(c, s_wg_);
   tstop(TM_GEMM, 2.0 * g.M * g.N * g.K,
         (double)asz_ * ((double)g.M * g.K + (double)g.K * g.N) +
@@ -852,16 +919,25 @@ void Engine::forward(bool need_grad) {
                                                            : table_[iq + 1].offset - table_[iq].offset)};
     q.c = y.qkv; q.ldc = 3 * d_; q.ct = at_;
     gemm_t(q);
-    tstart(TM_ATTN);
-    if (attn_long_)
-      attention_fwd_long(b, H_, (int)m_.max_seq, y.qkv, y.o, y.lse, s_main_);
-    else if (attn_tc_)
-      attention_fwd_tc(b, H_, y.qkv, y.o, y.lse, s_main_);
-    else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
-      attention_fwd_mma(b, H_, y.qkv, y.o, y.lse, s_main_);
-    else
-      attention_fwd(b, H_, dk_, y.qkv, y.o, y.lse, at_, s_main_);
-    tstop(TM_ATTN, 4.0 * H_ * dk_ * (double)T * (double)m_.max_seq, 0);
+    {
+      const DevBatch bb = b;
+      const Layer yy = y;
+      auto op = [this, bb, yy](cudaStream_t st) {
+        if (attn_long_)
+          attention_fwd_long(bb, H_, (int)m_.max_seq, yy.qkv, yy.o, yy.lse, st);
+        else if (attn_tc_)
+          attention_fwd_tc(bb, H_, yy.qkv, yy.o, yy.lse, st);
+        else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
+          attention_fwd_mma(bb, H_, yy.qkv, yy.o, yy.lse, st);
+        else
+          attention_fwd(bb, H_, dk_, yy.qkv, yy.o, yy.lse, at_, st);
+      };
+      const double fl = 4.0 * H_ * dk_ * (double)T * (double)m_.max_seq;
+      tstart(TM_ATTN);
+      op(s_main_);
+      tstop(TM_ATTN, fl, 0);
+      record(TM_ATTN, fl, op);
+    }
     void* out = (l + 1 < L_) ? layers_[l + 1].x : x_final_;
     if (!bert_) {
       GemmArgs o;
@@ -1140,16 +1216,26 @@ void Engine::backward() {
     gemm_t(dO);
     void* const dqkv = bert_ ? qbuf_[slot(l)] : dqkv_;
     if (bert_ && l + rd_ < L_) wait_wg(ev_wq_[l + rd_]);  // the slot: layer l+2's d(wqkv) read it
-    tstart(TM_ATTN);
-    if (attn_long_)
-      attention_bwd_long(b, H_, (int)m_.max_seq, y.qkv, y.o, dC_, y.lse, dqkv, s_main_);
-    else if (attn_tc_)
-      attention_bwd_tc(b, H_, y.qkv, y.o, dC_, y.lse, dqkv, s_main_);
-    else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
-      attention_bwd_mma(b, H_, y.qkv, y.o, dC_, y.lse, dqkv, s_main_);
-    else
-      attention_bwd(b, H_, dk_, y.qkv, y.o, dC_, y.lse, dqkv, at_, s_main_);
-    tstop(TM_ATTN, 8.0 * H_ * dk_ * (double)T * (double)m_.max_seq, 0);
+    {
+      const DevBatch bb = b;
+      const Layer yy = y;
+      void* const dO = dC_;
+      auto op = [this, bb, yy, dO, dqkv](cudaStream_t st) {
+        if (attn_long_)
+          attention_bwd_long(bb, H_, (int)m_.max_seq, yy.qkv, yy.o, dO, yy.lse, dqkv, st);
+        else if (attn_tc_)
+          attention_bwd_tc(bb, H_, yy.qkv, yy.o, dO, yy.lse, dqkv, st);
+        else if (bf16_ && attention_mma_supported(dk_, (int)m_.max_seq))
+          attention_bwd_mma(bb, H_, yy.qkv, yy.o, dO, yy.lse, dqkv, st);
+        else
+          attention_bwd(bb, H_, dk_, yy.qkv, yy.o, dO, yy.lse, dqkv, at_, st);
+      };
+      const double fl = 8.0 * H_ * dk_ * (double)T * (double)m_.max_seq;
+      tstart(TM_ATTN);
+      op(s_main_);
+      tstop(TM_ATTN, fl, 0);
+      record(TM_ATTN, fl, op);
+    }
     const int64_t gstride_w = bf16_ ? (int64_t)(shadow_off_[iq + 1] - shadow_off_[iq])
                                     : (int64_t)(table_[iq + 1].offset - table_[iq].offset);
     GemmArgs wq;  // d(wq.*, wk.*, wv.*) = X^T dQKV, scattered into the 3h blocks

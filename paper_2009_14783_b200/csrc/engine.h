@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <array>
+#include <functional>
 #include <map>
 #include <string>
 #include <tuple>
@@ -65,6 +66,7 @@ class Engine {
   uint64_t readback_bytes() const { return 6 * 8 + kErrWords * 8; }
   void timer_read(int which, std::string* name, double* ms, uint64_t* launches, double* bytes,
                   double* flops);
+  void class_replay(int cls, int iters, double* ms, double* flops, uint64_t* launches);
 
  private:
   struct Buf {
@@ -78,6 +80,15 @@ class Engine {
   float* pp(int idx) const { return params_ + table_[idx].offset; }
   int pidx(const std::string& name) const;
   void gemm_t(const GemmArgs& g);
+  // launches of a class recorded during one eager round (class_replay)
+  struct RecOp {
+    int cls;
+    double flops;
+    std::function<void(cudaStream_t)> fn;
+  };
+  std::vector<RecOp> rec_;
+  bool rec_on_ = false;
+  void record(int cls, double flops, std::function<void(cudaStream_t)> fn);
   // a weight-gradient GEMM on the wgrad stream (see backward): forks from the
   // compute stream, records `done` when finished
   void wgrad_t(const GemmArgs& g, cudaEvent_t fork, cudaEvent_t done);
