@@ -88,12 +88,31 @@ hp_status hp_mlm_generate(const hp_mlm_gen_desc* d, uint64_t* tok_off,
                           uint64_t* mask_off, int64_t* mask_pos,
                           int64_t* mask_orig, int64_t* label);
 
+/* Synthetic translation pairs for the seq2seq extension (repo generator, no
+ * reference counterpart): pair k draws, from SeededRng(seed) in this order,
+ * its source length and target length (min_len + bounded(max_len - min_len
+ * + 1) each), then the source and the target word ids (4 + bounded(vocab - 4)
+ * each).  Record k = tokens [source..., target...] with segments 0 / 1; no
+ * masks, label 0 -- the hp_batch encoding of a pair (see hp_engine_round). */
+typedef struct {
+  uint64_t n;
+  int64_t vocab;
+  uint64_t min_len, max_len;
+  uint64_t seed;
+} hp_pair_gen_desc;
+hp_status hp_pairs_generate_size(const hp_pair_gen_desc* d, uint64_t* tokens_total);
+hp_status hp_pairs_generate(const hp_pair_gen_desc* d, uint64_t* tok_off, int64_t* tokens,
+                            int64_t* segments);
+
 /* ------------------------------------------------------------------------
  * Model description and canonical parameter table.
  * ---------------------------------------------------------------------- */
 enum {
   HP_ARCH_MASKED_TOKEN_MODEL = 3, /* Arch::masked_token_model, model.hpp:16 */
-  HP_ARCH_BERT_ENCODER = 16       /* repo extension: L post-LN BERT blocks   */
+  HP_ARCH_BERT_ENCODER = 16,      /* repo extension: L post-LN BERT blocks   */
+  HP_ARCH_SEQ2SEQ = 17            /* repo extension: L + L encoder-decoder
+                                     Transformer, shared
+                                     embedding / output projection */
 };
 
 /* ModelSpec (include/hetpar/model.hpp:28-67) + the extension's fields. */
@@ -103,9 +122,9 @@ typedef struct {
   uint64_t heads;
   uint64_t vocab;
   uint64_t max_seq;
-  uint64_t layers; /* bert_encoder only */
-  uint64_t d_ff;   /* bert_encoder only */
-  int with_nsp;
+  uint64_t layers; /* bert_encoder; seq2seq: encoder layers = decoder layers */
+  uint64_t d_ff;   /* bert_encoder, seq2seq */
+  int with_nsp;    /* ignored by seq2seq (no NSP head) */
   double label_smooth_eps;
 } hp_model_desc;
 

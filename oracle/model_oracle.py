@@ -7,11 +7,15 @@ here is checked against the reference compiled from /root/reference
 (oracle/_ref, fixtures in tests/golden/, made by tools/make_golden.py): the
 per-rank pre-reduce gradients and the 10-step C1 trajectory.
 
-The ``bert_encoder`` extension (LayerNorm, GELU FFN, residual, L layers) has
-NO reference counterpart: it follows the Tape conventions (tape.hpp:21-324)
-and the parameter naming/order convention (model.hpp:91-142) and is pinned
-only by finite differences (tests/test_model_oracle.py) -- "parity unpinned"
-against the reference itself, as DESIGN.md states.
+The ``bert_encoder`` extension (LayerNorm, GELU FFN, residual, L layers) and
+the ``transformer_seq2seq`` extension (the encoder-decoder Transformer of the
+paper's translation workload: post-LN encoder and decoder
+blocks, causal decoder self-attention, encoder-decoder cross-attention, one
+embedding table shared by both inputs and the output projection) have NO
+reference counterpart: they follow the Tape conventions (tape.hpp:21-324) and
+the parameter naming/order convention (model.hpp:91-142) and are pinned only
+by finite differences (tests/test_oracle.py) -- "parity unpinned" against the
+reference itself, as DESIGN.md states.
 """
 from __future__ import annotations
 
@@ -28,12 +32,12 @@ LN_EPS = 1e-12  # extension only; BERT's LayerNorm epsilon
 # spec / parameter table (model.hpp:28-142)
 @dataclass
 class Spec:
-    arch: str = "masked_token_model"  # or "bert_encoder" (repo extension)
+    arch: str = "masked_token_model"  # or "bert_encoder" / "transformer_seq2seq" (extensions)
     d_model: int = 128
     heads: int = 4
     vocab: int = 1000
     max_seq: int = 512
-    layers: int = 1  # bert_encoder only
+    layers: int = 1  # bert_encoder; transformer_seq2seq: encoder = decoder layers
     d_ff: int = 512  # bert_encoder only
     with_nsp: bool = True
     label_smooth_eps: float = 0.1
@@ -81,6 +85,40 @@ def param_shapes(s: Spec):
             b(p + "ffn.b2", d)
             out.append((p + "ln2.g", 1, d, False, False))
             b(p + "ln2.b", d)
+    elif s.arch == "transformer_seq2seq":
+        tbl("embed", s.vocab, d)  # shared: encoder / decoder inputs, output projection
+        for l in range(s.layers):
+            p = f"enc{l}."
+            attn(p)
+            b(p + "bo", d)
+            out.append((p + "ln1.g", 1, d, False, False))
+            b(p + "ln1.b", d)
+            w(p + "ffn.w1", d, s.d_ff)
+            b(p + "ffn.b1", s.d_ff)
+            w(p + "ffn.w2", s.d_ff, d)
+            b(p + "ffn.b2", d)
+            out.append((p + "ln2.g", 1, d, False, False))
+            b(p + "ln2.b", d)
+        for l in range(s.layers):
+            p = f"dec{l}."
+            attn(p)
+            b(p + "bo", d)
+            out.append((p + "ln1.g", 1, d, False, False))
+            b(p + "ln1.b", d)
+            for kind in ("cq", "ck", "cv"):
+                for i in range(s.heads):
+                    w(f"{p}{kind}.{i}", d, dk)
+            w(p + "co", d, d)
+            b(p + "cbo", d)
+            out.append((p + "ln2.g", 1, d, False, False))
+            b(p + "ln2.b", d)
+            w(p + "ffn.w1", d, s.d_ff)
+            b(p + "ffn.b1", s.d_ff)
+            w(p + "ffn.w2", s.d_ff, d)
+            b(p + "ffn.b2", d)
+            out.append((p + "ln3.g", 1, d, False, False))
+            b(p + "ln3.b", d)
+        return out
     else:
         raise ValueError(s.arch)
     w("mlm.w", d, s.vocab)
@@ -244,11 +282,179 @@ def _mha_bwd(dout, x, P, G, prefix, s, mcache):
     return dx
 
 
+BOS = 2  # decoder start token (fairseq's prev_output_tokens start with EOS = 2)
+
+
+def _attn(q, k, v, causal, scale):
+    z = (q @ k.T) * scale
+    if causal:
+        z = np.where(np.tril(np.ones(z.shape, bool)), z, -np.inf)
+    p = softmax_rows(z)
+    return p @ v, p
+
+
+def _attn_bwd(dout, q, k, v, p, scale):
+    dp = dout @ v.T
+    dv = p.T @ dout
+    ds = p * (dp - (dp * p).sum(axis=1, keepdims=True)) * scale
+    return ds @ k, ds.T @ q, dv
+
+
+def _heads(P, prefix, kinds, h):
+    return [np.concatenate([P[f"{prefix}{kd}.{i}"] for i in range(h)], axis=1) for kd in kinds]
+
+
+def _mha2_fwd(xq, xkv, P, prefix, kinds, out_w, s, causal):
+    """multi-head attention with the per-head [d x dk] blocks of `kinds`
+    (q, k, v), queries from xq, keys / values from xkv"""
+    h, dk = s.heads, s.dk
+    scale = 1.0 / math.sqrt(dk)
+    wq, wk, wv = _heads(P, prefix, kinds, h)
+    Q, K, Vv = xq @ wq, xkv @ wk, xkv @ wv
+    outs, ps = [], []
+    for i in range(h):
+        sl = slice(i * dk, (i + 1) * dk)
+        o, pr = _attn(Q[:, sl], K[:, sl], Vv[:, sl], causal, scale)
+        outs.append(o)
+        ps.append(pr)
+    cat = np.concatenate(outs, axis=1)
+    return cat @ P[prefix + out_w], (Q, K, Vv, ps, cat)
+
+
+def _mha2_bwd(dout, xq, xkv, P, G, prefix, kinds, out_w, s, cache):
+    h, dk = s.heads, s.dk
+    scale = 1.0 / math.sqrt(dk)
+    Q, K, Vv, ps, cat = cache
+    G[prefix + out_w] += cat.T @ dout
+    dcat = dout @ P[prefix + out_w].T
+    dQ, dK, dV = np.zeros_like(Q), np.zeros_like(K), np.zeros_like(Vv)
+    for i in range(h):
+        sl = slice(i * dk, (i + 1) * dk)
+        dq, dkk, dv = _attn_bwd(dcat[:, sl], Q[:, sl], K[:, sl], Vv[:, sl], ps[i], scale)
+        dQ[:, sl], dK[:, sl], dV[:, sl] = dq, dkk, dv
+    wq, wk, wv = _heads(P, prefix, kinds, h)
+    for kd, dd, xx in ((kinds[0], dQ, xq), (kinds[1], dK, xkv), (kinds[2], dV, xkv)):
+        gw = xx.T @ dd
+        for i in range(h):
+            G[f"{prefix}{kd}.{i}"] += gw[:, i * dk:(i + 1) * dk]
+    return dQ @ wq.T, dK @ wk.T + dV @ wv.T
+
+
+def _ffn_block_fwd(x, P, p, lnname):
+    u = x @ P[p + "ffn.w1"] + P[p + "ffn.b1"]
+    gu = gelu(u)
+    f = gu @ P[p + "ffn.w2"] + P[p + "ffn.b2"]
+    y, ln = layer_norm(x + f, P[p + lnname + ".g"], P[p + lnname + ".b"])
+    return y, (x, u, gu, ln)
+
+
+def _ffn_block_bwd(dy, P, G, p, lnname, cache):
+    x, u, gu, ln = cache
+    dy2, dg, db = layer_norm_bwd(dy, P[p + lnname + ".g"], ln)
+    G[p + lnname + ".g"] += dg
+    G[p + lnname + ".b"] += db
+    G[p + "ffn.b2"] += dy2.sum(axis=0)
+    G[p + "ffn.w2"] += gu.T @ dy2
+    du = (dy2 @ P[p + "ffn.w2"].T) * gelu_grad(u)
+    G[p + "ffn.b1"] += du.sum(axis=0)
+    G[p + "ffn.w1"] += x.T @ du
+    return dy2 + du @ P[p + "ffn.w1"].T
+
+
+def seq2seq_split(inst):
+    """Instance -> (source ids, decoder input ids, target ids): tokens holds
+    the source (segment 0) then the target (segment 1); the decoder reads
+    [BOS] + target[:-1] and predicts target."""
+    tok = np.asarray(inst.tokens, dtype=np.int64)
+    seg = np.asarray(inst.segments, dtype=np.int64)
+    src, tgt = tok[seg == 0], tok[seg == 1]
+    return src, np.concatenate([[BOS], tgt[:-1]]).astype(np.int64), tgt
+
+
+def _seq2seq_forward_backward(s, P, G, batch, policy, need_grad):
+    eps = s.label_smooth_eps
+    d = s.d_model
+    es = math.sqrt(d)  # embedding scale (fairseq embed_scale)
+    loss_total, weight = 0.0, 0.0
+    for inst in batch:
+        src, din, tgt = seq2seq_split(inst)
+        ns, nt = src.size, tgt.size
+        if ns == 0 or nt == 0 or ns > s.max_seq or nt > s.max_seq:
+            raise ValueError("sequence length")
+        x = es * P["embed"][src] + sinusoidal_positions(ns, d)
+        enc_c = []
+        for l in range(s.layers):
+            p = f"enc{l}."
+            a, mc = _mha2_fwd(x, x, P, p, ("wq", "wk", "wv"), "wo", s, False)
+            x1, ln1 = layer_norm(x + a + P[p + "bo"], P[p + "ln1.g"], P[p + "ln1.b"])
+            x2, fc = _ffn_block_fwd(x1, P, p, "ln2")
+            enc_c.append((x, mc, ln1, fc))
+            x = x2
+        mem = x
+        y = es * P["embed"][din] + sinusoidal_positions(nt, d)
+        dec_c = []
+        for l in range(s.layers):
+            p = f"dec{l}."
+            a, mc = _mha2_fwd(y, y, P, p, ("wq", "wk", "wv"), "wo", s, True)
+            y1, ln1 = layer_norm(y + a + P[p + "bo"], P[p + "ln1.g"], P[p + "ln1.b"])
+            c, cc = _mha2_fwd(y1, mem, P, p, ("cq", "ck", "cv"), "co", s, False)
+            y2, ln2 = layer_norm(y1 + c + P[p + "cbo"], P[p + "ln2.g"], P[p + "ln2.b"])
+            y3, fc = _ffn_block_fwd(y2, P, p, "ln3")
+            dec_c.append((y, mc, ln1, y1, cc, ln2, fc))
+            y = y3
+        z = y @ P["embed"].T  # tied output projection, no bias
+        l_, dz = ls_ce(z, tgt, eps)
+        loss_total += l_
+        weight += 1.0 if policy == "sentences" else float(nt)
+        if not need_grad:
+            continue
+        G["embed"] += dz.T @ y
+        dy = dz @ P["embed"]
+        dmem = np.zeros_like(mem)
+        for l in reversed(range(s.layers)):
+            p = f"dec{l}."
+            yin, mc, ln1, y1, cc, ln2, fc = dec_c[l]
+            dy2 = _ffn_block_bwd(dy, P, G, p, "ln3", fc)
+            dc, dg2, db2 = layer_norm_bwd(dy2, P[p + "ln2.g"], ln2)
+            G[p + "ln2.g"] += dg2
+            G[p + "ln2.b"] += db2
+            G[p + "cbo"] += dc.sum(axis=0)
+            dq_in, dkv_in = _mha2_bwd(dc, y1, mem, P, G, p, ("cq", "ck", "cv"), "co", s, cc)
+            dmem += dkv_in
+            dy1 = dc + dq_in
+            da, dg1, db1 = layer_norm_bwd(dy1, P[p + "ln1.g"], ln1)
+            G[p + "ln1.g"] += dg1
+            G[p + "ln1.b"] += db1
+            G[p + "bo"] += da.sum(axis=0)
+            dq_s, dkv_s = _mha2_bwd(da, yin, yin, P, G, p, ("wq", "wk", "wv"), "wo", s, mc)
+            dy = da + dq_s + dkv_s
+        np.add.at(G["embed"], din, es * dy)
+        dx = dmem
+        for l in reversed(range(s.layers)):
+            p = f"enc{l}."
+            xin, mc, ln1, fc = enc_c[l]
+            dx1 = _ffn_block_bwd(dx, P, G, p, "ln2", fc)
+            da, dg1, db1 = layer_norm_bwd(dx1, P[p + "ln1.g"], ln1)
+            G[p + "ln1.g"] += dg1
+            G[p + "ln1.b"] += db1
+            G[p + "bo"] += da.sum(axis=0)
+            dq_s, dkv_s = _mha2_bwd(da, xin, xin, P, G, p, ("wq", "wk", "wv"), "wo", s, mc)
+            dx = da + dq_s + dkv_s
+        np.add.at(G["embed"], src, es * dx)
+    return loss_total, weight
+
+
 def forward_backward(s: Spec, flat: np.ndarray, batch, policy="sentences",
                      need_grad=True):
     """model_forward (model.hpp:260-403) + backward_gradients (405-417) for
     one batch: returns (loss_sum, weight, flat f64 gradient)."""
     offs = offsets(s)
+    if s.arch == "transformer_seq2seq":
+        P = {n: flat[o:o + r * c].reshape(r, c) for n, (o, r, c) in offs.items()}
+        grad = np.zeros_like(flat)
+        G = {n: grad[o:o + r * c].reshape(r, c) for n, (o, r, c) in offs.items()}
+        l, w = _seq2seq_forward_backward(s, P, G, batch, policy, need_grad)
+        return l, w, grad
     P = {n: flat[o:o + r * c].reshape(r, c) for n, (o, r, c) in offs.items()}
     grad = np.zeros_like(flat)
     G = {n: grad[o:o + r * c].reshape(r, c) for n, (o, r, c) in offs.items()}
@@ -389,3 +595,34 @@ def protocol_round(s, params, per_rank, policy="sentences"):
         tot_w += ws[r]
         tot_g += gs[r]
     return tot_l, tot_w, tot_g
+
+
+def pairs_generate(n, vocab, min_len, max_len, seed):
+    """The seq2seq extension's synthetic pair stream (hp_pairs_generate,
+    include/hetpar_b200.h): per pair the source and target lengths, then the
+    source and target word ids, all from one SeededRng(seed) stream
+    (bounded(n) = hi64(u * n), rng.hpp:15-55).  Returns CSR (tok_off, tokens,
+    segments)."""
+    state = seed & (2**64 - 1)
+    M = 2**64
+
+    def nxt():
+        nonlocal state
+        state = (state + 0x9E3779B97F4A7C15) % M
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) % M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) % M
+        return z ^ (z >> 31)
+
+    def bounded(k):
+        return (nxt() * k) >> 64
+
+    tok_off, tokens, segments = [0], [], []
+    for _ in range(n):
+        ls = min_len + bounded(max_len - min_len + 1)
+        lt = min_len + bounded(max_len - min_len + 1)
+        for i in range(ls + lt):
+            tokens.append(4 + bounded(vocab - 4))
+            segments.append(0 if i < ls else 1)
+        tok_off.append(len(tokens))
+    return (np.array(tok_off, np.uint64), np.array(tokens, np.int64), np.array(segments, np.int64))

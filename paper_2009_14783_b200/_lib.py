@@ -17,6 +17,7 @@ if os.environ.get("HP_LIB_VARIANT"):  # A/B builds (tools/build_native.py HP_VAR
 HP_OK, HP_ESHAPE, HP_ECONFIG, HP_EINDEX, HP_EIO, HP_ECOMM, HP_ENUMERIC, HP_ECUDA = range(8)
 HP_ARCH_MASKED_TOKEN_MODEL = 3
 HP_ARCH_BERT_ENCODER = 16
+HP_ARCH_SEQ2SEQ = 17
 HP_OPT_SGD, HP_OPT_ADAM = 0, 1
 HP_POLICY_SENTENCES, HP_POLICY_TOKENS = 1, 2
 HP_COMPUTE_F32, HP_COMPUTE_BF16 = 0, 1
@@ -65,6 +66,11 @@ class MlmGenDesc(C.Structure):
                 ("sentences_per_doc", C.c_uint64), ("min_words", C.c_uint64),
                 ("max_words", C.c_uint64), ("p_select", C.c_double), ("p_mask", C.c_double),
                 ("p_random", C.c_double), ("seed", C.c_uint64), ("max_seq_tokens", C.c_uint64)]
+
+
+class PairGenDesc(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("vocab", C.c_int64), ("min_len", C.c_uint64),
+                ("max_len", C.c_uint64), ("seed", C.c_uint64)]
 
 
 class ModelDesc(C.Structure):
@@ -123,6 +129,8 @@ _SIGS = {
     "hp_partition_for_rank": [U64, U64, U64, P, P, P],
     "hp_mlm_generate_size": [P, P, P],
     "hp_mlm_generate": [P, P, P, P, P, P, P, P],
+    "hp_pairs_generate_size": [P, P],
+    "hp_pairs_generate": [P, P, P, P],
     "hp_param_count": [P, P, P],
     "hp_param_info": [P, U64, C.c_char_p, U64, P, P, P, P],
     "hp_init_parameters": [P, U64, P],

@@ -28,6 +28,7 @@ __all__ = [
     "ModelSpec", "ParamShape", "param_shapes", "flat_size", "init_parameters", "bucket_plan",
     "Instance", "BatchCSR", "pack_batch", "BatchPlan", "RankBatch", "build_epoch_batches",
     "partition_for_rank", "MlmGenConfig", "Records", "generate_mlm_records", "splitmix64",
+    "PairGenConfig", "generate_pair_records",
     "shuffle_iota", "OptimConfig", "ExecConfig", "StepReport", "Communicator", "StepEngine",
     "SchedulerConfig", "scheduled_lr", "inverse_sqrt_lr", "linear_warmup_decay_lr",
     "BaseError", "ShapeError", "ConfigError", "IndexError_", "IoError", "CommError",
@@ -56,15 +57,20 @@ def shuffle_iota(seed: int, n: int) -> np.ndarray:
 
 # --------------------------------------------------------------------- model
 _ARCH = {"masked_token_model": _lib.HP_ARCH_MASKED_TOKEN_MODEL,
-         "bert_encoder": _lib.HP_ARCH_BERT_ENCODER}
+         "bert_encoder": _lib.HP_ARCH_BERT_ENCODER,
+         "transformer_seq2seq": _lib.HP_ARCH_SEQ2SEQ}
 _POLICY = {"sentences": _lib.HP_POLICY_SENTENCES, "tokens": _lib.HP_POLICY_TOKENS}
 
 
 @dataclass
 class ModelSpec:
-    """ModelSpec (model.hpp:28-67).  ``bert_encoder`` is the repo extension
-    (L post-LN blocks with a GELU FFN); ``masked_token_model`` is exactly the
-    reference architecture (one attention block)."""
+    """ModelSpec (model.hpp:28-67).  ``masked_token_model`` is exactly the
+    reference architecture (one attention block); the repo extensions are
+    ``bert_encoder`` (L post-LN blocks with a GELU FFN) and
+    ``transformer_seq2seq`` (L encoder + L decoder blocks of the paper's
+    translation Transformer, one embedding shared by the inputs and the output
+    projection; a pair is an Instance whose tokens are the source (segment 0)
+    then the target (segment 1), see generate_pair_records)."""
     arch: str = "masked_token_model"
     d_model: int = 128
     heads: int = 4
@@ -294,6 +300,33 @@ class Records:
         return BatchCSR(tl, self.tokens[tidx].copy(), self.segments[tidx].copy(), ml,
                         self.mask_pos[midx].copy(), self.mask_orig[midx].copy(),
                         self.label[ids].copy())
+
+
+@dataclass
+class PairGenConfig:
+    """Synthetic translation pairs (repo generator for transformer_seq2seq,
+    include/hetpar_b200.h hp_pairs_generate)."""
+    n: int = 64
+    vocab: int = 32768
+    min_len: int = 64
+    max_len: int = 64
+    seed: int = 7
+
+    def desc(self) -> _lib.PairGenDesc:
+        return _lib.PairGenDesc(self.n, self.vocab, self.min_len, self.max_len, self.seed)
+
+
+def generate_pair_records(cfg: PairGenConfig) -> Records:
+    """Translation pairs as Records: tokens = source ++ target per record,
+    segments 0 / 1, no masks."""
+    d = cfg.desc()
+    nt = C.c_uint64()
+    call("hp_pairs_generate_size", C.byref(d), C.byref(nt))
+    r = Records(np.empty(cfg.n + 1, np.uint64), np.empty(nt.value, np.int64),
+                np.empty(nt.value, np.int64), np.zeros(cfg.n + 1, np.uint64),
+                np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(cfg.n, np.int64))
+    call("hp_pairs_generate", C.byref(d), _p(r.tok_off), _p(r.tokens), _p(r.segments))
+    return r
 
 
 def generate_mlm_records(cfg: MlmGenConfig) -> Records:
@@ -577,7 +610,7 @@ def read_checkpoint(path: str):
     md, cd = _lib.ModelDesc(), _lib.CkptDesc()
     call("hp_checkpoint_read", path.encode(), C.byref(md), C.byref(cd), None, None, None, 0)
     spec = ModelSpec(_ARCH_NAME[md.arch], md.d_model, md.heads, md.vocab, md.max_seq,
-                     md.layers if md.arch == _ARCH["bert_encoder"] else 1, md.d_ff,
+                     md.layers if md.arch != _ARCH["masked_token_model"] else 1, md.d_ff,
                      bool(md.with_nsp), md.label_smooth_eps)
     n = flat_size(spec)
     p, m, v = (np.empty(n, np.float32) for _ in range(3))

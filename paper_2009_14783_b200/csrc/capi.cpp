@@ -123,6 +123,25 @@ hp_status hp_mlm_generate(const hp_mlm_gen_desc* d, uint64_t* tok_off, int64_t* 
   HP_API_END
 }
 
+hp_status hp_pairs_generate_size(const hp_pair_gen_desc* d, uint64_t* tokens_total) {
+  HP_API_BEGIN
+  need(d, "desc");
+  need(tokens_total, "tokens_total");
+  *tokens_total = hp::pairs_generate(*d).tokens.size();
+  HP_API_END
+}
+
+hp_status hp_pairs_generate(const hp_pair_gen_desc* d, uint64_t* tok_off, int64_t* tokens,
+                            int64_t* segments) {
+  HP_API_BEGIN
+  need(d, "desc");
+  auto r = hp::pairs_generate(*d);
+  std::memcpy(tok_off, r.tok_off.data(), r.tok_off.size() * 8);
+  std::memcpy(tokens, r.tokens.data(), r.tokens.size() * 8);
+  std::memcpy(segments, r.segments.data(), r.segments.size() * 8);
+  HP_API_END
+}
+
 hp_status hp_param_count(const hp_model_desc* m, uint64_t* nparams, uint64_t* nelems) {
   HP_API_BEGIN
   need(m, "model");

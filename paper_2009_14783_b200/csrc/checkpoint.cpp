@@ -91,14 +91,16 @@ std::string json_number(double x) {
 }
 
 const char* arch_name(int arch) {
-  return arch == HP_ARCH_BERT_ENCODER ? "bert_encoder" : "masked_token_model";
+  return arch == HP_ARCH_BERT_ENCODER ? "bert_encoder"
+         : arch == HP_ARCH_SEQ2SEQ    ? "transformer_seq2seq"
+                                      : "masked_token_model";
 }
 const char* sched_name(int k) { return k == 1 ? "inverse_sqrt" : k == 2 ? "linear" : "fixed"; }
 
 // build_spec_json (checkpoint.cpp:54-79); the bert_encoder extension adds
 // d_ff and encoder_layers (keys stay sorted).
 std::string spec_json(const hp_model_desc& m, const hp_ckpt_desc& c) {
-  const bool bert = m.arch == HP_ARCH_BERT_ENCODER;
+  const bool bert = m.arch == HP_ARCH_BERT_ENCODER || m.arch == HP_ARCH_SEQ2SEQ;
   std::string j = "{";
   j += "\"arch\":\"" + std::string(arch_name(m.arch)) + "\"";
   j += ",\"classes\":2";
@@ -316,8 +318,8 @@ void hck1_parse(const std::vector<uint8_t>& bytes, hp_model_desc* m, hp_ckpt_des
   const std::string arch = fs(j, "arch");
   if (arch == "masked_token_model") {
     md.arch = HP_ARCH_MASKED_TOKEN_MODEL;
-  } else if (arch == "bert_encoder") {
-    md.arch = HP_ARCH_BERT_ENCODER;
+  } else if (arch == "bert_encoder" || arch == "transformer_seq2seq") {
+    md.arch = arch == "bert_encoder" ? HP_ARCH_BERT_ENCODER : HP_ARCH_SEQ2SEQ;
     md.layers = fu(j, "encoder_layers");
     md.d_ff = fu(j, "d_ff");
   } else {

@@ -153,10 +153,32 @@ MlmRecords mlm_generate(const hp_mlm_gen_desc& d) {
   return out;
 }
 
+MlmRecords pairs_generate(const hp_pair_gen_desc& d) {
+  constexpr int64_t kFirstWord = 4;
+  if (d.vocab < kFirstWord + 2) fail(HP_ECONFIG, "datagen: pair vocab needs >= 2 word ids");
+  if (d.min_len == 0 || d.min_len > d.max_len) fail(HP_ECONFIG, "datagen: bad pair length range");
+  SplitMix r(d.seed);
+  const uint64_t n_words = static_cast<uint64_t>(d.vocab - kFirstWord);
+  MlmRecords out;
+  for (uint64_t k = 0; k < d.n; ++k) {
+    const uint64_t ls = d.min_len + r.bounded(d.max_len - d.min_len + 1);
+    const uint64_t lt = d.min_len + r.bounded(d.max_len - d.min_len + 1);
+    for (uint64_t i = 0; i < ls + lt; ++i) {
+      out.tokens.push_back(kFirstWord + static_cast<int64_t>(r.bounded(n_words)));
+      out.segments.push_back(i < ls ? 0 : 1);
+    }
+    out.label.push_back(0);
+    out.tok_off.push_back(out.tokens.size());
+    out.mask_off.push_back(0);
+  }
+  return out;
+}
+
 void validate_model(const hp_model_desc& m) {
   if (!(m.label_smooth_eps >= 0.0 && m.label_smooth_eps < 1.0))
     fail(HP_ECONFIG, "label_smooth_eps outside [0,1)");
-  if (m.arch != HP_ARCH_MASKED_TOKEN_MODEL && m.arch != HP_ARCH_BERT_ENCODER)
+  if (m.arch != HP_ARCH_MASKED_TOKEN_MODEL && m.arch != HP_ARCH_BERT_ENCODER &&
+      m.arch != HP_ARCH_SEQ2SEQ)
     fail(HP_ECONFIG, "unsupported architecture id " + std::to_string(m.arch));
   if (m.d_model == 0 || m.vocab == 0 || m.max_seq == 0)
     fail(HP_ECONFIG, "masked model needs d_model/vocab/max_seq");
@@ -165,6 +187,8 @@ void validate_model(const hp_model_desc& m) {
   if (m.d_model % 2 != 0) fail(HP_ECONFIG, "d_model must be even");
   if (m.arch == HP_ARCH_BERT_ENCODER && (m.layers == 0 || m.d_ff == 0))
     fail(HP_ECONFIG, "bert_encoder needs layers >= 1 and d_ff >= 1");
+  if (m.arch == HP_ARCH_SEQ2SEQ && (m.layers == 0 || m.d_ff == 0))
+    fail(HP_ECONFIG, "transformer_seq2seq needs layers >= 1 and d_ff >= 1");
 }
 
 std::vector<ParamEntry> param_table(const hp_model_desc& m) {
@@ -182,6 +206,45 @@ std::vector<ParamEntry> param_table(const hp_model_desc& m) {
         add(p + k + std::to_string(i), d, dk, HP_PARAM_WEIGHT);
     add(p + "wo", d, d, HP_PARAM_WEIGHT);
   };
+  auto ffn = [&](const std::string& p, const char* ln) {
+    add(p + "ffn.w1", d, m.d_ff, HP_PARAM_WEIGHT);
+    add(p + "ffn.b1", 1, m.d_ff, HP_PARAM_BIAS);
+    add(p + "ffn.w2", m.d_ff, d, HP_PARAM_WEIGHT);
+    add(p + "ffn.b2", 1, d, HP_PARAM_BIAS);
+    add(p + ln + ".g", 1, d, HP_PARAM_GAIN);
+    add(p + ln + ".b", 1, d, HP_PARAM_BIAS);
+  };
+  if (m.arch == HP_ARCH_SEQ2SEQ) {
+    // one table for the encoder / decoder inputs and the output projection;
+    // encoder blocks as the bert_encoder layer, decoder blocks add the
+    // cross-attention projections cq / ck / cv / co (+ cbo, ln2) between the
+    // self-attention and the FFN (whose LayerNorm becomes ln3)
+    add("embed", m.vocab, d, HP_PARAM_TABLE);
+    for (uint64_t l = 0; l < m.layers; ++l) {
+      const std::string p = "enc" + std::to_string(l) + ".";
+      attention(p);
+      add(p + "bo", 1, d, HP_PARAM_BIAS);
+      add(p + "ln1.g", 1, d, HP_PARAM_GAIN);
+      add(p + "ln1.b", 1, d, HP_PARAM_BIAS);
+      ffn(p, "ln2");
+    }
+    for (uint64_t l = 0; l < m.layers; ++l) {
+      const std::string p = "dec" + std::to_string(l) + ".";
+      attention(p);
+      add(p + "bo", 1, d, HP_PARAM_BIAS);
+      add(p + "ln1.g", 1, d, HP_PARAM_GAIN);
+      add(p + "ln1.b", 1, d, HP_PARAM_BIAS);
+      for (const char* k : {"cq.", "ck.", "cv."})
+        for (uint64_t i = 0; i < m.heads; ++i)
+          add(p + k + std::to_string(i), d, dk, HP_PARAM_WEIGHT);
+      add(p + "co", d, d, HP_PARAM_WEIGHT);
+      add(p + "cbo", 1, d, HP_PARAM_BIAS);
+      add(p + "ln2.g", 1, d, HP_PARAM_GAIN);
+      add(p + "ln2.b", 1, d, HP_PARAM_BIAS);
+      ffn(p, "ln3");
+    }
+    return t;
+  }
   add("embed", m.vocab, d, HP_PARAM_TABLE);
   add("seg0", 1, d, HP_PARAM_TABLE);
   add("seg1", 1, d, HP_PARAM_TABLE);

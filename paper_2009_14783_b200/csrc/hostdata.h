@@ -48,6 +48,7 @@ struct MlmRecords {
   std::vector<int64_t> tokens, segments, mask_pos, mask_orig, label;
 };
 MlmRecords mlm_generate(const hp_mlm_gen_desc& d);
+MlmRecords pairs_generate(const hp_pair_gen_desc& d);  // seq2seq extension
 
 // Parameter table (model.hpp:91-142 + the bert_encoder extension).
 struct ParamEntry {

@@ -146,3 +146,24 @@ def test_bucket_layout_contract(mb):
     assert b == want
     for lo, hi in b:
         assert lo in starts and hi in starts
+
+
+def test_seq2seq_param_table_init_and_pairs_match_oracle():
+    """transformer_seq2seq (repo extension): the product's parameter table
+    and init equal the oracle's (names, shapes, order, draws), and the pair
+    generator equals the oracle's restatement bit for bit."""
+    kw = dict(arch="transformer_seq2seq", d_model=16, heads=2, vocab=40, max_seq=12, layers=2,
+              d_ff=24, label_smooth_eps=0.1)
+    spec, ospec = hp.ModelSpec(**kw, with_nsp=False), mo.Spec(**kw, with_nsp=False)
+    assert [(s.name, s.rows, s.cols) for s in hp.param_shapes(spec)] == \
+           [(n, r, c) for n, r, c, _, _ in mo.param_shapes(ospec)]
+    names = [s.name for s in hp.param_shapes(spec)]
+    assert names[0] == "embed" and "dec1.cv.1" in names and names[-1] == "dec1.ln3.b"
+    assert np.array_equal(hp.init_parameters(spec, 3), mo.init_parameters(ospec, 3))
+    r = hp.generate_pair_records(hp.PairGenConfig(n=37, vocab=40, min_len=3, max_len=11, seed=9))
+    to, tk, sg = mo.pairs_generate(37, 40, 3, 11, 9)
+    assert np.array_equal(r.tok_off, to) and np.array_equal(r.tokens, tk)
+    assert np.array_equal(r.segments, sg)
+    assert r.tokens.min() >= 4 and r.tokens.max() < 40 and len(r) == 37
+    with pytest.raises(hp.ConfigError):
+        hp.generate_pair_records(hp.PairGenConfig(n=2, vocab=40, min_len=5, max_len=4))

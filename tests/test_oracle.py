@@ -297,3 +297,40 @@ def test_torch_restatement_matches_numpy_oracle():
     z = torch.zeros_like(gt)
     got, _, _ = tm.adam_update_f32(torch.from_numpy(p32), z, z.clone(), gt, 1, 1e-3)
     assert rel_norm(got.numpy(), want) <= 1e-7
+
+
+def _s2s_spec():
+    return mo.Spec(arch="transformer_seq2seq", d_model=8, heads=2, vocab=13, max_seq=8, layers=2,
+                   d_ff=12, label_smooth_eps=0.1)
+
+
+def _s2s_batch(s, rng, shapes=((5, 4), (3, 6))):
+    batch = []
+    for ns, nt in shapes:
+        tok = rng.integers(4, s.vocab, ns + nt)
+        seg = np.array([0] * ns + [1] * nt)
+        batch.append(mo.Instance(tok, seg, np.zeros(0, np.int64), np.zeros(0, np.int64), 0))
+    return batch
+
+
+@pytest.mark.parametrize("policy", ["sentences", "tokens"])
+def test_seq2seq_extension_gradcheck(policy):
+    """Finite-difference check of the encoder-decoder extension (causal
+    decoder self-attention, cross-attention, shared embedding / output
+    projection, 2 + 2 layers) at rel <= 1e-6 (gradcheck.hpp:13-34)."""
+    s = _s2s_spec()
+    rng = np.random.default_rng(4)
+    p = mo.init_parameters(s, 5) + 0.05 * rng.standard_normal(mo.flat_size(s))
+    batch = _s2s_batch(s, rng)
+    l, w, g = mo.forward_backward(s, p, batch, policy)
+    assert w == (2.0 if policy == "sentences" else 10.0)
+    idx = rng.choice(p.size, 200, replace=False)
+    h = 1e-6
+    for i in idx:
+        q = p.copy()
+        q[i] += h
+        lp = mo.forward_backward(s, q, batch, policy, need_grad=False)[0]
+        q[i] -= 2 * h
+        lm = mo.forward_backward(s, q, batch, policy, need_grad=False)[0]
+        fd = (lp - lm) / (2 * h)
+        assert abs(fd - g[i]) / max(abs(fd), abs(g[i]), 1.0) <= 1e-6, i
