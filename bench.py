@@ -44,11 +44,21 @@ SEQ = 128
 # line): BERT-large-shaped, seq 512, per-GPU batch 16
 C4 = dict(arch="bert_encoder", d_model=1024, heads=16, vocab=30522, max_seq=512, layers=24,
           d_ff=4096, with_nsp=True, label_smooth_eps=0.1)
+# BASELINE configs[2] ("C3"), --workload c3: the paper's Transformer-base
+# translation model (fairseq transformer_wmt_en_de shape: 6 + 6 layers, d 512,
+# h 8, f 2048, shared 32768-word embedding), 64 synthetic pairs of 64 source +
+# 64 target tokens per GPU (4096 target tokens), label smoothing 0.1, the
+# "tokens" weight policy; samples = sentence pairs
+C3 = dict(arch="transformer_seq2seq", d_model=512, heads=8, vocab=32768, max_seq=64, layers=6,
+          d_ff=2048, with_nsp=False, label_smooth_eps=0.1)
 WORKLOADS = {
     "c2": (C2, 32, 128, 64, 96, "C2: BERT-base-shaped encoder MLM+NSP step (bert_encoder L12 d768 "
            "h12 ff3072 V30522), seq 128, Adam", "bert_encoder-L12-d768"),
     "c4": (C4, 16, 512, 256, 384, "C4: BERT-large-shaped encoder MLM+NSP step (bert_encoder L24 "
            "d1024 h16 ff4096 V30522), seq 512, Adam", "bert_encoder-L24-d1024"),
+    "c3": (C3, 64, 64, 64, 64, "C3: Transformer-base translation step (transformer_seq2seq 6+6 "
+           "layers d512 h8 ff2048, shared V32768), 64 pairs x (64 source + 64 target tokens), Adam, "
+           "tokens weight policy", "transformer_seq2seq-6+6-d512"),
 }
 
 
@@ -209,7 +219,7 @@ def ref_threads() -> int:
     return max(1, min(os.cpu_count() or 1, 32))
 
 
-def check_first_loss(eng, wspec, batch) -> dict:
+def check_first_loss(eng, wspec, batch, policy="sentences") -> dict:
     """Round 1's local loss (the engine's forward on batch 0 under the initial
     parameters) against the numpy f64 oracle's forward of the same batch from
     its own init of seed 21.  Tolerance 1e-2 relative (bf16 GEMM operands)."""
@@ -227,7 +237,7 @@ def check_first_loss(eng, wspec, batch) -> dict:
         c, d = int(batch.mask_off[i]), int(batch.mask_off[i + 1])
         insts.append(mo.Instance(batch.tokens[a:b], batch.segments[a:b], batch.mask_pos[c:d],
                                  batch.mask_orig[c:d], int(batch.label[i])))
-    ol, ow, _ = mo.forward_backward(ospec, p, insts, need_grad=False)
+    ol, ow, _ = mo.forward_backward(ospec, p, insts, policy, need_grad=False)
     rel = abs(ls - ol) / abs(ol)
     out = {"engine_loss": ls / w, "oracle_loss": ol / ow, "rel": rel, "tol": 1e-2,
            "ok": bool(rel <= 1e-2 and w == ow), "seconds": time.perf_counter() - t0,
@@ -290,6 +300,8 @@ def main(argv=None):
     if args.workload != "c2":
         args.no_cpu_baseline = True  # the CPU baseline is quoted on the headline config
         args.no_same_config = True
+    if args.workload == "c4":
+        args.no_loss_check = True  # the numpy oracle's 24-layer seq-512 forward takes minutes
     args.warmup = max(args.warmup, 3)
 
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
@@ -322,8 +334,11 @@ def main(argv=None):
 
     comm = hp.Communicator(world, rank, local) if world > 1 else None
     spec = hp.ModelSpec(**wspec)
-    ex = hp.ExecConfig(compute="bf16", policy="sentences", device=local, bucket_mb=args.bucket_mb,
-                       max_tokens=BATCH * SEQ, max_batch=BATCH, max_masks=BATCH * SEQ // 2)
+    s2s = wspec["arch"] == "transformer_seq2seq"
+    tok_cap = BATCH * SEQ * (2 if s2s else 1)  # seq2seq: source + target tokens
+    ex = hp.ExecConfig(compute="bf16", policy="tokens" if s2s else "sentences", device=local,
+                       bucket_mb=args.bucket_mb, max_tokens=tok_cap, max_batch=BATCH,
+                       max_masks=1 if s2s else BATCH * SEQ // 2)
     eng = hp.StepEngine(spec, hp.OptimConfig("adam", 0.9, 0.98, 1e-9), ex, comm=comm,
                         seed=21 if rank == 0 else None)
     if comm:
@@ -332,10 +347,15 @@ def main(argv=None):
     # synthetic records (reference generator + exact-length truncation), the
     # epoch plan and this rank's schedule -- identical on every rank
     rounds_needed = args.warmup + args.steps
-    gen = hp.MlmGenConfig(n=BATCH * world * min(rounds_needed, 8), vocab=wspec["vocab"], docs=64,
-                          sentences_per_doc=32, min_sentence_words=wmin, max_sentence_words=wmax,
-                          seed=7, max_seq_tokens=SEQ)
-    rec = hp.generate_mlm_records(gen)
+    if s2s:
+        rec = hp.generate_pair_records(hp.PairGenConfig(n=BATCH * world * min(rounds_needed, 8),
+                                                        vocab=wspec["vocab"], min_len=wmin,
+                                                        max_len=wmax, seed=7))
+    else:
+        gen = hp.MlmGenConfig(n=BATCH * world * min(rounds_needed, 8), vocab=wspec["vocab"], docs=64,
+                              sentences_per_doc=32, min_sentence_words=wmin, max_sentence_words=wmax,
+                              seed=7, max_seq_tokens=SEQ)
+        rec = hp.generate_mlm_records(gen)
     plan = hp.build_epoch_batches(rec.token_lengths(), BATCH, 0, 21, 0)
     sched = hp.partition_for_rank(plan, world, rank)
     batches = [rec.batch(plan.batches[rb.batch_index]) for rb in sched]
@@ -348,7 +368,7 @@ def main(argv=None):
     # checker) recomputes it from its own init of the same seed
     loss_check = None
     if rank == 0 and not args.no_loss_check:
-        loss_check = check_first_loss(eng, wspec, batches[0])
+        loss_check = check_first_loss(eng, wspec, batches[0], "tokens" if s2s else "sentences")
 
     # ---- value: batch resident in HBM ----
     eng.stage(batches[0])

@@ -457,6 +457,19 @@ hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf1
 hp_status hp_debug_layernorm(int T, int d, int bf16, const void* x, const float* g, const float* b,
                              void* y, float* mean, float* rstd, const void* dy, void* dx, float* dg,
                              float* db, float* dbias, int deferred);
+/* Generalised attention (self or cross, causal or not; kernels.h AttnArgs)
+ * on caller-owned device buffers: queries of instance b are rows
+ * [cu_q[b], cu_q[b+1]) of q (pitch ldq, head h at column qcol + h dk), keys /
+ * values rows [cu_kv[b], cu_kv[b+1]) of k / v; o [T_q x H dk], lse [H x T_q];
+ * when dO is non-null the backward writes dq / dk / dv with their pitches
+ * and column offsets.  path: 0 auto, 1 SIMT, 3 tcgen05. */
+hp_status hp_debug_attention2(int B, const int* cu_q, const int* cu_kv, int T_q, int T_kv,
+                              int max_q, int max_kv, int H, int dk, int bf16, const void* q,
+                              int64_t ldq, int qcol, const void* k, int64_t ldk, int kcol,
+                              const void* v, int64_t ldv, int vcol, void* o, float* lse,
+                              const void* dO, void* dq, int64_t lddq, int dqcol, void* dkk,
+                              int64_t lddk, int dkcol, void* dv, int64_t lddv, int dvcol,
+                              int causal, int path);
 /* One Adam (sgd=0) or SGD (sgd=1) update of the device kernel on caller-owned
  * device fp32 buffers, no scaling: compare with kern::adam_update<float>. */
 hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n,

@@ -212,6 +212,8 @@ _SIGS = {
     "hp_debug_gemm_generic": [I],
     "hp_debug_attention": [I, P, I, I, I, I, P, P, P, P, P, I],
     "hp_debug_layernorm": [I, I, I, P, P, P, P, P, P, P, P, P, P, P, I],
+    "hp_debug_attention2": [I, P, P, I, I, I, I, I, I, I, P, I64, I, P, I64, I, P, I64, I, P, P,
+                            P, P, I64, I, P, I64, I, P, I64, I, I, I],
     "hp_debug_adam": [P, P, P, P, U64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float,
                       C.c_float, I],
 }

@@ -1,5 +1,8 @@
-// tcgen05 multi-head self-attention for the bf16 path (dk = 64, varlen
-// sequences of <= 128 tokens).  One CTA per (instance, head); every matrix of
+// tcgen05 multi-head attention for the bf16 path (dk = 64, varlen
+// sequences of <= 128 tokens; self-attention over the packed QKV activations,
+// cross-attention with queries and keys / values from different tensors and
+// instance lengths, optional causal mask -- AttnArgs, kernels.h).  One CTA per
+// (instance, head); every matrix of
 // the head fits one UMMA tile, so the whole head is a handful of tcgen05.mma
 // instructions with fp32 accumulators in TMEM:
 //
@@ -164,18 +167,18 @@ __device__ __forceinline__ void atr(unsigned long long* tr, int slot) {
 
 // ------------------------------------------------------------------ forward
 __global__ void __launch_bounds__(kThreadsF, 4)
-    attn_fwd_tc(const __grid_constant__ CUtensorMap map_qkv, const int* __restrict__ cu, int H,
-                bf16* __restrict__ o, float* __restrict__ lse, int T_total,
-                unsigned long long* tr) {
+    attn_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                const __grid_constant__ CUtensorMap map_v, const AttnArgs a, unsigned long long* tr) {
   if (threadIdx.x == 0) atr(tr, 0);
   extern __shared__ __align__(1024) uint8_t raw[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(raw));
   const int b = blockIdx.x, h = blockIdx.y;
-  const int row0 = cu[b], n = cu[b + 1] - row0;
-  if (n <= 0) return;
+  const int row0 = a.cu_q[b], n = a.cu_q[b + 1] - row0;  // queries
+  const int krow0 = a.cu_kv[b], nk = a.cu_kv[b + 1] - krow0;  // keys / values
+  if (n <= 0 || nk <= 0) return;
   if (threadIdx.x == 0) atr(tr, 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = H * DK;
+  const int d = a.H * DK;
   constexpr uint32_t kCols = 128;  // S [0,128), then O [0,64)
   if (threadIdx.x == 0) {
     mbar_init(&sm.full, 1);
@@ -198,9 +201,9 @@ __global__ void __launch_bounds__(kThreadsF, 4)
   if (warp == 0) {
     if (elect_one()) {
       mbar_expect_tx(&sm.full, 3 * kTile);
-      tma_2d(&map_qkv, &sm.full, sm.tile[0], h * DK, row0);
-      tma_2d(&map_qkv, &sm.full, sm.tile[1], d + h * DK, row0);
-      tma_2d(&map_qkv, &sm.full, sm.tile[2], 2 * d + h * DK, row0);
+      tma_2d(&map_q, &sm.full, sm.tile[0], a.qcol + h * DK, row0);
+      tma_2d(&map_k, &sm.full, sm.tile[1], a.kcol + h * DK, krow0);
+      tma_2d(&map_v, &sm.full, sm.tile[2], a.vcol + h * DK, krow0);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -236,6 +239,8 @@ __global__ void __launch_bounds__(kThreadsF, 4)
     const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
     const float scale = rsqrtf(static_cast<float>(DK));
     const float sl2 = scale * 1.4426950408889634f;
+    // keys this row sees: [0, nk), and <= r under the causal mask
+    const int nj = a.causal ? min(nk, r + 1) : nk;
     mbar_wait(&sm.s_done, 0);
     if (r == 0) atr(tr, 4);
     tmem_fence_after();
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(kThreadsF, 4)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (32 * c + i < n) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(v[i]));
+        if (32 * c + i < nj) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(v[i]));
     }
     const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     const float mo = -mx * sl2;
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(kThreadsF, 4)
       float p[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        p[i] = (32 * c + i < n) ? ex2(fmaf(__uint_as_float(v[i]), sl2, mo)) : 0.f;
+        p[i] = (32 * c + i < nj) ? ex2(fmaf(__uint_as_float(v[i]), sl2, mo)) : 0.f;
         s4[i & 3] += p[i];
       }
       put_row32(pb, r, c, p);
@@ -275,10 +280,10 @@ __global__ void __launch_bounds__(kThreadsF, 4)
     if (r == 0) atr(tr, 7);
     tmem_fence_after();
     const bool ok = r < n;
-    bf16* orow = o + (int64_t)(row0 + r) * d + h * DK;
+    bf16* orow = static_cast<bf16*>(a.o) + (int64_t)(row0 + r) * d + h * DK;
     tmem_row32_to_global(trow, 1.f / sum, orow, ok);
     tmem_row32_to_global(trow + 32, 1.f / sum, orow + 32, ok);
-    if (ok) lse[(int64_t)h * T_total + row0 + r] = mx * scale + logf(sum);
+    if (ok) a.lse[(int64_t)h * a.T_q + row0 + r] = mx * scale + logf(sum);
     if (r == 0) atr(tr, 8);
   }
   tmem_fence_before();
@@ -292,17 +297,19 @@ __global__ void __launch_bounds__(kThreadsF, 4)
 
 // ------------------------------------------------------------------ backward
 __global__ void __launch_bounds__(kThreadsB, 2)
-    attn_bwd_tc(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
-                const int* __restrict__ cu, int H, const bf16* __restrict__ o,
-                const bf16* __restrict__ dO, const float* __restrict__ lse, bf16* __restrict__ dqkv,
-                int T_total) {
+    attn_bwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
+                const AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t raw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(align1024(raw));
   const int b = blockIdx.x, h = blockIdx.y;
-  const int row0 = cu[b], n = cu[b + 1] - row0;
-  if (n <= 0) return;
+  const int row0 = a.cu_q[b], n = a.cu_q[b + 1] - row0;  // queries
+  const int krow0 = a.cu_kv[b], nk = a.cu_kv[b + 1] - krow0;  // keys / values
+  if (n <= 0 || nk <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = H * DK;
+  const int d = a.H * DK;
+  const bf16* o = static_cast<const bf16*>(a.o);
+  const bf16* dO = static_cast<const bf16*>(a.dO);
   // TMEM: S [0,128), dP [128,256); then dV [0,64), dK [64,128), dQ [128,192)
   constexpr uint32_t kCols = 256;
   if (threadIdx.x == 0) {
@@ -327,9 +334,9 @@ __global__ void __launch_bounds__(kThreadsB, 2)
   if (warp == 0) {
     if (elect_one()) {
       mbar_expect_tx(&sm.full, 4 * kTile);
-      tma_2d(&map_qkv, &sm.full, sm.tile[0], h * DK, row0);
-      tma_2d(&map_qkv, &sm.full, sm.tile[1], d + h * DK, row0);
-      tma_2d(&map_qkv, &sm.full, sm.tile[2], 2 * d + h * DK, row0);
+      tma_2d(&map_q, &sm.full, sm.tile[0], a.qcol + h * DK, row0);
+      tma_2d(&map_k, &sm.full, sm.tile[1], a.kcol + h * DK, krow0);
+      tma_2d(&map_v, &sm.full, sm.tile[2], a.vcol + h * DK, krow0);
       tma_2d(&map_do, &sm.full, sm.tile[3], h * DK, row0);
     }
     __syncwarp();
@@ -382,7 +389,9 @@ __global__ void __launch_bounds__(kThreadsB, 2)
     const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
     const float scale = rsqrtf(static_cast<float>(DK));
     const float l2e = 1.4426950408889634f;
-    const bool rok = r < n;
+    const bool rok = r < n;        // query row r (S, dP, dQ)
+    const bool kok = r < nk;       // key row r (dK, dV)
+    const int nj = a.causal ? min(nk, r + 1) : nk;  // keys query row r sees
     // D_r = rowsum(dO * O), lse_r -- while the MMAs run
     float Dr = 0.f, lr = 0.f;
     if (rok) {
@@ -402,7 +411,7 @@ __global__ void __launch_bounds__(kThreadsB, 2)
         }
       }
       Dr = (d4[0] + d4[1]) + (d4[2] + d4[3]);
-      lr = lse[(int64_t)h * T_total + row0 + r];
+      lr = a.lse[(int64_t)h * a.T_q + row0 + r];
     }
     const float sl2 = scale * l2e, lo = -lr * l2e;
     mbar_wait(&sm.s_done, 0);
@@ -418,7 +427,7 @@ __global__ void __launch_bounds__(kThreadsB, 2)
       float p[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const bool ok = rok && (32 * c + i < n);
+        const bool ok = rok && (32 * c + i < nj);
         p[i] = ok ? ex2(fmaf(__uint_as_float(sv[i]), sl2, lo)) : 0.f;
       }
       put_row32(xb, r, c, p, kXs);
@@ -447,10 +456,13 @@ __global__ void __launch_bounds__(kThreadsB, 2)
     mbar_arrive(&sm.ds_ready);
     mbar_wait(&sm.o_done, 0);
     tmem_fence_after();
-    bf16* row = dqkv + (int64_t)(row0 + r) * 3 * d + h * DK + 32 * half;
-    tmem_row32_to_global(trow + 128 + 32 * half, 1.f, row, rok);        // dQ
-    tmem_row32_to_global(trow + 64 + 32 * half, 1.f, row + d, rok);     // dK
-    tmem_row32_to_global(trow + 32 * half, 1.f, row + 2 * d, rok);      // dV
+    const int c0 = h * DK + 32 * half;
+    tmem_row32_to_global(trow + 128 + 32 * half, 1.f,
+                         static_cast<bf16*>(a.dq) + (int64_t)(row0 + r) * a.lddq + a.dqcol + c0, rok);   // dQ
+    tmem_row32_to_global(trow + 64 + 32 * half, 1.f,
+                         static_cast<bf16*>(a.dk_) + (int64_t)(krow0 + r) * a.lddk + a.dkcol + c0, kok);  // dK
+    tmem_row32_to_global(trow + 32 * half, 1.f,
+                         static_cast<bf16*>(a.dv) + (int64_t)(krow0 + r) * a.lddv + a.dvcol + c0, kok);   // dV
   }
   tmem_fence_before();
   __syncthreads();
@@ -952,40 +964,57 @@ CUtensorMap act_map(const void* base, int rows, int cols) {
 }
 }  // namespace
 
-void attention_fwd_tc(const DevBatch& b, int H, const void* qkv, void* o, float* lse, cudaStream_t s) {
-  if (b.B == 0) return;
-  const int d = H * attn_tc::DK;
-  const CUtensorMap mq = act_map(qkv, b.T, 3 * d);
+// [rows][cols] bf16 activations with row pitch ld as a 128 x 64 box map
+static CUtensorMap act_map_ld(const void* base, int rows, int cols, int64_t ld) {
+  const uint64_t dims[2] = {static_cast<uint64_t>(cols), static_cast<uint64_t>(rows)};
+  const uint64_t str[1] = {static_cast<uint64_t>(ld)};
+  const uint32_t box[2] = {64, 128};
+  return make_map(base, 2, dims, str, box);
+}
+
+void attention_tc_fwd(const AttnArgs& a, cudaStream_t s) {
+  if (a.B == 0) return;
+  const CUtensorMap mq = act_map_ld(a.q, a.T_q, (int)a.ldq, a.ldq);
+  const CUtensorMap mk = act_map_ld(a.k, a.T_kv, (int)a.ldk, a.ldk);
+  const CUtensorMap mv = act_map_ld(a.v, a.T_kv, (int)a.ldv, a.ldv);
   const int sm = static_cast<int>(sizeof(attn_tc::FwdSmem)) + 1024;
   static bool attr = false;
   if (!attr) {
     HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr = true;
   }
-  launch_ex(attn_tc::attn_fwd_tc, dim3(b.B, H), dim3(attn_tc::kThreadsF), sm, s, 1, mq,
-             (const int*)b.cu, H, static_cast<attn_tc::bf16*>(o), lse, b.T, g_attn_trace);
+  launch_ex(attn_tc::attn_fwd_tc, dim3(a.B, a.H), dim3(attn_tc::kThreadsF), sm, s, 1, mq, mk, mv, a,
+            g_attn_trace);
   HP_CUDA(cudaGetLastError());
   count_launch();
 }
 
-void attention_bwd_tc(const DevBatch& b, int H, const void* qkv, const void* o, const void* dO,
-                      const float* lse, void* dqkv, cudaStream_t s) {
-  if (b.B == 0) return;
-  const int d = H * attn_tc::DK;
-  const CUtensorMap mq = act_map(qkv, b.T, 3 * d);
-  const CUtensorMap mg = act_map(dO, b.T, d);
+void attention_tc_bwd(const AttnArgs& a, cudaStream_t s) {
+  if (a.B == 0) return;
+  const int d = a.H * attn_tc::DK;
+  const CUtensorMap mq = act_map_ld(a.q, a.T_q, (int)a.ldq, a.ldq);
+  const CUtensorMap mk = act_map_ld(a.k, a.T_kv, (int)a.ldk, a.ldk);
+  const CUtensorMap mv = act_map_ld(a.v, a.T_kv, (int)a.ldv, a.ldv);
+  const CUtensorMap mg = act_map(a.dO, a.T_q, d);
   const int sm = static_cast<int>(sizeof(attn_tc::BwdSmem)) + 1024;
   static bool attr = false;
   if (!attr) {
     HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr = true;
   }
-  launch_ex(attn_tc::attn_bwd_tc, dim3(b.B, H), dim3(attn_tc::kThreadsB), sm, s, 1, mq, mg,
-             (const int*)b.cu, H, static_cast<const attn_tc::bf16*>(o),
-             static_cast<const attn_tc::bf16*>(dO), (const float*)lse,
-             static_cast<attn_tc::bf16*>(dqkv), b.T);
+  launch_ex(attn_tc::attn_bwd_tc, dim3(a.B, a.H), dim3(attn_tc::kThreadsB), sm, s, 1, mq, mk, mv, mg, a);
   HP_CUDA(cudaGetLastError());
   count_launch();
+}
+
+void attention_fwd_tc(const DevBatch& b, int H, const void* qkv, void* o, float* lse, cudaStream_t s) {
+  attention_tc_fwd(self_attn_args(b, H, attn_tc::DK, attn_tc::NQ, qkv, o, lse), s);
+}
+
+void attention_bwd_tc(const DevBatch& b, int H, const void* qkv, const void* o, const void* dO,
+                      const float* lse, void* dqkv, cudaStream_t s) {
+  attention_tc_bwd(self_attn_args(b, H, attn_tc::DK, attn_tc::NQ, qkv, const_cast<void*>(o),
+                                  const_cast<float*>(lse), dO, dqkv), s);
 }
 
 }  // namespace hp

@@ -532,6 +532,38 @@ hp_status hp_debug_layernorm(int T, int d, int bf16, const void* x, const float*
   HP_API_END
 }
 
+hp_status hp_debug_attention2(int B, const int* cu_q, const int* cu_kv, int T_q, int T_kv,
+                              int max_q, int max_kv, int H, int dk, int bf16, const void* q,
+                              int64_t ldq, int qcol, const void* k, int64_t ldk, int kcol,
+                              const void* v, int64_t ldv, int vcol, void* o, float* lse,
+                              const void* dO, void* dq, int64_t lddq, int dqcol, void* dkk,
+                              int64_t lddk, int dkcol, void* dv, int64_t lddv, int dvcol,
+                              int causal, int path) {
+  HP_API_BEGIN
+  hp::AttnArgs a;
+  a.B = B; a.H = H; a.dk = dk;
+  a.cu_q = cu_q; a.cu_kv = cu_kv; a.T_q = T_q; a.T_kv = T_kv; a.max_q = max_q; a.max_kv = max_kv;
+  a.q = q; a.ldq = ldq; a.qcol = qcol;
+  a.k = k; a.ldk = ldk; a.kcol = kcol;
+  a.v = v; a.ldv = ldv; a.vcol = vcol;
+  a.o = o; a.lse = lse; a.causal = causal;
+  a.dO = dO;
+  a.dq = dq; a.lddq = lddq; a.dqcol = dqcol;
+  a.dk_ = dkk; a.lddk = lddk; a.dkcol = dkcol;
+  a.dv = dv; a.lddv = lddv; a.dvcol = dvcol;
+  const hp::DType t = bf16 ? hp::DType::bf16 : hp::DType::f32;
+  if (path == 3 && !hp::attention2_tc_ok(a, t)) fail(HP_ECONFIG, "tcgen05 attention: unsupported shape");
+  if (path == 3 || (path == 0 && hp::attention2_tc_ok(a, t))) {
+    hp::attention_tc_fwd(a, 0);
+    if (dO) hp::attention_tc_bwd(a, 0);
+  } else {
+    hp::attention_simt_fwd(a, t, 0);
+    if (dO) hp::attention_simt_bwd(a, t, 0);
+  }
+  HP_CUDA(cudaDeviceSynchronize());
+  HP_API_END
+}
+
 hp_status hp_debug_attention(int B, const int* cu, int T, int H, int dk, int bf16,
                              const void* qkv, void* o, float* lse, const void* dO, void* dqkv,
                              int path) {

@@ -42,7 +42,6 @@ struct NvtxRange {
 };
 }  // namespace
 
-constexpr int kEmbHotTokens = 32;  // = kEmbHot in kernels.cu
 
 namespace {
 uint64_t pad8(uint64_t v) { return (v + 7) & ~uint64_t(7); }
@@ -85,7 +84,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     fail(HP_ECONFIG, "exec capacities max_tokens/max_batch must be > 0");
   if (m_.max_seq > static_cast<uint64_t>(kAttnMaxSeq) &&
       !(x_.compute == HP_COMPUTE_BF16 && m_.heads > 0 && m_.d_model / m_.heads == 64 &&
-        m_.max_seq <= 512))
+        m_.max_seq <= 512 && m_.arch != HP_ARCH_SEQ2SEQ))
     fail(HP_ECONFIG, "max_seq > 128 needs the bf16 path with d_model / heads == 64 (max 512)");
   if (o_.kind != HP_OPT_ADAM && o_.kind != HP_OPT_SGD) fail(HP_ECONFIG, "unknown optimizer kind");
   if (x_.policy != HP_POLICY_SENTENCES && x_.policy != HP_POLICY_TOKENS)
@@ -98,13 +97,16 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   at_ = bf16_ ? DType::bf16 : DType::f32;
   asz_ = bf16_ ? 2 : 4;
   bert_ = m_.arch == HP_ARCH_BERT_ENCODER;
+  s2s_ = m_.arch == HP_ARCH_SEQ2SEQ;
+  if (s2s_) m_.with_nsp = 0;  // no NSP head
+  emb_scale_ = s2s_ ? static_cast<float>(std::sqrt(static_cast<double>(m_.d_model))) : 1.f;
   d_ = static_cast<int>(m_.d_model);
   H_ = static_cast<int>(m_.heads);
   dk_ = d_ / H_;
   V_ = static_cast<int>(m_.vocab);
   Vp_ = static_cast<int>(pad8(m_.vocab));
-  L_ = bert_ ? static_cast<int>(m_.layers) : 1;
-  F_ = bert_ ? static_cast<int>(m_.d_ff) : 0;
+  L_ = (bert_ || s2s_) ? static_cast<int>(m_.layers) : 1;
+  F_ = (bert_ || s2s_) ? static_cast<int>(m_.d_ff) : 0;
   n_ = table_.back().offset + table_.back().size();
   buckets_ = bucket_plan(table_, x_.bucket_mb > 0 ? x_.bucket_mb : 25.0);
 
@@ -150,9 +152,10 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     // (HP_SPARSE_EMB=1 forces it whenever the engine has a communicator --
     // world 1 included, so one GPU runs the exchange's collectives)
     const bool forced = comm_ && e && std::string(e) == "1";
+    // (seq2seq: the output projection makes the embedding gradient dense)
     sparse_emb_ = (forced || (W > 1 && !(e && std::string(e) == "0") &&
                               x_.max_tokens * (d_ + 4) * W < 2 * (W - 1) * m_.vocab * d_)) &&
-                  last.first_param == 0 && last.last_param == 0 && d_ % 8 == 0;
+                  last.first_param == 0 && last.last_param == 0 && d_ % 8 == 0 && !s2s_;
     if (sparse_emb_) {
       emb_cap_ = static_cast<int>(x_.max_tokens);
       emb_rows_ = static_cast<float*>(dalloc((size_t)emb_cap_ * (d_ + 4) * 4));
@@ -238,7 +241,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     // opt-in (HP_EMB_SPLIT=1): bit-identical, measured neutral on C2 at N = 1
     // (profiles/r01_ab_emb_split.txt) -- the dense tail is not what bounds the step
     const char* es = std::getenv("HP_EMB_SPLIT");
-    split_emb_ = es && std::string(es) == "1" && lb.first_param == 0 &&
+    split_emb_ = es && std::string(es) == "1" && lb.first_param == 0 && !s2s_ &&
                  table_[0].rows == static_cast<uint64_t>(V_) && table_[0].cols == static_cast<uint64_t>(d_) &&
                  d_ % 4 == 0 && table_[0].offset % 4 == 0;
     if (split_emb_) {
@@ -286,7 +289,9 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   // staged batch block (fixed layout at capacity)
   const uint64_t Tm = x_.max_tokens, Bm = x_.max_batch,
                  Mm = (std::max<uint64_t>(x_.max_masks, 1) + mpad_ - 1) / mpad_ * mpad_;
-  const size_t ints = 3 * Tm + (Bm + 1) + 2 * Mm + Bm + (4 * Tm + 3);
+  // (seq2seq layout: see stage_s2s)
+  const size_t ints = std::max<size_t>(3 * Tm + (Bm + 1) + 2 * Mm + Bm + (4 * Tm + 3),
+                                       9 * Tm + 2 * (Bm + 1) + 3);
   stage_bytes_ = ((ints * 4 + 7) & ~size_t(7)) + 8;
   for (int i = 0; i < kStageBufs; ++i) {
     HP_CUDA(cudaMallocHost(&h_stage_[i], stage_bytes_));
@@ -309,10 +314,27 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     batch_.ulist = batch_.useg + Tm + 1;
     batch_.ucount = batch_.ulist + Tm;
     d_weight_ = reinterpret_cast<double*>(static_cast<char*>(d_stage_) + stage_bytes_ - 8);
+    if (s2s_) {  // [enc tok, pos | cu | dec tok, pos | cu | targets | embedding plan]
+      enc_.tok = base;
+      enc_.pos = base + Tm;
+      enc_.cu = base + 2 * Tm;
+      dec_.tok = enc_.cu + Bm + 1;
+      dec_.pos = dec_.tok + Tm;
+      dec_.cu = dec_.pos + Tm;
+      tgt_ = dec_.cu + Bm + 1;
+      embp_.perm = tgt_ + Tm;
+      embp_.uid = embp_.perm + Tm;
+      embp_.useg = embp_.uid + Tm;
+      embp_.ulist = embp_.useg + Tm + 1;
+      embp_.ucount = embp_.ulist + Tm;
+    }
   }
 
   // activations
   const size_t T = Tm;
+  if (s2s_) {
+    s2s_alloc();
+  } else {
   layers_.resize(L_);
   for (int l = 0; l < L_; ++l) {
     Layer& y = layers_[l];
@@ -344,10 +366,9 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
   dz_ = dalloc(Mm * Vp_ * asz_);
   HP_CUDA(cudaMemset(dz_, 0, Mm * Vp_ * asz_));
   row_loss_ = static_cast<float*>(dalloc((Mm + Bm) * 4));
-  const size_t wmax = std::max<size_t>(d_, F_);
   dA_ = dalloc(T * d_ * asz_);
   dB_ = dalloc(T * d_ * asz_);
-  dC_ = dalloc(T * wmax * asz_);
+  dC_ = dalloc(T * std::max<size_t>(d_, F_) * asz_);
   dU_ = bert_ ? dalloc(T * F_ * asz_) : nullptr;
   dqkv_ = dalloc(T * 3 * d_ * asz_);
   if (bert_) {
@@ -362,8 +383,10 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     qbuf_[0] = dqkv_;
     qbuf_[1] = dalloc(T * 3 * d_ * asz_);
   }
+  }  // !s2s_
+  const size_t wmax = std::max<size_t>(d_, F_);
   const size_t scratch = std::max({colsum_scratch_floats((int)T, (int)wmax),
-                                   colsum_scratch_floats((int)Mm, Vp_),
+                                   colsum_scratch_floats((int)(s2s_ ? T : Mm), Vp_),
                                    colsum_scratch_floats((int)T, d_)});
   scratch_ = static_cast<float*>(dalloc(scratch * 4));
   if (wg_on_) scratch_wg_ = static_cast<float*>(dalloc(colsum_scratch_floats((int)T, F_) * 4));
@@ -592,6 +615,18 @@ void Engine::stage_batch(const hp_batch& b) {
   // wait until the previous copy out of this pinned buffer finished
   HP_CUDA(cudaEventSynchronize(ev_stage_[stage_idx_]));
   int* h = static_cast<int*>(h_stage_[stage_idx_]);
+  if (s2s_) {
+    double w = 0.0;
+    stage_s2s(b, h, &w);
+    *reinterpret_cast<double*>(static_cast<char*>(h_stage_[stage_idx_]) + stage_bytes_ - 8) = w;
+    HP_CUDA(cudaMemcpyAsync(d_stage_, h_stage_[stage_idx_], stage_bytes_, cudaMemcpyHostToDevice,
+                            s_main_));
+    HP_CUDA(cudaEventRecord(ev_stage_[stage_idx_], s_main_));
+    stage_idx_ = (stage_idx_ + 1) % kStageBufs;
+    local_weight_ = w;
+    staged_ = true;
+    return;
+  }
   int *tok = h, *seg = h + Tm, *pos = h + 2 * Tm, *cu = h + 3 * Tm, *mrow = cu + Bm + 1,
       *morig = mrow + Mm, *label = morig + Mm, *perm = label + Bm, *uid = perm + Tm,
       *useg = uid + Tm, *ulist = useg + Tm + 1, *ucount = ulist + Tm;
@@ -892,6 +927,10 @@ void Engine::wait_wg(cudaEvent_t e) {
 // ------------------------------------------------------------------ forward
 void Engine::forward(bool need_grad) {
   NvtxRange nv("hp.forward");
+  if (s2s_) {
+    forward_s2s();
+    return;
+  }
   const DevBatch& b = batch_;
   const int T = b.T;
   const DType wt = bf16_ ? DType::bf16 : DType::f32;
@@ -1071,6 +1110,10 @@ void Engine::issue_bucket(size_t k) {
 
 void Engine::backward() {
   NvtxRange nv("hp.backward");
+  if (s2s_) {
+    backward_s2s();
+    return;
+  }
   const DevBatch& b = batch_;
   const int T = b.T;
   if (wg_on_) {

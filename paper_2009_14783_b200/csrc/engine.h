@@ -27,6 +27,8 @@ struct hp_comm {
 
 namespace hp {
 
+constexpr int kEmbHotTokens = 32;  // = kEmbHot in kernels.cu (embedding-gradient plan)
+
 // Timer classes for the roofline accounting (CUDA events on the launching
 // stream around every launch of the class).
 enum TimerClass { TM_GEMM = 0, TM_ATTN, TM_NORM, TM_HEAD, TM_ADAM, TM_EMBED, TM_COUNT };
@@ -98,6 +100,18 @@ class Engine {
   void tstop(int cls, double flops, double bytes, cudaStream_t st = nullptr);
   void forward(bool need_grad_state);
   void backward();
+  // transformer_seq2seq extension (engine_s2s.cpp)
+  void stage_s2s(const hp_batch& b, int* h, double* weight);
+  void forward_s2s();
+  void backward_s2s();
+  void s2s_alloc();
+  GemmArgs grouped_b(int first_block, int N, int K, const void* a, int64_t lda, int a_trans,
+                     int b_trans) const;
+  void ln_fwd(int T, const void* x, int ig, void* y, float* mean, float* rstd);
+  void ln_bwd(int T, const void* dy, const void* x, const float* mean, const float* rstd, int ig,
+              void* dx, float* dbias);
+  void attn_op_fwd(const AttnArgs& a);
+  void attn_op_bwd(const AttnArgs& a);
   void grads_ready(int first_done_param);
   void issue_bucket(size_t b);
   void round_body(int dummy);  // the device work of one round (eager or captured)
@@ -113,6 +127,8 @@ class Engine {
   size_t asz_;
   int d_, H_, dk_, V_, Vp_, L_, F_;
   bool bert_;
+  bool s2s_ = false;  // HP_ARCH_SEQ2SEQ
+  float emb_scale_ = 1.f;
   std::vector<ParamEntry> table_;
   std::vector<Bucket> buckets_;
   std::vector<uint64_t> shadow_off_, shadow_ld_;
@@ -145,8 +161,20 @@ class Engine {
     void *x = nullptr, *qkv = nullptr, *o = nullptr, *p1 = nullptr, *x1 = nullptr, *u = nullptr,
          *g = nullptr, *p2 = nullptr;
     float *lse = nullptr, *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr;
+    // seq2seq decoder: cross-attention (qc, kvc, oc, lsec), x2 = LN2 output,
+    // p3 / LN3 around the FFN
+    void *qc = nullptr, *kvc = nullptr, *oc = nullptr, *x2 = nullptr, *p3 = nullptr;
+    float *lsec = nullptr, *mean3 = nullptr, *rstd3 = nullptr;
   };
   std::vector<Layer> layers_;
+  // seq2seq: decoder layers (layers_ holds the encoder), the encoder output
+  // (memory), per-side batches, decoder targets, the embedding-gradient plan
+  // over [source tokens, decoder-input tokens], its input-gradient rows
+  std::vector<Layer> dec_layers_;
+  void* mem_ = nullptr;
+  DevBatch enc_, dec_, embp_;
+  const int* tgt_ = nullptr;
+  void *dqc_ = nullptr, *dkvc_ = nullptr, *dmem_ = nullptr, *demb_ = nullptr;
   void *x_final_ = nullptr, *p0_ = nullptr;
   float *mean0_ = nullptr, *rstd0_ = nullptr;
   void *hm_ = nullptr, *dz_ = nullptr, *dhm_ = nullptr;

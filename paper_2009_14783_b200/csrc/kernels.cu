@@ -132,6 +132,30 @@ __global__ void embed_fwd_kernel(int T, int d, const int* __restrict__ tok,
     x[(int64_t)t * d + c] = fromf<XT>((tof(e[c]) + tof(sg[c])) + p[c]);
 }
 
+// seq2seq extension: x[t] = scale * E[tok] + PE[pos] (fairseq's embed_scale
+// = sqrt(d), no segment rows)
+template <class WT, class XT>
+__global__ void embed_scaled_kernel(int T, int d, const int* __restrict__ tok,
+                                    const int* __restrict__ pos, const WT* __restrict__ E,
+                                    float scale, const float* __restrict__ pe, XT* __restrict__ x) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const WT* e = E + (int64_t)tok[t] * d;
+  const float* p = pe + (int64_t)pos[t] * d;
+  for (int c = lane; c < d; c += 32) x[(int64_t)t * d + c] = fromf<XT>(scale * tof(e[c]) + p[c]);
+}
+
+void embed_scaled_fwd(int T, int d, const int* tok, const int* pos, const void* E, DType wt,
+                      float scale, const float* pe, void* x, DType xt, cudaStream_t s) {
+  if (T == 0) return;
+  DISPATCH1(wt, W, DISPATCH1(xt, X,
+      embed_scaled_kernel<W, X><<<(T + 7) / 8, 256, 0, s>>>(T, d, tok, pos, (const W*)E, scale, pe,
+                                                            (X*)x)));
+  LAUNCH_CHECK();
+  count_launch();
+}
+
 void embed_fwd(const DevBatch& b, int d, const void* E, const void* seg0,
                const void* seg1, DType wt, const float* pe, void* x, DType xt,
                cudaStream_t s) {
@@ -417,7 +441,7 @@ __global__ void emb_slot_ids_kernel(const int* __restrict__ counts, const int* _
   rows[(int64_t)u * stride] = __int_as_float(u < U ? uid[u] : -1);
 }
 __global__ void emb_scatter_kernel(const float* __restrict__ rows, int cap, int d,
-                                   float* __restrict__ dE) {
+                                   float* __restrict__ dE, float scale) {
   const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (u >= cap) return;
   const float* r = rows + (int64_t)u * (d + 4);
@@ -427,14 +451,14 @@ __global__ void emb_scatter_kernel(const float* __restrict__ rows, int cap, int 
   for (int c = 4 * lane; c < d; c += 128) {
     const float4 v = *reinterpret_cast<const float4*>(r + 4 + c);
     float4 w = *reinterpret_cast<float4*>(o + c);
-    w.x += v.x; w.y += v.y; w.z += v.z; w.w += v.w;
+    w.x += scale * v.x; w.y += scale * v.y; w.z += scale * v.z; w.w += scale * v.w;
     *reinterpret_cast<float4*>(o + c) = w;
   }
 }
-void embed_rows_scatter(const float* rows, int cap, int d, float* dE, cudaStream_t s) {
+void embed_rows_scatter(const float* rows, int cap, int d, float* dE, cudaStream_t s, float scale) {
   if (cap == 0) return;
   if (d % 4) fail(HP_ECONFIG, "embedding rows: d_model must be a multiple of 4");
-  emb_scatter_kernel<<<(cap + 7) / 8, 256, 0, s>>>(rows, cap, d, dE);
+  emb_scatter_kernel<<<(cap + 7) / 8, 256, 0, s>>>(rows, cap, d, dE, scale);
   LAUNCH_CHECK();
   count_launch();
 }
@@ -473,7 +497,7 @@ static void embed_bwd_impl(const DevBatch& b, int d, const void* dx, DType xt, f
       LAUNCH_CHECK();
     }
     count_launch(2);
-    {
+    if (dseg0) {
       // both segment rows in one pass over dx (rows of 32, 8 columns a thread)
       const int rows_per = 32, chunks = (b.T + rows_per - 1) / rows_per;
       dim3 g1((d / 8 + 127) / 128, chunks);
@@ -1043,143 +1067,209 @@ __device__ void load_head(float* dst, int ld_dst, int n, int n4, int dk, const T
 }
 
 template <class T>
-__global__ void attn_fwd_kernel(const int* __restrict__ cu, int H, int dk,
-                                const T* __restrict__ qkv, T* __restrict__ o,
-                                float* __restrict__ lse, int T_total) {
+__global__ void attn_fwd_kernel(const AttnArgs a) {
   extern __shared__ float sm[];
-  const int b = blockIdx.x, h = blockIdx.y;
-  const int row0 = cu[b], n = cu[b + 1] - row0;
-  if (n <= 0) return;
-  const int n4 = (n + 3) & ~3, ldh = dk + 1, lds = n4 + 1;
-  const int d = H * dk;
-  const int64_t ldq = 3 * (int64_t)d;
+  const int b = blockIdx.x, h = blockIdx.y, dk = a.dk;
+  const int rq = a.cu_q[b], nq = a.cu_q[b + 1] - rq;
+  const int rk = a.cu_kv[b], nk = a.cu_kv[b + 1] - rk;
+  if (nq <= 0 || nk <= 0) return;
+  const int nq4 = (nq + 3) & ~3, nk4 = (nk + 3) & ~3, ldh = dk + 1, lds = nk4 + 1;
+  const int d = a.H * dk;
   float* Q = sm;
-  float* K = Q + n4 * ldh;
-  float* V = K + n4 * ldh;
-  float* S = V + n4 * ldh;
-  load_head(Q, ldh, n, n4, dk, qkv, row0, ldq, h * dk);
-  load_head(K, ldh, n, n4, dk, qkv, row0, ldq, d + h * dk);
-  load_head(V, ldh, n, n4, dk, qkv, row0, ldq, 2 * d + h * dk);
+  float* K = Q + nq4 * ldh;
+  float* V = K + nk4 * ldh;
+  float* S = V + nk4 * ldh;
+  load_head(Q, ldh, nq, nq4, dk, (const T*)a.q, rq, a.ldq, a.qcol + h * dk);
+  load_head(K, ldh, nk, nk4, dk, (const T*)a.k, rk, a.ldk, a.kcol + h * dk);
+  load_head(V, ldh, nk, nk4, dk, (const T*)a.v, rk, a.ldv, a.vcol + h * dk);
   __syncthreads();
-  // scores = (Q K^T) * (1/sqrt(dk))   attention.hpp:21-23
+  // scores = (Q K^T) * (1/sqrt(dk))   attention.hpp:21-23; causal: keys j <= i
   const float scale = 1.f / sqrtf((float)dk);
-  smem_mm(n, n, dk, SMat{Q, ldh, 1}, SMat{K, 1, ldh},
-          [&](int i, int j, float v) { S[i * lds + j] = v * scale; });
+  const int causal = a.causal;
+  smem_mm(nq, nk, dk, SMat{Q, ldh, 1}, SMat{K, 1, ldh},
+          [&](int i, int j, float v) { S[i * lds + j] = (causal && j > i) ? -FLT_MAX : v * scale; });
   __syncthreads();
   // row softmax with max shift (tape.hpp:129-137)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int i = w; i < n; i += nw) {
+  for (int i = w; i < nq; i += nw) {
     float* r = S + i * lds;
+    const int nj = causal ? min(nk, i + 1) : nk;
     float mx = -FLT_MAX;
-    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, r[j]);
+    for (int j = lane; j < nj; j += 32) mx = fmaxf(mx, r[j]);
     mx = warp_max(mx);
     float se = 0.f;
-    for (int j = lane; j < n; j += 32) {
-      const float e = expf(r[j] - mx);
+    for (int j = lane; j < nk; j += 32) {
+      const float e = j < nj ? expf(r[j] - mx) : 0.f;
       r[j] = e;
       se += e;
     }
     se = warp_sum(se);
     const float inv = 1.f / se;
-    for (int j = lane; j < n; j += 32) r[j] = r[j] * inv;
-    if (lane == 0) lse[(int64_t)h * T_total + row0 + i] = mx + logf(se);
+    for (int j = lane; j < nk; j += 32) r[j] = r[j] * inv;
+    if (lane == 0) a.lse[(int64_t)h * a.T_q + rq + i] = mx + logf(se);
   }
   __syncthreads();
   // O = P V -> columns h*dk.. of the concat (concat_cols order)
-  smem_mm(n, dk, n, SMat{S, lds, 1}, SMat{V, ldh, 1}, [&](int i, int c, float v) {
-    o[(int64_t)(row0 + i) * d + h * dk + c] = fromf<T>(v);
+  T* o = (T*)a.o;
+  smem_mm(nq, dk, nk, SMat{S, lds, 1}, SMat{V, ldh, 1}, [&](int i, int c, float v) {
+    o[(int64_t)(rq + i) * d + h * dk + c] = fromf<T>(v);
   });
 }
 
 template <class T>
-__global__ void attn_bwd_kernel(const int* __restrict__ cu, int H, int dk,
-                                const T* __restrict__ qkv, const T* __restrict__ o,
-                                const T* __restrict__ dO, const float* __restrict__ lse,
-                                T* __restrict__ dqkv, int T_total) {
+__global__ void attn_bwd_kernel(const AttnArgs a) {
   extern __shared__ float sm[];
-  const int b = blockIdx.x, h = blockIdx.y;
-  const int row0 = cu[b], n = cu[b + 1] - row0;
-  if (n <= 0) return;
-  const int n4 = (n + 3) & ~3, ldh = dk + 1, lds = n4 + 1;
-  const int d = H * dk;
-  const int64_t ldq = 3 * (int64_t)d;
+  const int b = blockIdx.x, h = blockIdx.y, dk = a.dk;
+  const int rq = a.cu_q[b], nq = a.cu_q[b + 1] - rq;
+  const int rk = a.cu_kv[b], nk = a.cu_kv[b + 1] - rk;
+  if (nq <= 0 || nk <= 0) return;
+  const int nq4 = (nq + 3) & ~3, nk4 = (nk + 3) & ~3, ldh = dk + 1, lds = nk4 + 1;
+  const int d = a.H * dk;
   float* Q = sm;
-  float* K = Q + n4 * ldh;
-  float* V = K + n4 * ldh;
-  float* G = V + n4 * ldh;  // dO
-  float* S = G + n4 * ldh;
-  float* D = S + n4 * lds;  // rowsum(dO * O)
-  load_head(Q, ldh, n, n4, dk, qkv, row0, ldq, h * dk);
-  load_head(K, ldh, n, n4, dk, qkv, row0, ldq, d + h * dk);
-  load_head(V, ldh, n, n4, dk, qkv, row0, ldq, 2 * d + h * dk);
-  load_head(G, ldh, n, n4, dk, dO, row0, d, h * dk);
+  float* K = Q + nq4 * ldh;
+  float* V = K + nk4 * ldh;
+  float* G = V + nk4 * ldh;  // dO
+  float* S = G + nq4 * ldh;
+  float* D = S + nq4 * lds;  // rowsum(dO * O)
+  const T* o = (const T*)a.o;
+  load_head(Q, ldh, nq, nq4, dk, (const T*)a.q, rq, a.ldq, a.qcol + h * dk);
+  load_head(K, ldh, nk, nk4, dk, (const T*)a.k, rk, a.ldk, a.kcol + h * dk);
+  load_head(V, ldh, nk, nk4, dk, (const T*)a.v, rk, a.ldv, a.vcol + h * dk);
+  load_head(G, ldh, nq, nq4, dk, (const T*)a.dO, rq, d, h * dk);
   __syncthreads();  // D below reads rows other warps loaded
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int i = w; i < n; i += nw) {
+  for (int i = w; i < nq; i += nw) {
     float acc = 0.f;
-    for (int c = lane; c < dk; c += 32)
-      acc += G[i * ldh + c] * tof(o[(int64_t)(row0 + i) * d + h * dk + c]);
+    for (int c = lane; c < dk; c += 32) acc += G[i * ldh + c] * tof(o[(int64_t)(rq + i) * d + h * dk + c]);
     acc = warp_sum(acc);
     if (lane == 0) D[i] = acc;
   }
   __syncthreads();
   const float scale = 1.f / sqrtf((float)dk);
-  // P = exp(S*scale - lse)
-  smem_mm(n, n, dk, SMat{Q, ldh, 1}, SMat{K, 1, ldh}, [&](int i, int j, float v) {
-    S[i * lds + j] = expf(v * scale - lse[(int64_t)h * T_total + row0 + i]);
+  const int causal = a.causal;
+  // P = exp(S*scale - lse); masked keys 0
+  smem_mm(nq, nk, dk, SMat{Q, ldh, 1}, SMat{K, 1, ldh}, [&](int i, int j, float v) {
+    S[i * lds + j] = (causal && j > i) ? 0.f : expf(v * scale - a.lse[(int64_t)h * a.T_q + rq + i]);
   });
   __syncthreads();
   // dV = P^T dO
-  smem_mm(n, dk, n, SMat{S, 1, lds}, SMat{G, ldh, 1}, [&](int j, int c, float v) {
-    dqkv[(int64_t)(row0 + j) * ldq + 2 * d + h * dk + c] = fromf<T>(v);
+  T* dv = (T*)a.dv;
+  smem_mm(nk, dk, nq, SMat{S, 1, lds}, SMat{G, ldh, 1}, [&](int j, int c, float v) {
+    dv[(int64_t)(rk + j) * a.lddv + a.dvcol + h * dk + c] = fromf<T>(v);
   });
   __syncthreads();
   // dS = P * (dO V^T - D)   (tape.hpp:274-286), in place
-  smem_mm(n, n, dk, SMat{G, ldh, 1}, SMat{V, 1, ldh}, [&](int i, int j, float v) {
+  smem_mm(nq, nk, dk, SMat{G, ldh, 1}, SMat{V, 1, ldh}, [&](int i, int j, float v) {
     float* p = S + i * lds + j;
     *p = *p * (v - D[i]) * scale;
   });
   __syncthreads();
   // dQ = dS K ; dK = dS^T Q
-  smem_mm(n, dk, n, SMat{S, lds, 1}, SMat{K, ldh, 1}, [&](int i, int c, float v) {
-    dqkv[(int64_t)(row0 + i) * ldq + h * dk + c] = fromf<T>(v);
+  T* dq = (T*)a.dq;
+  T* dkk = (T*)a.dk_;
+  smem_mm(nq, dk, nk, SMat{S, lds, 1}, SMat{K, ldh, 1}, [&](int i, int c, float v) {
+    dq[(int64_t)(rq + i) * a.lddq + a.dqcol + h * dk + c] = fromf<T>(v);
   });
-  smem_mm(n, dk, n, SMat{S, 1, lds}, SMat{Q, ldh, 1}, [&](int j, int c, float v) {
-    dqkv[(int64_t)(row0 + j) * ldq + d + h * dk + c] = fromf<T>(v);
+  smem_mm(nk, dk, nq, SMat{S, 1, lds}, SMat{Q, ldh, 1}, [&](int j, int c, float v) {
+    dkk[(int64_t)(rk + j) * a.lddk + a.dkcol + h * dk + c] = fromf<T>(v);
   });
 }
 
-static size_t attn_smem(int n4, int dk, bool bwd) {
-  const int ldh = dk + 1, lds = n4 + 1;
-  return sizeof(float) * ((size_t)(bwd ? 4 : 3) * n4 * ldh + (size_t)n4 * lds + (bwd ? n4 : 0));
+static size_t attn_smem(int nq4, int nk4, int dk, bool bwd) {
+  const int ldh = dk + 1, lds = nk4 + 1;
+  return sizeof(float) * ((size_t)(bwd ? 2 : 1) * nq4 * ldh + 2 * (size_t)nk4 * ldh +
+                          (size_t)nq4 * lds + (bwd ? nq4 : 0));
 }
 
 static constexpr int kAttnMaxSeq = 128;
 
-void attention_fwd(const DevBatch& b, int H, int dk, const void* qkv, void* o,
-                   float* lse, DType t, cudaStream_t s) {
-  if (b.B == 0) return;
-  const size_t sm = attn_smem(kAttnMaxSeq, dk, false);
+static void attn_check(const AttnArgs& a) {
+  if (a.max_q > kAttnMaxSeq || a.max_kv > kAttnMaxSeq)
+    fail(HP_ECONFIG, "attention: sequences longer than 128 need the bf16 blocked kernels");
+}
+
+void attention_simt_fwd(const AttnArgs& a, DType t, cudaStream_t s) {
+  if (a.B == 0) return;
+  attn_check(a);
+  const size_t sm = attn_smem(kAttnMaxSeq, kAttnMaxSeq, a.dk, false);
   DISPATCH1(t, X, {
-    HP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_fwd_kernel<X><<<dim3(b.B, H), 256, sm, s>>>(b.cu, H, dk, (const X*)qkv, (X*)o, lse, b.T);
+    static size_t set = 0;
+    if (set < sm) {
+      HP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      set = sm;
+    }
+    attn_fwd_kernel<X><<<dim3(a.B, a.H), 256, sm, s>>>(a);
   });
   LAUNCH_CHECK();
   count_launch();
+}
+
+void attention_simt_bwd(const AttnArgs& a, DType t, cudaStream_t s) {
+  if (a.B == 0) return;
+  attn_check(a);
+  const size_t sm = attn_smem(kAttnMaxSeq, kAttnMaxSeq, a.dk, true);
+  DISPATCH1(t, X, {
+    static size_t set = 0;
+    if (set < sm) {
+      HP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      set = sm;
+    }
+    attn_bwd_kernel<X><<<dim3(a.B, a.H), 256, sm, s>>>(a);
+  });
+  LAUNCH_CHECK();
+  count_launch();
+}
+
+AttnArgs self_attn_args(const DevBatch& b, int H, int dk, int max_seq, const void* qkv, void* o,
+                        float* lse, const void* dO, void* dqkv, int causal) {
+  AttnArgs a;
+  const int d = H * dk;
+  a.B = b.B; a.H = H; a.dk = dk;
+  a.cu_q = a.cu_kv = b.cu;
+  a.T_q = a.T_kv = b.T;
+  a.max_q = a.max_kv = max_seq;
+  a.q = a.k = a.v = qkv;
+  a.ldq = a.ldk = a.ldv = 3 * (int64_t)d;
+  a.qcol = 0; a.kcol = d; a.vcol = 2 * d;
+  a.o = o; a.lse = lse; a.causal = causal;
+  a.dO = dO;
+  a.dq = a.dk_ = a.dv = dqkv;
+  a.lddq = a.lddk = a.lddv = 3 * (int64_t)d;
+  a.dqcol = 0; a.dkcol = d; a.dvcol = 2 * d;
+  return a;
+}
+
+void attention_fwd(const DevBatch& b, int H, int dk, const void* qkv, void* o,
+                   float* lse, DType t, cudaStream_t s) {
+  attention_simt_fwd(self_attn_args(b, H, dk, kAttnMaxSeq, qkv, o, lse), t, s);
 }
 
 void attention_bwd(const DevBatch& b, int H, int dk, const void* qkv,
                    const void* o, const void* dO, const float* lse, void* dqkv,
                    DType t, cudaStream_t s) {
-  if (b.B == 0) return;
-  const size_t sm = attn_smem(kAttnMaxSeq, dk, true);
-  DISPATCH1(t, X, {
-    HP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attn_bwd_kernel<X><<<dim3(b.B, H), 256, sm, s>>>(b.cu, H, dk, (const X*)qkv, (const X*)o,
-                                                    (const X*)dO, lse, (X*)dqkv, b.T);
-  });
-  LAUNCH_CHECK();
-  count_launch();
+  attention_simt_bwd(self_attn_args(b, H, dk, kAttnMaxSeq, qkv, const_cast<void*>(o),
+                                    const_cast<float*>(lse), dO, dqkv), t, s);
+}
+
+bool attention2_tc_ok(const AttnArgs& a, DType t) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return t == DType::bf16 && a.dk == 64 && a.max_q <= 128 && a.max_kv <= 128 &&
+         al16(a.q) && al16(a.k) && al16(a.v) && a.ldq % 8 == 0 && a.ldk % 8 == 0 &&
+         a.ldv % 8 == 0 && a.qcol % 8 == 0 && a.kcol % 8 == 0 && a.vcol % 8 == 0;
+}
+
+void attention2_fwd(const AttnArgs& a, DType t, cudaStream_t s) {
+  if (attention2_tc_ok(a, t))
+    attention_tc_fwd(a, s);
+  else
+    attention_simt_fwd(a, t, s);
+}
+
+void attention2_bwd(const AttnArgs& a, DType t, cudaStream_t s) {
+  if (attention2_tc_ok(a, t))
+    attention_tc_bwd(a, s);
+  else
+    attention_simt_bwd(a, t, s);
 }
 
 // ------------------------------------------------------------------ rows

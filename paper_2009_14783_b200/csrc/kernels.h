@@ -87,12 +87,16 @@ void embed_fwd(const DevBatch& b, int d, const void* E, const void* seg0,
 // Row-sparse form of the word-embedding gradient for the N > 1 exchange:
 // slot u of `rows` (stride d + 4 floats) = [distinct token id u as int bits,
 // 3 pad, its d gradient values]; slots [U, cap) carry id -1.  Segment
-// gradients as embed_bwd.
+// gradients as embed_bwd (skipped when dseg0 is null).
 void embed_bwd_rows(const DevBatch& b, int d, const void* dx, DType xt, float* rows, int cap,
                     float* dseg0, float* dseg1, float* scratch, cudaStream_t s);
-// dE[id] += row for every slot of one rank's gathered row set (ids are
-// distinct within a set; call once per rank, in rank order)
-void embed_rows_scatter(const float* rows, int cap, int d, float* dE, cudaStream_t s);
+// dE[id] += scale * row for every slot of one rank's gathered row set (ids
+// are distinct within a set; call once per rank, in rank order)
+void embed_rows_scatter(const float* rows, int cap, int d, float* dE, cudaStream_t s,
+                        float scale = 1.f);
+// seq2seq: x[t] = scale * E[tok[t]] + PE[pos[t]]
+void embed_scaled_fwd(int T, int d, const int* tok, const int* pos, const void* E, DType wt,
+                      float scale, const float* pe, void* x, DType xt, cudaStream_t s);
 // dE[id] = sum of dx over the tokens with that id (dE zeroed by the caller;
 // deterministic, position order), dseg{0,1} = column sums over the segment's tokens.
 void embed_bwd(const DevBatch& b, int d, const void* dx, DType xt, float* dE,
@@ -125,6 +129,43 @@ void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
                    cudaStream_t s, DeferredFinal* df = nullptr);
 // scratch floats the column-sum kernels need for an R x N reduction
 size_t colsum_scratch_floats(int R, int N);
+
+// Varlen multi-head attention, self or cross, optionally causal (the
+// seq2seq decoder): instance b's queries are rows [cu_q[b], cu_q[b+1]) of Q,
+// its keys / values rows [cu_kv[b], cu_kv[b+1]) of K / V; head h reads the dk
+// columns starting at col + h * dk of each operand (row pitch ld).  O is
+// [T_q x H dk] (row pitch H dk, head h at columns h dk), lse [H x T_q].  The
+// backward writes dQ / dK / dV with their own pitches and column offsets.
+// causal: query i sees keys j <= i (positions within the instance).
+struct AttnArgs {
+  int B = 0, H = 0, dk = 0;
+  const int* cu_q = nullptr;
+  const int* cu_kv = nullptr;
+  int T_q = 0, T_kv = 0;
+  int max_q = 0, max_kv = 0;  // longest instance on each side
+  const void* q = nullptr; int64_t ldq = 0; int qcol = 0;
+  const void* k = nullptr; int64_t ldk = 0; int kcol = 0;
+  const void* v = nullptr; int64_t ldv = 0; int vcol = 0;
+  void* o = nullptr;
+  float* lse = nullptr;
+  int causal = 0;
+  const void* dO = nullptr;  // backward
+  void* dq = nullptr; int64_t lddq = 0; int dqcol = 0;
+  void* dk_ = nullptr; int64_t lddk = 0; int dkcol = 0;
+  void* dv = nullptr; int64_t lddv = 0; int dvcol = 0;
+};
+// self-attention over packed QKV [T x 3d] (q heads | k heads | v heads)
+AttnArgs self_attn_args(const DevBatch& b, int H, int dk, int max_seq, const void* qkv, void* o,
+                        float* lse, const void* dO = nullptr, void* dqkv = nullptr, int causal = 0);
+// dispatch: tcgen05 kernels for bf16, dk = 64, both sides <= 128 tokens;
+// the SIMT kernels otherwise (fp32 parity path)
+void attention2_fwd(const AttnArgs& a, DType t, cudaStream_t s);
+void attention2_bwd(const AttnArgs& a, DType t, cudaStream_t s);
+bool attention2_tc_ok(const AttnArgs& a, DType t);
+void attention_simt_fwd(const AttnArgs& a, DType t, cudaStream_t s);
+void attention_simt_bwd(const AttnArgs& a, DType t, cudaStream_t s);
+void attention_tc_fwd(const AttnArgs& a, cudaStream_t s);
+void attention_tc_bwd(const AttnArgs& a, cudaStream_t s);
 
 // Varlen multi-head self-attention over packed QKV [T x 3d] (columns:
 // q heads | k heads | v heads, dk each).  O [T x d], lse [H x T].

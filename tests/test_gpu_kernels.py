@@ -477,3 +477,79 @@ def test_layernorm_fwd_bwd_vs_torch(d, dtype, T):
         assert rel(db, br.grad) < tol
         # colsum of the dx the kernel wrote (what the next kernel reads)
         assert rel(dbias, dx.float().sum(0)) < 1e-4 + (1e-3 if T > 1 else 0)
+
+
+def _attn2_ref(q, k, v, cu_q, cu_kv, H, dk, causal, dO):
+    """torch fp32 autograd reference: per instance and head softmax(q k^T /
+    sqrt(dk)) v over the instance's keys, causal mask j <= i."""
+    q = q.float().detach().requires_grad_(True)
+    k = k.float().detach().requires_grad_(True)
+    v = v.float().detach().requires_grad_(True)
+    outs = []
+    for b in range(len(cu_q) - 1):
+        a, e = cu_q[b], cu_q[b + 1]
+        c, f = cu_kv[b], cu_kv[b + 1]
+        qq = q[a:e].reshape(e - a, H, dk)
+        kk = k[c:f].reshape(f - c, H, dk)
+        vv = v[c:f].reshape(f - c, H, dk)
+        s = torch.einsum("qhd,khd->hqk", qq, kk) / dk ** 0.5
+        if causal:
+            s = s.masked_fill(torch.ones(e - a, f - c, device=s.device).triu(1).bool(), float("-inf"))
+        outs.append(torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), vv).reshape(e - a, H * dk))
+    o = torch.cat(outs)
+    o.backward(dO.float())
+    return o.detach(), q.grad, k.grad, v.grad
+
+
+@pytest.mark.parametrize("path,dtype", [(3, torch.bfloat16), (1, torch.float32), (1, torch.bfloat16)])
+@pytest.mark.parametrize("mode", ["cross", "causal"])
+def test_attention_cross_and_causal(path, dtype, mode):
+    """Generalised attention (AttnArgs): cross-attention with queries from one
+    tensor and keys / values from another, different lengths per side (the
+    seq2seq decoder's encoder-decoder attention), and causal self-attention
+    over packed QKV (the decoder's self-attention), against torch fp32."""
+    L = _lib()
+    H, dk = 3, 64
+    g = torch.Generator(device="cpu").manual_seed(7)
+    if mode == "cross":
+        lq, lk = [64, 1, 17, 128, 40], [64, 90, 3, 128, 7]
+    else:
+        lq = lk = [64, 1, 17, 128, 100]
+    cq = np.concatenate([[0], np.cumsum(lq)]).astype(np.int32)
+    ck = np.concatenate([[0], np.cumsum(lk)]).astype(np.int32)
+    Tq, Tk, d = int(cq[-1]), int(ck[-1]), H * dk
+    if mode == "cross":
+        qb = (torch.randn(Tq, d, generator=g) * 1.5).to("cuda", dtype)
+        kvb = (torch.randn(Tk, 2 * d, generator=g) * 1.5).to("cuda", dtype)
+        q, ldq, qcol = qb, d, 0
+        k, ldk, kcol = kvb, 2 * d, 0
+        v, ldv, vcol = kvb, 2 * d, d
+        q_l, k_l, v_l = qb, kvb[:, :d], kvb[:, d:]
+        dq = torch.zeros_like(qb)
+        dkv = torch.zeros_like(kvb)
+        outs = (dq, d, 0, dkv, 2 * d, 0, dkv, 2 * d, d)
+    else:
+        qkv = (torch.randn(Tq, 3 * d, generator=g) * 1.5).to("cuda", dtype)
+        q = k = v = qkv
+        ldq = ldk = ldv = 3 * d
+        qcol, kcol, vcol = 0, d, 2 * d
+        q_l, k_l, v_l = qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:]
+        dqkv = torch.zeros_like(qkv)
+        outs = (dqkv, 3 * d, 0, dqkv, 3 * d, d, dqkv, 3 * d, 2 * d)
+    dO = torch.randn(Tq, d, generator=g).to("cuda", dtype)
+    o = torch.zeros(Tq, d, device="cuda", dtype=dtype)
+    lse = torch.zeros(H, Tq, device="cuda")
+    dcq, dck = torch.from_numpy(cq).cuda(), torch.from_numpy(ck).cuda()
+    L.call("hp_debug_attention2", len(lq), _ptr(dcq), _ptr(dck), Tq, Tk, max(lq), max(lk), H, dk,
+           int(dtype == torch.bfloat16), _ptr(q), ldq, qcol, _ptr(k), ldk, kcol, _ptr(v), ldv, vcol,
+           _ptr(o), _ptr(lse), _ptr(dO), _ptr(outs[0]), outs[1], outs[2], _ptr(outs[3]), outs[4],
+           outs[5], _ptr(outs[6]), outs[7], outs[8], int(mode == "causal"), path)
+    ref, gq, gk, gv = _attn2_ref(q_l, k_l, v_l, cq.tolist(), ck.tolist(), H, dk, mode == "causal", dO)
+    if mode == "cross":
+        got_q, got_k, got_v = dq, dkv[:, :d], dkv[:, d:]
+    else:
+        got_q, got_k, got_v = dqkv[:, :d], dqkv[:, d:2 * d], dqkv[:, 2 * d:]
+    tol = 3e-2 if dtype == torch.bfloat16 else 1e-4
+    for got, want in ((o, ref), (got_q, gq), (got_k, gk), (got_v, gv)):
+        err = (got.float() - want).abs().max().item() / want.abs().max().item()
+        assert err < tol, (mode, err)
