@@ -190,13 +190,15 @@ hp_status hp_comm_allreduce_bench(hp_comm* c, uint64_t bytes, double bucket_mb, 
  * ---------------------------------------------------------------------- */
 typedef struct hp_engine hp_engine;
 
-enum { HP_OPT_SGD = 0, HP_OPT_ADAM = 1 };           /* OptKind, optim.hpp:77 */
+enum { HP_OPT_SGD = 0, HP_OPT_ADAM = 1,            /* OptKind, optim.hpp:77 */
+       HP_OPT_ADAMW = 2 };  /* extension: Adam + decoupled weight decay (p -= lr wd p, then Adam) */
 enum { HP_POLICY_SENTENCES = 1, HP_POLICY_TOKENS = 2 }; /* WeightPolicy */
 enum { HP_COMPUTE_F32 = 0, HP_COMPUTE_BF16 = 1 };
 
 typedef struct {
   int kind;
   double beta1, beta2, eps;
+  double weight_decay; /* HP_OPT_ADAMW only */
 } hp_optim_desc;
 
 typedef struct {
@@ -293,6 +295,7 @@ typedef struct {
   int opt_kind;                /* HP_OPT_* */
   double beta1, beta2, eps;
   uint64_t opt_t;              /* Adam step counter */
+  double weight_decay;         /* HP_OPT_ADAMW (spec key "weight_decay") */
 } hp_ckpt_desc;
 /* Host-side writer / reader of one f32 checkpoint; params, m, v are flat
  * canonical vectors (m, v read/written only for Adam).  hp_checkpoint_read
@@ -471,10 +474,11 @@ hp_status hp_debug_attention2(int B, const int* cu_q, const int* cu_kv, int T_q,
                               int64_t lddk, int dkcol, void* dv, int64_t lddv, int dvcol,
                               int causal, int path);
 /* One Adam (sgd=0) or SGD (sgd=1) update of the device kernel on caller-owned
- * device fp32 buffers, no scaling: compare with kern::adam_update<float>. */
+ * device fp32 buffers, no scaling: compare with kern::adam_update<float>;
+ * wd != 0: AdamW (p -= (lr wd) p before the Adam step, fp32, RN). */
 hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n,
                         float lr, float b1, float b2, float eps, float c1, float c2,
-                        int sgd);
+                        int sgd, float wd);
 
 #ifdef __cplusplus
 }

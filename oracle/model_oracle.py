@@ -556,9 +556,10 @@ class AdamState:
     v: np.ndarray | None = None
 
 
-def adam_step(params, grad, st: AdamState, lr, dtype=np.float64):
+def adam_step(params, grad, st: AdamState, lr, dtype=np.float64, weight_decay=0.0):
     """optim.hpp:107-146 -> kern::adam_update (kernels_scalar.cpp:74-83):
-    c1, c2 in double, then everything cast to the parameter dtype."""
+    c1, c2 in double, then everything cast to the parameter dtype.
+    weight_decay != 0: the AdamW extension, p -= (lr wd) p (in dtype) first."""
     st.t += 1
     c1 = 1.0 / (1.0 - st.beta1 ** st.t)
     c2 = 1.0 / (1.0 - st.beta2 ** st.t)
@@ -568,6 +569,8 @@ def adam_step(params, grad, st: AdamState, lr, dtype=np.float64):
         st.v = np.zeros(params.size, dtype=T)
     g = grad.astype(T)
     b1, b2, e, lr_, c1_, c2_ = (T(st.beta1), T(st.beta2), T(st.eps), T(lr), T(c1), T(c2))
+    if weight_decay:
+        params = params - (lr_ * T(weight_decay)) * params
     st.m = b1 * st.m + (T(1) - b1) * g
     st.v = b2 * st.v + (T(1) - b2) * (g * g)
     mh = st.m * c1_

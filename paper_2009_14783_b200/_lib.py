@@ -18,7 +18,7 @@ HP_OK, HP_ESHAPE, HP_ECONFIG, HP_EINDEX, HP_EIO, HP_ECOMM, HP_ENUMERIC, HP_ECUDA
 HP_ARCH_MASKED_TOKEN_MODEL = 3
 HP_ARCH_BERT_ENCODER = 16
 HP_ARCH_SEQ2SEQ = 17
-HP_OPT_SGD, HP_OPT_ADAM = 0, 1
+HP_OPT_SGD, HP_OPT_ADAM, HP_OPT_ADAMW = 0, 1, 2
 HP_POLICY_SENTENCES, HP_POLICY_TOKENS = 1, 2
 HP_COMPUTE_F32, HP_COMPUTE_BF16 = 0, 1
 
@@ -81,7 +81,7 @@ class ModelDesc(C.Structure):
 
 class OptimDesc(C.Structure):
     _fields_ = [("kind", C.c_int), ("beta1", C.c_double), ("beta2", C.c_double),
-                ("eps", C.c_double)]
+                ("eps", C.c_double), ("weight_decay", C.c_double)]
 
 
 class ExecDesc(C.Structure):
@@ -106,7 +106,7 @@ class CkptDesc(C.Structure):
                 ("sched_kind", C.c_int), ("peak_lr", C.c_double), ("sched_d_model", C.c_uint64),
                 ("warmup_steps", C.c_uint64), ("total_steps", C.c_uint64), ("opt_kind", C.c_int),
                 ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
-                ("opt_t", C.c_uint64)]
+                ("opt_t", C.c_uint64), ("weight_decay", C.c_double)]
 
 
 class RoundOut(C.Structure):
@@ -215,7 +215,7 @@ _SIGS = {
     "hp_debug_attention2": [I, P, P, I, I, I, I, I, I, I, P, I64, I, P, I64, I, P, I64, I, P, P,
                             P, P, I64, I, P, I64, I, P, I64, I, I, I],
     "hp_debug_adam": [P, P, P, P, U64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float,
-                      C.c_float, I],
+                      C.c_float, I, C.c_float],
 }
 
 EXPORTED = sorted(_SIGS) + ["hp_last_error", "hp_version"]

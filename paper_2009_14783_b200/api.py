@@ -392,16 +392,17 @@ def scheduled_lr(c: SchedulerConfig, step: int) -> float:
 # --------------------------------------------------------------------- engine
 @dataclass
 class OptimConfig:
-    kind: str = "adam"  # adam | sgd  (OptKind, optim.hpp:77)
+    kind: str = "adam"  # adam | sgd (OptKind, optim.hpp:77) | adamw (extension)
     beta1: float = 0.9
     beta2: float = 0.98
     eps: float = 1e-9
+    weight_decay: float = 0.0  # adamw: p -= lr * wd * p before the Adam step
 
     def desc(self) -> _lib.OptimDesc:
-        k = {"adam": _lib.HP_OPT_ADAM, "sgd": _lib.HP_OPT_SGD}.get(self.kind)
+        k = {"adam": _lib.HP_OPT_ADAM, "sgd": _lib.HP_OPT_SGD, "adamw": _lib.HP_OPT_ADAMW}.get(self.kind)
         if k is None:
             raise ConfigError(f"config: unknown optimizer {self.kind}")
-        return _lib.OptimDesc(k, self.beta1, self.beta2, self.eps)
+        return _lib.OptimDesc(k, self.beta1, self.beta2, self.eps, self.weight_decay)
 
 
 @dataclass
@@ -553,6 +554,10 @@ class ShardDataset:
             pass
 
 
+_OPT = {"sgd": _lib.HP_OPT_SGD, "adam": _lib.HP_OPT_ADAM, "adamw": _lib.HP_OPT_ADAMW}
+_OPT_NAME = {v: k for k, v in _OPT.items()}
+
+
 @dataclass
 class CheckpointMeta:
     """TrainState fields an HCK1 file carries besides the tensors
@@ -570,14 +575,15 @@ class CheckpointMeta:
     beta2: float = 0.98
     eps: float = 1e-9
     opt_t: int = 0
+    weight_decay: float = 0.0
 
     def desc(self) -> _lib.CkptDesc:
         sk = {"fixed": 0, "inverse_sqrt": 1, "linear": 2}[self.scheduler.kind]
         return _lib.CkptDesc(self.epoch, self.step, self.seed, _POLICY[self.policy],
                              self.world_size, self.update_freq, sk, self.scheduler.peak_lr,
                              self.scheduler.d_model, self.scheduler.warmup_steps,
-                             self.scheduler.total_steps, 1 if self.optimizer == "adam" else 0,
-                             self.beta1, self.beta2, self.eps, self.opt_t)
+                             self.scheduler.total_steps, _OPT[self.optimizer],
+                             self.beta1, self.beta2, self.eps, self.opt_t, self.weight_decay)
 
     @staticmethod
     def from_desc(d: _lib.CkptDesc) -> "CheckpointMeta":
@@ -586,7 +592,7 @@ class CheckpointMeta:
                                 warmup_steps=d.warmup_steps, total_steps=d.total_steps)
         return CheckpointMeta(d.epoch, d.step, d.seed, "tokens" if d.policy == 2 else "sentences",
                               d.world_size, d.update_freq, sched,
-                              "adam" if d.opt_kind == 1 else "sgd", d.beta1, d.beta2, d.eps, d.opt_t)
+                              _OPT_NAME[d.opt_kind], d.beta1, d.beta2, d.eps, d.opt_t, d.weight_decay)
 
 
 _ARCH_NAME = {v: k for k, v in _ARCH.items()}
@@ -616,7 +622,7 @@ def read_checkpoint(path: str):
     p, m, v = (np.empty(n, np.float32) for _ in range(3))
     call("hp_checkpoint_read", path.encode(), None, None, _p(p), _p(m), _p(v), n)
     meta = CheckpointMeta.from_desc(cd)
-    if meta.optimizer != "adam":
+    if meta.optimizer == "sgd":
         m = v = None
     return spec, meta, p, m, v
 
@@ -785,7 +791,7 @@ class StepEngine:
         cd = _lib.CkptDesc()
         call("hp_engine_load_checkpoint", self._h, path.encode(), C.byref(cd))
         meta = CheckpointMeta.from_desc(cd)
-        self.optim = OptimConfig(meta.optimizer, meta.beta1, meta.beta2, meta.eps)
+        self.optim = OptimConfig(meta.optimizer, meta.beta1, meta.beta2, meta.eps, meta.weight_decay)
         self.exec.policy = meta.policy
         return meta
 

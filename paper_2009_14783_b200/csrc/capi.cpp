@@ -480,7 +480,7 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
 }
 
 hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n, float lr,
-                        float b1, float b2, float eps, float c1, float c2, int sgd) {
+                        float b1, float b2, float eps, float c1, float c2, int sgd, float wd) {
   HP_API_BEGIN
   unsigned long long* err = nullptr;
   HP_CUDA(cudaMalloc(&err, hp::kErrWords * 8));
@@ -489,7 +489,7 @@ hp_status hp_debug_adam(float* p, float* m, float* v, const float* g, uint64_t n
   hp::AdamArgs a{};
   a.p = p; a.m = m; a.v = v; a.g = g; a.n = n;
   a.lr = lr; a.b1 = b1; a.b2 = b2; a.eps = eps; a.c1 = c1; a.c2 = c2;
-  a.err = err; a.sgd = sgd;
+  a.err = err; a.sgd = sgd; a.wd = wd;
   std::vector<uint64_t> items;
   for (uint64_t o = 0; o < n; o += 65536)
     items.insert(items.end(), {o, std::min<uint64_t>(65536, n - o), o, 1, 1});

@@ -114,7 +114,9 @@ std::string spec_json(const hp_model_desc& m, const hp_ckpt_desc& c) {
   j += ",\"max_seq\":" + std::to_string(m.max_seq);
   j += ",\"optimizer\":{\"beta1\":" + json_number(c.beta1) + ",\"beta2\":" + json_number(c.beta2) +
        ",\"eps\":" + json_number(c.eps) + ",\"kind\":\"" +
-       (c.opt_kind == HP_OPT_ADAM ? "adam" : "sgd") + "\"}";
+       (c.opt_kind == HP_OPT_ADAM ? "adam" : c.opt_kind == HP_OPT_ADAMW ? "adamw" : "sgd") + "\"" +
+       (c.opt_kind == HP_OPT_ADAMW ? ",\"weight_decay\":" + json_number(c.weight_decay) : std::string()) +
+       "}";
   j += ",\"scheduler\":{\"d_model\":" + std::to_string(c.sched_d_model) + ",\"kind\":\"" +
        sched_name(c.sched_kind) + "\",\"peak_lr\":" + json_number(c.peak_lr) +
        ",\"total_steps\":" + std::to_string(c.total_steps) +
@@ -255,9 +257,9 @@ std::vector<uint8_t> hck1_serialize(const hp_model_desc& m, const hp_ckpt_desc& 
   validate_model(m);
   if (c.policy != HP_POLICY_SENTENCES && c.policy != HP_POLICY_TOKENS)
     fail(HP_ECONFIG, "checkpoint: invalid weight policy");
-  if (c.opt_kind != HP_OPT_ADAM && c.opt_kind != HP_OPT_SGD)
+  if (c.opt_kind != HP_OPT_ADAM && c.opt_kind != HP_OPT_SGD && c.opt_kind != HP_OPT_ADAMW)
     fail(HP_ECONFIG, "checkpoint: invalid optimizer kind");
-  if (c.opt_kind == HP_OPT_ADAM && (!adam_m || !adam_v))
+  if (c.opt_kind != HP_OPT_SGD && (!adam_m || !adam_v))
     fail(HP_ECONFIG, "checkpoint: Adam moments missing");
   const auto table = param_table(m);
   std::vector<uint8_t> b;
@@ -281,7 +283,7 @@ std::vector<uint8_t> hck1_serialize(const hp_model_desc& m, const hp_ckpt_desc& 
     put_bytes(b, params + e.offset, e.size() * 4);
   }
   put<uint8_t>(b, static_cast<uint8_t>(c.opt_kind));
-  if (c.opt_kind == HP_OPT_ADAM) {
+  if (c.opt_kind != HP_OPT_SGD) {
     put<uint64_t>(b, c.opt_t);
     for (const auto& e : table) put_bytes(b, adam_m + e.offset, e.size() * 4);
     for (const auto& e : table) put_bytes(b, adam_v + e.offset, e.size() * 4);
@@ -370,11 +372,13 @@ void hck1_parse(const std::vector<uint8_t>& bytes, hp_model_desc* m, hp_ckpt_des
     if (params) std::memcpy(params + e.offset, p, e.size() * 4);
   }
   cd.opt_kind = r.get<uint8_t>();
-  if (cd.opt_kind != HP_OPT_SGD && cd.opt_kind != HP_OPT_ADAM)
+  if (cd.opt_kind != HP_OPT_SGD && cd.opt_kind != HP_OPT_ADAM && cd.opt_kind != HP_OPT_ADAMW)
     fail(HP_EIO, "checkpoint carries invalid optimizer kind");
-  if ((cd.opt_kind == HP_OPT_ADAM) != (fs(oj, "kind") == "adam"))
+  const std::string kname = fs(oj, "kind");
+  if (kname != (cd.opt_kind == HP_OPT_ADAM ? "adam" : cd.opt_kind == HP_OPT_ADAMW ? "adamw" : "sgd"))
     fail(HP_EIO, "optimizer kind disagrees between spec block and blocks");
-  if (cd.opt_kind == HP_OPT_ADAM) {
+  if (cd.opt_kind == HP_OPT_ADAMW) cd.weight_decay = fd(oj, "weight_decay");
+  if (cd.opt_kind != HP_OPT_SGD) {
     cd.opt_t = r.get<uint64_t>();
     for (const auto& e : table) {
       const uint8_t* p = r.raw(e.size() * 4);

@@ -86,7 +86,10 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
       !(x_.compute == HP_COMPUTE_BF16 && m_.heads > 0 && m_.d_model / m_.heads == 64 &&
         m_.max_seq <= 512 && m_.arch != HP_ARCH_SEQ2SEQ))
     fail(HP_ECONFIG, "max_seq > 128 needs the bf16 path with d_model / heads == 64 (max 512)");
-  if (o_.kind != HP_OPT_ADAM && o_.kind != HP_OPT_SGD) fail(HP_ECONFIG, "unknown optimizer kind");
+  if (o_.kind != HP_OPT_ADAM && o_.kind != HP_OPT_SGD && o_.kind != HP_OPT_ADAMW)
+    fail(HP_ECONFIG, "unknown optimizer kind");
+  if (o_.kind == HP_OPT_ADAMW && !(o_.weight_decay >= 0.0))
+    fail(HP_ECONFIG, "AdamW weight_decay must be >= 0");
   if (x_.policy != HP_POLICY_SENTENCES && x_.policy != HP_POLICY_TOKENS)
     fail(HP_ECONFIG, "unknown weight policy");
   if (comm_ && comm_->device != x_.device)
@@ -532,6 +535,7 @@ void Engine::save_checkpoint(const std::string& path, const hp_ckpt_desc& c) {
   d.beta1 = o_.beta1;
   d.beta2 = o_.beta2;
   d.eps = o_.eps;
+  d.weight_decay = o_.kind == HP_OPT_ADAMW ? o_.weight_decay : 0.0;
   d.opt_t = adam_t_;
   write_file_atomic(path, hck1_serialize(m_, d, p.data(), m.data(), v.data()));
 }
@@ -551,7 +555,7 @@ void Engine::load_checkpoint(const std::string& path, hp_ckpt_desc* out) {
       fail(HP_ECONFIG, "resume model spec does not match the checkpoint");
   // the optimizer and the weight policy come from the file, as
   // load_checkpoint's TrainState does (checkpoint.cpp:254, 282-289)
-  if (d.opt_kind != HP_OPT_ADAM && d.opt_kind != HP_OPT_SGD)
+  if (d.opt_kind != HP_OPT_ADAM && d.opt_kind != HP_OPT_SGD && d.opt_kind != HP_OPT_ADAMW)
     fail(HP_EIO, "checkpoint has an unknown optimizer kind");
   if (d.policy != HP_POLICY_SENTENCES && d.policy != HP_POLICY_TOKENS)
     fail(HP_EIO, "checkpoint has an unknown weight policy");
@@ -560,9 +564,10 @@ void Engine::load_checkpoint(const std::string& path, hp_ckpt_desc* out) {
   o_.beta1 = d.beta1;
   o_.beta2 = d.beta2;
   o_.eps = d.eps;
+  o_.weight_decay = d.opt_kind == HP_OPT_ADAMW ? d.weight_decay : 0.0;
   x_.policy = d.policy;
   set_params(p.data(), n_, 0);
-  if (d.opt_kind == HP_OPT_ADAM) {
+  if (d.opt_kind != HP_OPT_SGD) {
     set_adam(m.data(), v.data(), d.opt_t);
   } else {
     HP_CUDA(cudaMemset(adam_m_, 0, n_ * 4));
@@ -1371,6 +1376,7 @@ void Engine::round_async(int dummy, double lr) {
   a.inv_w64 = inv_w64_;  // g = (float)((double)sum * (1 / total weight))
   a.err = err_;
   a.sgd = o_.kind == HP_OPT_SGD;
+  a.wd = o_.kind == HP_OPT_ADAMW ? static_cast<float>(o_.weight_decay) : 0.f;
   a.shadow = shadow_;
   // the first round after a sync starts a fresh error state; later unsynced
   // rounds keep it (sticky), so round_sync reports the first error

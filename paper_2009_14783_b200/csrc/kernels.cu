@@ -1604,6 +1604,8 @@ __device__ __forceinline__ void adam_one(const AdamArgs& a, float& p, float& m, 
     p = __fsub_rn(p, __fmul_rn(a.lr, g));
     return;
   }
+  // AdamW (extension): decoupled decay p -= (lr wd) p before the Adam step
+  if (a.wd != 0.f) p = __fsub_rn(p, __fmul_rn(__fmul_rn(a.lr, a.wd), p));
   // explicit round-to-nearest ops: no FMA contraction, matching the
   // reference's -ffp-contract=off scalar loop bit for bit
   m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(__fsub_rn(1.f, a.b1), g));

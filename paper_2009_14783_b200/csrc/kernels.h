@@ -257,6 +257,7 @@ struct AdamArgs {
   // (optim.hpp:131-133) skips that element and records its flat index
   unsigned long long* err;
   int sgd;
+  float wd;               // AdamW decoupled weight decay (0: Adam)
   void* shadow;
   // work items [nitems][5] = {flat_lo, count, shadow_lo, cols, pcols}; one
   // CTA per item (see Engine: contiguous runs merged, <= 64K elements each)

@@ -35,6 +35,7 @@ class EngineConfig:
     beta1: float = 0.9
     beta2: float = 0.98
     eps: float = 1e-9
+    weight_decay: float = 0.0  # adamw (extension)
     sched: api.SchedulerConfig = field(default_factory=api.SchedulerConfig)
     seed: int = 1
     data_dir: str = ""
@@ -121,11 +122,11 @@ def train_run(cfg: EngineConfig, comm: Optional[api.Communicator] = None,
     # policy, the scheduler and the seed from the checkpoint (TrainState,
     # checkpoint.cpp:254, 282-289), not from cfg
     if state:
-        opt = api.OptimConfig(state.optimizer, state.beta1, state.beta2, state.eps)
+        opt = api.OptimConfig(state.optimizer, state.beta1, state.beta2, state.eps, state.weight_decay)
         policy = state.policy
         ex.policy = policy
     else:
-        opt = api.OptimConfig(cfg.opt_kind, cfg.beta1, cfg.beta2, cfg.eps)
+        opt = api.OptimConfig(cfg.opt_kind, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay)
         policy = cfg.policy
     seed = state.seed if state else cfg.seed
     eng = api.StepEngine(spec, opt, ex, comm=comm, seed=seed)

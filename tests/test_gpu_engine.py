@@ -612,3 +612,37 @@ def test_resume_takes_the_optimizer_from_the_checkpoint(tmp_path):
                                      resume_path=str(ck / "checkpoint_000004.hck")),
                       exec_cfg=hp.ExecConfig(compute="f32"))
     assert [s.loss for s in rb.steps] == [s.loss for s in ra.steps[4:]]
+
+
+def test_adamw_trajectory_and_checkpoint(tmp_path):
+    """AdamW (extension; north_star's "fused multi-tensor Adam/AdamW"): the
+    engine's 3-update fp32 trajectory equals the oracle's (decoupled decay,
+    then the reference's Adam) at the parity tolerance, and the optimizer
+    round-trips through an HCK1 checkpoint (kind "adamw", weight_decay)."""
+    from paper_2009_14783_b200.api import read_checkpoint
+    rec, plan = c1_batches()
+    spec = hp.ModelSpec(**C1_SPEC)
+    opt = hp.OptimConfig("adamw", 0.9, 0.98, 1e-9, weight_decay=0.05)
+    eng = hp.StepEngine(spec, opt, hp.ExecConfig(compute="f32", max_tokens=1024, max_batch=16,
+                                                  max_masks=256), seed=21)
+    s = mo.Spec()
+    p = mo.init_parameters(s, 21).astype(np.float32)
+    st = mo.AdamState()
+    for k in range(3):
+        b = plan.batches[k]
+        rep = eng.round(rec.batch(b), lr=1e-3)
+        l, w, g = mo.forward_backward(s, p.astype(np.float64), oracle_instances(golden("c1_records.npz"), b))
+        p = mo.adam_step(p, g / w, st, 1e-3, np.float32, weight_decay=0.05)
+        assert abs(rep.loss - l / w) <= 1e-4 * abs(l / w)
+    assert rel_norm(eng.get_params(), p) <= 1e-4
+    f = str(tmp_path / "adamw.hck")
+    eng.save_checkpoint(f, hp.api.CheckpointMeta(seed=21))
+    _, meta, pp, mm, vv = read_checkpoint(f)
+    assert meta.optimizer == "adamw" and meta.weight_decay == 0.05 and meta.opt_t == 3
+    e2 = hp.StepEngine(spec, hp.OptimConfig("sgd"), hp.ExecConfig(compute="f32", max_tokens=1024,
+                                                                  max_batch=16, max_masks=256))
+    e2.load_checkpoint(f)
+    assert e2.optim.kind == "adamw" and e2.optim.weight_decay == 0.05
+    b = plan.batches[3]
+    r1, r2 = eng.round(rec.batch(b), lr=1e-3), e2.round(rec.batch(b), lr=1e-3)
+    assert r1.loss == r2.loss and eng.digest() == e2.digest()

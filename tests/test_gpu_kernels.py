@@ -181,7 +181,7 @@ def test_adam_bit_exact_vs_reference_scalar():
         args = (f(1e-3), f(0.9), f(0.98), f(1e-9), f(c1), f(c2))
         orc.orc_adam_update_f32(pp(p), pp(m), pp(v), pp(g), C.c_uint64(n), *args)
         dg = torch.from_numpy(g).cuda()
-        L.call("hp_debug_adam", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(dg), n, *[a.value for a in args], 0)
+        L.call("hp_debug_adam", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(dg), n, *[a.value for a in args], 0, 0.0)
     assert np.array_equal(dp.cpu().numpy().view(np.uint32), p.view(np.uint32))
     assert np.array_equal(dm.cpu().numpy().view(np.uint32), m.view(np.uint32))
     assert np.array_equal(dv.cpu().numpy().view(np.uint32), v.view(np.uint32))
@@ -189,7 +189,7 @@ def test_adam_bit_exact_vs_reference_scalar():
     g = rng.standard_normal(n).astype(np.float32)
     orc.orc_sgd_update_f32(pp(p), pp(g), C.c_uint64(n), f(0.1))
     L.call("hp_debug_adam", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(torch.from_numpy(g).cuda()), n,
-           0.1, 0.9, 0.98, 1e-9, 1.0, 1.0, 1)
+           0.1, 0.9, 0.98, 1e-9, 1.0, 1.0, 1, 0.0)
     assert np.array_equal(dp.cpu().numpy().view(np.uint32), p.view(np.uint32))
 
 
@@ -209,7 +209,7 @@ def test_adam_non_finite_gradient_reported_with_lowest_index():
     dp, dm, dv, dg = (torch.from_numpy(x.copy()).cuda() for x in (p, m, v, g))
     with pytest.raises(L.NumericError, match="flat index 12345"):
         L.call("hp_debug_adam", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(dg), n, 1e-3, 0.9, 0.98, 1e-9,
-               10.0, 50.0, 0)
+               10.0, 50.0, 0, 0.0)
     ok = np.isfinite(g)
     f = C.c_float
     pp = lambda a: C.c_void_p(a.ctypes.data)
@@ -220,6 +220,26 @@ def test_adam_non_finite_gradient_reported_with_lowest_index():
     got = dp.cpu().numpy()
     assert np.array_equal(got[ok].view(np.uint32), p2[ok].view(np.uint32))
     assert np.array_equal(got[~ok].view(np.uint32), p[~ok].view(np.uint32))
+
+
+def test_adamw_bit_exact_vs_f32_restatement():
+    """AdamW (extension): the device update equals the oracle's fp32
+    restatement -- p -= (lr wd) p, then kern::adam_update<float> -- bit for
+    bit over 5 steps."""
+    import model_oracle as mo
+    L = _lib()
+    rng = np.random.default_rng(3)
+    n = 50021
+    p = rng.standard_normal(n).astype(np.float32)
+    dp, dm, dv = (torch.from_numpy(x.copy()).cuda() for x in (p, np.zeros(n, np.float32), np.zeros(n, np.float32)))
+    st = mo.AdamState()
+    for t in range(1, 6):
+        g = (rng.standard_normal(n) * 10.0 ** rng.integers(-6, 1, n)).astype(np.float32)
+        c1, c2 = 1 / (1 - 0.9**t), 1 / (1 - 0.98**t)
+        L.call("hp_debug_adam", _ptr(dp), _ptr(dm), _ptr(dv), _ptr(torch.from_numpy(g).cuda()), n,
+               1e-3, 0.9, 0.98, 1e-9, c1, c2, 0, 0.01)
+        p = mo.adam_step(p, g.astype(np.float64), st, 1e-3, np.float32, weight_decay=0.01)
+    assert np.array_equal(dp.cpu().numpy().view(np.uint32), p.view(np.uint32))
 
 
 def _attn_ref(qkv, cu, H, dk):
