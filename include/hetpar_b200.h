@@ -370,6 +370,10 @@ hp_status hp_engine_timer_read(hp_engine* e, int which, char* name, uint64_t cap
 hp_status hp_engine_class_replay(hp_engine* e, int which, int iters, double* ms, double* flops,
                                  uint64_t* launches);
 hp_status hp_engine_step_count(hp_engine* e, uint64_t* step);
+/* TrainState::step (checkpoint.hpp:27) of a state handed to the engine by a
+ * caller that owns it (the C++ drop-in for StepEngine<T>, reference_dropin.hpp):
+ * P, the completed updates; refused inside a partial update group. */
+hp_status hp_engine_set_step(hp_engine* e, uint64_t step);
 /* StepEngine::pending_rounds (engine.hpp:165): rounds accumulated since the
  * last update (0 .. update_freq - 1). */
 hp_status hp_engine_pending_rounds(hp_engine* e, uint64_t* n);

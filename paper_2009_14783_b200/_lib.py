@@ -176,6 +176,7 @@ _SIGS = {
     "hp_engine_timer_read": [P, I, C.c_char_p, U64, P, P, P, P],
     "hp_engine_class_replay": [P, I, I, P, P, P],
     "hp_engine_step_count": [P, P],
+    "hp_engine_set_step": [P, U64],
     "hp_engine_pending_rounds": [P, P],
     "hp_engine_mark": [P, I],
     "hp_engine_elapsed": [P, I, I, P],

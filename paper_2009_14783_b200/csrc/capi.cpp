@@ -401,6 +401,13 @@ hp_status hp_engine_step_count(hp_engine* e, uint64_t* step) {
   HP_API_END
 }
 
+hp_status hp_engine_set_step(hp_engine* e, uint64_t step) {
+  HP_API_BEGIN
+  ENG(e);
+  E.set_step(step);
+  HP_API_END
+}
+
 hp_status hp_engine_pending_rounds(hp_engine* e, uint64_t* n) {
   HP_API_BEGIN
   ENG(e);

@@ -502,6 +502,11 @@ void Engine::broadcast_params(int root) {
   HP_CUDA(cudaStreamSynchronize(s_main_));
 }
 
+void Engine::set_step(uint64_t s) {
+  if (in_flight_ || acc_count_ != 0) fail(HP_ECONFIG, "set_step inside a round or an update group");
+  step_ = s;
+}
+
 void Engine::get_adam(float* m, float* v, uint64_t* t) {
   HP_CUDA(cudaMemcpyAsync(m, adam_m_, n_ * 4, cudaMemcpyDeviceToHost, s_main_));
   HP_CUDA(cudaMemcpyAsync(v, adam_v_, n_ * 4, cudaMemcpyDeviceToHost, s_main_));

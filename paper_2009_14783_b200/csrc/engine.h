@@ -59,6 +59,7 @@ class Engine {
   void forward_only(double* loss_sum, double* weight);
   uint64_t digest();
   uint64_t step() const { return step_; }
+  void set_step(uint64_t s);
   uint64_t pending_rounds() const { return acc_count_; }
   void timers(bool on);
   void mark(int slot);

@@ -40,3 +40,37 @@ def test_cpp_device_round(tmp_path):
     want = golden("c1_ref_train.npz")["losses_f64"]
     got = np.array(out["losses"])
     assert np.max(np.abs(got - want) / want) <= 1e-4
+
+
+DROPIN = os.path.join(ROOT, "oracle", "_ref", "dropin_demo")
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"), reason="reference headers absent")
+def test_reference_dropin_compiles_against_reference_headers():
+    """include/hetpar_b200/reference_dropin.hpp builds with the reference's own
+    headers and objects (hetpar::TrainState, ProcessGroup, Batch, StepReport)
+    in the reference's round loop (tests/cpp/dropin_demo.cpp)."""
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref", "dropin"], check=True)
+    assert os.path.exists(DROPIN)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(DROPIN), reason="oracle/_ref/dropin_demo not built")
+def test_reference_round_loop_with_the_dropin(tmp_path):
+    """The reference's own round loop (train_run's, engine.hpp:274-310) with
+    hetpar::StepEngine<float> swapped for hetpar::b200::StepEngine<float> (and
+    an NcclProcessGroup over the reference's in-process group): the same
+    10-update trajectory as the reference engine on the CPU, the TrainState
+    kept in step, and the device-backed state through the reference's own
+    save_checkpoint / load_checkpoint."""
+    out = json.loads(subprocess.run([DROPIN, str(tmp_path / "d")], check=True, capture_output=True,
+                                    text=True, timeout=600).stdout.strip().splitlines()[-1])
+    ref, dev = np.array(out["ref_losses"]), np.array(out["dev_losses"])
+    assert len(ref) == len(dev) == 10
+    assert np.max(np.abs(dev - ref) / np.abs(ref)) <= 1e-4
+    assert out["params_rel"] <= 1e-4
+    assert out["ref_step"] == out["dev_step"] == 10 and out["ref_t"] == out["dev_t"] == 10
+    assert out["pending"] == 0 and out["ckpt_rel"] == 0.0 and out["ckpt_step"] == 10
+    # and it is the reference's W = 2 trajectory (W x K equivalence)
+    assert np.max(np.abs(dev - golden("c1_ref_train.npz")["losses_f64"]) /
+                  golden("c1_ref_train.npz")["losses_f64"]) <= 1e-4
