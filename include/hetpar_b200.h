@@ -428,7 +428,8 @@ hp_status hp_kern_adam_update_f64(double* p, double* m, double* v, const double*
 
 /* ------------------------------------------------------------------------
  * Test hooks (used by tests/ only): run one GEMM of the engine's dispatch on
- * caller-owned device buffers.  path: 0 auto, 1 SIMT fp32, 2 tcgen05.
+ * caller-owned device buffers.  path: 0 auto, 1 SIMT fp32, 2 tcgen05, 4 fp32
+ * operands on tcgen05 through the bf16x6 split (kernels.cu).
  * act: 0 none, 1 GELU (pre-activation to aux), 2 dGELU (multiply by
  * GELU'(aux)).  bn = 10000 * s + 1000 * cg + tile: tile width (0 = heuristic,
  * 128, 192 or 256), cg CTA group (0 heuristic, 1 single CTA, 2 CTA pair), s a

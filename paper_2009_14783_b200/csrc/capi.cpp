@@ -480,6 +480,8 @@ hp_status hp_debug_gemm(int M, int N, int K, int ab_bf16, const void* A, int64_t
     hp::gemm_tc_set_bn(0);
     hp::gemm_tc_set_cg(0);
     hp::gemm_tc_set_splits(0);
+  } else if (path == 4) {  // fp32 operands through the bf16x6 tensor-core split
+    if (!hp::gemm_x6(g, g_debug_stream)) fail(HP_ECONFIG, "bf16x6: unsupported operand layout");
   } else {
     hp::gemm(g, g_debug_stream);
   }

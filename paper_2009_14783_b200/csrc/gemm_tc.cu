@@ -126,6 +126,17 @@ __device__ __forceinline__ float dgelu_fast(float x) {
   return fmaf(hx * fmaf(-t, t, 1.f), du, fmaf(0.5f, t, 0.5f));
 }
 
+// fp32 outputs (the fp32 parity path's GEMMs, bf16x6 operands) keep the
+// exact erf form, as the oracle and the SIMT kernels do
+__device__ __forceinline__ float gelu_exact(float x) {
+  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float dgelu_exact(float x) {
+  return 0.5f * (1.f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * expf(-0.5f * x * x);
+}
+__device__ __forceinline__ float gelu_by(bool exact, float x) { return exact ? gelu_exact(x) : gelu_fast(x); }
+__device__ __forceinline__ float dgelu_by(bool exact, float x) { return exact ? dgelu_exact(x) : dgelu_fast(x); }
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -203,13 +214,13 @@ __device__ __forceinline__ void epilogue_cols(const Params& p, int m, int n, flo
       }
     }
 #pragma unroll
-    for (int i = 0; i < NC; ++i) v[i] = gelu_fast(v[i]);
+    for (int i = 0; i < NC; ++i) v[i] = gelu_by(p.c_f32, v[i]);
   } else if (p.act == ACT_DGELU) {
     if (p.c_f32) {
       const float* a = static_cast<const float*>(p.aux) + co;
 #pragma unroll
       for (int i = 0; i < NC; ++i)
-        if (n + i < p.N) v[i] *= dgelu_fast(a[i]);
+        if (n + i < p.N) v[i] *= dgelu_exact(a[i]);
     } else {
       const __nv_bfloat16* a = static_cast<const __nv_bfloat16*>(p.aux) + co;
       if (full) {
@@ -519,7 +530,7 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, in
     // pre-activation to aux (same type and layout as C)
     staged_out(f32, st, lane, v, static_cast<char*>(p.aux) + co0 * cs, p.ldc * cs, rows_left, 0);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = gelu_fast(v[i]);
+    for (int i = 0; i < 32; ++i) v[i] = gelu_by(EK == EK_GENERIC && p.c_f32, v[i]);
   } else if (EK == EK_DGELU || (EK == EK_GENERIC && p.act == ACT_DGELU)) {
     if (EK == EK_DGELU || pre_kind == 1) {
 #pragma unroll
@@ -533,7 +544,7 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, in
       float a[32];
       staged_in(f32, st, lane, a, static_cast<const char*>(p.aux) + co0 * cs, p.ldc * cs, rows_left);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(a[i]);
+      for (int i = 0; i < 32; ++i) v[i] *= dgelu_by(p.c_f32, a[i]);
     }
   }
   if constexpr (EK == EK_BF16 || EK == EK_GENERIC) {

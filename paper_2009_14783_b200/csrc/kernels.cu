@@ -15,6 +15,11 @@
 #include <cfloat>
 #include <cmath>
 #include <type_traits>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+#include <cstdlib>
 
 #include "hp_common.h"
 #include "kernels.h"
@@ -2028,16 +2033,115 @@ void gemm_simt(const GemmArgs& g, cudaStream_t s) {
   count_launch();
 }
 
+// ---- fp32-accurate GEMMs on the bf16 tensor cores ("bf16x6") -------------
+// Every fp32 operand element splits exactly into three bf16 terms,
+// x = x0 + x1 + x2 (x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1),
+// 24 significant bits), and
+//   a b ~= a0 b0 + a0 b1 + a1 b0 + a0 b2 + a2 b0 + a1 b1
+// (the dropped terms a1 b2, a2 b1, a2 b2 are O(2^-24) of |a||b|, below fp32
+// rounding) -- i.e. ONE bf16 GEMM with fp32 accumulation over K' = 6K of
+//   A' = [a0 | a0 | a1 | a0 | a2 | a1],  B' = [b0 ; b1 ; b0 ; b2 ; b0 ; b1]
+// on the same tcgen05 kernel (and epilogues) as the bf16 path.  The split
+// kernel writes A' / B' dense in the operand's own major-ness (grouped per-head
+// operands are ungrouped on the way); six bf16 UMMAs per product cost what
+// three TF32 ones would (TF32 runs at half the bf16 rate).
+__constant__ int kX6PatA[6] = {0, 0, 1, 0, 2, 1};
+__constant__ int kX6PatB[6] = {0, 1, 0, 2, 0, 1};
+
+// logical A (m, k) / B (k, n): r = m or n, K the contracted extent
+__global__ void split6_kernel(Operand src, int is_b, int R, int K, bf16* __restrict__ dst, int64_t ldd) {
+  const float* x = static_cast<const float*>(src.p);
+  // walk the source's contiguous dimension fastest
+  const bool kfast = is_b ? src.trans != 0 : src.trans == 0;
+  const int64_t total = (int64_t)R * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = kfast ? e / K : e % R, k = kfast ? e % K : e / R;
+    const float v = x[is_b ? b_off(src, k, r) : a_off(src, r, k)];
+    bf16 part[3];
+    part[0] = __float2bfloat16_rn(v);
+    const float r1 = v - __bfloat162float(part[0]);
+    part[1] = __float2bfloat16_rn(r1);
+    part[2] = __float2bfloat16_rn(r1 - __bfloat162float(part[1]));
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      const int64_t kk = (int64_t)j * K + k;
+      // A: trans -> [K'][M] else [M][K'];  B: trans -> [N][K'] else [K'][N]
+      const int64_t o = is_b ? (src.trans ? r * ldd + kk : kk * ldd + r)
+                             : (src.trans ? kk * ldd + r : r * ldd + kk);
+      dst[o] = part[is_b ? kX6PatB[j] : kX6PatA[j]];
+    }
+  }
+}
+
 namespace {
 int g_tc_mode = 0;
+// per-stream split buffers, grown on demand; superseded buffers stay alive
+// (CUDA graphs captured with them keep their addresses)
+struct X6Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+std::mutex g_x6_mu;
+std::map<std::pair<cudaStream_t, int>, X6Buf> g_x6;
+std::vector<void*> g_x6_old;
+void* x6_buffer(cudaStream_t s, int which, size_t bytes) {
+  std::lock_guard<std::mutex> l(g_x6_mu);
+  X6Buf& b = g_x6[{s, which}];
+  if (b.cap < bytes) {
+    if (b.p) g_x6_old.push_back(b.p);
+    const size_t cap = std::max(bytes, b.cap * 3 / 2);
+    HP_CUDA(cudaMalloc(&b.p, cap));
+    b.cap = cap;
+  }
+  return b.p;
 }
+int64_t pad8i(int64_t v) { return (v + 7) & ~int64_t(7); }
+bool f32_x6() {
+  static const bool on = [] {
+    const char* e = std::getenv("HP_F32_GEMM");  // "simt": the fp32 SIMT kernel (A/B, parity checks)
+    return !(e && std::string(e) == "simt");
+  }();
+  return on;
+}
+}  // namespace
 void gemm_tc_force(int mode) { g_tc_mode = mode; }
+
+bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
+  if (g.M == 0 || g.N == 0) return true;
+  const int64_t K6 = 6LL * g.K;
+  const int64_t lda = g.a.trans ? pad8i(g.M) : pad8i(K6);
+  const int64_t ldb = g.b.trans ? pad8i(K6) : pad8i(g.N);
+  const size_t abytes = (size_t)(g.a.trans ? K6 * lda : (int64_t)g.M * lda) * 2;
+  const size_t bbytes = (size_t)(g.b.trans ? (int64_t)g.N * ldb : K6 * ldb) * 2;
+  GemmArgs h = g;
+  h.ab = DType::bf16;
+  h.K = static_cast<int>(K6);
+  bf16* A = static_cast<bf16*>(x6_buffer(s, 0, abytes));
+  bf16* B = static_cast<bf16*>(x6_buffer(s, 1, bbytes));
+  h.a = Operand{A, lda, g.a.trans, 0, 0};
+  h.b = Operand{B, ldb, g.b.trans, 0, 0};
+  // split-K of at most 2: two fp32 partials reduce into the zeroed output in
+  // either order to the same bits (a + b == b + a), so the fp32 path stays
+  // run-to-run deterministic
+  h.max_splits = g.max_splits > 0 ? std::min(g.max_splits, 2) : 2;
+  if (!gemm_tc_supported(h)) return false;
+  const int grid = 148 * 8;
+  split6_kernel<<<grid, 256, 0, s>>>(g.a, 0, g.M, g.K, A, lda);
+  LAUNCH_CHECK();
+  split6_kernel<<<grid, 256, 0, s>>>(g.b, 1, g.N, g.K, B, ldb);
+  LAUNCH_CHECK();
+  count_launch(2);
+  gemm_tc(h, s);
+  return true;
+}
 
 int gemm(const GemmArgs& g, cudaStream_t s) {
   if (g_tc_mode == 0 && g.ab == DType::bf16 && gemm_tc_supported(g)) {
     gemm_tc(g, s);
     return 1;
   }
+  if (g_tc_mode == 0 && g.ab == DType::f32 && f32_x6() && gemm_x6(g, s)) return 2;
   gemm_simt(g, s);
   return 0;
 }

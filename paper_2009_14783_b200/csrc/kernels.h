@@ -46,9 +46,13 @@ struct GemmArgs {
   int max_splits = 0;          // split-K cap for the tcgen05 path (0: heuristic)
 };
 
-// Dispatch: tcgen05 path for bf16 operands whose layout TMA can describe,
-// fp32 SIMT path otherwise.  Returns the path used (0 SIMT, 1 tcgen05).
-int gemm(const GemmArgs& g, cudaStream_t s);
+// Dispatch: tcgen05 for bf16 operands whose layout TMA can describe; fp32
+// operands on the same tcgen05 kernel through the bf16x6 split (HP_F32_GEMM=simt:
+// the fp32 SIMT kernel); SIMT otherwise.
+int gemm(const GemmArgs& g, cudaStream_t s);  // 0 SIMT, 1 tcgen05 bf16, 2 tcgen05 bf16x6 (fp32)
+// fp32 operands on the bf16 tensor cores, fp32-accurate (bf16x6 split, see
+// kernels.cu); false when the split operands' layout is unsupported
+bool gemm_x6(const GemmArgs& g, cudaStream_t s);
 void gemm_simt(const GemmArgs& g, cudaStream_t s);
 bool gemm_tc_supported(const GemmArgs& g);
 void gemm_tc(const GemmArgs& g, cudaStream_t s);

@@ -573,3 +573,26 @@ def test_attention_cross_and_causal(path, dtype, mode):
     for got, want in ((o, ref), (got_q, gq), (got_k, gk), (got_v, gv)):
         err = (got.float() - want).abs().max().item() / want.abs().max().item()
         assert err < tol, (mode, err)
+
+
+@pytest.mark.parametrize("a_trans,b_trans", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_x6_fp32_gemm_on_tensor_cores(a_trans, b_trans):
+    """fp32 operands on the tcgen05 kernel through the bf16x6 split (path 4):
+    fp32-level accuracy -- within 3x of the fp32 SIMT kernel's error against
+    the same torch fp32 reference and <= 1e-5 of the output scale -- for every
+    operand major-ness, grouped per-head B (dk 32 and 64), GELU / dGELU /
+    residual / accumulate epilogues and grouped C."""
+    cases = [dict(M=300, N=200, K=1000), dict(M=128, N=96, K=64, group=32),
+             dict(M=256, N=192, K=128, group=64), dict(M=512, N=256, K=384, bias=True, act=1),
+             dict(M=256, N=256, K=256, act=2, resid=True), dict(M=200, N=128, K=512, accumulate=True),
+             dict(M=256, N=256, K=200, c_group=64)]
+    for c in cases:
+        if c.get("group") and (c["group"] and ((not b_trans and c["N"] % c["group"]) or (b_trans and c["K"] % c["group"]))):
+            continue
+        kw = {k: v for k, v in c.items() if k not in ("M", "N", "K")}
+        x6 = run_gemm(c["M"], c["N"], c["K"], torch.float32, a_trans, b_trans, path=4, seed=3, **kw)
+        simt = run_gemm(c["M"], c["N"], c["K"], torch.float32, a_trans, b_trans, path=1, seed=3, **kw)
+        scale = x6["ref"].abs().max().item()
+        e6 = (x6["out"] - x6["ref"]).abs().max().item()
+        es = (simt["out"] - simt["ref"]).abs().max().item()
+        assert e6 <= 3 * es + 1e-7 * scale and e6 <= 1e-5 * scale, (c, e6, es, scale)
