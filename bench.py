@@ -274,6 +274,27 @@ def same_config_runs(hp, batch, args) -> dict:
         out[comp] = {"value": BATCH * steps / (ms / 1e3), "unit": "samples/s", "steps": steps,
                      "ms_per_step": ms / steps}
         e.close()
+    # the headline C2 model itself on the fp32 path (the reference's precision:
+    # fp32 operands, fp32-accurate GEMMs on the tensor cores via the bf16x6
+    # split), beside the bf16 headline
+    ex = hp.ExecConfig(compute="f32", policy="sentences", device=0, bucket_mb=200.0,
+                       max_tokens=BATCH * SEQ, max_batch=BATCH, max_masks=BATCH * SEQ // 2)
+    e = hp.StepEngine(hp.ModelSpec(**C2), hp.OptimConfig("adam", 0.9, 0.98, 1e-9), ex, seed=21)
+    e.stage(batch)
+    for _ in range(3):
+        e.round_async(False, 1e-4)
+    e.round_sync()
+    steps = 5
+    e.mark(0)
+    for _ in range(steps):
+        e.round_async(False, 1e-4)
+    e.mark(1)
+    ms = e.elapsed_ms(0, 1)
+    e.round_sync()
+    e.close()
+    out["c2_f32"] = {"workload": "the C2 model (bert_encoder L12 d768) on the fp32 path", "value":
+                     BATCH * steps / (ms / 1e3), "unit": "samples/s", "steps": steps,
+                     "ms_per_step": ms / steps}
     return out
 
 
