@@ -2107,6 +2107,20 @@ bool f32_x6() {
 }  // namespace
 void gemm_tc_force(int mode) { g_tc_mode = mode; }
 
+// sum of the K-chunk partials (fixed order, fp32 round-to-nearest), then the
+// GEMM's own epilogue (alpha, bias, GELU / dGELU, residual, accumulate,
+// grouped C) -- the SIMT kernel's epi_store
+template <class CT>
+__global__ void x6_reduce_kernel(const float* __restrict__ part, int chunks, GemmArgs g) {
+  const int64_t MN = (int64_t)g.M * g.N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int c = 0; c < chunks; ++c) acc += part[c * MN + e];
+    epi_store<CT>(g, static_cast<int>(e / g.N), static_cast<int>(e % g.N), acc);
+  }
+}
+
 bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
   if (g.M == 0 || g.N == 0) return true;
   const int64_t K6 = 6LL * g.K;
@@ -2114,17 +2128,28 @@ bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
   const int64_t ldb = g.b.trans ? pad8i(K6) : pad8i(g.N);
   const size_t abytes = (size_t)(g.a.trans ? K6 * lda : (int64_t)g.M * lda) * 2;
   const size_t bbytes = (size_t)(g.b.trans ? (int64_t)g.N * ldb : K6 * ldb) * 2;
-  GemmArgs h = g;
-  h.ab = DType::bf16;
-  h.K = static_cast<int>(K6);
   bf16* A = static_cast<bf16*>(x6_buffer(s, 0, abytes));
   bf16* B = static_cast<bf16*>(x6_buffer(s, 1, bbytes));
-  h.a = Operand{A, lda, g.a.trans, 0, 0};
-  h.b = Operand{B, ldb, g.b.trans, 0, 0};
-  // split-K of at most 2: two fp32 partials reduce into the zeroed output in
-  // either order to the same bits (a + b == b + a), so the fp32 path stays
-  // run-to-run deterministic
-  h.max_splits = g.max_splits > 0 ? std::min(g.max_splits, 2) : 2;
+  // The tensor core's fp32 accumulation is not round-to-nearest across the
+  // MMA chain (its error grows with the chain, not with its square root), so
+  // K' is cut into chunks of <= 1024 (at most 48 chunks), each its own GEMM
+  // into an fp32 partial -- K <= 170: one GEMM, each chunk holds whole split
+  // terms otherwise (K' = 6K: 6 chunks of K when K <= 1024) -- and the partials
+  // are summed in a fixed order with RN: deterministic, no atomics.
+  int64_t kc = 1024;
+  if ((K6 + kc - 1) / kc > 48) kc = ((K6 + 47) / 48 + 63) / 64 * 64;
+  if (g.K <= 1024 && g.K % 64 == 0) kc = g.K;
+  const int chunks = static_cast<int>((K6 + kc - 1) / kc);
+  GemmArgs h;
+  h.M = g.M;
+  h.N = g.N;
+  h.ab = DType::bf16;
+  h.ct = DType::f32;
+  h.max_splits = 1;
+  Operand a{A, lda, g.a.trans, 0, 0}, b{B, ldb, g.b.trans, 0, 0};
+  h.a = a;
+  h.b = b;
+  h.K = static_cast<int>(std::min<int64_t>(kc, K6));
   if (!gemm_tc_supported(h)) return false;
   const int grid = 148 * 8;
   split6_kernel<<<grid, 256, 0, s>>>(g.a, 0, g.M, g.K, A, lda);
@@ -2132,7 +2157,23 @@ bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
   split6_kernel<<<grid, 256, 0, s>>>(g.b, 1, g.N, g.K, B, ldb);
   LAUNCH_CHECK();
   count_launch(2);
-  gemm_tc(h, s);
+  const int64_t MN = (int64_t)g.M * g.N;
+  float* part = static_cast<float*>(x6_buffer(s, 2, (size_t)chunks * MN * 4));
+  for (int c = 0; c < chunks; ++c) {
+    const int64_t k0 = c * kc;
+    h.K = static_cast<int>(std::min(kc, K6 - k0));
+    h.a.p = A + (g.a.trans ? k0 * lda : k0);
+    h.b.p = B + (g.b.trans ? k0 : k0 * ldb);
+    h.c = part + c * MN;
+    h.ldc = g.N;
+    if (!gemm_tc_supported(h)) {  // a chunk's pointer alignment (k0 % 8 == 0 keeps 16 B)
+      fail(HP_ECUDA, "bf16x6: chunk operand not TMA-describable");
+    }
+    gemm_tc(h, s);
+  }
+  DISPATCH1(g.ct, CT, x6_reduce_kernel<CT><<<148 * 8, 256, 0, s>>>(part, chunks, g));
+  LAUNCH_CHECK();
+  count_launch();
   return true;
 }
 
