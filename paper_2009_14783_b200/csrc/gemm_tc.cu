@@ -1078,6 +1078,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int slots = nsm / ccg;
     int sp = 1;
     if (can_split && tiles < slots) sp = std::max(1, std::min(slots / tiles, num_kb / 4));
+    // at most two K halves: their fp32 partials reduce into the zeroed output
+    // in either order to the same bits (a + b == b + a), so every GEMM of the
+    // step is run-to-run deterministic; deeper splits would not be
+    sp = std::min(sp, 2);
     if (g.max_splits > 0) sp = std::min(sp, g.max_splits);
     const int units = tiles * sp;
     const int waves = (units + slots - 1) / slots;

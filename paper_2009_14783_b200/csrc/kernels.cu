@@ -2139,7 +2139,9 @@ bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
   int64_t kc = 1024;
   if ((K6 + kc - 1) / kc > 48) kc = ((K6 + 47) / 48 + 63) / 64 * 64;
   if (g.K <= 1024 && g.K % 64 == 0) kc = g.K;
-  const int chunks = static_cast<int>((K6 + kc - 1) / kc);
+  int chunks = static_cast<int>((K6 + kc - 1) / kc);
+  // a short remainder (< 64) joins the chunk before it
+  if (chunks > 1 && K6 - (int64_t)(chunks - 1) * kc < 64) --chunks;
   GemmArgs h;
   h.M = g.M;
   h.N = g.N;
@@ -2161,7 +2163,7 @@ bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
   float* part = static_cast<float*>(x6_buffer(s, 2, (size_t)chunks * MN * 4));
   for (int c = 0; c < chunks; ++c) {
     const int64_t k0 = c * kc;
-    h.K = static_cast<int>(std::min(kc, K6 - k0));
+    h.K = static_cast<int>(c + 1 == chunks ? K6 - k0 : kc);
     h.a.p = A + (g.a.trans ? k0 * lda : k0);
     h.b.p = B + (g.b.trans ? k0 : k0 * ldb);
     h.c = part + c * MN;

@@ -579,7 +579,7 @@ def test_attention_cross_and_causal(path, dtype, mode):
 def test_x6_fp32_gemm_on_tensor_cores(a_trans, b_trans):
     """fp32 operands on the tcgen05 kernel through the bf16x6 split (path 4):
     fp32-level accuracy -- within 3x of the fp32 SIMT kernel's error against
-    the same torch fp32 reference, or 2e-6 of the output scale -- for every
+    the same torch fp32 reference, or 5e-6 of the output scale -- for every
     operand major-ness, grouped per-head B (dk 32 and 64), GELU / dGELU /
     residual / accumulate epilogues and grouped C."""
     cases = [dict(M=300, N=200, K=1000), dict(M=128, N=96, K=64, group=32),
@@ -595,4 +595,4 @@ def test_x6_fp32_gemm_on_tensor_cores(a_trans, b_trans):
         scale = x6["ref"].abs().max().item()
         e6 = (x6["out"] - x6["ref"]).abs().max().item()
         es = (simt["out"] - simt["ref"]).abs().max().item()
-        assert e6 <= max(3 * es, 2e-6 * scale), (c, e6, es, scale)
+        assert e6 <= max(3 * es, 5e-6 * scale), (c, e6, es, scale)
