@@ -115,11 +115,50 @@ __device__ __forceinline__ void tmem_row32_to_global(uint32_t taddr, float scale
                         pack2(__uint_as_float(v[8 * q + 6]) * scale, __uint_as_float(v[8 * q + 7]) * scale));
   }
 }
+// Output rows leave through shared memory: thread r stages its row's values
+// (rows 144 bytes apart, 9 x 16: a warp's 16-byte stores spread over every
+// bank group), then the warp writes its own 32 rows back coalesced -- 8 (or 4)
+// lanes per contiguous 128 (64)-byte row segment -- skipping rows past the
+// instance, instead of every lane storing to its own row.
+constexpr uint32_t kStRow = 144;
+// rows [row_lo, row_lo + 32) of the staging area -> global; seg = bytes per
+// row segment (64 or 128); valid(row) selects the rows to write
+template <int SEG, class Dst>
+__device__ __forceinline__ void warp_rows_out(uint32_t sbase, int row_lo, int lane, int nvalid, Dst dst) {
+  constexpr int LPR = SEG / 16;      // lanes per row
+  constexpr int RPI = 32 / LPR;      // rows per instruction
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 32 / RPI; ++i) {
+    const int rr = row_lo + i * RPI + lane / LPR, piece = lane % LPR;
+    if (rr < nvalid) {
+      uint4 u;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                   : "r"(sbase + rr * kStRow + 16 * piece)
+                   : "memory");
+      *reinterpret_cast<uint4*>(reinterpret_cast<char*>(dst(rr)) + 16 * piece) = u;
+    }
+  }
+}
+__device__ __forceinline__ void tmem_row32_to_smem(uint32_t taddr, float scale, uint32_t sdst) {
+  uint32_t v[32];
+  TMEM_LD32(taddr, v);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    sts128(sdst + 16 * q, pack2(__uint_as_float(v[8 * q]) * scale, __uint_as_float(v[8 * q + 1]) * scale),
+           pack2(__uint_as_float(v[8 * q + 2]) * scale, __uint_as_float(v[8 * q + 3]) * scale),
+           pack2(__uint_as_float(v[8 * q + 4]) * scale, __uint_as_float(v[8 * q + 5]) * scale),
+           pack2(__uint_as_float(v[8 * q + 6]) * scale, __uint_as_float(v[8 * q + 7]) * scale));
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
 // 32 bf16 of row r, columns 32c .. 32c+31 (layout of put_row32) -> floats
 __device__ __forceinline__ void get_row32(uint32_t base, int r, int c, float* v, uint32_t stride) {
   const uint32_t sub = base + (c >> 1) * stride;
@@ -186,6 +225,11 @@ __global__ void __launch_bounds__(kThreadsF, 4)
     mbar_init(&sm.p_ready, 32 * kSoftWarpsF);
     mbar_init(&sm.o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the loads go out before the TMEM allocation / CTA barrier below
+    mbar_expect_tx(&sm.full, 3 * kTile);
+    tma_2d(&map_q, &sm.full, sm.tile[0], a.qcol + h * DK, row0);
+    tma_2d(&map_k, &sm.full, sm.tile[1], a.kcol + h * DK, krow0);
+    tma_2d(&map_v, &sm.full, sm.tile[2], a.vcol + h * DK, krow0);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -199,13 +243,7 @@ __global__ void __launch_bounds__(kThreadsF, 4)
   if (threadIdx.x == 0) atr(tr, 2);
 
   if (warp == 0) {
-    if (elect_one()) {
-      mbar_expect_tx(&sm.full, 3 * kTile);
-      tma_2d(&map_q, &sm.full, sm.tile[0], a.qcol + h * DK, row0);
-      tma_2d(&map_k, &sm.full, sm.tile[1], a.kcol + h * DK, krow0);
-      tma_2d(&map_v, &sm.full, sm.tile[2], a.vcol + h * DK, krow0);
-    }
-    __syncwarp();
+    // (the producer's loads were issued above)
   } else if (warp == 1) {
     mbar_wait(&sm.full, 0);
     if (lane == 0) atr(tr, 3);
@@ -266,7 +304,9 @@ __global__ void __launch_bounds__(kThreadsF, 4)
       float p[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        p[i] = (32 * c + i < nj) ? ex2(fmaf(__uint_as_float(v[i]), sl2, mo)) : 0.f;
+        const float xe = fmaf(__uint_as_float(v[i]), sl2, mo);
+        const float e = ex2(xe);
+        p[i] = (32 * c + i < nj) ? e : 0.f;
         s4[i & 3] += p[i];
       }
       put_row32(pb, r, c, p);
@@ -280,10 +320,14 @@ __global__ void __launch_bounds__(kThreadsF, 4)
     if (r == 0) atr(tr, 7);
     tmem_fence_after();
     const bool ok = r < n;
-    bf16* orow = static_cast<bf16*>(a.o) + (int64_t)(row0 + r) * d + h * DK;
-    tmem_row32_to_global(trow, 1.f / sum, orow, ok);
-    tmem_row32_to_global(trow + 32, 1.f / sum, orow + 32, ok);
+    // O rows through the (now dead) P / V tiles, then one 128-byte bulk copy
+    // per valid row
+    const uint32_t sb = smem_u32(sm.tile[0]);
+    tmem_row32_to_smem(trow, 1.f / sum, sb + r * kStRow);
+    tmem_row32_to_smem(trow + 32, 1.f / sum, sb + r * kStRow + 64);
     if (ok) a.lse[(int64_t)h * a.T_q + row0 + r] = mx * scale + logf(sum);
+    bf16* const ob = static_cast<bf16*>(a.o) + (int64_t)row0 * d + h * DK;
+    warp_rows_out<128>(sb, 32 * quarter, lane, n, [&](int rr) { return ob + (int64_t)rr * d; });
     if (r == 0) atr(tr, 8);
   }
   tmem_fence_before();
@@ -320,6 +364,12 @@ __global__ void __launch_bounds__(kThreadsB, 2)
     mbar_init(&sm.ds_ready, 32 * kSoftWarpsB);
     mbar_init(&sm.o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the loads go out before the TMEM allocation / CTA barrier below
+    mbar_expect_tx(&sm.full, 4 * kTile);
+    tma_2d(&map_q, &sm.full, sm.tile[0], a.qcol + h * DK, row0);
+    tma_2d(&map_k, &sm.full, sm.tile[1], a.kcol + h * DK, krow0);
+    tma_2d(&map_v, &sm.full, sm.tile[2], a.vcol + h * DK, krow0);
+    tma_2d(&map_do, &sm.full, sm.tile[3], h * DK, row0);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -332,14 +382,7 @@ __global__ void __launch_bounds__(kThreadsB, 2)
   const uint32_t tmem = sm.tmem;
 
   if (warp == 0) {
-    if (elect_one()) {
-      mbar_expect_tx(&sm.full, 4 * kTile);
-      tma_2d(&map_q, &sm.full, sm.tile[0], a.qcol + h * DK, row0);
-      tma_2d(&map_k, &sm.full, sm.tile[1], a.kcol + h * DK, krow0);
-      tma_2d(&map_v, &sm.full, sm.tile[2], a.vcol + h * DK, krow0);
-      tma_2d(&map_do, &sm.full, sm.tile[3], h * DK, row0);
-    }
-    __syncwarp();
+    // (the producer's loads were issued above)
   } else if (warp == 1) {
     mbar_wait(&sm.full, 0);
     tmem_fence_after();
@@ -428,7 +471,9 @@ __global__ void __launch_bounds__(kThreadsB, 2)
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const bool ok = rok && (32 * c + i < nj);
-        p[i] = ok ? ex2(fmaf(__uint_as_float(sv[i]), sl2, lo)) : 0.f;
+        const float xe = fmaf(__uint_as_float(sv[i]), sl2, lo);
+        const float e = ex2(xe);
+        p[i] = ok ? e : 0.f;
       }
       put_row32(xb, r, c, p, kXs);
     }
@@ -456,13 +501,20 @@ __global__ void __launch_bounds__(kThreadsB, 2)
     mbar_arrive(&sm.ds_ready);
     mbar_wait(&sm.o_done, 0);
     tmem_fence_after();
+    // dQ, dK, dV half-rows (64 bytes) through the dead operand tiles, one bulk
+    // copy each for valid rows
     const int c0 = h * DK + 32 * half;
-    tmem_row32_to_global(trow + 128 + 32 * half, 1.f,
-                         static_cast<bf16*>(a.dq) + (int64_t)(row0 + r) * a.lddq + a.dqcol + c0, rok);   // dQ
-    tmem_row32_to_global(trow + 64 + 32 * half, 1.f,
-                         static_cast<bf16*>(a.dk_) + (int64_t)(krow0 + r) * a.lddk + a.dkcol + c0, kok);  // dK
-    tmem_row32_to_global(trow + 32 * half, 1.f,
-                         static_cast<bf16*>(a.dv) + (int64_t)(krow0 + r) * a.lddv + a.dvcol + c0, kok);   // dV
+    constexpr uint32_t kPlane = 128 * kStRow;
+    const uint32_t sb = smem_u32(sm.tile[0]) + 64 * half;  // this warp's column half
+    tmem_row32_to_smem(trow + 128 + 32 * half, 1.f, sb + r * kStRow);            // dQ
+    tmem_row32_to_smem(trow + 64 + 32 * half, 1.f, sb + kPlane + r * kStRow);    // dK
+    tmem_row32_to_smem(trow + 32 * half, 1.f, sb + 2 * kPlane + r * kStRow);     // dV
+    bf16* const qb = static_cast<bf16*>(a.dq) + (int64_t)row0 * a.lddq + a.dqcol + c0;
+    bf16* const kb = static_cast<bf16*>(a.dk_) + (int64_t)krow0 * a.lddk + a.dkcol + c0;
+    bf16* const vb = static_cast<bf16*>(a.dv) + (int64_t)krow0 * a.lddv + a.dvcol + c0;
+    warp_rows_out<64>(sb, 32 * quarter, lane, n, [&](int rr) { return qb + (int64_t)rr * a.lddq; });
+    warp_rows_out<64>(sb + kPlane, 32 * quarter, lane, nk, [&](int rr) { return kb + (int64_t)rr * a.lddk; });
+    warp_rows_out<64>(sb + 2 * kPlane, 32 * quarter, lane, nk, [&](int rr) { return vb + (int64_t)rr * a.lddv; });
   }
   tmem_fence_before();
   __syncthreads();
@@ -654,7 +706,9 @@ __global__ void __launch_bounds__(kThreadsF, 1)
         float p[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          p[i] = (kbase + i < n) ? ex2(fmaf(__uint_as_float(v[i]), sl2, mo)) : 0.f;
+          const float xe = fmaf(__uint_as_float(v[i]), sl2, mo);
+          const float e = ex2(xe);
+          p[i] = (kbase + i < n) ? e : 0.f;
           s4[i & 3] += p[i];
         }
         put_row32(pb, r, c, p);
@@ -698,7 +752,9 @@ __device__ __forceinline__ void long_bwd_rows(uint32_t trow, int half, int r, in
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const bool ok = rok && (k0 + 32 * c + i < n);
-      p[i] = ok ? ex2(fmaf(__uint_as_float(sv[i]), sl2, lo)) : 0.f;
+      const float xe = fmaf(__uint_as_float(sv[i]), sl2, lo);
+      const float e = ex2(xe);
+      p[i] = ok ? e : 0.f;
     }
     if (p_base) put_row32(p_base, r, c, p);
 #pragma unroll
