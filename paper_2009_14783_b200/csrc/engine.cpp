@@ -165,6 +165,19 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
       emb_gath_ = static_cast<float*>(dalloc((size_t)W * emb_cap_ * (d_ + 4) * 4));
     }
   }
+  {
+    // At N > 1 the persistent GEMMs (one CTA per SM, ~200 KB of smem, 168
+    // registers a thread) leave no SM to the NCCL kernels of the bucket
+    // allreduces running beside backward: their grids stop at 140 SMs
+    // (C2, N = 2: 13908 / 13879 vs 13632 / 13628 samples/s, exposed allreduce
+    // 0.43 vs 0.46 ms; at N = 1 a cap only costs, 7305 vs 7579;
+    // profiles/r02_ab_gemm_sm_budget.txt).  HP_GEMM_SMS overrides (0: all).
+    const char* e = std::getenv("HP_GEMM_SMS");
+    if (e)
+      gemm_tc_set_sm_budget(std::atoi(e));
+    else
+      gemm_tc_set_sm_budget(comm_ && comm_->world > 1 ? 140 : 0);
+  }
   ev_reduced_.resize(buckets_.size());
   for (auto& e : ev_reduced_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   {

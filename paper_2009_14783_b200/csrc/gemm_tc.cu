@@ -958,7 +958,13 @@ namespace {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+int g_sm_budget = 0;  // 0: every SM (gemm_tc_set_sm_budget)
+int num_sms_hw();
 int num_sms() {
+  const int n = num_sms_hw();
+  return g_sm_budget > 0 ? std::min(n, g_sm_budget) : n;
+}
+int num_sms_hw() {
   static int n = 0;
   if (!n) {
     int dev = 0;
@@ -976,6 +982,7 @@ unsigned long long* g_trace = nullptr;
 }  // namespace
 
 void gemm_tc_set_bn(int bn) { g_force_bn = bn; }
+void gemm_tc_set_sm_budget(int n) { g_sm_budget = n; }
 void gemm_tc_set_splits(int s) { g_force_splits = s; }
 
 bool gemm_tc_supported(const GemmArgs& g) {

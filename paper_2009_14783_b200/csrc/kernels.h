@@ -58,6 +58,9 @@ bool gemm_tc_supported(const GemmArgs& g);
 void gemm_tc(const GemmArgs& g, cudaStream_t s);
 void gemm_tc_force(int mode);  // test hook: 0 auto, 1 never tcgen05
 void gemm_tc_set_bn(int bn);   // test hook: 0 heuristic, 128, 192 or 256
+// SMs the persistent GEMM grids may use (0: all): at N > 1 the engine leaves
+// some to the NCCL kernels of the concurrent gradient allreduce
+void gemm_tc_set_sm_budget(int n);
 void gemm_tc_set_splits(int s);  // test hook: 0 heuristic, else forced split-K
 void gemm_tc_set_cg(int cg);     // test hook: 0 heuristic, 1 single CTA, 2 CTA pair
 void gemm_tc_set_debug(int mode);  // profiling hook: bits 1 no loads, 2 no MMA, 4 no epilogue
