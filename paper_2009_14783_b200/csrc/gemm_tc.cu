@@ -52,6 +52,7 @@ struct Params {
   int b_grouped;  // B uses the 3-D grouped map (group = 64)
   int a_atoms, b_atoms;  // MN-major operand loaded through the 3-D atom map
   int m_tiles, n_tiles, splits, kb_per_split, units;
+  int64_t part_stride;  // > 0: split s stores its own partial at c + s * part_stride (no reduction)
   void* c;
   int64_t ldc;
   int c_group;  // 32-bit: divided per chunk in the epilogue
@@ -163,15 +164,15 @@ __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c
 
 // Epilogue for NC consecutive columns [n, n+NC) of row m.
 template <int NC>
-__device__ __forceinline__ void epilogue_cols(const Params& p, int m, int n, float* v) {
+__device__ __forceinline__ void epilogue_cols(const Params& p, int m, int n, float* v, int64_t coff) {
   if (m >= p.M) return;
   const bool inb = n + NC <= p.N;
   const bool full = inb && p.vec == 1;
 #pragma unroll
   for (int i = 0; i < NC; ++i) v[i] *= p.alpha;
-  const int64_t co = p.c_group ? (n / p.c_group) * p.c_gstride + (int64_t)m * p.ldc + n % p.c_group
-                               : (int64_t)m * p.ldc + n;
-  if (p.splits > 1) {  // split-K partial: reduce into the (zeroed) fp32 output
+  const int64_t co = (p.c_group ? (n / p.c_group) * p.c_gstride + (int64_t)m * p.ldc + n % p.c_group
+                                : (int64_t)m * p.ldc + n) + coff;
+  if (p.splits > 1 && !p.part_stride) {  // split-K partial: reduce into the (zeroed) fp32 output
     float* c = static_cast<float*>(p.c) + co;
     if (full) {
 #pragma unroll
@@ -498,12 +499,14 @@ enum EpiKind : int {
 // the prefetched aux (pre_kind 1, dGELU) or residual (pre_kind 2) chunk.
 template <int EK>
 __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, int lane, int row0,
-                                                int n, float* v, const uint4 (&pre)[4], int pre_kind) {
+                                                int n, float* v, const uint4 (&pre)[4], int pre_kind,
+                                                int64_t coff) {
   constexpr bool kAnyF32 = EK == EK_GENERIC || EK == EK_F32;
   const int rows_left = p.M - row0;
   int64_t co0 = (int64_t)row0 * p.ldc + n;
   if constexpr (kAnyF32) {
     if (p.c_group) co0 = (n / p.c_group) * p.c_gstride + (int64_t)row0 * p.ldc + n % p.c_group;
+    co0 += coff;
   }
   const bool f32 = EK == EK_F32 || (EK == EK_GENERIC && p.c_f32);
   const int cs = f32 ? 4 : 2;
@@ -512,7 +515,7 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t st, in
     for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
   }
   if constexpr (kAnyF32) {
-    if (p.splits > 1) {
+    if (p.splits > 1 && !p.part_stride) {
       staged_out(true, st, lane, v, static_cast<char*>(p.c) + co0 * 4, p.ldc * 4, rows_left, 1);
       return;
     }
@@ -868,9 +871,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (EK != EK_GENERIC || (n + 32 <= p.N && p.vec == 1)) {
             uint4 pre[4];
             if (pre_kind) pre_consume(st, lane, cur, pre);
-            epilogue_staged<EK>(p, st, lane, row0, n, v, pre, pre_kind);
+            epilogue_staged<EK>(p, st, lane, row0, n, v, pre, pre_kind,
+                                p.part_stride ? (u % p.splits) * p.part_stride : 0);
           } else if constexpr (EK == EK_GENERIC) {
-            epilogue_cols<32>(p, row0 + lane, n, v);
+            epilogue_cols<32>(p, row0 + lane, n, v, p.part_stride ? (u % p.splits) * p.part_stride : 0);
           }
         }
         if (tr) trace_at(p, tslot + 2, 1024);
@@ -1085,10 +1089,11 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int slots = nsm / ccg;
     int sp = 1;
     if (can_split && tiles < slots) sp = std::max(1, std::min(slots / tiles, num_kb / 4));
+    if (g.part_chunks > 1) sp = g.part_chunks;  // chunk partials: the split count is given
     // at most two K halves: their fp32 partials reduce into the zeroed output
     // in either order to the same bits (a + b == b + a), so every GEMM of the
     // step is run-to-run deterministic; deeper splits would not be
-    sp = std::min(sp, 2);
+    if (g.part_chunks <= 1) sp = std::min(sp, 2);
     if (g.max_splits > 0) sp = std::min(sp, g.max_splits);
     const int units = tiles * sp;
     const int waves = (units + slots - 1) / slots;
@@ -1103,8 +1108,15 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (g_force_splits && can_split) splits = g_force_splits;
   if (!can_split) splits = 1;
   const int m_tiles = (g.M + tc::BM * cg - 1) / (tc::BM * cg);
-  const int kb_per_split = (num_kb + splits - 1) / splits;
+  int kb_per_split = (num_kb + splits - 1) / splits;
+  if (g.part_chunks > 1) {  // chunk partials: K-chunk boundaries as given
+    if (!can_split || g.part_kc % tc::BK || g.max_splits == 1)
+      fail(HP_ECONFIG, "gemm_tc: K-chunk partials need an fp32 C without epilogue, part_kc % 64 == 0");
+    kb_per_split = g.part_kc / tc::BK;
+  }
   splits = (num_kb + kb_per_split - 1) / kb_per_split;  // no empty splits
+  if (g.part_chunks > 1 && splits != g.part_chunks)
+    fail(HP_ECONFIG, "gemm_tc: K-chunk count does not match K / part_kc");
   const int bnl = bn / cg;  // B columns per CTA
 
   // MN-major operands: "atom" maps view the row-major [K][MN] matrix as
@@ -1172,6 +1184,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.splits = splits;
   p.kb_per_split = kb_per_split;
   p.units = m_tiles * p.n_tiles * splits;
+  p.part_stride = g.part_chunks > 1 ? g.part_stride : 0;
   p.c = g.c; p.ldc = g.ldc; p.c_group = static_cast<int>(g.c_group); p.c_gstride = g.c_gstride;
   p.c_f32 = g.ct == DType::f32;
   p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias; p.act = g.act;
@@ -1180,7 +1193,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.debug = g_debug_mode;
   p.trace = g_trace;
 
-  if (splits > 1) {
+  if (splits > 1 && !p.part_stride) {
     // partial sums are reduced into C: clear the output region first
     if (g.c_group) {
       HP_CUDA(cudaMemsetAsync(g.c, 0, sizeof(float) * (size_t)(g.N / g.c_group) * g.c_gstride, s));

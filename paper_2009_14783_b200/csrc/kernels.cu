@@ -2132,26 +2132,24 @@ bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
   bf16* B = static_cast<bf16*>(x6_buffer(s, 1, bbytes));
   // The tensor core's fp32 accumulation is not round-to-nearest across the
   // MMA chain (its error grows with the chain, not with its square root), so
-  // K' is cut into chunks of <= 1024 (at most 48 chunks), each its own GEMM
-  // into an fp32 partial -- K <= 170: one GEMM, each chunk holds whole split
-  // terms otherwise (K' = 6K: 6 chunks of K when K <= 1024) -- and the partials
-  // are summed in a fixed order with RN: deterministic, no atomics.
+  // K' is cut into chunks of <= 1024 (at most 48 chunks; whole split terms,
+  // K' = 6K: 6 chunks of K, when K <= 1024), each accumulated into its own
+  // fp32 partial -- all chunks in ONE launch (split-K units that store their
+  // partials side by side) -- and the partials are summed in a fixed order
+  // with RN: deterministic, no atomics.
   int64_t kc = 1024;
   if ((K6 + kc - 1) / kc > 48) kc = ((K6 + 47) / 48 + 63) / 64 * 64;
   if (g.K <= 1024 && g.K % 64 == 0) kc = g.K;
-  int chunks = static_cast<int>((K6 + kc - 1) / kc);
-  // a short remainder (< 64) joins the chunk before it
-  if (chunks > 1 && K6 - (int64_t)(chunks - 1) * kc < 64) --chunks;
+  const int chunks = static_cast<int>((K6 + kc - 1) / kc);
   GemmArgs h;
   h.M = g.M;
   h.N = g.N;
   h.ab = DType::bf16;
   h.ct = DType::f32;
-  h.max_splits = 1;
   Operand a{A, lda, g.a.trans, 0, 0}, b{B, ldb, g.b.trans, 0, 0};
   h.a = a;
   h.b = b;
-  h.K = static_cast<int>(std::min<int64_t>(kc, K6));
+  h.K = static_cast<int>(K6);
   if (!gemm_tc_supported(h)) return false;
   const int grid = 148 * 8;
   split6_kernel<<<grid, 256, 0, s>>>(g.a, 0, g.M, g.K, A, lda);
@@ -2161,18 +2159,16 @@ bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
   count_launch(2);
   const int64_t MN = (int64_t)g.M * g.N;
   float* part = static_cast<float*>(x6_buffer(s, 2, (size_t)chunks * MN * 4));
-  for (int c = 0; c < chunks; ++c) {
-    const int64_t k0 = c * kc;
-    h.K = static_cast<int>(c + 1 == chunks ? K6 - k0 : kc);
-    h.a.p = A + (g.a.trans ? k0 * lda : k0);
-    h.b.p = B + (g.b.trans ? k0 : k0 * ldb);
-    h.c = part + c * MN;
-    h.ldc = g.N;
-    if (!gemm_tc_supported(h)) {  // a chunk's pointer alignment (k0 % 8 == 0 keeps 16 B)
-      fail(HP_ECUDA, "bf16x6: chunk operand not TMA-describable");
-    }
-    gemm_tc(h, s);
+  h.c = part;
+  h.ldc = g.N;
+  if (chunks > 1) {
+    h.part_chunks = chunks;
+    h.part_kc = static_cast<int>(kc);
+    h.part_stride = MN;
+  } else {
+    h.max_splits = 1;  // one chunk: one accumulation chain, no reduction
   }
+  gemm_tc(h, s);
   DISPATCH1(g.ct, CT, x6_reduce_kernel<CT><<<148 * 8, 256, 0, s>>>(part, chunks, g));
   LAUNCH_CHECK();
   count_launch();

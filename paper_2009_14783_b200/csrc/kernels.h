@@ -44,6 +44,11 @@ struct GemmArgs {
   const void* resid = nullptr; // C = epi(...) + R(m,n), R of type ct
   int64_t ld_resid = 0;
   int max_splits = 0;          // split-K cap for the tcgen05 path (0: heuristic)
+  // K-chunk partials (tcgen05 path, fp32 C, no epilogue): chunk s covers
+  // K [s * part_kc, (s + 1) * part_kc) and is stored at c + s * part_stride;
+  // one launch for all chunks (the bf16x6 split's RN partial sums)
+  int part_chunks = 0, part_kc = 0;
+  int64_t part_stride = 0;
 };
 
 // Dispatch: tcgen05 for bf16 operands whose layout TMA can describe; fp32
