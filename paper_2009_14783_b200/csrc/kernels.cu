@@ -2049,28 +2049,53 @@ __constant__ int kX6PatA[6] = {0, 0, 1, 0, 2, 1};
 __constant__ int kX6PatB[6] = {0, 1, 0, 2, 0, 1};
 
 // logical A (m, k) / B (k, n): r = m or n, K the contracted extent
+__device__ __forceinline__ void split3(float v, bf16* p) {
+  p[0] = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(p[0]);
+  p[1] = __float2bfloat16_rn(r1);
+  p[2] = __float2bfloat16_rn(r1 - __bfloat162float(p[1]));
+}
 __global__ void split6_kernel(Operand src, int is_b, int R, int K, bf16* __restrict__ dst, int64_t ldd) {
   const float* x = static_cast<const float*>(src.p);
-  // walk the source's contiguous dimension fastest
+  // walk the source's contiguous dimension fastest; the destination's
+  // contiguous dimension is the same one, so two neighbours along it leave as
+  // one bf16x2 per term
   const bool kfast = is_b ? src.trans != 0 : src.trans == 0;
-  const int64_t total = (int64_t)R * K;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = kfast ? e / K : e % R, k = kfast ? e % K : e / R;
-    const float v = x[is_b ? b_off(src, k, r) : a_off(src, r, k)];
-    bf16 part[3];
-    part[0] = __float2bfloat16_rn(v);
-    const float r1 = v - __bfloat162float(part[0]);
-    part[1] = __float2bfloat16_rn(r1);
-    part[2] = __float2bfloat16_rn(r1 - __bfloat162float(part[1]));
+  const int F = kfast ? K : R;  // fast dimension
+  auto dst_off = [&](int64_t r, int64_t kk) -> int64_t {
+    // A: trans -> [K'][M] else [M][K'];  B: trans -> [N][K'] else [K'][N]
+    return is_b ? (src.trans ? r * ldd + kk : kk * ldd + r) : (src.trans ? kk * ldd + r : r * ldd + kk);
+  };
+  auto src_val = [&](int64_t r, int64_t k) { return x[is_b ? b_off(src, k, r) : a_off(src, r, k)]; };
+  const int* pat = is_b ? kX6PatB : kX6PatA;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (F % 2 == 0) {
+    const int64_t total2 = (int64_t)R * K / 2;
+    for (int64_t e2 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e2 < total2; e2 += stride) {
+      const int64_t e = 2 * e2;
+      const int64_t slow = e / F, fast = e - slow * F;
+      const int64_t r = kfast ? slow : fast, k = kfast ? fast : slow;
+      const int64_t r1 = kfast ? r : r + 1, k1 = kfast ? k + 1 : k;
+      bf16 p0[3], p1[3];
+      split3(src_val(r, k), p0);
+      split3(src_val(r1, k1), p1);
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-      const int64_t kk = (int64_t)j * K + k;
-      // A: trans -> [K'][M] else [M][K'];  B: trans -> [N][K'] else [K'][N]
-      const int64_t o = is_b ? (src.trans ? r * ldd + kk : kk * ldd + r)
-                             : (src.trans ? kk * ldd + r : r * ldd + kk);
-      dst[o] = part[is_b ? kX6PatB[j] : kX6PatA[j]];
+      for (int j = 0; j < 6; ++j) {
+        __nv_bfloat162 h;
+        h.x = p0[pat[j]];
+        h.y = p1[pat[j]];
+        *reinterpret_cast<__nv_bfloat162*>(dst + dst_off(r, (int64_t)j * K + k)) = h;
+      }
     }
+    return;
+  }
+  const int64_t total = (int64_t)R * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t r = kfast ? e / K : e % R, k = kfast ? e % K : e / R;
+    bf16 part[3];
+    split3(src_val(r, k), part);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) dst[dst_off(r, (int64_t)j * K + k)] = part[pat[j]];
   }
 }
 
@@ -2113,8 +2138,36 @@ void gemm_tc_force(int mode) { g_tc_mode = mode; }
 template <class CT>
 __global__ void x6_reduce_kernel(const float* __restrict__ part, int chunks, GemmArgs g) {
   const int64_t MN = (int64_t)g.M * g.N;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (g.N % 4 == 0) {  // four neighbours of one row per thread, float4 partial reads
+    const int64_t MN4 = MN / 4;
+    const float4* p4 = reinterpret_cast<const float4*>(part);
+    for (int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e4 < MN4; e4 += stride) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      int c = 0;
+      for (; c + 4 <= chunks; c += 4) {  // four loads in flight, added in chunk order
+        float4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = __ldcs(p4 + (c + u) * MN4 + e4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc.x += q[u].x; acc.y += q[u].y; acc.z += q[u].z; acc.w += q[u].w;
+        }
+      }
+      for (; c < chunks; ++c) {
+        const float4 q = __ldcs(p4 + c * MN4 + e4);
+        acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+      }
+      const int64_t e = 4 * e4;
+      const int m = static_cast<int>(e / g.N), n = static_cast<int>(e - (int64_t)m * g.N);
+      epi_store<CT>(g, m, n, acc.x);
+      epi_store<CT>(g, m, n + 1, acc.y);
+      epi_store<CT>(g, m, n + 2, acc.z);
+      epi_store<CT>(g, m, n + 3, acc.w);
+    }
+    return;
+  }
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN; e += stride) {
     float acc = 0.f;
     for (int c = 0; c < chunks; ++c) acc += part[c * MN + e];
     epi_store<CT>(g, static_cast<int>(e / g.N), static_cast<int>(e % g.N), acc);
