@@ -1033,33 +1033,43 @@ struct SMat {
   int si, sk;  // A: (i,k) ; B: (k,j) strides
 };
 
-template <class Store>
-__device__ void smem_mm(int n1, int n2, int kd, SMat A, SMat B, Store store) {
-  const int ti_n = (n1 + 3) >> 2, tj_n = (n2 + 3) >> 2;
+template <int BR, int BC, class Store>
+__device__ __forceinline__ void smem_mm_t(int n1, int n2, int kd, SMat A, SMat B, Store store) {
+  const int ti_n = (n1 + BR - 1) / BR, tj_n = (n2 + BC - 1) / BC;
   for (int t = threadIdx.x; t < ti_n * tj_n; t += blockDim.x) {
-    const int i0 = (t / tj_n) * 4, j0 = (t % tj_n) * 4;
-    float acc[4][4];
+    const int i0 = (t / tj_n) * BR, j0 = (t % tj_n) * BC;
+    float acc[BR][BC];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < BR; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
+      for (int c = 0; c < BC; ++c) acc[r][c] = 0.f;
     for (int k = 0; k < kd; ++k) {
-      float a[4], bb[4];
+      float a[BR], bb[BC];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = A.p[(i0 + r) * A.si + k * A.sk];
+      for (int r = 0; r < BR; ++r) a[r] = A.p[(i0 + r) * A.si + k * A.sk];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) bb[c] = B.p[k * B.si + (j0 + c) * B.sk];
+      for (int c = 0; c < BC; ++c) bb[c] = B.p[k * B.si + (j0 + c) * B.sk];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < BR; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] += a[r] * bb[c];
+        for (int c = 0; c < BC; ++c) acc[r][c] += a[r] * bb[c];
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < BR; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < BC; ++c)
         if (i0 + r < n1 && j0 + c < n2) store(i0 + r, j0 + c, acc[r][c]);
   }
+}
+// register blocks of 8 x 8 (8 x 4 for the 64-column products): one block per
+// thread at 128 x 128 / 128 x 64, a quarter / three eighths of a shared-memory
+// load per FMA; every element's k-sum runs in the same order as any blocking.
+// Operand rows past n1 / n2 (up to the next multiple of 8) are read but never
+// stored: the arrays are packed in an allocation sized for 128-row operands.
+template <class Store>
+__device__ void smem_mm(int n1, int n2, int kd, SMat A, SMat B, Store store) {
+  if (n2 > 64) smem_mm_t<8, 8>(n1, n2, kd, A, B, store);
+  else smem_mm_t<8, 4>(n1, n2, kd, A, B, store);
 }
 
 template <class T>
