@@ -53,6 +53,7 @@ struct Params {
   int a_atoms, b_atoms;  // MN-major operand loaded through the 3-D atom map
   int m_tiles, n_tiles, splits, kb_per_split, units;
   int64_t part_stride;  // > 0: split s stores its own partial at c + s * part_stride (no reduction)
+  int rs_kb;            // running-sum kinds: k-blocks per accumulation stint
   void* c;
   int64_t ldc;
   int c_group;  // 32-bit: divided per chunk in the epilogue
@@ -492,6 +493,12 @@ enum EpiKind : int {
   EK_GELU = 2,     // bf16 C = GELU(acc + bias), pre-activation -> aux
   EK_DGELU = 3,    // bf16 C = acc * GELU'(aux), aux prefetched
   EK_F32 = 4,      // fp32 C (+ bias) (accumulate | split-K reduction), grouped C
+  // running-sum variants (Params::rs_kb): the unit's K range in stints of
+  // rs_kb k-blocks, each its own accumulation chain, summed in stint order in
+  // fp32 (round-to-nearest) in a third TMEM region, then the EK_F32 /
+  // EK_GENERIC epilogue -- the bf16x6 fp32 path without partials in HBM
+  EK_F32_RS = 5,
+  EK_GENERIC_RS = 6,
 };
 
 // Full 32-column chunk [n, n+32) of the warp's 32 rows starting at row0.
@@ -619,8 +626,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int BNL = TL::BNL;
   constexpr int STAGES = TL::kStages;
   constexpr uint32_t kStageBytes = TL::kStageBytes;
+  constexpr bool kRS = EK == EK_F32_RS || EK == EK_GENERIC_RS;
+  constexpr int EKB = EK == EK_F32_RS ? EK_F32 : (EK == EK_GENERIC_RS ? EK_GENERIC : EK);
+  static_assert(!kRS || BN == 128, "running-sum kinds use 128-wide tiles");
   constexpr uint32_t kAccStride = BN <= 128 ? 128 : 256;  // TMEM columns per accumulator
-  constexpr uint32_t kTmemCols = 2 * kAccStride;
+  // two accumulators (+ the running sum at column 256 for the RS kinds)
+  constexpr uint32_t kTmemCols = kRS ? 512 : 2 * kAccStride;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
@@ -767,17 +778,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t db0 = umma_desc(s0 + kATileBytes, p.b_mn ? 8192 : 16, 1024);
       const uint64_t dak = p.a_mn ? (2048 >> 4) : (32 >> 4);
       const uint64_t dbk = p.b_mn ? (2048 >> 4) : (32 >> 4);
-      uint32_t it = 0, lt = 0;
-      for (;; ++lt) {
-        const int u = take_unit(lt);
+      uint32_t it = 0, lt = 0;  // lt: accumulation stints (one per unit unless kRS)
+      for (uint32_t ui = 0;; ++ui) {
+        const int u = take_unit(ui);
         if (u < 0) break;
         int m0, nt, kb0, kb1;
         decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
+        const int kbs = kRS ? p.rs_kb : kb1 - kb0;
+        for (int sb = kb0; sb < kb1; sb += kbs, ++lt) {
+        const int se = min(kb1, sb + kbs);
         const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
         mbar_wait(&tmem_empty[as], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dacc = tmem_base + as * kAccStride;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        for (int kb = sb; kb < se; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
@@ -790,9 +804,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int k = 0; k < BK / 16; ++k) {
                 const uint64_t ad = da0 + soff + k * dak, bd = db0 + soff + k * dbk;
                 if constexpr (CG == 2)
-                  umma_bf16_cg2(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                  umma_bf16_cg2(dacc, ad, bd, idesc, (kb > sb || k > 0) ? 1u : 0u);
                 else
-                  umma_bf16(dacc, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                  umma_bf16(dacc, ad, bd, idesc, (kb > sb || k > 0) ? 1u : 0u);
               }
             }
             if constexpr (CG == 2) umma_commit_cg2(&empty[s]);
@@ -805,6 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (CG == 2) umma_commit_cg2(&tmem_full[as]); else umma_commit(&tmem_full[as]);
         }
         __syncwarp();
+        }
       }
     }
   } else {
@@ -819,21 +834,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t st = smem_u32(smem + STAGES * kStageBytes + 1024 + ew * kEpiStageBytes);
     // operand prefetched a chunk ahead: 1 = dGELU pre-activation, 2 = residual
     int pre_kind = 0;
-    if constexpr (EK == EK_DGELU) pre_kind = 1;
-    if constexpr (EK == EK_BF16) pre_kind = p.resid ? 2 : 0;
-    if constexpr (EK == EK_GENERIC)
+    if constexpr (EKB == EK_DGELU) pre_kind = 1;
+    if constexpr (EKB == EK_BF16) pre_kind = p.resid ? 2 : 0;
+    if constexpr (EKB == EK_GENERIC)
       pre_kind = (!p.c_f32 && p.vec == 1 && p.splits == 1) ? (p.act == ACT_DGELU ? 1 : (p.resid ? 2 : 0)) : 0;
     const char* pre_base = static_cast<const char*>(pre_kind == 1 ? p.aux : p.resid);
     const int64_t pre_ld = pre_kind == 1 ? p.ldc : p.ld_resid;
-    uint32_t lt = 0;
+    uint32_t lt = 0;  // accumulation stints, as the MMA warp counts them
     const uint32_t empty_leader[2] = {CG == 2 ? mapa_shared(smem_u32(&tmem_empty[0]), 0) : 0u,
                                       CG == 2 ? mapa_shared(smem_u32(&tmem_empty[1]), 0) : 0u};
-    for (;; ++lt) {
-      const int u = take_unit(lt);
+    const uint32_t rsum = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + 2 * kAccStride;
+    for (uint32_t ui = 0;; ++ui) {
+      const int u = take_unit(ui);
       if (u < 0) break;
       int m0, nt, kb0, kb1;
       decode_unit(p, u, BM * CG, m0, nt, kb0, kb1);
       const int n0 = nt * BN;
+      const int nst = kRS ? (kb1 - kb0 + p.rs_kb - 1) / p.rs_kb : 1;
+      // RS kinds: stints 0 .. nst-2 fold into the running sum, the last one
+      // finishes it and runs the epilogue
+      for (int j = 0; j + 1 < nst; ++j, ++lt) {
+        if constexpr (kRS) {
+          const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
+          mbar_wait(&tmem_full[as], aph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * kAccStride;
+#pragma unroll 1
+          for (int c = first; c < BN; c += kChunkStep) {
+            uint32_t r[32];
+            TMEM_LD32(taddr + c, r);
+            if (j > 0) {
+              uint32_t q[32];
+              TMEM_LD32(rsum + c, q);
+              asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(q[i]) + __uint_as_float(r[i]));
+            } else {
+              asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            }
+            TMEM_ST32(rsum + c, r);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2)
+              mbar_arrive_cluster(empty_leader[as]);
+            else
+              mbar_arrive(&tmem_empty[as]);
+          }
+        }
+      }
       const uint32_t as = lt & 1, aph = (lt >> 1) & 1;
       const int row0 = m0 + static_cast<int>(row_rank) * BM + quarter * 32;
       const int rows_left = p.M - row0;
@@ -860,7 +911,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tr) trace_at(p, tslot, 1024);
         uint32_t r[32];
         TMEM_LD32(taddr + c, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (kRS && nst > 1) {
+          uint32_t q[32];
+          TMEM_LD32(rsum + c, q);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(q[i]) + __uint_as_float(r[i]));
+        } else {
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
         if (tr) trace_at(p, tslot + 1, 1024);
         const int n = n0 + c;
         if (n < p.N && rows_left > 0 && !debug_bit(p, 4)) {
@@ -868,12 +927,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           // specialised kinds are only launched with N % 32 == 0, vec == 1
-          if (EK != EK_GENERIC || (n + 32 <= p.N && p.vec == 1)) {
+          if (EKB != EK_GENERIC || (n + 32 <= p.N && p.vec == 1)) {
             uint4 pre[4];
             if (pre_kind) pre_consume(st, lane, cur, pre);
-            epilogue_staged<EK>(p, st, lane, row0, n, v, pre, pre_kind,
-                                p.part_stride ? (u % p.splits) * p.part_stride : 0);
-          } else if constexpr (EK == EK_GENERIC) {
+            epilogue_staged<EKB>(p, st, lane, row0, n, v, pre, pre_kind,
+                                 p.part_stride ? (u % p.splits) * p.part_stride : 0);
+          } else if constexpr (EKB == EK_GENERIC) {
             epilogue_cols<32>(p, row0 + lane, n, v, p.part_stride ? (u % p.splits) * p.part_stride : 0);
           }
         }
@@ -890,6 +949,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           mbar_arrive(&tmem_empty[as]);
       }
+      ++lt;
     }
   }
   __syncthreads();
@@ -1080,6 +1140,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int ccg = c[0], cbn = c[1];
     if (g_force_cg && ccg != g_force_cg) continue;
     if (g_force_bn && cbn != g_force_bn) continue;
+    if (g.rs_kc > 0 && cbn != 128) continue;  // running sum: a third 128-column TMEM region
     if (g.b.group && !g.b.trans && (cbn / ccg) % 64) continue;
     // a 96-column half of B per CTA: only as a K-major operand (rows of the
     // box); an MN-major B tile is whole 64-column swizzle atoms
@@ -1106,7 +1167,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     }
   }
   if (g_force_splits && can_split) splits = g_force_splits;
-  if (!can_split) splits = 1;
+  if (!can_split || g.rs_kc > 0) splits = 1;
   const int m_tiles = (g.M + tc::BM * cg - 1) / (tc::BM * cg);
   int kb_per_split = (num_kb + splits - 1) / splits;
   if (g.part_chunks > 1) {  // chunk partials: K-chunk boundaries as given
@@ -1185,6 +1246,9 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.kb_per_split = kb_per_split;
   p.units = m_tiles * p.n_tiles * splits;
   p.part_stride = g.part_chunks > 1 ? g.part_stride : 0;
+  p.rs_kb = g.rs_kc > 0 ? g.rs_kc / tc::BK : 0;
+  if (g.rs_kc > 0 && (g.rs_kc % tc::BK || g.ct != DType::f32 || bn != 128))
+    fail(HP_ECONFIG, "gemm_tc: running-sum stints need fp32 C, 128-wide tiles, rs_kc % 64 == 0");
   p.c = g.c; p.ldc = g.ldc; p.c_group = static_cast<int>(g.c_group); p.c_gstride = g.c_gstride;
   p.c_f32 = g.ct == DType::f32;
   p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias; p.act = g.act;
@@ -1213,7 +1277,15 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
       ek = tc::EK_F32;
     }
   }
+  if (p.rs_kb > 0) ek = ek == tc::EK_F32 ? tc::EK_F32_RS : tc::EK_GENERIC_RS;
   switch (ek) {
+    case tc::EK_F32_RS:
+      if (cg == 2) launch_tc<128, 2, tc::EK_F32_RS>(ma, mb, p, s); else launch_tc<128, 1, tc::EK_F32_RS>(ma, mb, p, s);
+      break;
+    case tc::EK_GENERIC_RS:
+      if (cg == 2) launch_tc<128, 2, tc::EK_GENERIC_RS>(ma, mb, p, s);
+      else launch_tc<128, 1, tc::EK_GENERIC_RS>(ma, mb, p, s);
+      break;
     case tc::EK_BF16: launch_ek<tc::EK_BF16>(cg, bn, ma, mb, p, s); break;
     case tc::EK_GELU: launch_ek<tc::EK_GELU>(cg, bn, ma, mb, p, s); break;
     case tc::EK_DGELU: launch_ek<tc::EK_DGELU>(cg, bn, ma, mb, p, s); break;

@@ -2132,6 +2132,13 @@ void* x6_buffer(cudaStream_t s, int which, size_t bytes) {
   return b.p;
 }
 int64_t pad8i(int64_t v) { return (v + 7) & ~int64_t(7); }
+bool x6_rs_on() {  // HP_X6_RS=0: always partials + reduction (A/B)
+  static const bool on = [] {
+    const char* e = std::getenv("HP_X6_RS");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
 bool f32_x6() {
   static const bool on = [] {
     const char* e = std::getenv("HP_F32_GEMM");  // "simt": the fp32 SIMT kernel (A/B, parity checks)
@@ -2221,6 +2228,24 @@ bool gemm_x6(const GemmArgs& g, cudaStream_t s) {
   LAUNCH_CHECK();
   count_launch(2);
   const int64_t MN = (int64_t)g.M * g.N;
+  // Enough 128-wide tiles to fill the GPU: the chunks are summed on chip
+  // (running-sum stints, same order) and the GEMM applies the epilogue --
+  // no partials in HBM, no reduction launch.  Otherwise each chunk is a
+  // split-K unit of its own (more parallelism) and x6_reduce_kernel sums them.
+  const int64_t tiles128 = ((g.M + 127) / 128) * ((g.N + 127) / 128);
+  if (chunks > 1 && g.ct == DType::f32 && tiles128 >= 148 && x6_rs_on()) {
+    GemmArgs r = g;
+    r.ab = DType::bf16;
+    r.a = a;
+    r.b = b;
+    r.K = static_cast<int>(K6);
+    r.rs_kc = static_cast<int>(kc);
+    r.max_splits = 1;
+    if (gemm_tc_supported(r)) {
+      gemm_tc(r, s);
+      return true;
+    }
+  }
   float* part = static_cast<float*>(x6_buffer(s, 2, (size_t)chunks * MN * 4));
   h.c = part;
   h.ldc = g.N;

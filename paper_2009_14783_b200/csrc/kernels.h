@@ -49,6 +49,9 @@ struct GemmArgs {
   // one launch for all chunks (the bf16x6 split's RN partial sums)
   int part_chunks = 0, part_kc = 0;
   int64_t part_stride = 0;
+  // > 0 (tcgen05 path, fp32 C): K in stints of rs_kc, each its own
+  // accumulation chain, summed in order in fp32 on chip (128-wide tiles)
+  int rs_kc = 0;
 };
 
 // Dispatch: tcgen05 for bf16 operands whose layout TMA can describe; fp32
