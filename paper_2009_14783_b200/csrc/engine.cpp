@@ -1082,6 +1082,7 @@ void Engine::emb_rows_update(int mode, cudaStream_t su) {
 
 void Engine::issue_bucket(size_t k) {
   const Bucket& bk = buckets_[k];
+  flush_finals();
   HP_CUDA(cudaEventRecord(ev_bucket_[k], s_main_));
   HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_bucket_[k], 0));
   if (wg_forked_) {  // and every weight gradient issued so far this round
@@ -1503,17 +1504,29 @@ DeferredFinal Engine::final_slot(size_t floats) {
   return f;
 }
 
+// The column-reduction finals (LayerNorm gamma / beta, bias gradients) of a
+// stretch of backward are queued and leave in ONE launch on the side stream
+// when a gradient bucket needs them (or backward ends) -- a dozen launches
+// per bucket become one.  Every queued final's partials come from the compute
+// stream, so the side stream waits on the last one's event.
 void Engine::issue_final(DeferredFinal& f) {
   if (!f.queued) return;
   HP_CUDA(cudaEventRecord(final_evs_[final_n_], s_main_));
-  HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[final_n_], 0));
-  launch_final(f, s_comm_);
-  serialize_if_timed(s_comm_);
+  finals_q_.push_back(f);
   ++final_n_;
+}
+
+void Engine::flush_finals() {
+  if (finals_q_.empty()) return;
+  HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[final_n_ - 1], 0));
+  launch_finals(finals_q_.data(), static_cast<int>(finals_q_.size()), s_comm_);
+  serialize_if_timed(s_comm_);
+  finals_q_.clear();
 }
 
 void Engine::round_body(int dummy) {
   final_n_ = 0;
+  finals_q_.clear();
   wg_forked_ = false;
   upd_forked_ = false;
   emb_sparse_round_ = false;
@@ -1588,6 +1601,10 @@ void Engine::round_body(int dummy) {
   }
   if (capture_) {
     if (!local_grads_) local_grads_ = static_cast<float*>(dalloc(n_ * 4));
+    // the column-reduction finals complete the local gradient before the copy
+    flush_finals();
+    HP_CUDA(cudaEventRecord(ev_comm_done_, s_comm_));
+    HP_CUDA(cudaStreamWaitEvent(s_main_, ev_comm_done_, 0));
     HP_CUDA(cudaMemcpyAsync(local_grads_, grads_, n_ * 4, cudaMemcpyDeviceToDevice, s_main_));
     capture_ = false;
     grads_ready(0);

@@ -117,7 +117,9 @@ class Engine {
   void issue_bucket(size_t b);
   void round_body(int dummy);  // the device work of one round (eager or captured)
   DeferredFinal final_slot(size_t floats);  // partial buffer for the next deferred final
-  void issue_final(DeferredFinal& f);        // its final on the side stream
+  void issue_final(DeferredFinal& f);        // queued for the side stream
+  void flush_finals();                       // the queued finals, one launch
+  std::vector<DeferredFinal> finals_q_;
 
   hp_model_desc m_;
   hp_optim_desc o_;
