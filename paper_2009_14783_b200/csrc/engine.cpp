@@ -782,6 +782,7 @@ void Engine::tstart(int cls, cudaStream_t st) {
   }
   HP_CUDA(cudaEventRecordWithFlags(t.ev[t.used].first, st ? st : s_main_,
                                   capturing_ ? cudaEventRecordExternal : cudaEventRecordDefault));
+  t.k_open = kernel_launch_count();
 }
 void Engine::tstop(int cls, double flops, double bytes, cudaStream_t st) {
   if (!timers_on_) return;
@@ -791,7 +792,7 @@ void Engine::tstop(int cls, double flops, double bytes, cudaStream_t st) {
   ++t.used;
   t.flops += flops;
   t.bytes += bytes;
-  ++t.launches;
+  t.launches += kernel_launch_count() - t.k_open;
 }
 // Event spans of a timed graph replay (graph nodes: no host launch gaps in
 // the spans) -> the class accumulators.
@@ -1232,9 +1233,12 @@ void Engine::backward() {
         if (wg_on_) {
           // d(ffn.b1) = colsum(dU) beside the chain (its own scratch), before
           // the event that lets the next layer reuse dU_
+          // (its final joins the batched finals, issued from the wgrad stream)
           tstop(TM_NORM, 0, 0);
           tstart(TM_NORM, s_wg_);
-          col_sum(T, F_, dU, F_, at_, gp(ib1), scratch_wg_, s_wg_);
+          DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, F_));
+          col_sum(T, F_, dU, F_, at_, gp(ib1), scratch_wg_, s_wg_, &f);
+          issue_final(f, s_wg_);
           tstop(TM_NORM, 0, 0, s_wg_);
           HP_CUDA(cudaEventRecord(ev_w1_[l], s_wg_));
           tstart(TM_NORM);
@@ -1509,17 +1513,23 @@ DeferredFinal Engine::final_slot(size_t floats) {
 // when a gradient bucket needs them (or backward ends) -- a dozen launches
 // per bucket become one.  Every queued final's partials come from the compute
 // stream, so the side stream waits on the last one's event.
-void Engine::issue_final(DeferredFinal& f) {
+void Engine::issue_final(DeferredFinal& f, cudaStream_t st) {
   if (!f.queued) return;
-  HP_CUDA(cudaEventRecord(final_evs_[final_n_], s_main_));
+  const bool wg = st && st != s_main_;
+  HP_CUDA(cudaEventRecord(final_evs_[final_n_], wg ? st : s_main_));
+  (wg ? finals_last_wg_ : finals_last_main_) = static_cast<int>(final_n_);
   finals_q_.push_back(f);
   ++final_n_;
 }
 
 void Engine::flush_finals() {
   if (finals_q_.empty()) return;
-  HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[final_n_ - 1], 0));
+  if (finals_last_main_ >= 0) HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[finals_last_main_], 0));
+  if (finals_last_wg_ >= 0) HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[finals_last_wg_], 0));
+  finals_last_main_ = finals_last_wg_ = -1;
+  tstart(TM_NORM, s_comm_);
   launch_finals(finals_q_.data(), static_cast<int>(finals_q_.size()), s_comm_);
+  tstop(TM_NORM, 0, 0, s_comm_);
   serialize_if_timed(s_comm_);
   finals_q_.clear();
 }
@@ -1527,6 +1537,7 @@ void Engine::flush_finals() {
 void Engine::round_body(int dummy) {
   final_n_ = 0;
   finals_q_.clear();
+  finals_last_main_ = finals_last_wg_ = -1;
   wg_forked_ = false;
   upd_forked_ = false;
   emb_sparse_round_ = false;

@@ -117,9 +117,11 @@ class Engine {
   void issue_bucket(size_t b);
   void round_body(int dummy);  // the device work of one round (eager or captured)
   DeferredFinal final_slot(size_t floats);  // partial buffer for the next deferred final
-  void issue_final(DeferredFinal& f);        // queued for the side stream
+  // queued for the side stream; `st` ran the final's partials (null: compute stream)
+  void issue_final(DeferredFinal& f, cudaStream_t st = nullptr);
   void flush_finals();                       // the queued finals, one launch
   std::vector<DeferredFinal> finals_q_;
+  int finals_last_main_ = -1, finals_last_wg_ = -1;  // last queued event per stream
 
   hp_model_desc m_;
   hp_optim_desc o_;
@@ -271,7 +273,8 @@ class Engine {
     size_t used = 0;
     double flops = 0, bytes = 0;
     double ms = 0;
-    uint64_t launches = 0;
+    uint64_t launches = 0;      // kernels launched inside the class's spans
+    uint64_t k_open = 0;        // kernel_launch_count() at the open span's start
     cudaEvent_t cur = nullptr;
   };
   std::array<TimerAcc, TM_COUNT> tm_;
