@@ -1069,7 +1069,7 @@ void launch_final(const DeferredFinal& f, cudaStream_t s) {
 
 // ------------------------------------------------------------------ attention
 // One CTA per (instance, head); the whole (<=128 token) sequence lives in
-// shared memory in fp32.  smem_mm is a register-blocked (4x4) product
+// shared memory in fp32.  smem_mm is a register-blocked (8x8 / 8x4) product
 // C(i,j) = sum_k A(i,k) B(k,j) over strided smem operands.
 struct SMat {
   const float* p;
