@@ -204,6 +204,34 @@ __device__ __forceinline__ void atr(unsigned long long* tr, int slot) {
   if (tr && blockIdx.x == 0 && blockIdx.y == 0) tr[slot] = clock64();
 }
 
+// The CTA's instances [i0, i1) (one, or a packed group) and the keys query
+// row r of the tile sees: [klo, khi) -- its own instance's, causal-limited
+__device__ __forceinline__ bool cta_instances(const AttnArgs& a, int b, int& i0, int& i1) {
+  i0 = b;
+  i1 = b + 1;
+  if (a.grp) {
+    if (b >= *a.ngrp) return false;
+    i0 = a.grp[b];
+    i1 = a.grp[b + 1];
+  }
+  return true;
+}
+__device__ __forceinline__ void row_keys(const AttnArgs& a, int i0, int i1, int row0, int krow0, int nk,
+                                         int r, int& klo, int& khi) {
+  klo = 0;
+  khi = nk;
+  if (i1 - i0 > 1) {
+    const int q = row0 + r;
+    int i = i0;
+    while (i + 1 < i1 && a.cu_q[i + 1] <= q) ++i;
+    klo = a.cu_kv[i] - krow0;
+    khi = a.cu_kv[i + 1] - krow0;
+    if (a.causal) khi = min(khi, klo + (q - a.cu_q[i]) + 1);
+  } else if (a.causal) {
+    khi = min(nk, r + 1);
+  }
+}
+
 // ------------------------------------------------------------------ forward
 __global__ void __launch_bounds__(kThreadsF, 4)
     attn_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -212,8 +240,10 @@ __global__ void __launch_bounds__(kThreadsF, 4)
   extern __shared__ __align__(1024) uint8_t raw[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(raw));
   const int b = blockIdx.x, h = blockIdx.y;
-  const int row0 = a.cu_q[b], n = a.cu_q[b + 1] - row0;  // queries
-  const int krow0 = a.cu_kv[b], nk = a.cu_kv[b + 1] - krow0;  // keys / values
+  int i0, i1;
+  if (!cta_instances(a, b, i0, i1)) return;
+  const int row0 = a.cu_q[i0], n = a.cu_q[i1] - row0;  // queries
+  const int krow0 = a.cu_kv[i0], nk = a.cu_kv[i1] - krow0;  // keys / values
   if (n <= 0 || nk <= 0) return;
   if (threadIdx.x == 0) atr(tr, 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -277,8 +307,9 @@ __global__ void __launch_bounds__(kThreadsF, 4)
     const uint32_t trow = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
     const float scale = rsqrtf(static_cast<float>(DK));
     const float sl2 = scale * 1.4426950408889634f;
-    // keys this row sees: [0, nk), and <= r under the causal mask
-    const int nj = a.causal ? min(nk, r + 1) : nk;
+    // keys this row sees: its instance's, and <= r under the causal mask
+    int klo, khi;
+    row_keys(a, i0, i1, row0, krow0, nk, r, klo, khi);
     mbar_wait(&sm.s_done, 0);
     if (r == 0) atr(tr, 4);
     tmem_fence_after();
@@ -290,7 +321,7 @@ __global__ void __launch_bounds__(kThreadsF, 4)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (32 * c + i < nj) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(v[i]));
+        if (32 * c + i >= klo && 32 * c + i < khi) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(v[i]));
     }
     const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
     const float mo = -mx * sl2;
@@ -306,7 +337,7 @@ __global__ void __launch_bounds__(kThreadsF, 4)
       for (int i = 0; i < 32; ++i) {
         const float xe = fmaf(__uint_as_float(v[i]), sl2, mo);
         const float e = ex2(xe);
-        p[i] = (32 * c + i < nj) ? e : 0.f;
+        p[i] = (32 * c + i >= klo && 32 * c + i < khi) ? e : 0.f;
         s4[i & 3] += p[i];
       }
       put_row32(pb, r, c, p);
@@ -347,8 +378,10 @@ __global__ void __launch_bounds__(kThreadsB, 2)
   extern __shared__ __align__(1024) uint8_t raw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(align1024(raw));
   const int b = blockIdx.x, h = blockIdx.y;
-  const int row0 = a.cu_q[b], n = a.cu_q[b + 1] - row0;  // queries
-  const int krow0 = a.cu_kv[b], nk = a.cu_kv[b + 1] - krow0;  // keys / values
+  int i0, i1;
+  if (!cta_instances(a, b, i0, i1)) return;
+  const int row0 = a.cu_q[i0], n = a.cu_q[i1] - row0;  // queries
+  const int krow0 = a.cu_kv[i0], nk = a.cu_kv[i1] - krow0;  // keys / values
   if (n <= 0 || nk <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = a.H * DK;
@@ -434,7 +467,8 @@ __global__ void __launch_bounds__(kThreadsB, 2)
     const float l2e = 1.4426950408889634f;
     const bool rok = r < n;        // query row r (S, dP, dQ)
     const bool kok = r < nk;       // key row r (dK, dV)
-    const int nj = a.causal ? min(nk, r + 1) : nk;  // keys query row r sees
+    int klo, khi;  // keys query row r sees
+    row_keys(a, i0, i1, row0, krow0, nk, r, klo, khi);
     // D_r = rowsum(dO * O), lse_r -- while the MMAs run
     float Dr = 0.f, lr = 0.f;
     if (rok) {
@@ -470,7 +504,7 @@ __global__ void __launch_bounds__(kThreadsB, 2)
       float p[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const bool ok = rok && (32 * c + i < nj);
+        const bool ok = rok && 32 * c + i >= klo && 32 * c + i < khi;
         const float xe = fmaf(__uint_as_float(sv[i]), sl2, lo);
         const float e = ex2(xe);
         p[i] = ok ? e : 0.f;

@@ -307,7 +307,7 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
                  Mm = (std::max<uint64_t>(x_.max_masks, 1) + mpad_ - 1) / mpad_ * mpad_;
   // (seq2seq layout: see stage_s2s)
   const size_t ints = std::max<size_t>(3 * Tm + (Bm + 1) + 2 * Mm + Bm + (4 * Tm + 3),
-                                       9 * Tm + 2 * (Bm + 1) + 3);
+                                       9 * Tm + 3 * (Bm + 1) + 4);
   stage_bytes_ = ((ints * 4 + 7) & ~size_t(7)) + 8;
   for (int i = 0; i < kStageBufs; ++i) {
     HP_CUDA(cudaMallocHost(&h_stage_[i], stage_bytes_));
@@ -343,6 +343,10 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
       embp_.useg = embp_.uid + Tm;
       embp_.ulist = embp_.useg + Tm + 1;
       embp_.ucount = embp_.ulist + Tm;
+      s2s_grp_ = embp_.ucount + 2;
+      s2s_ngrp_ = s2s_grp_ + Bm + 1;
+      const char* e = std::getenv("HP_ATTN_PACK");  // A/B: 0 = one pair per CTA
+      attn_pack_ = !(e && std::string(e) == "0");
     }
   }
 

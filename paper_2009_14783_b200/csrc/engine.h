@@ -179,6 +179,11 @@ class Engine {
   void* mem_ = nullptr;
   DevBatch enc_, dec_, embp_;
   const int* tgt_ = nullptr;
+  // seq2seq attention packing: consecutive pairs whose sources and targets
+  // each fit one 128-row tile share a CTA (s2s_grp_[0..*s2s_ngrp_], staged)
+  const int* s2s_grp_ = nullptr;
+  const int* s2s_ngrp_ = nullptr;
+  bool attn_pack_ = true;
   void *dqc_ = nullptr, *dkvc_ = nullptr, *dmem_ = nullptr, *demb_ = nullptr;
   void *x_final_ = nullptr, *p0_ = nullptr;
   float *mean0_ = nullptr, *rstd0_ = nullptr;

@@ -97,7 +97,7 @@ void Engine::stage_s2s(const hp_batch& b, int* h, double* weight) {
   int *etok = h, *epos = h + Tm, *ecu = h + 2 * Tm;
   int *dtok = ecu + Bm + 1, *dpos = dtok + Tm, *dcu = dpos + Tm, *tgt = dcu + Bm + 1;
   int *perm = tgt + Tm, *uid = perm + Tm, *useg = uid + Tm, *ulist = useg + Tm + 1,
-      *ucount = ulist + Tm;
+      *ucount = ulist + Tm, *grp = ucount + 2, *ngrp = grp + Bm + 1;
   uint64_t Ts = 0, Tt = 0;
   double w = 0.0;
   for (uint64_t i = 0; i < B; ++i) {
@@ -159,6 +159,22 @@ void Engine::stage_s2s(const hp_batch& b, int* h, double* weight) {
     if (useg[u + 1] - useg[u] > kEmbHotTokens) ulist[ns + nh++] = u;
   ucount[0] = ns;
   ucount[1] = nh;
+  // attention packing: greedy runs of consecutive pairs whose sources and
+  // whose targets each total <= 128 tokens (one tile for all three kinds:
+  // encoder self, decoder self, cross)
+  int G = 0;
+  for (uint64_t i = 0; i < B;) {
+    grp[G++] = static_cast<int>(i);
+    int src = ecu[i + 1] - ecu[i], dst = dcu[i + 1] - dcu[i];
+    ++i;
+    while (i < B && src + (ecu[i + 1] - ecu[i]) <= 128 && dst + (dcu[i + 1] - dcu[i]) <= 128) {
+      src += ecu[i + 1] - ecu[i];
+      dst += dcu[i + 1] - dcu[i];
+      ++i;
+    }
+  }
+  grp[G] = static_cast<int>(B);
+  *ngrp = G;
   enc_.T = static_cast<int>(Ts);
   enc_.B = static_cast<int>(B);
   dec_.T = static_cast<int>(Tt);
@@ -204,8 +220,13 @@ void Engine::ln_bwd(int T, const void* dy, const void* x, const float* mean, con
   tstop(TM_NORM, 0, (double)T * d_ * asz_ * 3);
 }
 
-void Engine::attn_op_fwd(const AttnArgs& a) {
+void Engine::attn_op_fwd(const AttnArgs& a0) {
   const DType t = at_;
+  AttnArgs a = a0;
+  if (attn_pack_) {
+    a.grp = s2s_grp_;
+    a.ngrp = s2s_ngrp_;
+  }
   auto op = [a, t](cudaStream_t st) { attention2_fwd(a, t, st); };
   const double fl = 4.0 * a.H * a.dk * (double)a.T_q * (double)std::max(a.max_kv, 1);
   tstart(TM_ATTN);
@@ -214,8 +235,13 @@ void Engine::attn_op_fwd(const AttnArgs& a) {
   record(TM_ATTN, fl, op);
 }
 
-void Engine::attn_op_bwd(const AttnArgs& a) {
+void Engine::attn_op_bwd(const AttnArgs& a0) {
   const DType t = at_;
+  AttnArgs a = a0;
+  if (attn_pack_) {
+    a.grp = s2s_grp_;
+    a.ngrp = s2s_ngrp_;
+  }
   auto op = [a, t](cudaStream_t st) { attention2_bwd(a, t, st); };
   const double fl = 8.0 * a.H * a.dk * (double)a.T_q * (double)std::max(a.max_kv, 1);
   tstart(TM_ATTN);

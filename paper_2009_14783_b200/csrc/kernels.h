@@ -170,6 +170,11 @@ struct AttnArgs {
   void* dq = nullptr; int64_t lddq = 0; int dqcol = 0;
   void* dk_ = nullptr; int64_t lddk = 0; int dkcol = 0;
   void* dv = nullptr; int64_t lddv = 0; int dvcol = 0;
+  // packing (tcgen05 kernels only): CTA b takes instances [grp[b], grp[b+1])
+  // -- consecutive instances whose queries and keys each fit one 128-row
+  // tile, block-diagonal mask -- for b < *ngrp; the grid stays B wide
+  const int* grp = nullptr;
+  const int* ngrp = nullptr;
 };
 // self-attention over packed QKV [T x 3d] (q heads | k heads | v heads)
 AttnArgs self_attn_args(const DevBatch& b, int H, int dk, int max_seq, const void* qkv, void* o,

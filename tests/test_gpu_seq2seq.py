@@ -132,3 +132,23 @@ def test_seq2seq_input_validation():
     with pytest.raises(hp.ShapeError):
         eng.stage([long])
     eng.close()
+
+
+def test_seq2seq_packed_attention_matches_unpacked(monkeypatch):
+    """bf16 tcgen05 attention with consecutive short pairs packed into one
+    128-row tile per CTA (block-diagonal mask; the default) against one pair
+    per CTA (HP_ATTN_PACK=0): the same losses and local gradient up to the
+    tensor cores' summation order over the zero-masked keys."""
+    spec, _, rec = _case(128, 2, 2, 256, 211, 16, 3, 45, seed=5)
+    ids = np.arange(12)
+    out = {}
+    for pack in ("1", "0"):
+        monkeypatch.setenv("HP_ATTN_PACK", pack)
+        eng = _engine(spec, "bf16")
+        eng.set_capture(True)
+        rep = eng.round(rec.batch(ids), lr=0.0)
+        out[pack] = (rep.local_loss_sum, eng.local_grads())
+        eng.close()
+    (l1, g1), (l0, g0) = out["1"], out["0"]
+    assert abs(l1 - l0) <= 2e-3 * abs(l0)
+    assert rel_norm(g1, g0) <= 1e-2
