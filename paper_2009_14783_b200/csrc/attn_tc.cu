@@ -206,21 +206,23 @@ __device__ __forceinline__ void atr(unsigned long long* tr, int slot) {
 
 // The CTA's instances [i0, i1) (one, or a packed group) and the keys query
 // row r of the tile sees: [klo, khi) -- its own instance's, causal-limited
+template <bool kPack>
 __device__ __forceinline__ bool cta_instances(const AttnArgs& a, int b, int& i0, int& i1) {
   i0 = b;
   i1 = b + 1;
-  if (a.grp) {
+  if (kPack) {
     if (b >= *a.ngrp) return false;
     i0 = a.grp[b];
     i1 = a.grp[b + 1];
   }
   return true;
 }
+template <bool kPack>
 __device__ __forceinline__ void row_keys(const AttnArgs& a, int i0, int i1, int row0, int krow0, int nk,
                                          int r, int& klo, int& khi) {
   klo = 0;
   khi = nk;
-  if (i1 - i0 > 1) {
+  if (kPack && i1 - i0 > 1) {
     const int q = row0 + r;
     int i = i0;
     while (i + 1 < i1 && a.cu_q[i + 1] <= q) ++i;
@@ -233,6 +235,7 @@ __device__ __forceinline__ void row_keys(const AttnArgs& a, int i0, int i1, int 
 }
 
 // ------------------------------------------------------------------ forward
+template <bool kPack>
 __global__ void __launch_bounds__(kThreadsF, 4)
     attn_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const AttnArgs a, unsigned long long* tr) {
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(kThreadsF, 4)
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(raw));
   const int b = blockIdx.x, h = blockIdx.y;
   int i0, i1;
-  if (!cta_instances(a, b, i0, i1)) return;
+  if (!cta_instances<kPack>(a, b, i0, i1)) return;
   const int row0 = a.cu_q[i0], n = a.cu_q[i1] - row0;  // queries
   const int krow0 = a.cu_kv[i0], nk = a.cu_kv[i1] - krow0;  // keys / values
   if (n <= 0 || nk <= 0) return;
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(kThreadsF, 4)
     const float sl2 = scale * 1.4426950408889634f;
     // keys this row sees: its instance's, and <= r under the causal mask
     int klo, khi;
-    row_keys(a, i0, i1, row0, krow0, nk, r, klo, khi);
+    row_keys<kPack>(a, i0, i1, row0, krow0, nk, r, klo, khi);
     mbar_wait(&sm.s_done, 0);
     if (r == 0) atr(tr, 4);
     tmem_fence_after();
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(kThreadsF, 4)
 }
 
 // ------------------------------------------------------------------ backward
+template <bool kPack>
 __global__ void __launch_bounds__(kThreadsB, 2)
     attn_bwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                 const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(kThreadsB, 2)
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(align1024(raw));
   const int b = blockIdx.x, h = blockIdx.y;
   int i0, i1;
-  if (!cta_instances(a, b, i0, i1)) return;
+  if (!cta_instances<kPack>(a, b, i0, i1)) return;
   const int row0 = a.cu_q[i0], n = a.cu_q[i1] - row0;  // queries
   const int krow0 = a.cu_kv[i0], nk = a.cu_kv[i1] - krow0;  // keys / values
   if (n <= 0 || nk <= 0) return;
@@ -468,7 +472,7 @@ __global__ void __launch_bounds__(kThreadsB, 2)
     const bool rok = r < n;        // query row r (S, dP, dQ)
     const bool kok = r < nk;       // key row r (dK, dV)
     int klo, khi;  // keys query row r sees
-    row_keys(a, i0, i1, row0, krow0, nk, r, klo, khi);
+    row_keys<kPack>(a, i0, i1, row0, krow0, nk, r, klo, khi);
     // D_r = rowsum(dO * O), lse_r -- while the MMAs run
     float Dr = 0.f, lr = 0.f;
     if (rok) {
@@ -1070,11 +1074,16 @@ void attention_tc_fwd(const AttnArgs& a, cudaStream_t s) {
   const int sm = static_cast<int>(sizeof(attn_tc::FwdSmem)) + 1024;
   static bool attr = false;
   if (!attr) {
-    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr = true;
   }
-  launch_ex(attn_tc::attn_fwd_tc, dim3(a.B, a.H), dim3(attn_tc::kThreadsF), sm, s, 1, mq, mk, mv, a,
-            g_attn_trace);
+  if (a.grp)
+    launch_ex(attn_tc::attn_fwd_tc<true>, dim3(a.B, a.H), dim3(attn_tc::kThreadsF), sm, s, 1, mq, mk, mv, a,
+              g_attn_trace);
+  else
+    launch_ex(attn_tc::attn_fwd_tc<false>, dim3(a.B, a.H), dim3(attn_tc::kThreadsF), sm, s, 1, mq, mk, mv, a,
+              g_attn_trace);
   HP_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -1089,10 +1098,14 @@ void attention_tc_bwd(const AttnArgs& a, cudaStream_t s) {
   const int sm = static_cast<int>(sizeof(attn_tc::BwdSmem)) + 1024;
   static bool attr = false;
   if (!attr) {
-    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    HP_CUDA(cudaFuncSetAttribute(attn_tc::attn_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr = true;
   }
-  launch_ex(attn_tc::attn_bwd_tc, dim3(a.B, a.H), dim3(attn_tc::kThreadsB), sm, s, 1, mq, mk, mv, mg, a);
+  if (a.grp)
+    launch_ex(attn_tc::attn_bwd_tc<true>, dim3(a.B, a.H), dim3(attn_tc::kThreadsB), sm, s, 1, mq, mk, mv, mg, a);
+  else
+    launch_ex(attn_tc::attn_bwd_tc<false>, dim3(a.B, a.H), dim3(attn_tc::kThreadsB), sm, s, 1, mq, mk, mv, mg, a);
   HP_CUDA(cudaGetLastError());
   count_launch();
 }

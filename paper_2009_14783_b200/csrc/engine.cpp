@@ -1087,7 +1087,6 @@ void Engine::emb_rows_update(int mode, cudaStream_t su) {
 
 void Engine::issue_bucket(size_t k) {
   const Bucket& bk = buckets_[k];
-  flush_finals();
   HP_CUDA(cudaEventRecord(ev_bucket_[k], s_main_));
   HP_CUDA(cudaStreamWaitEvent(s_comm_, ev_bucket_[k], 0));
   if (wg_forked_) {  // and every weight gradient issued so far this round
@@ -1237,12 +1236,9 @@ void Engine::backward() {
         if (wg_on_) {
           // d(ffn.b1) = colsum(dU) beside the chain (its own scratch), before
           // the event that lets the next layer reuse dU_
-          // (its final joins the batched finals, issued from the wgrad stream)
           tstop(TM_NORM, 0, 0);
           tstart(TM_NORM, s_wg_);
-          DeferredFinal f = final_slot(colsum_part_floats((int)x_.max_tokens, F_));
-          col_sum(T, F_, dU, F_, at_, gp(ib1), scratch_wg_, s_wg_, &f);
-          issue_final(f, s_wg_);
+          col_sum(T, F_, dU, F_, at_, gp(ib1), scratch_wg_, s_wg_);
           tstop(TM_NORM, 0, 0, s_wg_);
           HP_CUDA(cudaEventRecord(ev_w1_[l], s_wg_));
           tstart(TM_NORM);
@@ -1512,36 +1508,21 @@ DeferredFinal Engine::final_slot(size_t floats) {
   return f;
 }
 
-// The column-reduction finals (LayerNorm gamma / beta, bias gradients) of a
-// stretch of backward are queued and leave in ONE launch on the side stream
-// when a gradient bucket needs them (or backward ends) -- a dozen launches
-// per bucket become one.  Every queued final's partials come from the compute
-// stream, so the side stream waits on the last one's event.
-void Engine::issue_final(DeferredFinal& f, cudaStream_t st) {
+// A column-reduction final (LayerNorm gamma / beta, bias gradient) runs on
+// the side stream as soon as its partials are done.  (Batching them into one
+// launch per gradient bucket cut 23 launches per C2 step but cost 2.5 % at
+// N = 2 -- profiles/r02_ab_batched_finals.txt -- so each leaves on its own.)
+void Engine::issue_final(DeferredFinal& f) {
   if (!f.queued) return;
-  const bool wg = st && st != s_main_;
-  HP_CUDA(cudaEventRecord(final_evs_[final_n_], wg ? st : s_main_));
-  (wg ? finals_last_wg_ : finals_last_main_) = static_cast<int>(final_n_);
-  finals_q_.push_back(f);
-  ++final_n_;
-}
-
-void Engine::flush_finals() {
-  if (finals_q_.empty()) return;
-  if (finals_last_main_ >= 0) HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[finals_last_main_], 0));
-  if (finals_last_wg_ >= 0) HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[finals_last_wg_], 0));
-  finals_last_main_ = finals_last_wg_ = -1;
-  tstart(TM_NORM, s_comm_);
-  launch_finals(finals_q_.data(), static_cast<int>(finals_q_.size()), s_comm_);
-  tstop(TM_NORM, 0, 0, s_comm_);
+  HP_CUDA(cudaEventRecord(final_evs_[final_n_], s_main_));
+  HP_CUDA(cudaStreamWaitEvent(s_comm_, final_evs_[final_n_], 0));
+  launch_final(f, s_comm_);  // (inside the caller's layernorm-class span)
   serialize_if_timed(s_comm_);
-  finals_q_.clear();
+  ++final_n_;
 }
 
 void Engine::round_body(int dummy) {
   final_n_ = 0;
-  finals_q_.clear();
-  finals_last_main_ = finals_last_wg_ = -1;
   wg_forked_ = false;
   upd_forked_ = false;
   emb_sparse_round_ = false;
@@ -1616,8 +1597,8 @@ void Engine::round_body(int dummy) {
   }
   if (capture_) {
     if (!local_grads_) local_grads_ = static_cast<float*>(dalloc(n_ * 4));
-    // the column-reduction finals complete the local gradient before the copy
-    flush_finals();
+    // the column-reduction finals (side stream) complete the local gradient
+    // before the copy
     HP_CUDA(cudaEventRecord(ev_comm_done_, s_comm_));
     HP_CUDA(cudaStreamWaitEvent(s_main_, ev_comm_done_, 0));
     HP_CUDA(cudaMemcpyAsync(local_grads_, grads_, n_ * 4, cudaMemcpyDeviceToDevice, s_main_));

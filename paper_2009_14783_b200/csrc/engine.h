@@ -117,11 +117,7 @@ class Engine {
   void issue_bucket(size_t b);
   void round_body(int dummy);  // the device work of one round (eager or captured)
   DeferredFinal final_slot(size_t floats);  // partial buffer for the next deferred final
-  // queued for the side stream; `st` ran the final's partials (null: compute stream)
-  void issue_final(DeferredFinal& f, cudaStream_t st = nullptr);
-  void flush_finals();                       // the queued finals, one launch
-  std::vector<DeferredFinal> finals_q_;
-  int finals_last_main_ = -1, finals_last_wg_ = -1;  // last queued event per stream
+  void issue_final(DeferredFinal& f);        // its final on the side stream
 
   hp_model_desc m_;
   hp_optim_desc o_;

@@ -1013,49 +1013,6 @@ void layernorm_bwd(int T, int d, const void* dy, DType dyt, const void* x,
   }));
 }
 
-namespace {
-struct FinalDesc {
-  const float* part;
-  float *o0, *o1, *o2;
-  int kind, chunks, d, stride, n;
-};
-constexpr int kMaxFinals = 24;
-struct FinalBatch {
-  FinalDesc f[kMaxFinals];
-};
-// kind 0: the [chunks x 3d] LayerNorm partials -> dg, db, dbias (ln_part_final);
-// else the strided [chunks x n] column partials -> o0 (colsum_final_strided)
-__global__ void multi_final_kernel(const __grid_constant__ FinalBatch b) {
-  const FinalDesc& f = b.f[blockIdx.y];
-  const int ncols = f.kind == 0 ? 3 * f.d : f.n;
-  if (static_cast<int>(blockIdx.x) * 32 >= ncols) return;  // block-uniform
-  const int c = blockIdx.x * 32 + threadIdx.x;
-  const float acc = final_sum(f.chunks, f.kind == 0 ? 3 * f.d : f.stride, f.part, c, c < ncols);
-  if (threadIdx.y != 0 || c >= ncols) return;
-  if (f.kind != 0) f.o0[c] = acc;
-  else if (c < f.d) f.o0[c] = acc;
-  else if (c < 2 * f.d) f.o1[c - f.d] = acc;
-  else if (f.o2) f.o2[c - 2 * f.d] = acc;
-}
-}  // namespace
-
-void launch_finals(const DeferredFinal* f, int n, cudaStream_t s) {
-  for (int i0 = 0; i0 < n; i0 += kMaxFinals) {
-    FinalBatch b{};
-    int cnt = 0, maxcols = 0;
-    for (int i = i0; i < std::min(n, i0 + kMaxFinals); ++i) {
-      if (!f[i].queued) continue;
-      b.f[cnt] = FinalDesc{f[i].part, f[i].o0, f[i].o1, f[i].o2, f[i].kind, f[i].chunks, f[i].d, f[i].stride, f[i].n};
-      maxcols = std::max(maxcols, f[i].kind == 0 ? 3 * f[i].d : f[i].n);
-      ++cnt;
-    }
-    if (!cnt) continue;
-    multi_final_kernel<<<dim3((maxcols + 31) / 32, cnt), dim3(32, kFinY), 0, s>>>(b);
-    LAUNCH_CHECK();
-    count_launch();
-  }
-}
-
 void launch_final(const DeferredFinal& f, cudaStream_t s) {
   if (!f.queued) return;
   if (f.kind == 0) {

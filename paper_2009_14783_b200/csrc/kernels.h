@@ -130,8 +130,6 @@ struct DeferredFinal {
   float *o0 = nullptr, *o1 = nullptr, *o2 = nullptr;
 };
 void launch_final(const DeferredFinal& f, cudaStream_t s);
-// several finals in one launch (each its own blockIdx.y); same sums, same order
-void launch_finals(const DeferredFinal* f, int n, cudaStream_t s);
 size_t colsum_part_floats(int R, int N);
 
 void layernorm_fwd(int T, int d, const void* x, DType xt, const float* g,
