@@ -172,11 +172,14 @@ Engine::Engine(const hp_model_desc& m, const hp_optim_desc& o, const hp_exec_des
     // (C2, N = 2: 13908 / 13879 vs 13632 / 13628 samples/s, exposed allreduce
     // 0.43 vs 0.46 ms; at N = 1 a cap only costs, 7305 vs 7579;
     // profiles/r02_ab_gemm_sm_budget.txt).  HP_GEMM_SMS overrides (0: all).
+    // Forward has no bucket allreduce beside it (the previous round's last
+    // update has joined the compute stream): its GEMMs take every SM
+    // (HP_GEMM_SMS_FWD overrides).
     const char* e = std::getenv("HP_GEMM_SMS");
-    if (e)
-      gemm_tc_set_sm_budget(std::atoi(e));
-    else
-      gemm_tc_set_sm_budget(comm_ && comm_->world > 1 ? 140 : 0);
+    sms_bwd_ = e ? std::atoi(e) : (comm_ && comm_->world > 1 ? 140 : 0);
+    const char* f = std::getenv("HP_GEMM_SMS_FWD");
+    sms_fwd_ = f ? std::atoi(f) : (e ? sms_bwd_ : 0);
+    gemm_tc_set_sm_budget(sms_bwd_);
   }
   ev_reduced_.resize(buckets_.size());
   for (auto& e : ev_reduced_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1528,7 +1531,9 @@ void Engine::round_body(int dummy) {
   emb_sparse_round_ = false;
   emb_split_round_ = false;
   // Dummies run the forward too (symmetric compute, engine.hpp:128-129).
+  gemm_tc_set_sm_budget(sms_fwd_);
   forward(!dummy);
+  gemm_tc_set_sm_budget(sms_bwd_);
   loss_reduce(row_loss_, batch_.M, row_loss_ + batch_.M, m_.with_nsp ? batch_.B : 0, d_lw_,
               s_main_);
   // d_lw_ = [loss, weight, local loss, local weight]

@@ -180,6 +180,7 @@ class Engine {
   const int* s2s_grp_ = nullptr;
   const int* s2s_ngrp_ = nullptr;
   bool attn_pack_ = true;
+  int sms_fwd_ = 0, sms_bwd_ = 0;  // GEMM grid SM budget in forward / the rest (0: all)
   void *dqc_ = nullptr, *dkvc_ = nullptr, *dmem_ = nullptr, *demb_ = nullptr;
   void *x_final_ = nullptr, *p0_ = nullptr;
   float *mean0_ = nullptr, *rstd0_ = nullptr;
