@@ -196,19 +196,20 @@ __device__ __forceinline__ void emb_load8(const XT* p, float* f) {
   }
 }
 
+// small ids: warp `gw` of `nw` warps (across the blocks taking this role)
 template <class XT>
-__global__ void __launch_bounds__(256) embed_grad_small(const int* __restrict__ counts,
-                                                        const int* __restrict__ ulist,
-                                                        const int* __restrict__ uid,
-                                                        const int* __restrict__ useg,
-                                                        const int* __restrict__ perm, int d,
-                                                        const XT* __restrict__ dx,
-                                                        float* __restrict__ dE, int64_t ostride,
-                                                        int by_slot) {
+__device__ __forceinline__ void embed_grad_small_warps(int gw, int nw, const int* __restrict__ counts,
+                                                       const int* __restrict__ ulist,
+                                                       const int* __restrict__ uid,
+                                                       const int* __restrict__ useg,
+                                                       const int* __restrict__ perm, int d,
+                                                       const XT* __restrict__ dx,
+                                                       float* __restrict__ dE, int64_t ostride,
+                                                       int by_slot) {
   const int n_small = counts[0];
-  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int d8 = d / 8;
-  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_small; i += gridDim.x * wpb) {
+  for (int i = gw; i < n_small; i += nw) {
     const int u = ulist[i];
     const int k0 = useg[u], cnt = useg[u + 1] - k0;  // <= kEmbHot = 32: one position per lane
     const int mine = lane < cnt ? perm[k0 + lane] : 0;
@@ -238,20 +239,21 @@ __global__ void __launch_bounds__(256) embed_grad_small(const int* __restrict__ 
   }
 }
 
+// hot ids: block `hb` of `nhb` (1024 threads: 32 warps)
 template <class XT>
-__global__ void __launch_bounds__(1024) embed_grad_hot(const int* __restrict__ counts,
-                                                       const int* __restrict__ ulist,
-                                                       const int* __restrict__ uid,
-                                                       const int* __restrict__ useg,
-                                                       const int* __restrict__ perm, int d,
-                                                       const XT* __restrict__ dx,
-                                                       float* __restrict__ dE, int64_t ostride,
-                                                       int by_slot) {
-  extern __shared__ float part[];  // [32 warps][d]
+__device__ __forceinline__ void embed_grad_hot_block(int hb, int nhb, float* part,
+                                                     const int* __restrict__ counts,
+                                                     const int* __restrict__ ulist,
+                                                     const int* __restrict__ uid,
+                                                     const int* __restrict__ useg,
+                                                     const int* __restrict__ perm, int d,
+                                                     const XT* __restrict__ dx,
+                                                     float* __restrict__ dE, int64_t ostride,
+                                                     int by_slot) {
   const int n_small = counts[0], n_hot = counts[1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d8 = d / 8;
-  for (int i = blockIdx.x; i < n_hot; i += gridDim.x) {
+  for (int i = hb; i < n_hot; i += nhb) {
     const int u = ulist[n_small + i];
     const int k0 = useg[u], k1 = useg[u + 1];
     for (int c8 = lane; c8 < d8; c8 += 32) {
@@ -278,6 +280,30 @@ __global__ void __launch_bounds__(1024) embed_grad_hot(const int* __restrict__ c
       o[c] = acc;
     }
     __syncthreads();
+  }
+}
+
+// One launch for both: blocks [0, kEmbHotBlocks) take the hot ids, the rest
+// the small ones -- the two disjoint row sets are summed side by side.
+constexpr int kEmbHotBlocks = 64;
+template <class XT>
+__global__ void __launch_bounds__(1024) embed_grad_kernel(const int* __restrict__ counts,
+                                                          const int* __restrict__ ulist,
+                                                          const int* __restrict__ uid,
+                                                          const int* __restrict__ useg,
+                                                          const int* __restrict__ perm, int d,
+                                                          const XT* __restrict__ dx,
+                                                          float* __restrict__ dE, int64_t ostride,
+                                                          int by_slot) {
+  extern __shared__ float part[];  // hot blocks: [32 warps][d]
+  if (blockIdx.x < kEmbHotBlocks) {
+    embed_grad_hot_block<XT>(blockIdx.x, kEmbHotBlocks, part, counts, ulist, uid, useg, perm, d, dx, dE,
+                             ostride, by_slot);
+  } else {
+    const int wpb = blockDim.x >> 5;
+    embed_grad_small_warps<XT>((blockIdx.x - kEmbHotBlocks) * wpb + (threadIdx.x >> 5),
+                               (gridDim.x - kEmbHotBlocks) * wpb, counts, ulist, uid, useg, perm, d, dx,
+                               dE, ostride, by_slot);
   }
 }
 
@@ -487,21 +513,20 @@ static void embed_bwd_impl(const DevBatch& b, int d, const void* dx, DType xt, f
   if (b.T == 0) return;
   DISPATCH1(xt, X, {
     if (d % 8) fail(HP_ECONFIG, "embedding gradient: d_model must be a multiple of 8");
-    embed_grad_small<X><<<148 * 4, 256, 0, s>>>(b.ucount, b.ulist, b.uid, b.useg, b.perm, d,
-                                                (const X*)dx, dE, ostride, by_slot);
-    LAUNCH_CHECK();
     {
       const int sm = 32 * d * (int)sizeof(float);
       static int set_for = 0;
       if (sm > 48 * 1024 && sm > set_for) {
-        HP_CUDA(cudaFuncSetAttribute(embed_grad_hot<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        HP_CUDA(cudaFuncSetAttribute(embed_grad_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         set_for = sm;
       }
-      embed_grad_hot<X><<<64, 1024, sm, s>>>(b.ucount, b.ulist, b.uid, b.useg, b.perm, d,
-                                             (const X*)dx, dE, ostride, by_slot);
+      // 64 hot-id blocks + 148 blocks of 32 warps for the small ids
+      embed_grad_kernel<X><<<kEmbHotBlocks + 148, 1024, sm, s>>>(b.ucount, b.ulist, b.uid, b.useg,
+                                                                  b.perm, d, (const X*)dx, dE,
+                                                                  ostride, by_slot);
       LAUNCH_CHECK();
     }
-    count_launch(2);
+    count_launch(1);
     if (dseg0) {
       // both segment rows in one pass over dx (rows of 32, 8 columns a thread)
       const int rows_per = 32, chunks = (b.T + rows_per - 1) / rows_per;
